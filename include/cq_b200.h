@@ -1,0 +1,193 @@
+/* cq_b200 — C ABI of the B200-native CodeQuant Stage-4 path (LUT MoE matmul).
+ *
+ * Plain pointers and sizes only.  Every pointer argument is DEVICE memory
+ * unless its name ends in `_host`; `stream` is a cudaStream_t passed as void*.
+ * Every entry point returns a cq_status; cq_last_error() gives the message.
+ *
+ * Each entry point replaces one reference interface (reference tree
+ * /root/reference/pkg/src/codequant/, file:line):
+ *
+ *   cq_quantize_a4          quant.py:89-100        quantize_activations(x, QuantSpec(4))
+ *   cq_unpack_ids           kernels/fallback.py:35-42  unpack_ids(ids_packed, d_in)
+ *   cq_reference_gemm_f32   kernels/_core.pyx:154-211  reference_gemm_f32 (via
+ *                           kernels/__init__.py:91-94, lutgemm.py:147-161)
+ *   cq_lut_gemm_f32         kernels/_core.pyx:41-151   lut_gemm_f32 (via
+ *                           kernels/__init__.py:86-88, lutgemm.py:133-144)
+ *   cq_matmul_f32           kernels/_core.pyx:27-38    matmul_f32 (kernels/__init__.py:72-78)
+ *   cq_route_topk           model.py:324-330 + 377-385 select_top_k on the router logits
+ *   cq_moe_*                model.py:377-404       the MoE block of forward(), promoted to an
+ *                                                  operator; the reference
+ *                                                  has no such entry point.
+ *   cq_lut8_prepare         (new) one-time device re-layout of PackedClusteredWeights for the
+ *                           tensor-core path; consumes lutgemm.py:53-87 tensors unchanged.
+ */
+#ifndef CQ_B200_H
+#define CQ_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CQ_API __attribute__((visibility("default")))
+#else
+#define CQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CQ_OK = 0,
+    CQ_ERR_SHAPE = 1,      /* -> ShapeError       (errors.py:12)  */
+    CQ_ERR_CONFIG = 2,     /* -> ConfigError      (errors.py:20)  */
+    CQ_ERR_DIVERGENCE = 3, /* -> DivergenceError  (errors.py:28)  */
+    CQ_ERR_CUDA = 4,       /* -> RuntimeError (CUDA launch / device fault) */
+    CQ_ERR_UNSUPPORTED = 5 /* -> ConfigError: shape outside a kernel's envelope */
+} cq_status;
+
+enum { CQ_DTYPE_F32 = 0, CQ_DTYPE_BF16 = 1 };
+
+/* Last error message of the calling thread ("" when none). */
+CQ_API const char *cq_last_error(void);
+/* ABI version, bumped on any signature change. */
+CQ_API int cq_abi_version(void);
+/* Number of kernels this library launched so far (all entry points). */
+CQ_API int64_t cq_launch_count(void);
+
+/* Per-token symmetric 4-bit quantization, bit-exact with quant.py:89-100 for
+ * float32 input (bf16 input is quantized as its exact float32 upcast).
+ * x: (n, d) row-major, dtype CQ_DTYPE_*.  codes: (n, d) int8, scales: (n,) f32.
+ * Non-finite input -> CQ_ERR_DIVERGENCE (checked on the host after a sync;
+ * pass check_finite=0 on the hot path to skip the sync). */
+CQ_API cq_status cq_quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes,
+                         float *scales, int check_finite, void *stream);
+
+/* Low-nibble-first unpack, bit-exact: ids[r, 2m] = b & 15, ids[r, 2m+1] = b >> 4.
+ * packed: (rows, ceil(d_in/2)) u8 -> ids: (rows, d_in) u8. */
+CQ_API cq_status cq_unpack_ids(const uint8_t *packed, int64_t rows, int64_t d_in, uint8_t *ids,
+                        void *stream);
+
+/* Ordered per-element GEMM, BIT-EXACT with reference_gemm_f32 / lut_gemm_f32:
+ * out[t,i] = s_t * (((0 + c(i,0)*q(t,0)) + c(i,1)*q(t,1)) + ...), fp32, no FMA.
+ * codes (n, d_in) int8 (4- or 8-bit values), scales (n,), ids_packed
+ * (d_out, ceil(d_in/2)), centroids (d_out, d_in/g, 16) f32, out (n, d_out) f32.
+ * Any g >= 1 dividing d_in, any d_in (odd included). */
+CQ_API cq_status cq_reference_gemm_f32(const int8_t *codes, const float *scales,
+                                const uint8_t *ids_packed, const float *centroids, int64_t n,
+                                int64_t d_in, int64_t d_out, int64_t g, float *out,
+                                void *stream);
+
+/* LUT GEMM, fp32 CUDA-core path: same contract as cq_reference_gemm_f32 but
+ * accumulated in parallel (FMA, warp-split K), so equal within ~1e-6 relative
+ * rather than bitwise.  Falls through to the ordered kernel for shapes
+ * outside its envelope (g % 8 != 0 or d_in % 8 != 0). */
+CQ_API cq_status cq_lut_gemm_f32(const int8_t *codes, const float *scales, const uint8_t *ids_packed,
+                          const float *centroids, int64_t n, int64_t d_in, int64_t d_out,
+                          int64_t g, float *out, void *stream);
+
+/* Ordered fp32 matmul, bit-exact with _core.matmul_f32: out (m, n) = a (m, k) @ b (k, n),
+ * k ascending, one rounding per multiply and per add. */
+CQ_API cq_status cq_matmul_f32(const float *a, const float *b, float *out, int64_t m, int64_t k,
+                        int64_t n, void *stream);
+
+/* select_top_k (model.py:324-330) on fp32 logits (n, E): stable descending order,
+ * ties -> lower expert id, weights = softmax over the selected logits.
+ * selected (n, k) int32, weights (n, k) f32. */
+CQ_API cq_status cq_route_topk(const float *logits, int64_t n, int64_t n_experts, int64_t top_k,
+                        int32_t *selected, float *weights, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * MoE layer operator (model.py:377-404).
+ *
+ * Expert weights are stacked per site: ids [E][d_out][d_in/2] u8 and centroids
+ * [E][d_out][d_in/g][16] f32 — exactly PackedClusteredWeights (lutgemm.py:53-87)
+ * of each expert laid end to end.  gate/up: d_in = d_model, d_out = d_ff;
+ * down: d_in = d_ff, d_out = d_model.  Optional lut8 tensors (from
+ * cq_lut8_prepare) enable the tensor-core path. */
+typedef struct {
+    const uint8_t *ids;        /* [E][d_out][d_in/2] */
+    const float *centroids;    /* [E][d_out][d_in/g][16] */
+    int64_t group_size;        /* g */
+    /* tensor-core device layout (cq_lut8_prepare); NULL -> fp32 path */
+    const uint8_t *tc_ids;     /* fragment-ordered nibbles, same bytes as ids */
+    const int8_t *tc_lut;      /* [E][d_out][d_in/g][3][16] int8 digit planes */
+    const float *tc_rowscale;  /* [E][d_out] */
+} cq_expert_site;
+
+typedef struct {
+    int64_t d_model, d_ff, n_experts, top_k;
+    int64_t n_local_experts;   /* experts held by this rank (== n_experts w/o EP) */
+    int64_t expert_begin;      /* global id of the first local expert */
+    const float *w_router;     /* [d_model][n_experts] f32 (full precision, pipeline.py:455-467) */
+    const float *rotation;     /* optional online rotation R [d_model][d_model] f32, v = x @ R */
+    cq_expert_site gate, up, down;
+    int64_t n_shared;          /* builder-defined always-on experts (weight 1), stacked like the above */
+    cq_expert_site sh_gate, sh_up, sh_down;
+    int32_t path;              /* CQ_PATH_* */
+} cq_moe_desc;
+
+enum { CQ_PATH_AUTO = 0, CQ_PATH_F32 = 1, CQ_PATH_TC = 2, CQ_PATH_ORDERED = 3 };
+
+/* Named scratch buffers inside the caller-provided workspace. */
+enum {
+    CQ_WS_CODES = 0,    /* int8 [n][d_model]   layer-input codes            */
+    CQ_WS_SCALES,       /* f32  [n]                                          */
+    CQ_WS_LOGITS,       /* f32  [n][E]         ordered router logits         */
+    CQ_WS_SELECTED,     /* i32  [n][k]                                       */
+    CQ_WS_WEIGHTS,      /* f32  [n][k]                                       */
+    CQ_WS_COUNTS,       /* i32  [E]                                          */
+    CQ_WS_OFFSETS,      /* i32  [E+1]          local expert segments         */
+    CQ_WS_PERM_TOKEN,   /* i32  [n*k]                                        */
+    CQ_WS_PERM_SLOT,    /* i32  [n*k]                                        */
+    CQ_WS_INV,          /* i32  [n][k]         route -> segment row          */
+    CQ_WS_CODES_PERM,   /* int8 [n*k][d_model] codes gathered per segment    */
+    CQ_WS_SCALES_PERM,  /* f32  [n*k]                                        */
+    CQ_WS_HIDDEN,       /* f32  [n*k][d_ff]    silu(a)*b                     */
+    CQ_WS_HCODES,       /* int8 [n*k][d_ff]    re-quantized hidden           */
+    CQ_WS_HSCALES,      /* f32  [n*k]                                        */
+    CQ_WS_FOUT,         /* f32  [n*k][d_model] per-route down output         */
+    CQ_WS_ROTATED,      /* f32  [n][d_model]   x @ R (online rotation only)  */
+    CQ_WS_SHARED,       /* f32  [n][d_model]   shared-expert sum             */
+    CQ_WS_COUNT_
+};
+
+/* Byte offsets of every CQ_WS_* buffer for n tokens; returns the total size. */
+CQ_API int64_t cq_moe_workspace(const cq_moe_desc *desc, int64_t n_tokens, int64_t *offsets_out);
+
+/* Full layer: x (n, d_model) dtype CQ_DTYPE_* -> out (n, d_model) f32 = moe_sum.
+ * No host synchronisation; deterministic for a given path. */
+CQ_API cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int dtype, int64_t n_tokens,
+                         float *out, void *workspace, int64_t workspace_bytes, void *stream);
+
+/* The stages of cq_moe_forward, exposed for expert parallelism (the EP driver
+ * runs routing on every rank, exchanges codes, and runs the expert stage on the
+ * rank that owns the expert). */
+CQ_API cq_status cq_moe_route(const cq_moe_desc *desc, const void *x, int dtype, int64_t n_tokens,
+                       void *workspace, int64_t workspace_bytes, void *stream);
+/* Grouped experts over segment rows: codes_perm (rows, d_model), scales_perm,
+ * offsets (n_local+1) -> fout (rows, d_model).  `rows` is a host-known bound. */
+CQ_API cq_status cq_moe_experts(const cq_moe_desc *desc, const int8_t *codes_perm,
+                         const float *scales_perm, const int32_t *offsets, int64_t rows,
+                         float *fout, void *workspace, int64_t workspace_bytes, void *stream);
+/* Weighted combine in ascending expert order (model.py:389-401). */
+CQ_API cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
+                         const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
+                         const float *add, float *out, void *stream);
+
+/* One-time re-layout of one stacked site for the tensor-core path.
+ * ids (E*d_out, d_in/2), centroids (E*d_out, d_in/g, 16) ->
+ * tc_ids (same bytes, fragment order), tc_lut [E*d_out][d_in/g][3][16] int8,
+ * tc_rowscale [E*d_out] f32.  Requires d_out % 16 == 0, d_in % 64 == 0, g % 32 == 0. */
+CQ_API cq_status cq_lut8_prepare(const uint8_t *ids, const float *centroids, int64_t rows,
+                          int64_t d_in, int64_t g, uint8_t *tc_ids, int8_t *tc_lut,
+                          float *tc_rowscale, void *stream);
+
+/* Tensor-core LUT GEMM on prepared weights (one matrix): out (n, d_out) f32. */
+CQ_API cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, const uint8_t *tc_ids,
+                         const int8_t *tc_lut, const float *tc_rowscale, int64_t n,
+                         int64_t d_in, int64_t d_out, int64_t g, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CQ_B200_H */

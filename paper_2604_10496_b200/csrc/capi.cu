@@ -1,0 +1,12 @@
+// Error state, launch counter and version of the cq_b200 C ABI.
+#include "common.cuh"
+
+namespace cq {
+static thread_local std::string t_error;
+std::atomic<int64_t> g_launches{0};
+void set_error(const std::string &msg) { t_error = msg; }
+}  // namespace cq
+
+extern "C" const char *cq_last_error(void) { return cq::t_error.c_str(); }
+extern "C" int cq_abi_version(void) { return 1; }
+extern "C" int64_t cq_launch_count(void) { return cq::g_launches.load(); }

@@ -1,0 +1,88 @@
+// Shared helpers for the cq_b200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/cq_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "cq_b200 targets sm_100a only"
+#endif
+
+namespace cq {
+
+// Thread-local last error + a process-wide launch counter (cq_launch_count).
+void set_error(const std::string &msg);
+extern std::atomic<int64_t> g_launches;
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline cq_status check_launch(const char *what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(what) + ": " + cudaGetErrorString(e));
+        return CQ_ERR_CUDA;
+    }
+    return CQ_OK;
+}
+
+#define CQ_TRY(expr)                         \
+    do {                                     \
+        cq_status _st = (expr);              \
+        if (_st != CQ_OK) return _st;        \
+    } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
+    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+// quant.py:76-86 for float32: clear (bits-1)=3 low significand bits.
+__device__ __forceinline__ float snap_scale(float s) {
+    return __uint_as_float(__float_as_uint(s) & ~7u);
+}
+
+// quant.py:89-100 scale for one row with max|x| = mx (mx finite).
+__device__ __forceinline__ float a4_scale(float mx) {
+    float s = snap_scale(__fdiv_rn(mx, 7.0f));
+    return mx == 0.0f ? 1.0f : s;
+}
+
+// round half away from zero (quant.py:69-73) then clip to [-8, 7].
+__device__ __forceinline__ int8_t a4_code(float x, float s) {
+    float r = roundf(__fdiv_rn(x, s));
+    r = fminf(fmaxf(r, -8.0f), 7.0f);
+    return static_cast<int8_t>(static_cast<int>(r));
+}
+
+// model.py:233-237: x * sigmoid(x), sigmoid split at 0.
+__device__ __forceinline__ float silu_f32(float x) {
+    const bool pos = x >= 0.0f;
+    const float ex = expf(pos ? -x : x);
+    const float sig = pos ? __fdiv_rn(1.0f, __fadd_rn(1.0f, ex)) : __fdiv_rn(ex, __fadd_rn(1.0f, ex));
+    return __fmul_rn(x, sig);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+}  // namespace cq

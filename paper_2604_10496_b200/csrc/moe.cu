@@ -1,0 +1,426 @@
+// MoE layer operator: the MoE block of model.forward (model.py:377-404) on the
+// device, stage by stage, all on the caller's stream with no host sync:
+//
+//   [rotation x@R] -> A4 quantize (quant.py:89-100) -> ordered router logits
+//   -> top-k + counts -> permute into expert segments -> gather codes
+//   -> grouped gate|up LUT GEMM with fused silu(a)*b  (model.py:392-396)
+//   -> A4 re-quantize of the hidden               (model.py:397-398)
+//   -> grouped down LUT GEMM                      (model.py:399)
+//   -> weighted combine, experts ascending        (model.py:389-401)
+//   [+ shared experts, weight 1 — builder-defined, SURVEY §8(a) a18]
+#include "common.cuh"
+
+namespace cq {
+
+// --- stage kernels defined in other units
+cq_status quantize_a4(const void *, int, int64_t, int64_t, int8_t *, float *, int *, cudaStream_t);
+cq_status router_logits(const int8_t *, const float *, const float *, int64_t, int64_t, int64_t, float *,
+                        cudaStream_t);
+cq_status topk(const float *, int64_t, int64_t, int64_t, int32_t *, float *, int32_t *, int64_t, int64_t,
+               cudaStream_t);
+cq_status permute(const int32_t *, const int32_t *, int64_t, int64_t, int64_t, int64_t, int32_t *,
+                  int32_t *, int32_t *, int32_t *, cudaStream_t);
+cq_status gather_rows(const int8_t *, const float *, const int32_t *, const int32_t *, int64_t, int64_t,
+                      int64_t, int8_t *, float *, cudaStream_t);
+cq_status lut_f32_grouped(const int8_t *, const float *, const int32_t *, int64_t, int64_t,
+                          const uint8_t *, const float *, const uint8_t *, const float *, int64_t,
+                          int64_t, int64_t, float *, cudaStream_t);
+bool f32_path_ok(int64_t d_in, int64_t g);
+cq_status lut_tc_grouped(const int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
+                         const cq_expert_site *, const cq_expert_site *, int64_t, int64_t, float *,
+                         cudaStream_t);
+bool tc_path_ok(int64_t d_in, int64_t d_out, int64_t g);
+
+// --- ordered grouped GEMM (GPU oracle path): bit-exact chains per segment.
+constexpr int OG_ROWS = 8, OG_TOK = 32, OG_J = 64;
+
+__global__ void __launch_bounds__(256) ordered_grouped_kernel(
+    const int8_t *__restrict__ codes, const float *__restrict__ scales, const int32_t *__restrict__ offsets,
+    int64_t seg_first, const uint8_t *__restrict__ ids, const float *__restrict__ cent, int64_t d_in,
+    int64_t d_out, int64_t g, float *__restrict__ out) {
+    __shared__ int8_t tile[OG_J][OG_TOK];
+    const int lane = threadIdx.x, wy = threadIdx.y;
+    const int64_t seg = blockIdx.z;
+    const int64_t rb = offsets[seg], re = offsets[seg + 1];
+    const int64_t t_blk = rb + blockIdx.x * (int64_t)OG_TOK;
+    if (t_blk >= re) return;
+    const int64_t t = t_blk + lane;
+    const int64_t i = blockIdx.y * (int64_t)OG_ROWS + wy;
+    const int64_t e = seg + seg_first;
+    const int64_t row_bytes = (d_in + 1) >> 1, n_groups = d_in / g;
+    const int64_t ii = i < d_out ? i : 0;
+    const uint8_t *idrow = ids + (e * d_out + ii) * row_bytes;
+    const float *crow = cent + (e * d_out + ii) * n_groups * 16;
+    float acc = 0.0f;
+    for (int64_t j0 = 0; j0 < d_in; j0 += OG_J) {
+        __syncthreads();
+        for (int x = wy * 32 + lane; x < OG_J * OG_TOK; x += 256) {
+            const int tt = x / OG_J, jj = x % OG_J;
+            const int64_t gt = t_blk + tt, gj = j0 + jj;
+            tile[jj][tt] = (gt < re && gj < d_in) ? codes[gt * d_in + gj] : (int8_t)0;
+        }
+        __syncthreads();
+        const int jn = (int)((d_in - j0) < OG_J ? (d_in - j0) : OG_J);
+        for (int jj = 0; jj < jn; ++jj) {
+            const int64_t j = j0 + jj;
+            const uint8_t b = __ldg(idrow + (j >> 1));
+            const int id = (j & 1) ? (b >> 4) : (b & 15);
+            acc = __fadd_rn(acc, __fmul_rn(__ldg(crow + (j / g) * 16 + id), (float)tile[jj][lane]));
+        }
+    }
+    if (t < re && i < d_out) out[t * d_out + i] = __fmul_rn(__ldg(scales + t), acc);
+}
+
+cq_status ordered_grouped(const int8_t *codes, const float *scales, const int32_t *offsets, int64_t n_seg,
+                          int64_t seg_first, int64_t rows_bound, const uint8_t *ids, const float *cent,
+                          int64_t d_in, int64_t d_out, int64_t g, float *out, cudaStream_t st) {
+    if (n_seg == 0 || rows_bound == 0 || d_out == 0) return CQ_OK;
+    dim3 grid((unsigned)ceil_div(rows_bound, OG_TOK), (unsigned)ceil_div(d_out, OG_ROWS), (unsigned)n_seg);
+    ordered_grouped_kernel<<<grid, dim3(32, OG_ROWS), 0, st>>>(codes, scales, offsets, seg_first, ids, cent,
+                                                               d_in, d_out, g, out);
+    return check_launch("ordered_grouped");
+}
+
+// h = silu(a) * b elementwise (model.py:396), in place into a.
+__global__ void silu_mul_kernel(float *__restrict__ a, const float *__restrict__ b, int64_t count) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count; x += (int64_t)gridDim.x * blockDim.x)
+        a[x] = __fmul_rn(silu_f32(a[x]), b[x]);
+}
+
+// out[t, :] = ((0 + w_e1 f_e1) + w_e2 f_e2) + ...  with e ascending (model.py:401),
+// then + add[t, :] (shared experts) when given.
+__global__ void combine_kernel(const int32_t *__restrict__ selected, const float *__restrict__ weights,
+                               const int32_t *__restrict__ inv, const float *__restrict__ fout, int64_t k,
+                               int64_t d, const float *__restrict__ add, float *__restrict__ out) {
+    __shared__ int32_t s_pos[16];
+    __shared__ float s_w[16];
+    const int64_t t = blockIdx.x;
+    if (threadIdx.x == 0) {
+        int32_t ex[16], pos[16];
+        float w[16];
+        for (int s = 0; s < k; ++s) {
+            ex[s] = selected[t * k + s];
+            pos[s] = inv[t * k + s];
+            w[s] = weights[t * k + s];
+        }
+        for (int a = 1; a < k; ++a)  // insertion sort by expert id (ids are distinct)
+            for (int b = a; b > 0 && ex[b - 1] > ex[b]; --b) {
+                int32_t te = ex[b]; ex[b] = ex[b - 1]; ex[b - 1] = te;
+                int32_t tp = pos[b]; pos[b] = pos[b - 1]; pos[b - 1] = tp;
+                float tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
+            }
+        for (int s = 0; s < k; ++s) {
+            s_pos[s] = pos[s];
+            s_w[s] = w[s];
+        }
+    }
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+        float acc = 0.0f;
+        for (int s = 0; s < k; ++s) acc = __fadd_rn(acc, __fmul_rn(s_w[s], fout[(int64_t)s_pos[s] * d + j]));
+        if (add != nullptr) acc = __fadd_rn(acc, add[t * d + j]);
+        out[t * d + j] = acc;
+    }
+}
+
+// Online rotation v = x @ R in fp32 (CUDA cores, 64x64 tiles).
+template <int DT>
+__global__ void __launch_bounds__(256) rotate_kernel(const void *__restrict__ x, const float *__restrict__ r,
+                                                     int64_t n, int64_t d, float *__restrict__ v) {
+    __shared__ float xs[16][64 + 1];
+    __shared__ float rs[16][64 + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+    float acc[4][4] = {};
+    for (int64_t k0 = 0; k0 < d; k0 += 16) {
+        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+            const int kk = e & 15, rr = e >> 4;
+            const int64_t gr = row0 + rr, gk = k0 + kk;
+            float xv = 0.0f;
+            if (gr < n && gk < d)
+                xv = DT == CQ_DTYPE_F32 ? reinterpret_cast<const float *>(x)[gr * d + gk]
+                                        : bf16_bits_to_f32(reinterpret_cast<const uint16_t *>(x)[gr * d + gk]);
+            xs[kk][rr] = xv;
+            const int cc = e & 63, k2 = e >> 6;
+            const int64_t gc = col0 + cc, gk2 = k0 + k2;
+            rs[k2][cc] = (gc < d && gk2 < d) ? r[gk2 * d + gc] : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xs[kk][ty * 4 + a], rs[kk][tx * 4 + b], acc[a][b]);
+        __syncthreads();
+    }
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            const int64_t gr = row0 + ty * 4 + a, gc = col0 + tx * 4 + b;
+            if (gr < n && gc < d) v[gr * d + gc] = acc[a][b];
+        }
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+
+int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
+    const int64_t d = dsc->d_model, ff = dsc->d_ff, E = dsc->n_experts, k = dsc->top_k;
+    const int64_t R = n * k;
+    const int64_t rows_sh = dsc->n_shared > 0 ? n : 0;
+    const int64_t Rh = R > rows_sh ? R : rows_sh;
+    int64_t sz[CQ_WS_COUNT_] = {};
+    sz[CQ_WS_CODES] = n * d;
+    sz[CQ_WS_SCALES] = n * 4;
+    sz[CQ_WS_LOGITS] = n * E * 4;
+    sz[CQ_WS_SELECTED] = n * k * 4;
+    sz[CQ_WS_WEIGHTS] = n * k * 4;
+    sz[CQ_WS_COUNTS] = (E + 1) * 4;
+    sz[CQ_WS_OFFSETS] = (E + 2) * 4;
+    sz[CQ_WS_PERM_TOKEN] = R * 4;
+    sz[CQ_WS_PERM_SLOT] = R * 4;
+    sz[CQ_WS_INV] = R * 4;
+    sz[CQ_WS_CODES_PERM] = R * d;
+    sz[CQ_WS_SCALES_PERM] = R * 4;
+    sz[CQ_WS_HIDDEN] = Rh * ff * 4 * (dsc->path == CQ_PATH_ORDERED ? 2 : 1);
+    sz[CQ_WS_HCODES] = Rh * ff;
+    sz[CQ_WS_HSCALES] = Rh * 4;
+    sz[CQ_WS_FOUT] = Rh * d * 4;
+    sz[CQ_WS_ROTATED] = dsc->rotation ? n * d * 4 : 0;
+    sz[CQ_WS_SHARED] = dsc->n_shared > 0 ? n * d * 4 : 0;
+    int64_t pos = 0;
+    for (int b = 0; b < CQ_WS_COUNT_; ++b) {
+        if (off) off[b] = pos;
+        pos += (sz[b] + 255) / 256 * 256;
+    }
+    return pos;
+}
+
+struct Ws {
+    int8_t *codes;
+    float *scales, *logits, *weights, *scales_perm, *hidden, *hscales, *fout, *rotated, *shared;
+    int32_t *selected, *counts, *offsets, *perm_token, *perm_slot, *inv;
+    int8_t *codes_perm, *hcodes;
+};
+
+Ws carve(void *base, const int64_t *o) {
+    char *b = reinterpret_cast<char *>(base);
+    Ws w;
+    w.codes = reinterpret_cast<int8_t *>(b + o[CQ_WS_CODES]);
+    w.scales = reinterpret_cast<float *>(b + o[CQ_WS_SCALES]);
+    w.logits = reinterpret_cast<float *>(b + o[CQ_WS_LOGITS]);
+    w.selected = reinterpret_cast<int32_t *>(b + o[CQ_WS_SELECTED]);
+    w.weights = reinterpret_cast<float *>(b + o[CQ_WS_WEIGHTS]);
+    w.counts = reinterpret_cast<int32_t *>(b + o[CQ_WS_COUNTS]);
+    w.offsets = reinterpret_cast<int32_t *>(b + o[CQ_WS_OFFSETS]);
+    w.perm_token = reinterpret_cast<int32_t *>(b + o[CQ_WS_PERM_TOKEN]);
+    w.perm_slot = reinterpret_cast<int32_t *>(b + o[CQ_WS_PERM_SLOT]);
+    w.inv = reinterpret_cast<int32_t *>(b + o[CQ_WS_INV]);
+    w.codes_perm = reinterpret_cast<int8_t *>(b + o[CQ_WS_CODES_PERM]);
+    w.scales_perm = reinterpret_cast<float *>(b + o[CQ_WS_SCALES_PERM]);
+    w.hidden = reinterpret_cast<float *>(b + o[CQ_WS_HIDDEN]);
+    w.hcodes = reinterpret_cast<int8_t *>(b + o[CQ_WS_HCODES]);
+    w.hscales = reinterpret_cast<float *>(b + o[CQ_WS_HSCALES]);
+    w.fout = reinterpret_cast<float *>(b + o[CQ_WS_FOUT]);
+    w.rotated = reinterpret_cast<float *>(b + o[CQ_WS_ROTATED]);
+    w.shared = reinterpret_cast<float *>(b + o[CQ_WS_SHARED]);
+    return w;
+}
+
+cq_status validate_desc(const cq_moe_desc *d) {
+    if (d == nullptr || d->d_model < 1 || d->d_ff < 1 || d->n_experts < 1 || d->top_k < 1) {
+        set_error("moe: bad descriptor dimensions");
+        return CQ_ERR_SHAPE;
+    }
+    if (d->top_k > d->n_experts || d->top_k > 16) {
+        set_error("moe: top_k must be <= n_experts and <= 16");
+        return CQ_ERR_CONFIG;
+    }
+    if (d->expert_begin < 0 || d->n_local_experts < 0 || d->expert_begin + d->n_local_experts > d->n_experts) {
+        set_error("moe: local expert range outside [0, n_experts)");
+        return CQ_ERR_CONFIG;
+    }
+    const cq_expert_site *sites[3] = {&d->gate, &d->up, &d->down};
+    const int64_t din[3] = {d->d_model, d->d_model, d->d_ff};
+    for (int s = 0; s < 3; ++s) {
+        const int64_t g = sites[s]->group_size;
+        if (g < 1 || din[s] % g) {
+            set_error("moe: group size does not divide the site's input dimension");
+            return CQ_ERR_SHAPE;
+        }
+    }
+    if (d->gate.group_size != d->up.group_size) {
+        set_error("moe: gate and up must share a group size (fused kernel)");
+        return CQ_ERR_CONFIG;
+    }
+    return CQ_OK;
+}
+
+int choose_path(const cq_moe_desc *d) {
+    if (d->path != CQ_PATH_AUTO) return d->path;
+    const bool tc = d->gate.tc_lut && d->up.tc_lut && d->down.tc_lut &&
+                    tc_path_ok(d->d_model, d->d_ff, d->gate.group_size) &&
+                    tc_path_ok(d->d_ff, d->d_model, d->down.group_size);
+    if (tc) return CQ_PATH_TC;
+    if (f32_path_ok(d->d_model, d->gate.group_size) && f32_path_ok(d->d_ff, d->down.group_size))
+        return CQ_PATH_F32;
+    return CQ_PATH_ORDERED;
+}
+
+// Expert stage over segment rows (gate|up -> silu*b -> requant -> down).
+cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &gate, const cq_expert_site &up,
+                      const cq_expert_site &down, int64_t n_seg, int64_t seg_first, const int8_t *codes,
+                      const float *scales, const int32_t *offsets, int64_t rows, float *hidden,
+                      int8_t *hcodes, float *hscales, float *fout, cudaStream_t st) {
+    const int64_t d = dsc->d_model, ff = dsc->d_ff;
+    if (rows == 0 || n_seg == 0) return CQ_OK;
+    if (path == CQ_PATH_TC) {
+        CQ_TRY(lut_tc_grouped(codes, scales, offsets, n_seg, seg_first, rows, &gate, &up, d, ff, hidden, st));
+    } else if (path == CQ_PATH_F32) {
+        CQ_TRY(lut_f32_grouped(codes, scales, offsets, n_seg, seg_first, gate.ids, gate.centroids, up.ids,
+                               up.centroids, d, ff, gate.group_size, hidden, st));
+    } else {
+        float *bbuf = hidden + rows * ff;
+        CQ_TRY(ordered_grouped(codes, scales, offsets, n_seg, seg_first, rows, gate.ids, gate.centroids, d, ff,
+                               gate.group_size, hidden, st));
+        CQ_TRY(ordered_grouped(codes, scales, offsets, n_seg, seg_first, rows, up.ids, up.centroids, d, ff,
+                               up.group_size, bbuf, st));
+        silu_mul_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * ff, 256), 148 * 16), 256, 0, st>>>(
+            hidden, bbuf, rows * ff);
+        CQ_TRY(check_launch("silu_mul"));
+    }
+    CQ_TRY(quantize_a4(hidden, CQ_DTYPE_F32, rows, ff, hcodes, hscales, nullptr, st));
+    if (path == CQ_PATH_TC)
+        return lut_tc_grouped(hcodes, hscales, offsets, n_seg, seg_first, rows, &down, nullptr, ff, d, fout, st);
+    if (path == CQ_PATH_F32)
+        return lut_f32_grouped(hcodes, hscales, offsets, n_seg, seg_first, down.ids, down.centroids, nullptr,
+                               nullptr, ff, d, down.group_size, fout, st);
+    return ordered_grouped(hcodes, hscales, offsets, n_seg, seg_first, rows, down.ids, down.centroids, ff, d,
+                           down.group_size, fout, st);
+}
+
+__global__ void add_inplace_kernel(float *__restrict__ a, const float *__restrict__ b, int64_t count) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count; x += (int64_t)gridDim.x * blockDim.x)
+        a[x] = __fadd_rn(a[x], b[x]);
+}
+
+__global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n) {
+    for (int64_t s = 0; s <= n_shared; ++s) off[s] = (int32_t)(s * n);
+}
+
+cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, const Ws &w, cudaStream_t st) {
+    const int64_t d = dsc->d_model;
+    const void *qin = x;
+    int qdt = dtype;
+    if (dsc->rotation != nullptr) {
+        dim3 grid((unsigned)ceil_div(d, 64), (unsigned)ceil_div(n, 64));
+        if (dtype == CQ_DTYPE_F32)
+            rotate_kernel<CQ_DTYPE_F32><<<grid, 256, 0, st>>>(x, dsc->rotation, n, d, w.rotated);
+        else
+            rotate_kernel<CQ_DTYPE_BF16><<<grid, 256, 0, st>>>(x, dsc->rotation, n, d, w.rotated);
+        CQ_TRY(check_launch("rotate"));
+        qin = w.rotated;
+        qdt = CQ_DTYPE_F32;
+    }
+    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, st));
+    CQ_TRY(router_logits(w.codes, w.scales, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
+    if (cudaMemsetAsync(w.counts, 0, (dsc->n_experts + 1) * 4, st) != cudaSuccess) {
+        set_error("moe: memset counts failed");
+        return CQ_ERR_CUDA;
+    }
+    CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, w.counts, dsc->expert_begin,
+                dsc->n_local_experts, st));
+    CQ_TRY(permute(w.selected, w.counts, n, dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets,
+                   w.perm_token, w.perm_slot, w.inv, st));
+    return gather_rows(w.codes, w.scales, w.perm_token, w.offsets, dsc->n_local_experts, n * dsc->top_k, d,
+                       w.codes_perm, w.scales_perm, st);
+}
+
+}  // namespace cq
+
+using namespace cq;
+
+extern "C" int64_t cq_moe_workspace(const cq_moe_desc *desc, int64_t n_tokens, int64_t *offsets_out) {
+    if (desc == nullptr || n_tokens < 0) return -1;
+    return workspace_layout(desc, n_tokens, offsets_out);
+}
+
+extern "C" cq_status cq_moe_route(const cq_moe_desc *desc, const void *x, int dtype, int64_t n_tokens,
+                                  void *workspace, int64_t workspace_bytes, void *stream) {
+    CQ_TRY(validate_desc(desc));
+    int64_t off[CQ_WS_COUNT_];
+    if (workspace_layout(desc, n_tokens, off) > workspace_bytes) {
+        set_error("moe: workspace too small");
+        return CQ_ERR_SHAPE;
+    }
+    if (n_tokens == 0) return CQ_OK;
+    return route(desc, x, dtype, n_tokens, carve(workspace, off), as_stream(stream));
+}
+
+extern "C" cq_status cq_moe_experts(const cq_moe_desc *desc, const int8_t *codes_perm, const float *scales_perm,
+                                    const int32_t *offsets, int64_t rows, float *fout, void *workspace,
+                                    int64_t workspace_bytes, void *stream) {
+    CQ_TRY(validate_desc(desc));
+    // the expert stage needs hidden/hcodes sized for `rows`; size the layout for rows/top_k tokens
+    const int64_t n_equiv = ceil_div(rows, desc->top_k);
+    int64_t off[CQ_WS_COUNT_];
+    if (workspace_layout(desc, n_equiv, off) > workspace_bytes) {
+        set_error("moe: workspace too small");
+        return CQ_ERR_SHAPE;
+    }
+    Ws w = carve(workspace, off);
+    return run_experts(desc, choose_path(desc), desc->gate, desc->up, desc->down, desc->n_local_experts, 0,
+                       codes_perm, scales_perm, offsets, rows, w.hidden, w.hcodes, w.hscales, fout,
+                       as_stream(stream));
+}
+
+extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
+                                    const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
+                                    const float *add, float *out, void *stream) {
+    if (n_tokens == 0) return CQ_OK;
+    if (top_k < 1 || top_k > 16) {
+        set_error("combine: top_k out of range");
+        return CQ_ERR_CONFIG;
+    }
+    combine_kernel<<<(unsigned)n_tokens, 256, 0, as_stream(stream)>>>(selected, weights, inv, fout, top_k, d_model,
+                                                                       add, out);
+    return check_launch("combine");
+}
+
+extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int dtype, int64_t n_tokens, float *out,
+                                    void *workspace, int64_t workspace_bytes, void *stream) {
+    CQ_TRY(validate_desc(desc));
+    if (desc->expert_begin != 0 || desc->n_local_experts != desc->n_experts) {
+        set_error("moe_forward runs all experts locally; use the EP driver for sharded experts");
+        return CQ_ERR_CONFIG;
+    }
+    int64_t off[CQ_WS_COUNT_];
+    if (workspace_layout(desc, n_tokens, off) > workspace_bytes) {
+        set_error("moe: workspace too small");
+        return CQ_ERR_SHAPE;
+    }
+    if (n_tokens == 0) return CQ_OK;
+    cudaStream_t st = as_stream(stream);
+    Ws w = carve(workspace, off);
+    const int path = choose_path(desc);
+    CQ_TRY(route(desc, x, dtype, n_tokens, w, st));
+    const int64_t R = n_tokens * desc->top_k;
+    CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes_perm,
+                       w.scales_perm, w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, st));
+    CQ_TRY(cq_moe_combine(w.selected, w.weights, w.inv, w.fout, n_tokens, desc->top_k, desc->d_model, nullptr,
+                          out, stream));
+    // builder-defined shared experts: out = ((routed + sh_0) + sh_1) ...,
+    // each shared expert run as one segment over all n tokens (un-permuted codes).
+    for (int64_t s = 0; s < desc->n_shared; ++s) {
+        int32_t *soff = w.counts;  // counts were consumed by permute; E+1 >= 2 ints
+        shared_offsets_kernel<<<1, 1, 0, st>>>(soff, 1, n_tokens);
+        CQ_TRY(check_launch("shared_offsets"));
+        const int sp = (path == CQ_PATH_TC && desc->sh_gate.tc_lut == nullptr) ? CQ_PATH_F32 : path;
+        CQ_TRY(run_experts(desc, sp, desc->sh_gate, desc->sh_up, desc->sh_down, 1, s, w.codes, w.scales, soff,
+                           n_tokens, w.hidden, w.hcodes, w.hscales, w.shared, st));
+        add_inplace_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_tokens * desc->d_model, 256), 148 * 16), 256, 0,
+                             st>>>(out, w.shared, n_tokens * desc->d_model);
+        CQ_TRY(check_launch("add_shared"));
+    }
+    return CQ_OK;
+}

@@ -1,0 +1,127 @@
+// Per-token A4 quantization (quant.py:89-100) and nibble unpack
+// (kernels/fallback.py:35-42), both bit-exact.
+#include "common.cuh"
+
+namespace cq {
+
+template <int DT>
+__device__ __forceinline__ float load_x(const void *x, int64_t idx) {
+    if (DT == CQ_DTYPE_F32) return __ldg(reinterpret_cast<const float *>(x) + idx);
+    return bf16_bits_to_f32(__ldg(reinterpret_cast<const uint16_t *>(x) + idx));
+}
+
+// One CTA per row.  Pass 1: max|x| (order-free, exact) + finiteness; pass 2:
+// codes with the IEEE-division recipe of common.cuh (no fast math anywhere).
+template <int DT>
+__global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict__ x, int64_t d,
+                                                          int8_t *__restrict__ codes,
+                                                          float *__restrict__ scales,
+                                                          int *__restrict__ nonfinite) {
+    const int64_t row = blockIdx.x;
+    const int64_t base = row * d;
+    float mx = 0.0f;
+    bool bad = false;
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+        float v = load_x<DT>(x, base + j);
+        bad |= !isfinite(v);
+        mx = fmaxf(mx, fabsf(v));
+    }
+    __shared__ float red[8];
+    __shared__ float s_sh;
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0) {
+            float s = a4_scale(m);
+            s_sh = s;
+            scales[row] = s;
+        }
+    }
+    __syncthreads();
+    const float s = s_sh;
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) codes[base + j] = a4_code(load_x<DT>(x, base + j), s);
+}
+
+__global__ void unpack_ids_kernel(const uint8_t *__restrict__ packed, int64_t rows, int64_t d_in,
+                                  uint8_t *__restrict__ ids) {
+    const int64_t row_bytes = (d_in + 1) >> 1;
+    const int64_t total = rows * d_in;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / d_in, j = idx - r * d_in;
+        const uint8_t b = packed[r * row_bytes + (j >> 1)];
+        ids[idx] = (j & 1) ? (uint8_t)(b >> 4) : (uint8_t)(b & 15);
+    }
+}
+
+cq_status quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes, float *scales,
+                      int *nonfinite_dev, cudaStream_t st) {
+    if (n == 0) return CQ_OK;
+    if (dtype == CQ_DTYPE_F32)
+        quantize_a4_kernel<CQ_DTYPE_F32><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev);
+    else
+        quantize_a4_kernel<CQ_DTYPE_BF16><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev);
+    return check_launch("quantize_a4");
+}
+
+}  // namespace cq
+
+using namespace cq;
+
+extern "C" cq_status cq_quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes,
+                                    float *scales, int check_finite, void *stream) {
+    if (n < 0 || d < 0) {
+        set_error("quantize: negative shape");
+        return CQ_ERR_SHAPE;
+    }
+    if (dtype != CQ_DTYPE_F32 && dtype != CQ_DTYPE_BF16) {
+        set_error("quantize: dtype must be float32 or bfloat16");
+        return CQ_ERR_SHAPE;
+    }
+    if (n == 0) return CQ_OK;
+    if (d == 0) {  // empty rows: max over nothing -> reference errors; mirror as shape
+        set_error("quantize: zero-width rows");
+        return CQ_ERR_SHAPE;
+    }
+    cudaStream_t st = as_stream(stream);
+    int *flag = nullptr;
+    if (check_finite) {
+        if (cudaMallocAsync(&flag, sizeof(int), st) != cudaSuccess ||
+            cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess) {
+            set_error("quantize: flag alloc failed");
+            return CQ_ERR_CUDA;
+        }
+    }
+    cq_status rc = quantize_a4(x, dtype, n, d, codes, scales, flag, st);
+    if (check_finite) {
+        int host = 0;
+        cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+        cudaFreeAsync(flag, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) {
+            set_error("quantize: sync failed");
+            return CQ_ERR_CUDA;
+        }
+        if (rc == CQ_OK && host) {
+            set_error("non-finite activation input to quantizer");
+            return CQ_ERR_DIVERGENCE;
+        }
+    }
+    return rc;
+}
+
+extern "C" cq_status cq_unpack_ids(const uint8_t *packed, int64_t rows, int64_t d_in, uint8_t *ids,
+                                   void *stream) {
+    if (rows < 0 || d_in < 0) {
+        set_error("unpack: negative shape");
+        return CQ_ERR_SHAPE;
+    }
+    if (rows * d_in == 0) return CQ_OK;
+    int64_t blocks = ceil_div(rows * d_in, 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    unpack_ids_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(packed, rows, d_in, ids);
+    return check_launch("unpack_ids");
+}

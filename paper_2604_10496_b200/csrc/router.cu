@@ -1,0 +1,219 @@
+// Router (model.py:379-385), top-k (model.py:324-330) and the builder-defined
+// token permutation into per-expert segments.
+//
+// Bit-exactness: logits reproduce the ordered fp32 chain of _core.matmul_f32
+// (k ascending, no FMA) on the exact fake-quant input codes*scale
+// (quant.py:8-13); top-k ids, their order, counts, offsets and the permutation
+// are therefore bit-exact.  Route weights use CUDA expf (ulp-bounded vs numpy).
+#include "common.cuh"
+
+namespace cq {
+
+// logits[t, e] = sum_k (q[t,k] * s_t) * W[k, e], ordered.  One thread per
+// (token, expert), expert fastest so W loads coalesce across lanes.
+__global__ void router_logits_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
+                                     const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp,
+                                     float *__restrict__ logits) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * n_exp) return;
+    const int64_t t = idx / n_exp, e = idx - t * n_exp;
+    const int8_t *q = codes + t * d;
+    const float s = __ldg(scales + t);
+    float acc = 0.0f;
+    int64_t k = 0;
+    for (; k + 4 <= d; k += 4) {  // loads batched, chain order unchanged
+        const char4 c4 = *reinterpret_cast<const char4 *>(q + k);
+        const float w0 = __ldg(w + (k + 0) * n_exp + e), w1 = __ldg(w + (k + 1) * n_exp + e);
+        const float w2 = __ldg(w + (k + 2) * n_exp + e), w3 = __ldg(w + (k + 3) * n_exp + e);
+        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.x, s), w0));
+        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.y, s), w1));
+        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.z, s), w2));
+        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.w, s), w3));
+    }
+    for (; k < d; ++k) acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)q[k], s), __ldg(w + k * n_exp + e)));
+    logits[idx] = acc;
+}
+
+// numpy's float32 sum of a short row: a plain loop below 8 elements, eight
+// interleaved partial sums combined as a tree from 8 up (pairwise_sum).
+__device__ __forceinline__ float np_sum(const float *v, int n) {
+    if (n < 8) {
+        float r = 0.0f;  // numpy starts from the first element; 0 + x == x exactly
+        for (int i = 0; i < n; ++i) r = __fadd_rn(r, v[i]);
+        return r;
+    }
+    float r[8];
+    for (int j = 0; j < 8; ++j) r[j] = v[j];
+    int i = 8;
+    for (; i + 8 <= n; i += 8)
+        for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], v[i + j]);
+    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __fadd_rn(res, v[i]);
+    return res;
+}
+
+constexpr int MAX_TOPK = 16;
+
+// One thread per token: stable descending selection (ties -> lower id; +0 and
+// -0 compare equal like numpy's sort), softmax over the selected logits, and
+// per-expert route counts for the local expert range.
+__global__ void topk_kernel(const float *__restrict__ logits, int64_t n, int64_t n_exp, int64_t k,
+                            int32_t *__restrict__ selected, float *__restrict__ weights,
+                            int32_t *__restrict__ counts, int64_t local_begin, int64_t n_local) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const float *row = logits + t * n_exp;
+    int sel[MAX_TOPK];
+    float val[MAX_TOPK];
+    for (int s = 0; s < k; ++s) {
+        int best = -1;
+        float bv = 0.0f;
+        for (int e = 0; e < n_exp; ++e) {
+            bool taken = false;
+            for (int p = 0; p < s; ++p) taken |= (sel[p] == e);
+            if (taken) continue;
+            const float v = row[e];
+            if (best < 0 || v > bv) {
+                best = e;
+                bv = v;
+            }
+        }
+        sel[s] = best;
+        val[s] = bv;
+    }
+    const float m = val[0];  // max of the selected logits
+    float ex[MAX_TOPK];
+    for (int s = 0; s < k; ++s) ex[s] = expf(__fsub_rn(val[s], m));
+    const float tot = np_sum(ex, (int)k);
+    for (int s = 0; s < k; ++s) {
+        selected[t * k + s] = sel[s];
+        weights[t * k + s] = __fdiv_rn(ex[s], tot);
+        const int64_t le = sel[s] - local_begin;
+        if (counts != nullptr && le >= 0 && le < n_local) atomicAdd(counts + le, 1);
+    }
+}
+
+// CTA per local expert: a stable block scan over tokens assigns each route of
+// this expert its row in the segment; CTA 0 also publishes offsets[0..E].
+constexpr int PERM_THREADS = 1024;
+
+__global__ void __launch_bounds__(PERM_THREADS) permute_kernel(
+    const int32_t *__restrict__ selected, const int32_t *__restrict__ counts, int64_t n, int64_t k,
+    int64_t local_begin, int64_t n_local, int32_t *__restrict__ offsets,
+    int32_t *__restrict__ perm_token, int32_t *__restrict__ perm_slot, int32_t *__restrict__ inv) {
+    __shared__ int32_t s_base;
+    __shared__ int32_t warp_tot[PERM_THREADS / 32];
+    const int e_loc = blockIdx.x;
+    const int64_t e_glob = e_loc + local_begin;
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int e = 0; e < e_loc; ++e) acc += counts[e];
+        s_base = acc;
+        if (e_loc == 0) {
+            int32_t run = 0;
+            for (int e = 0; e < n_local; ++e) {
+                offsets[e] = run;
+                run += counts[e];
+            }
+            offsets[n_local] = run;
+        }
+    }
+    __syncthreads();
+    int32_t base = s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t t0 = 0; t0 < n; t0 += PERM_THREADS) {
+        const int64_t t = t0 + threadIdx.x;
+        int slot = -1;
+        if (t < n)
+            for (int s = 0; s < k; ++s)
+                if (selected[t * k + s] == e_glob) slot = s;
+        const unsigned ball = __ballot_sync(0xffffffffu, slot >= 0);
+        const int in_warp = __popc(ball & ((1u << lane) - 1u));
+        if (lane == 0) warp_tot[warp] = __popc(ball);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < PERM_THREADS / 32; ++w) {
+            const int c = warp_tot[w];
+            before += (w < warp) ? c : 0;
+            total += c;
+        }
+        if (slot >= 0) {
+            const int32_t pos = base + before + in_warp;
+            perm_token[pos] = (int32_t)t;
+            perm_slot[pos] = slot;
+            if (inv != nullptr) inv[t * k + slot] = pos;
+        }
+        base += total;
+        __syncthreads();
+    }
+}
+
+// rows_out[r, :] = rows_in[perm_token[r], :], r < offsets[n_local]; also scales.
+__global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *__restrict__ sscale,
+                                   const int32_t *__restrict__ perm_token,
+                                   const int32_t *__restrict__ offsets, int64_t n_local, int64_t d,
+                                   int8_t *__restrict__ dst, float *__restrict__ dscale) {
+    const int64_t r = blockIdx.x;
+    if (r >= offsets[n_local]) return;
+    const int64_t t = perm_token[r];
+    if (threadIdx.x == 0) dscale[r] = sscale[t];
+    const int8_t *s = src + t * d;
+    int8_t *o = dst + r * d;
+    if ((d & 15) == 0) {
+        for (int64_t j = threadIdx.x * 16; j < d; j += blockDim.x * 16)
+            *reinterpret_cast<uint4 *>(o + j) = *reinterpret_cast<const uint4 *>(s + j);
+    } else {
+        for (int64_t j = threadIdx.x; j < d; j += blockDim.x) o[j] = s[j];
+    }
+}
+
+cq_status router_logits(const int8_t *codes, const float *scales, const float *w, int64_t n,
+                        int64_t d, int64_t n_exp, float *logits, cudaStream_t st) {
+    if (n * n_exp == 0) return CQ_OK;
+    router_logits_kernel<<<(unsigned)ceil_div(n * n_exp, 64), 64, 0, st>>>(codes, scales, w, n, d, n_exp, logits);
+    return check_launch("router_logits");
+}
+
+cq_status topk(const float *logits, int64_t n, int64_t n_exp, int64_t k, int32_t *sel, float *wts,
+               int32_t *counts, int64_t local_begin, int64_t n_local, cudaStream_t st) {
+    if (k < 1 || k > MAX_TOPK || k > n_exp) {
+        set_error("top_k must be in [1, min(16, n_experts)]");
+        return CQ_ERR_CONFIG;
+    }
+    if (n == 0) return CQ_OK;
+    topk_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(logits, n, n_exp, k, sel, wts, counts,
+                                                            local_begin, n_local);
+    return check_launch("topk");
+}
+
+cq_status permute(const int32_t *sel, const int32_t *counts, int64_t n, int64_t k, int64_t local_begin,
+                  int64_t n_local, int32_t *offsets, int32_t *perm_token, int32_t *perm_slot,
+                  int32_t *inv, cudaStream_t st) {
+    if (n_local == 0) return CQ_OK;
+    permute_kernel<<<(unsigned)n_local, PERM_THREADS, 0, st>>>(sel, counts, n, k, local_begin, n_local,
+                                                               offsets, perm_token, perm_slot, inv);
+    return check_launch("permute");
+}
+
+cq_status gather_rows(const int8_t *src, const float *sscale, const int32_t *perm_token,
+                      const int32_t *offsets, int64_t n_local, int64_t rows_bound, int64_t d,
+                      int8_t *dst, float *dscale, cudaStream_t st) {
+    if (rows_bound == 0) return CQ_OK;
+    gather_rows_kernel<<<(unsigned)rows_bound, 128, 0, st>>>(src, sscale, perm_token, offsets, n_local, d,
+                                                             dst, dscale);
+    return check_launch("gather_rows");
+}
+
+}  // namespace cq
+
+using namespace cq;
+
+extern "C" cq_status cq_route_topk(const float *logits, int64_t n, int64_t n_experts, int64_t top_k,
+                                   int32_t *selected, float *weights, void *stream) {
+    if (n < 0 || n_experts < 1) {
+        set_error("route: bad shape");
+        return CQ_ERR_SHAPE;
+    }
+    return topk(logits, n, n_experts, top_k, selected, weights, nullptr, 0, 0, as_stream(stream));
+}

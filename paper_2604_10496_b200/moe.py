@@ -1,0 +1,218 @@
+"""MoE-layer operator: the MoE block of the reference's forward pass
+(model.py:377-404) as one device call (`cq_moe_forward`).
+
+Inputs are the reference's own formats, unchanged: a full-precision router
+weight (d_model, E) (pipeline.py:455-467), per-expert PackedClusteredWeights
+for gate / up / down (lutgemm.py:53-87) and an optional rotation matrix R
+(rotation.py:83-87; applied online as v = x @ R, pipeline.py:516).  The
+weights are stacked per site once at construction so one grouped launch
+covers every expert.
+
+Semantics (bit-exact where the reference is integer/ordered):
+codes = A4(v); logits = ordered (codes*s) @ W_router; top-k stable, softmax
+over the selected; per expert e ascending over its routed tokens
+h = silu(gate) * up, d = down(A4(h)); out = sum_e w_e * d_e (e ascending).
+Builder-defined (not in the reference): token permutation into expert
+segments; shared experts added with weight 1 after the routed sum.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, ShapeError
+from .lutgemm import PackedClusteredWeights, prepare_tc_site
+
+_PATHS = {"auto": _lib.CQ_PATH_AUTO, "f32": _lib.CQ_PATH_F32, "tc": _lib.CQ_PATH_TC,
+          "ordered": _lib.CQ_PATH_ORDERED}
+
+
+@dataclass
+class ExpertStack:
+    """One site (gate, up or down) of several experts laid end to end."""
+
+    ids: torch.Tensor        # (E, d_out, d_in/2) uint8
+    centroids: torch.Tensor  # (E, d_out, d_in/g, 16) float32
+    d_in: int
+    d_out: int
+    group_size: int
+    tc: dict | None = None
+
+    @classmethod
+    def from_packed(cls, pws) -> "ExpertStack":
+        pws = list(pws)
+        if not pws:
+            raise ShapeError("no experts")
+        d_in, d_out, g = pws[0].d_in, pws[0].d_out, pws[0].group_size
+        for pw in pws:
+            if (pw.d_in, pw.d_out, pw.group_size) != (d_in, d_out, g):
+                raise ShapeError("experts of one site must share (d_in, d_out, group_size)")
+        if d_in % 2:
+            raise ShapeError("stacked expert sites need an even input dimension")
+        ids = torch.stack([pw.ids_packed for pw in pws]).contiguous()
+        cents = torch.stack([pw.centroids for pw in pws]).contiguous()
+        return cls(ids, cents, d_in, d_out, g)
+
+    @property
+    def n(self) -> int:
+        return self.ids.shape[0]
+
+    def prepare_tc(self) -> None:
+        if self.tc is None:
+            rows = self.n * self.d_out
+            self.tc = prepare_tc_site(self.ids.view(rows, -1), self.centroids.view(rows, -1, 16),
+                                      rows, self.d_in, self.group_size)
+
+    def site(self) -> _lib.ExpertSite:
+        s = _lib.ExpertSite()
+        s.ids = self.ids.data_ptr()
+        s.centroids = self.centroids.data_ptr()
+        s.group_size = self.group_size
+        if self.tc is not None:
+            s.tc_ids = self.tc["ids"].data_ptr()
+            s.tc_lut = self.tc["lut"].data_ptr()
+            s.tc_rowscale = self.tc["rowscale"].data_ptr()
+        return s
+
+
+def _as_f32_device(a) -> torch.Tensor:
+    if not isinstance(a, torch.Tensor):
+        a = torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.float32))
+    return a.to(device="cuda", dtype=torch.float32).contiguous()
+
+
+class MoELayer:
+    """A routed MoE FFN block on prepared device weights.
+
+    experts: sequence of (gate, up, down) PackedClusteredWeights, one per expert
+    (or pre-stacked ExpertStack triples via `from_stacks`).  `path`: "auto"
+    (tensor-core path when prepared, else fp32 LUT-GEMV), "f32", "tc",
+    "ordered" (bit-exact chains, the GPU-side oracle).
+    """
+
+    def __init__(self, w_router, experts, top_k: int, rotation=None, shared=(), path: str = "auto",
+                 expert_begin: int = 0, n_experts: int | None = None):
+        stacks = list(zip(*experts)) if experts else ([], [], [])
+        self.gate = ExpertStack.from_packed(stacks[0])
+        self.up = ExpertStack.from_packed(stacks[1])
+        self.down = ExpertStack.from_packed(stacks[2])
+        self._init(w_router, top_k, rotation, shared, path, expert_begin, n_experts)
+
+    @classmethod
+    def from_stacks(cls, w_router, gate: ExpertStack, up: ExpertStack, down: ExpertStack, top_k: int,
+                    rotation=None, shared=None, path: str = "auto", expert_begin: int = 0,
+                    n_experts: int | None = None) -> "MoELayer":
+        self = cls.__new__(cls)
+        self.gate, self.up, self.down = gate, up, down
+        self._init(w_router, top_k, rotation, shared or (), path, expert_begin, n_experts)
+        return self
+
+    def _init(self, w_router, top_k, rotation, shared, path, expert_begin, n_experts):
+        self.w_router = _as_f32_device(w_router)
+        self.d_model = self.gate.d_in
+        self.d_ff = self.gate.d_out
+        self.n_local = self.gate.n
+        self.n_experts = n_experts if n_experts is not None else self.n_local
+        self.expert_begin = expert_begin
+        if self.w_router.shape != (self.d_model, self.n_experts):
+            raise ShapeError(f"router weight {tuple(self.w_router.shape)} != "
+                             f"({self.d_model}, {self.n_experts})")
+        if self.up.d_in != self.d_model or self.up.d_out != self.d_ff:
+            raise ShapeError("up projection shape does not match gate")
+        if self.down.d_in != self.d_ff or self.down.d_out != self.d_model:
+            raise ShapeError("down projection shape does not match (d_ff, d_model)")
+        if not 1 <= top_k <= min(16, self.n_experts):
+            raise ConfigError(f"top_k {top_k} outside [1, min(16, n_experts)]")
+        self.top_k = int(top_k)
+        self.rotation = None if rotation is None else _as_f32_device(rotation)
+        if self.rotation is not None and self.rotation.shape != (self.d_model, self.d_model):
+            raise ShapeError("rotation must be (d_model, d_model)")
+        if isinstance(shared, tuple) and len(shared) == 3 and isinstance(shared[0], ExpertStack):
+            self.shared = shared
+        elif shared:
+            sh = list(zip(*shared))
+            self.shared = tuple(ExpertStack.from_packed(s) for s in sh)
+        else:
+            self.shared = None
+        if path not in _PATHS:
+            raise ConfigError(f"unknown path {path!r}; one of {sorted(_PATHS)}")
+        self.path = path
+        self._ws = {}
+
+    # ------------------------------------------------------------------
+    def prepare_tc(self) -> "MoELayer":
+        for s in (self.gate, self.up, self.down) + (self.shared or ()):
+            s.prepare_tc()
+        return self
+
+    def desc(self, path: str | None = None) -> _lib.MoEDesc:
+        d = _lib.MoEDesc()
+        d.d_model, d.d_ff, d.n_experts, d.top_k = self.d_model, self.d_ff, self.n_experts, self.top_k
+        d.n_local_experts, d.expert_begin = self.n_local, self.expert_begin
+        d.w_router = self.w_router.data_ptr()
+        d.rotation = self.rotation.data_ptr() if self.rotation is not None else None
+        d.gate, d.up, d.down = self.gate.site(), self.up.site(), self.down.site()
+        if self.shared is not None:
+            d.n_shared = self.shared[0].n
+            d.sh_gate, d.sh_up, d.sh_down = (s.site() for s in self.shared)
+        d.path = _PATHS[path or self.path]
+        return d
+
+    def workspace(self, n: int, path: str | None = None):
+        key = (n, path or self.path)
+        if key not in self._ws:
+            d = self.desc(path)
+            offs = (ctypes.c_int64 * len(_lib.WS_NAMES))()
+            size = _lib.load_library().cq_moe_workspace(ctypes.byref(d), n, offs)
+            buf = torch.empty(max(size, 256), dtype=torch.uint8, device="cuda")
+            self._ws[key] = (buf, list(offs))
+        return self._ws[key]
+
+    def forward(self, x, out: torch.Tensor | None = None, path: str | None = None) -> torch.Tensor:
+        """x: (N, d_model) float32/bfloat16 CUDA tensor -> moe_sum (N, d_model) float32."""
+        if not isinstance(x, torch.Tensor):
+            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        x = x.to("cuda").contiguous()
+        if x.dim() != 2 or x.shape[1] != self.d_model:
+            raise ShapeError(f"input has shape {tuple(x.shape)}, layer expects (N, {self.d_model})")
+        if self.n_local != self.n_experts or self.expert_begin != 0:
+            raise ConfigError("sharded layer: use paper_2604_10496_b200.ep.EPMoE")
+        n = x.shape[0]
+        if out is None:
+            out = torch.empty((n, self.d_model), dtype=torch.float32, device="cuda")
+        buf, _ = self.workspace(n, path)
+        d = self.desc(path)
+        _lib.check(_lib.lib().cq_moe_forward(ctypes.byref(d), x.data_ptr(), _lib.dtype_code(x), n,
+                                             out.data_ptr(), buf.data_ptr(), buf.numel(), _lib.stream()))
+        return out
+
+    __call__ = forward
+
+    def trace(self, n: int, path: str | None = None) -> dict:
+        """Views of the workspace buffers of the last forward over n tokens."""
+        buf, offs = self.workspace(n, path)
+        k, d, ff, E, R = self.top_k, self.d_model, self.d_ff, self.n_experts, n * self.top_k
+        spec = {"codes": (torch.int8, (n, d)), "scales": (torch.float32, (n,)),
+                "logits": (torch.float32, (n, E)), "selected": (torch.int32, (n, k)),
+                "weights": (torch.float32, (n, k)), "offsets": (torch.int32, (self.n_local + 1,)),
+                "perm_token": (torch.int32, (R,)), "perm_slot": (torch.int32, (R,)),
+                "inv": (torch.int32, (n, k)), "codes_perm": (torch.int8, (R, d)),
+                "scales_perm": (torch.float32, (R,)), "hidden": (torch.float32, (R, ff)),
+                "hcodes": (torch.int8, (R, ff)), "hscales": (torch.float32, (R,)),
+                "fout": (torch.float32, (R, d))}
+        res = {}
+        for name, (dt, shape) in spec.items():
+            o = offs[_lib.WS_NAMES.index(name)]
+            numel = int(np.prod(shape))
+            res[name] = buf[o:o + numel * torch.tensor([], dtype=dt).element_size()].view(dt).view(shape)
+        return res
+
+
+def moe_layer(v, w_router, experts, top_k: int, rotation=None, shared=(), path: str = "auto"):
+    """One-shot functional form: build the layer and run it on v."""
+    return MoELayer(w_router, experts, top_k, rotation=rotation, shared=shared, path=path).forward(v)

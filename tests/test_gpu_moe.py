@@ -1,0 +1,112 @@
+"""GPU parity of the MoE-layer operator against the composed reference path.
+
+Bit-exact: layer-input codes and scales, router logits, selected experts and
+their order, segment offsets and the permutation.  ulp-bounded: route weights
+(CUDA expf vs numpy float32 exp).  Tolerance (BASELINE north star): layer
+output Frobenius relative error <= 1e-2 vs the reference fp32 LUT path; the
+fp32 and ordered device paths are expected near 1e-6."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import oracle as o  # noqa: E402
+from paper_2604_10496_b200 import MoELayer  # noqa: E402
+from paper_2604_10496_b200.synthetic import (input_digest, moe_inputs_device,  # noqa: E402
+                                             moe_inputs_host, to_device_experts)
+from paper_2604_10496_b200.moe import ExpertStack  # noqa: E402
+
+LAYER_TOL = 1e-2
+
+
+def _layer(g, path):
+    seed, n, d, ff, E, k, gs = (int(v) for v in g["config"])
+    v, w, experts, _ = moe_inputs_host(seed, n, d, ff, E, gs)
+    assert input_digest(v, w, experts) == str(g["digest"])
+    return v, MoELayer(w, to_device_experts(experts), k, path=path), k, E
+
+
+def _check_routing(layer, tr, g, v, k, E):
+    assert np.array_equal(tr["codes"].cpu().numpy(), g["codes"])
+    assert np.array_equal(tr["scales"].cpu().numpy().view(np.uint32), g["scales"].view(np.uint32))
+    assert np.array_equal(tr["logits"].cpu().numpy().view(np.int32), g["logits"].view(np.int32))
+    assert np.array_equal(tr["selected"].cpu().numpy(), g["selected"])
+    ulp = np.abs(tr["weights"].cpu().numpy().view(np.int32) - g["weights"].astype(np.float32).view(np.int32))
+    assert ulp.max() <= 8
+    tok, slot, off, inv = o.route_permutation(g["selected"], E)
+    assert np.array_equal(tr["offsets"].cpu().numpy(), off)
+    R = off[-1]
+    assert np.array_equal(tr["perm_token"].cpu().numpy()[:R], tok)
+    assert np.array_equal(tr["perm_slot"].cpu().numpy()[:R], slot)
+    assert np.array_equal(tr["inv"].cpu().numpy(), inv)
+    assert np.array_equal(tr["codes_perm"].cpu().numpy()[:R], g["codes"][tok])
+
+
+@pytest.mark.parametrize("name", ["moe_small.npz", "moe_odd.npz", "moe_c1.npz"])
+@pytest.mark.parametrize("path", ["f32", "ordered"])
+def test_moe_layer_golden(golden, name, path):
+    g = golden(name)
+    v, layer, k, E = _layer(g, path)
+    x = torch.from_numpy(v).cuda()
+    out = layer(x).cpu().numpy()
+    _check_routing(layer, layer.trace(v.shape[0]), g, v, k, E)
+    err = o.relative_error(out, g["out"])
+    assert err <= (1e-5 if path != "tc" else LAYER_TOL), err
+    # bf16 input of the same (bf16-exact) values gives the identical result
+    out_b = layer(x.to(torch.bfloat16)).cpu().numpy()
+    assert np.array_equal(out_b.view(np.int32), out.view(np.int32))
+
+
+def test_moe_layer_deterministic_and_graph_capturable(golden):
+    g = golden("moe_c1.npz")
+    v, layer, k, E = _layer(g, "auto")
+    x = torch.from_numpy(v).cuda()
+    a = layer(x).clone()
+    out = torch.empty_like(a)
+    layer(x, out=out)  # warm workspace
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        layer(x, out=out)
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, a)
+
+
+def test_moe_top_k_equals_experts_and_ties():
+    # top_k = E recovers the full softmax order; equal logits break to lower ids
+    v, w, experts, _ = moe_inputs_host(5, 12, 64, 64, 4, 32)
+    w0 = np.zeros_like(w)
+    layer = MoELayer(w0, to_device_experts(experts), 4, path="f32")
+    out = layer(torch.from_numpy(v).cuda()).cpu().numpy()
+    tr = layer.trace(12)
+    assert np.array_equal(tr["selected"].cpu().numpy(), np.tile(np.arange(4), (12, 1)))
+    assert np.allclose(tr["weights"].cpu().numpy(), 0.25)
+    want = oracle.moe_layer_fast(v, w0, experts, 4)
+    assert o.relative_error(out, want) <= 1e-5
+
+
+def test_mixtral_decode_vs_oracle_subsample_and_ordered():
+    """Mixtral-8x7B layer shape (d=4096, ff=14336, E=8, top-2), decode b=64."""
+    n, d, ff, E, k, g = 64, 4096, 14336, 8, 2, 128
+    v, w, sites, _ = moe_inputs_device(11, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="f32")
+    out = layer(v).float()
+    ordered = layer(v, path="ordered").float()
+    assert o.relative_error(out.cpu().numpy(), ordered.cpu().numpy()) <= 1e-5
+    # CPU oracle on a token subsample (routing and quantization are per token)
+    sub = 6
+    host_experts = []
+    for e in range(E):
+        mats = []
+        for s in ("gate", "up", "down"):
+            ids, cents, di, do = sites[s]
+            mats.append((cents[e].cpu().numpy(), ids[e].cpu().numpy(), g))
+        host_experts.append(mats)
+    want = oracle.moe_layer_fast(v[:sub].float().cpu().numpy(), w.cpu().numpy(), host_experts, k)
+    assert o.relative_error(ordered[:sub].cpu().numpy(), want) <= 1e-5
+    assert o.relative_error(out[:sub].cpu().numpy(), want) <= 1e-5
