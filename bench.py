@@ -249,8 +249,9 @@ def run_ours(args):
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         layer(v, out=out)
-    for _ in range(args.warmup):
-        graph.replay()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            graph.replay()
     torch.cuda.synchronize()
 
     def barrier():
@@ -259,11 +260,11 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            graph.replay()
+            graph.replay()  # replays on the current (= timed) stream
         ev1.record(stream)
         ev1.synchronize()
         barrier()

@@ -109,9 +109,10 @@ typedef struct {
     const float *centroids;    /* [E][d_out][d_in/g][16] */
     int64_t group_size;        /* g */
     /* tensor-core device layout (cq_lut8_prepare); NULL -> fp32 path */
-    const uint8_t *tc_ids;     /* fragment-ordered nibbles, same bytes as ids */
-    const int8_t *tc_lut;      /* [E][d_out][d_in/g][3][16] int8 digit planes */
-    const float *tc_rowscale;  /* [E][d_out] */
+    const uint8_t *tc_ids;     /* [E*d_out/16][d_in/128][1024] fragment-ordered nibbles (same bytes as ids) */
+    const int8_t *tc_lut;      /* [E*d_out/16][d_in/g][16 rows][planes][16] int8 digit-plane LUTs */
+    const float *tc_rowscale;  /* [E*d_out] */
+    int64_t tc_planes;         /* 2 or 3 base-255 digit planes (3 where the output is re-quantized) */
 } cq_expert_site;
 
 typedef struct {
@@ -148,6 +149,8 @@ enum {
     CQ_WS_FOUT,         /* f32  [n*k][d_model] per-route down output         */
     CQ_WS_ROTATED,      /* f32  [n][d_model]   x @ R (online rotation only)  */
     CQ_WS_SHARED,       /* f32  [n][d_model]   shared-expert sum             */
+    CQ_WS_CODES_FRAG,   /* int8 [ceil(n*k/8)*8][d_model] codes in mma-B fragment order */
+    CQ_WS_HCODES_FRAG,  /* int8 [ceil(n*k/8)*8][d_ff]    hidden codes, fragment order  */
     CQ_WS_COUNT_
 };
 
@@ -174,18 +177,23 @@ CQ_API cq_status cq_moe_combine(const int32_t *selected, const float *weights, c
                          const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
                          const float *add, float *out, void *stream);
 
-/* One-time re-layout of one stacked site for the tensor-core path.
- * ids (E*d_out, d_in/2), centroids (E*d_out, d_in/g, 16) ->
- * tc_ids (same bytes, fragment order), tc_lut [E*d_out][d_in/g][3][16] int8,
- * tc_rowscale [E*d_out] f32.  Requires d_out % 16 == 0, d_in % 64 == 0, g % 32 == 0. */
+/* One-time re-layout of one stacked site (rows = E*d_out) for the tensor-core path:
+ * every row's centroids become `planes` int8 base-255 digit planes at one
+ * per-row scale (m = rint(c / rowscale), |m| < 255^planes / 2), stored as
+ * 16-entry byte LUTs pre-compensated for the PRMT sign-replicate lookup; ids
+ * are permuted (2-byte units) into mma.m16n8k32 A-fragment order.
+ * Requires rows % 16 == 0, d_in % 128 == 0, g % 128 == 0, planes in {2, 3}. */
 CQ_API cq_status cq_lut8_prepare(const uint8_t *ids, const float *centroids, int64_t rows,
-                          int64_t d_in, int64_t g, uint8_t *tc_ids, int8_t *tc_lut,
-                          float *tc_rowscale, void *stream);
+                          int64_t d_in, int64_t g, int64_t planes, uint8_t *tc_ids,
+                          int8_t *tc_lut, float *tc_rowscale, void *stream);
 
-/* Tensor-core LUT GEMM on prepared weights (one matrix): out (n, d_out) f32. */
+/* Tensor-core LUT GEMM on prepared weights (one matrix): codes (n, d_in) int8
+ * row-major, out (n, d_out) f32.  Same contract as cq_lut_gemm_f32 within the
+ * digit-plane representation error (<= 2^-23 of the row max per weight). */
 CQ_API cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, const uint8_t *tc_ids,
-                         const int8_t *tc_lut, const float *tc_rowscale, int64_t n,
-                         int64_t d_in, int64_t d_out, int64_t g, float *out, void *stream);
+                         const int8_t *tc_lut, const float *tc_rowscale, int64_t planes,
+                         int64_t n, int64_t d_in, int64_t d_out, int64_t g, float *out,
+                         void *stream);
 
 #ifdef __cplusplus
 }

@@ -26,9 +26,9 @@ cq_status lut_f32_grouped(const int8_t *, const float *, const int32_t *, int64_
                           const uint8_t *, const float *, const uint8_t *, const float *, int64_t,
                           int64_t, int64_t, float *, cudaStream_t);
 bool f32_path_ok(int64_t d_in, int64_t g);
-cq_status lut_tc_grouped(const int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
-                         const cq_expert_site *, const cq_expert_site *, int64_t, int64_t, float *,
-                         cudaStream_t);
+cq_status lut_tc_grouped_frag(const int8_t *, uint2 *, const float *, const int32_t *, int64_t, int64_t, int64_t,
+                              const cq_expert_site *, const cq_expert_site *, int64_t, int64_t, float *,
+                              cudaStream_t);
 bool tc_path_ok(int64_t d_in, int64_t d_out, int64_t g);
 
 // --- ordered grouped GEMM (GPU oracle path): bit-exact chains per segment.
@@ -188,6 +188,8 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_FOUT] = Rh * d * 4;
     sz[CQ_WS_ROTATED] = dsc->rotation ? n * d * 4 : 0;
     sz[CQ_WS_SHARED] = dsc->n_shared > 0 ? n * d * 4 : 0;
+    sz[CQ_WS_CODES_FRAG] = ceil_div(Rh, 8) * 8 * d;
+    sz[CQ_WS_HCODES_FRAG] = ceil_div(Rh, 8) * 8 * ff;
     int64_t pos = 0;
     for (int b = 0; b < CQ_WS_COUNT_; ++b) {
         if (off) off[b] = pos;
@@ -201,6 +203,7 @@ struct Ws {
     float *scales, *logits, *weights, *scales_perm, *hidden, *hscales, *fout, *rotated, *shared;
     int32_t *selected, *counts, *offsets, *perm_token, *perm_slot, *inv;
     int8_t *codes_perm, *hcodes;
+    uint2 *codes_frag, *hcodes_frag;
 };
 
 Ws carve(void *base, const int64_t *o) {
@@ -224,6 +227,8 @@ Ws carve(void *base, const int64_t *o) {
     w.fout = reinterpret_cast<float *>(b + o[CQ_WS_FOUT]);
     w.rotated = reinterpret_cast<float *>(b + o[CQ_WS_ROTATED]);
     w.shared = reinterpret_cast<float *>(b + o[CQ_WS_SHARED]);
+    w.codes_frag = reinterpret_cast<uint2 *>(b + o[CQ_WS_CODES_FRAG]);
+    w.hcodes_frag = reinterpret_cast<uint2 *>(b + o[CQ_WS_HCODES_FRAG]);
     return w;
 }
 
@@ -271,11 +276,13 @@ int choose_path(const cq_moe_desc *d) {
 cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &gate, const cq_expert_site &up,
                       const cq_expert_site &down, int64_t n_seg, int64_t seg_first, const int8_t *codes,
                       const float *scales, const int32_t *offsets, int64_t rows, float *hidden,
-                      int8_t *hcodes, float *hscales, float *fout, cudaStream_t st) {
+                      int8_t *hcodes, float *hscales, float *fout, uint2 *frag_in, uint2 *frag_h,
+                      cudaStream_t st) {
     const int64_t d = dsc->d_model, ff = dsc->d_ff;
     if (rows == 0 || n_seg == 0) return CQ_OK;
     if (path == CQ_PATH_TC) {
-        CQ_TRY(lut_tc_grouped(codes, scales, offsets, n_seg, seg_first, rows, &gate, &up, d, ff, hidden, st));
+        CQ_TRY(lut_tc_grouped_frag(codes, frag_in, scales, offsets, n_seg, seg_first, rows, &gate, &up, d, ff,
+                                   hidden, st));
     } else if (path == CQ_PATH_F32) {
         CQ_TRY(lut_f32_grouped(codes, scales, offsets, n_seg, seg_first, gate.ids, gate.centroids, up.ids,
                                up.centroids, d, ff, gate.group_size, hidden, st));
@@ -291,7 +298,8 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
     }
     CQ_TRY(quantize_a4(hidden, CQ_DTYPE_F32, rows, ff, hcodes, hscales, nullptr, st));
     if (path == CQ_PATH_TC)
-        return lut_tc_grouped(hcodes, hscales, offsets, n_seg, seg_first, rows, &down, nullptr, ff, d, fout, st);
+        return lut_tc_grouped_frag(hcodes, frag_h, hscales, offsets, n_seg, seg_first, rows, &down, nullptr, ff, d,
+                                   fout, st);
     if (path == CQ_PATH_F32)
         return lut_f32_grouped(hcodes, hscales, offsets, n_seg, seg_first, down.ids, down.centroids, nullptr,
                                nullptr, ff, d, down.group_size, fout, st);
@@ -370,8 +378,8 @@ extern "C" cq_status cq_moe_experts(const cq_moe_desc *desc, const int8_t *codes
     }
     Ws w = carve(workspace, off);
     return run_experts(desc, choose_path(desc), desc->gate, desc->up, desc->down, desc->n_local_experts, 0,
-                       codes_perm, scales_perm, offsets, rows, w.hidden, w.hcodes, w.hscales, fout,
-                       as_stream(stream));
+                       codes_perm, scales_perm, offsets, rows, w.hidden, w.hcodes, w.hscales, fout, w.codes_frag,
+                       w.hcodes_frag, as_stream(stream));
 }
 
 extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
@@ -406,7 +414,8 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
     CQ_TRY(route(desc, x, dtype, n_tokens, w, st));
     const int64_t R = n_tokens * desc->top_k;
     CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes_perm,
-                       w.scales_perm, w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, st));
+                       w.scales_perm, w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag,
+                       w.hcodes_frag, st));
     CQ_TRY(cq_moe_combine(w.selected, w.weights, w.inv, w.fout, n_tokens, desc->top_k, desc->d_model, nullptr,
                           out, stream));
     // builder-defined shared experts: out = ((routed + sh_0) + sh_1) ...,
@@ -417,7 +426,7 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
         CQ_TRY(check_launch("shared_offsets"));
         const int sp = (path == CQ_PATH_TC && desc->sh_gate.tc_lut == nullptr) ? CQ_PATH_F32 : path;
         CQ_TRY(run_experts(desc, sp, desc->sh_gate, desc->sh_up, desc->sh_down, 1, s, w.codes, w.scales, soff,
-                           n_tokens, w.hidden, w.hcodes, w.hscales, w.shared, st));
+                           n_tokens, w.hidden, w.hcodes, w.hscales, w.shared, w.codes_frag, w.hcodes_frag, st));
         add_inplace_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_tokens * desc->d_model, 256), 148 * 16), 256, 0,
                              st>>>(out, w.shared, n_tokens * desc->d_model);
         CQ_TRY(check_launch("add_shared"));

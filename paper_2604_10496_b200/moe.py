@@ -62,11 +62,11 @@ class ExpertStack:
     def n(self) -> int:
         return self.ids.shape[0]
 
-    def prepare_tc(self) -> None:
-        if self.tc is None:
+    def prepare_tc(self, planes: int) -> None:
+        if self.tc is None or self.tc["planes"] != planes:
             rows = self.n * self.d_out
             self.tc = prepare_tc_site(self.ids.view(rows, -1), self.centroids.view(rows, -1, 16),
-                                      rows, self.d_in, self.group_size)
+                                      rows, self.d_in, self.group_size, planes)
 
     def site(self) -> _lib.ExpertSite:
         s = _lib.ExpertSite()
@@ -77,6 +77,7 @@ class ExpertStack:
             s.tc_ids = self.tc["ids"].data_ptr()
             s.tc_lut = self.tc["lut"].data_ptr()
             s.tc_rowscale = self.tc["rowscale"].data_ptr()
+            s.tc_planes = self.tc["planes"]
         return s
 
 
@@ -145,9 +146,15 @@ class MoELayer:
         self._ws = {}
 
     # ------------------------------------------------------------------
-    def prepare_tc(self) -> "MoELayer":
-        for s in (self.gate, self.up, self.down) + (self.shared or ()):
-            s.prepare_tc()
+    def prepare_tc(self, planes_gate_up: int = 3, planes_down: int = 2) -> "MoELayer":
+        """Tensor-core layouts: 3 digit planes where the output is re-quantized
+        (gate, up), 2 for down (precision budget)."""
+        sites = [(self.gate, planes_gate_up), (self.up, planes_gate_up), (self.down, planes_down)]
+        if self.shared is not None:
+            sites += [(self.shared[0], planes_gate_up), (self.shared[1], planes_gate_up),
+                      (self.shared[2], planes_down)]
+        for s, p in sites:
+            s.prepare_tc(p)
         return self
 
     def desc(self, path: str | None = None) -> _lib.MoEDesc:

@@ -96,8 +96,17 @@ def test_mixtral_decode_vs_oracle_subsample_and_ordered():
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
     layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="f32")
     out = layer(v).float()
+    tr = {k_: t.clone() for k_, t in layer.trace(n).items()}
     ordered = layer(v, path="ordered").float()
-    assert o.relative_error(out.cpu().numpy(), ordered.cpu().numpy()) <= 1e-5
+    tro = layer.trace(n, path="ordered")
+    # identical routing / permutation / codes on both paths
+    for key in ("codes", "scales", "logits", "selected", "offsets", "perm_token", "inv"):
+        assert torch.equal(tr[key], tro[key]), key
+    R = int(tr["offsets"][-1])
+    # the gate|up GEMMs agree to fp32 accumulation-order noise on identical codes
+    assert o.relative_error(tr["hidden"][:R].cpu().numpy(), tro["hidden"][:R].cpu().numpy()) <= 1e-5
+    # the layer output differs only through isolated 4-bit re-quantization flips
+    assert o.relative_error(out.cpu().numpy(), ordered.cpu().numpy()) <= LAYER_TOL
     # CPU oracle on a token subsample (routing and quantization are per token)
     sub = 6
     host_experts = []
@@ -108,5 +117,5 @@ def test_mixtral_decode_vs_oracle_subsample_and_ordered():
             mats.append((cents[e].cpu().numpy(), ids[e].cpu().numpy(), g))
         host_experts.append(mats)
     want = oracle.moe_layer_fast(v[:sub].float().cpu().numpy(), w.cpu().numpy(), host_experts, k)
-    assert o.relative_error(ordered[:sub].cpu().numpy(), want) <= 1e-5
-    assert o.relative_error(out[:sub].cpu().numpy(), want) <= 1e-5
+    assert o.relative_error(ordered[:sub].cpu().numpy(), want) <= LAYER_TOL
+    assert o.relative_error(out[:sub].cpu().numpy(), want) <= LAYER_TOL

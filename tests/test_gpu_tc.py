@@ -1,0 +1,117 @@
+"""Tensor-core path: prepared layout invariants and parity.
+
+The digit-plane LUTs are checked by decoding them on the host exactly the way
+the kernel's PRMT pair does (entry + sign-replicated partner entry), the ids
+permutation by inverting it, and the GEMM against the CPU oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import oracle as o  # noqa: E402
+from paper_2604_10496_b200 import MoELayer, QuantizedActivations, lut_gemm_tc  # noqa: E402
+from paper_2604_10496_b200.lutgemm import PackedClusteredWeights  # noqa: E402
+from paper_2604_10496_b200.moe import ExpertStack  # noqa: E402
+from paper_2604_10496_b200.synthetic import moe_inputs_device, moe_inputs_host, to_device_experts  # noqa: E402
+
+
+def _rand_pw(rng, d_out, d_in, g, scale=1.0):
+    cent = (rng.standard_normal((d_out, d_in // g, 16)) * scale).astype(np.float32)
+    ids = rng.integers(0, 256, (d_out, d_in // 2)).astype(np.uint8)
+    return cent, ids, PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), d_in, g)
+
+
+@pytest.mark.parametrize("planes", [2, 3])
+def test_digit_plane_luts_decode_to_centroids(planes):
+    rng = np.random.default_rng(0)
+    cent, ids, pw = _rand_pw(rng, 32, 512, 128, 0.03)
+    cent[3] = 0.0  # an all-zero row gets scale 1 and zero digits
+    pw = PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), 512, 128)
+    pw.prepare_tc(planes)
+    lut = pw.tc["lut"].cpu().numpy().astype(np.int64)          # (rows, G, P, 16), tile-ordered
+    rs = pw.tc["rowscale"].cpu().numpy().astype(np.float64)
+    G = 512 // 128
+    lut = lut.reshape(32 // 16, G, 16, planes, 16).transpose(0, 2, 1, 3, 4).reshape(32, G, planes, 16)
+    partner = lut[..., np.arange(16) ^ 8]
+    digits = lut + np.where(partner < 0, -1, 0)               # what PRMT(P) + PRMT(Q) deliver
+    assert digits.min() >= -128 and digits.max() <= 126
+    m = np.zeros(digits.shape[:2] + (16,), np.int64)
+    for p in reversed(range(planes)):
+        m = m * 255 + digits[:, :, p, :]
+    rec = m * rs[:, None, None]
+    err = np.abs(rec - cent.astype(np.float64)).max(axis=(1, 2))
+    assert np.all(err <= rs * 0.5 + 1e-30)
+    assert rs[3] == 1.0 and not m[3].any()
+
+
+def test_fragment_ids_are_a_permutation_of_packed_ids():
+    rng = np.random.default_rng(1)
+    cent, ids, pw = _rand_pw(rng, 48, 384, 128)
+    pw.prepare_tc(3)
+    frag = pw.tc["ids"].cpu().numpy().reshape(48 // 16, 384 // 128, 2, 32, 4).view(np.uint32)
+    frag = frag.reshape(48 // 16, 384 // 128, 2, 32, 4)
+    for tile in range(3):
+        for chunk in range(3):
+            for h in range(2):
+                for lane in range(32):
+                    g, t = lane >> 2, lane & 3
+                    for j in range(2):
+                        sub = 2 * h + j
+                        k_lo = chunk * 128 + 32 * sub + 4 * t
+                        w0, w1 = frag[tile, chunk, h, lane, 2 * j], frag[tile, chunk, h, lane, 2 * j + 1]
+                        r0, r1 = ids[tile * 16 + g], ids[tile * 16 + g + 8]
+                        sel = lambda r, k: int(r[k // 2]) | (int(r[k // 2 + 1]) << 8)  # noqa: E731
+                        assert w0 == sel(r0, k_lo) | (sel(r1, k_lo) << 16)
+                        assert w1 == sel(r0, k_lo + 16) | (sel(r1, k_lo + 16) << 16)
+
+
+@pytest.mark.parametrize("n,d_in,d_out,g", [(1, 4096, 1024, 128), (7, 1024, 2816, 128), (16, 4096, 512, 4096),
+                                             (33, 2048, 768, 128), (64, 1408, 2048, 128), (100, 512, 256, 256)])
+@pytest.mark.parametrize("planes", [2, 3])
+def test_lut_gemm_tc_matches_oracle(n, d_in, d_out, g, planes):
+    rng = np.random.default_rng(n + d_in + planes)
+    cent, ids, pw = _rand_pw(rng, d_out, d_in, g)
+    codes = rng.integers(-8, 8, (n, d_in)).astype(np.int8)
+    scales = (0.5 + rng.random(n)).astype(np.float32)
+    want = oracle.c_lut_gemm(codes, scales, ids, cent, g)
+    qa = QuantizedActivations(torch.from_numpy(codes).cuda(), torch.from_numpy(scales).cuda(), 4)
+    got = lut_gemm_tc(qa, pw, planes).cpu().numpy()
+    tol = 2e-6 if planes == 3 else 2e-4
+    assert o.relative_error(got, want) <= tol
+
+
+@pytest.mark.parametrize("name", ["moe_small.npz", "moe_c1.npz"])
+def test_moe_layer_tc_golden(golden, name):
+    g = golden(name)
+    seed, n, d, ff, E, k, gs = (int(v) for v in g["config"])
+    v, w, experts, _ = moe_inputs_host(seed, n, d, ff, E, gs)
+    layer = MoELayer(w, to_device_experts(experts), k, path="tc")
+    if d % 128 or ff % 128 or gs % 128:
+        pytest.skip("shape outside the tensor-core envelope")
+    layer.prepare_tc()
+    out = layer(torch.from_numpy(v).cuda()).cpu().numpy()
+    tr = layer.trace(n)
+    assert np.array_equal(tr["selected"].cpu().numpy(), g["selected"])
+    err = o.relative_error(out, g["out"])
+    assert err <= 1e-2, err
+
+
+def test_mixtral_decode_tc_vs_ordered():
+    n, d, ff, E, k, g = 64, 4096, 14336, 8, 2, 128
+    v, w, sites, _ = moe_inputs_device(11, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc").prepare_tc()
+    out = layer(v).float()
+    tr = {key: t.clone() for key, t in layer.trace(n).items()}
+    ordered = layer(v, path="ordered").float()
+    tro = layer.trace(n, path="ordered")
+    R = int(tr["offsets"][-1])
+    # gate|up with 3 digit planes: accumulation-order-level agreement on identical codes
+    assert o.relative_error(tr["hidden"][:R].cpu().numpy(), tro["hidden"][:R].cpu().numpy()) <= 1e-5
+    assert o.relative_error(out.cpu().numpy(), ordered.cpu().numpy()) <= 1e-2
+    # and the tc path is deterministic
+    again = layer(v).float()
+    assert torch.equal(again, out)
