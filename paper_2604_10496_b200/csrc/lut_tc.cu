@@ -97,7 +97,8 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 template <int P>
 struct TcStage {
     static constexpr int LUT = 16 * P * 16;  // 16 rows x P planes x 16 entries
-    static constexpr int BYTES = TC_IDS + LUT;
+    static constexpr int B = TC_NT * 1024;    // activation fragments: NT tiles x 4 k32 x 32 lanes x 8 B
+    static constexpr int BYTES = TC_IDS + LUT + B;
 };
 
 template <int P>
@@ -110,8 +111,8 @@ __device__ __forceinline__ double combine_planes(const int (&acc)[P][TC_NT][4], 
 
 template <int P, bool GLU>
 __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
-    const uint2 *__restrict__ codes_frag, const float *__restrict__ scales, const int32_t *__restrict__ offsets,
-    int64_t seg_first, const uint8_t *__restrict__ ids_a, const int8_t *__restrict__ lut_a,
+    const uint2 *__restrict__ codes_frag, int64_t n_tiles, const float *__restrict__ scales,
+    const int32_t *__restrict__ offsets, int64_t seg_first, const uint8_t *__restrict__ ids_a, const int8_t *__restrict__ lut_a,
     const float *__restrict__ rs_a, const uint8_t *__restrict__ ids_b, const int8_t *__restrict__ lut_b,
     const float *__restrict__ rs_b, int d_in, int d_out, int g, float *__restrict__ out) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
     if (rb >= re || rowtile * 16 >= d_out) return;  // uniform per warp pair
 
     const int64_t e = seg + seg_first;
-    const int n_chunks = d_in / TC_CHUNK, cpg = g / TC_CHUNK, kc32 = d_in / 32;
+    const int n_chunks = d_in / TC_CHUNK, cpg = g / TC_CHUNK;
     const int64_t tile_g = e * (d_out / 16) + rowtile;
     const uint8_t *ids = (mat ? ids_b : ids_a) + tile_g * (int64_t)n_chunks * TC_IDS;
     const int8_t *lut = (mat ? lut_b : lut_a) + tile_g * (int64_t)(d_in / g) * TcStage<P>::LUT;
@@ -143,13 +144,16 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
     }
     __syncwarp();
 
-    auto issue = [&](int chunk, int stage) {
+    // one stage = 128 columns: fragment-ordered ids, the group's LUT block when
+    // the chunk opens a group, and the ntc activation tiles of this chunk
+    auto issue = [&](int chunk, int stage, int64_t j0, int ntc) {
         const uint32_t dst = smem_addr(ring + stage * SB);
         const uint32_t bar = smem_addr(bars + stage);
         const bool new_group = (chunk % cpg) == 0;
-        mbar_expect_tx(bar, TC_IDS + (new_group ? TcStage<P>::LUT : 0));
+        mbar_expect_tx(bar, TC_IDS + (new_group ? TcStage<P>::LUT : 0) + ntc * 1024);
         bulk_g2s(dst, ids + (int64_t)chunk * TC_IDS, TC_IDS, bar);
         if (new_group) bulk_g2s(dst + TC_IDS, lut + (int64_t)(chunk / cpg) * TcStage<P>::LUT, TcStage<P>::LUT, bar);
+        bulk_g2s(dst + TC_IDS + TcStage<P>::LUT, codes_frag + ((int64_t)chunk * n_tiles + j0) * 128, ntc * 1024, bar);
     };
 
     const int64_t j_first = rb >> 3, j_last = (re - 1) >> 3;
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
                 for (int r = 0; r < 4; ++r) acc[p][nt][r] = 0;
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            for (int c = 0; c < TC_STAGES && c < n_chunks; ++c) issue(c, (cnt + c) % TC_STAGES);
+            for (int c = 0; c < TC_STAGES && c < n_chunks; ++c) issue(c, (cnt + c) % TC_STAGES, j0, ntc);
         }
         uint4 L0[P], L1[P];  // LUT planes of rows g8 and g8 + 8
         for (int c = 0; c < n_chunks; ++c, ++cnt) {
@@ -185,11 +189,11 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
             const uint32_t wv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
-                const int kc = c * 4 + sub;
+                const uint2 *bs = reinterpret_cast<const uint2 *>(st + TC_IDS + TcStage<P>::LUT);
                 uint2 b[TC_NT];
 #pragma unroll
                 for (int nt = 0; nt < TC_NT; ++nt)
-                    if (nt < ntc) b[nt] = __ldg(codes_frag + ((j0 + nt) * kc32 + kc) * 32 + lane);
+                    if (nt < ntc) b[nt] = bs[(nt * 4 + sub) * 32 + lane];
                 const uint32_t w0 = wv[2 * sub], w1 = wv[2 * sub + 1];
                 const uint32_t x0 = w0 ^ 0x88888888u, x1 = w1 ^ 0x88888888u;
                 // selectors (low 16 bits used): a0 row g k-lo, a1 row g+8 k-lo, a2 row g k-hi, a3 row g+8 k-hi
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
             __syncwarp();
             if (lane == 0 && c + TC_STAGES < n_chunks) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(c + TC_STAGES, stage);
+                issue(c + TC_STAGES, stage, j0, ntc);
             }
         }
         // ---- epilogue: rows (g8, g8+8) x tokens (2 t4, 2 t4 + 1) per token tile
@@ -263,16 +267,17 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
     }
 }
 
-// codes (rows, K) row-major -> mma B-fragment order: for token tile j (8 rows)
-// and 32-column chunk kc, lane (g, t) holds row 8j+g, columns 32kc+4t..+3 and
-// 32kc+16+4t..+3.  Rows >= n are zero.
+// codes (rows, K) row-major -> mma B-fragment order [chunk128][tile8][sub][lane]
+// (8 B each): lane (g, t) of token tile j holds row 8j+g, columns
+// 128c+32sub+4t..+3 and +16.  A stage's ntc consecutive tiles are one
+// contiguous bulk copy.  Rows >= n are zero.
 __global__ void to_frag_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
                                uint2 *__restrict__ dst) {
-    const int64_t kc32 = K / 32;
-    const int64_t total = tiles * kc32 * 32;
+    const int64_t total = (K / 128) * tiles * 128;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-        const int lane = (int)(x & 31);
-        const int64_t kc = (x >> 5) % kc32, j = (x >> 5) / kc32;
+        const int lane = (int)(x & 31), sub = (int)((x >> 5) & 3);
+        const int64_t j = (x >> 7) % tiles, chunk = (x >> 7) / tiles;
+        const int64_t kc = chunk * 4 + sub;
         const int64_t row = j * 8 + (lane >> 2);
         uint2 v = make_uint2(0u, 0u);
         if (row < n) {
@@ -376,7 +381,7 @@ size_t tc_smem() {
 }
 
 template <int P, bool GLU>
-cq_status launch_tc(const uint2 *frag, const float *scales, const int32_t *offsets, int64_t n_seg, int64_t seg_first,
+cq_status launch_tc(const uint2 *frag, int64_t n_tiles, const float *scales, const int32_t *offsets, int64_t n_seg, int64_t seg_first,
                     const cq_expert_site *a, const cq_expert_site *b, int64_t d_in, int64_t d_out, float *out,
                     cudaStream_t st) {
     static bool attr = false;
@@ -388,14 +393,14 @@ cq_status launch_tc(const uint2 *frag, const float *scales, const int32_t *offse
     const int tiles_per_cta = GLU ? TC_WARPS / 2 : TC_WARPS;
     dim3 grid((unsigned)ceil_div(d_out / 16, tiles_per_cta), (unsigned)n_seg);
     lut_tc_kernel<P, GLU><<<grid, TC_WARPS * 32, smem, st>>>(
-        frag, scales, offsets, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, b ? b->tc_ids : nullptr,
+        frag, n_tiles, scales, offsets, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, b ? b->tc_ids : nullptr,
         b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, (int)d_in, (int)d_out, (int)a->group_size, out);
     return check_launch("lut_tc");
 }
 
 cq_status to_frag(const int8_t *codes, int64_t n, int64_t K, uint2 *frag, cudaStream_t st) {
     const int64_t tiles = ceil_div(n, 8);
-    const int64_t total = tiles * (K / 32) * 32;
+    const int64_t total = tiles * (K / 128) * 128;
     if (total == 0) return CQ_OK;
     to_frag_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(codes, n, K, tiles,
                                                                                               frag);
@@ -417,13 +422,14 @@ cq_status lut_tc_grouped_frag(const int8_t *codes, uint2 *frag, const float *sca
         return CQ_ERR_CONFIG;
     }
     CQ_TRY(to_frag(codes, rows, d_in, frag, st));
+    const int64_t nt = ceil_div(rows, 8);
     const bool glu = b != nullptr;
     if (a->tc_planes == 3)
-        return glu ? launch_tc<3, true>(frag, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st)
-                   : launch_tc<3, false>(frag, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st);
+        return glu ? launch_tc<3, true>(frag, nt, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st)
+                   : launch_tc<3, false>(frag, nt, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st);
     if (a->tc_planes == 2)
-        return glu ? launch_tc<2, true>(frag, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st)
-                   : launch_tc<2, false>(frag, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st);
+        return glu ? launch_tc<2, true>(frag, nt, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st)
+                   : launch_tc<2, false>(frag, nt, scales, offsets, n_seg, seg_first, a, b, d_in, d_out, out, st);
     set_error("tensor-core path: planes must be 2 or 3");
     return CQ_ERR_CONFIG;
 }

@@ -88,36 +88,27 @@ __global__ void silu_mul_kernel(float *__restrict__ a, const float *__restrict__
 }
 
 // out[t, :] = ((0 + w_e1 f_e1) + w_e2 f_e2) + ...  with e ascending (model.py:401),
-// then + add[t, :] (shared experts) when given.
+// then + add[t, :] (shared experts) when given.  grid (n, column blocks).
 __global__ void combine_kernel(const int32_t *__restrict__ selected, const float *__restrict__ weights,
                                const int32_t *__restrict__ inv, const float *__restrict__ fout, int64_t k,
                                int64_t d, const float *__restrict__ add, float *__restrict__ out) {
-    __shared__ int32_t s_pos[16];
-    __shared__ float s_w[16];
     const int64_t t = blockIdx.x;
-    if (threadIdx.x == 0) {
-        int32_t ex[16], pos[16];
-        float w[16];
-        for (int s = 0; s < k; ++s) {
-            ex[s] = selected[t * k + s];
-            pos[s] = inv[t * k + s];
-            w[s] = weights[t * k + s];
-        }
-        for (int a = 1; a < k; ++a)  // insertion sort by expert id (ids are distinct)
-            for (int b = a; b > 0 && ex[b - 1] > ex[b]; --b) {
-                int32_t te = ex[b]; ex[b] = ex[b - 1]; ex[b - 1] = te;
-                int32_t tp = pos[b]; pos[b] = pos[b - 1]; pos[b - 1] = tp;
-                float tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
-            }
-        for (int s = 0; s < k; ++s) {
-            s_pos[s] = pos[s];
-            s_w[s] = w[s];
-        }
+    int32_t ex[16], pos[16];
+    float w[16];
+    for (int s = 0; s < k; ++s) {
+        ex[s] = __ldg(selected + t * k + s);
+        pos[s] = __ldg(inv + t * k + s);
+        w[s] = __ldg(weights + t * k + s);
     }
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+    for (int a = 1; a < k; ++a)  // insertion sort by expert id (ids are distinct)
+        for (int b = a; b > 0 && ex[b - 1] > ex[b]; --b) {
+            int32_t te = ex[b]; ex[b] = ex[b - 1]; ex[b - 1] = te;
+            int32_t tp = pos[b]; pos[b] = pos[b - 1]; pos[b - 1] = tp;
+            float tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
+        }
+    for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < d; j += (int64_t)gridDim.y * blockDim.x) {
         float acc = 0.0f;
-        for (int s = 0; s < k; ++s) acc = __fadd_rn(acc, __fmul_rn(s_w[s], fout[(int64_t)s_pos[s] * d + j]));
+        for (int s = 0; s < k; ++s) acc = __fadd_rn(acc, __fmul_rn(w[s], __ldg(fout + (int64_t)pos[s] * d + j)));
         if (add != nullptr) acc = __fadd_rn(acc, add[t * d + j]);
         out[t * d + j] = acc;
     }
@@ -390,8 +381,8 @@ extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weight
         set_error("combine: top_k out of range");
         return CQ_ERR_CONFIG;
     }
-    combine_kernel<<<(unsigned)n_tokens, 256, 0, as_stream(stream)>>>(selected, weights, inv, fout, top_k, d_model,
-                                                                       add, out);
+    dim3 grid((unsigned)n_tokens, (unsigned)std::max<int64_t>(1, std::min<int64_t>(16, ceil_div(d_model, 256))));
+    combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(selected, weights, inv, fout, top_k, d_model, add, out);
     return check_launch("combine");
 }
 

@@ -9,29 +9,39 @@
 
 namespace cq {
 
-// logits[t, e] = sum_k (q[t,k] * s_t) * W[k, e], ordered.  One thread per
-// (token, expert), expert fastest so W loads coalesce across lanes.
+// logits[t, e] = sum_k (q[t,k] * s_t) * W[k, e], k ascending, one rounding per
+// multiply and per add (the chain of _core.matmul_f32).  A CTA owns TT tokens x
+// E experts (one thread per chain); W and the exact fake-quant inputs q*s are
+// staged in shared memory RK columns at a time so the chains read smem, not L2.
 __global__ void router_logits_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
-                                     const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp,
+                                     const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp, int rk,
                                      float *__restrict__ logits) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= n * n_exp) return;
-    const int64_t t = idx / n_exp, e = idx - t * n_exp;
-    const int8_t *q = codes + t * d;
-    const float s = __ldg(scales + t);
+    extern __shared__ float rsm[];
+    const int tt_n = blockDim.x / (int)n_exp;
+    float *ws = rsm;                 // [rk][E]
+    float *as = rsm + rk * n_exp;    // [tt_n][rk]
+    const int t_loc = threadIdx.x / (int)n_exp, e = threadIdx.x % (int)n_exp;
+    const int64_t t0 = blockIdx.x * (int64_t)tt_n;
+    const int64_t t = t0 + t_loc;
+    const bool live = t_loc < tt_n && t < n;
     float acc = 0.0f;
-    int64_t k = 0;
-    for (; k + 4 <= d; k += 4) {  // loads batched, chain order unchanged
-        const char4 c4 = *reinterpret_cast<const char4 *>(q + k);
-        const float w0 = __ldg(w + (k + 0) * n_exp + e), w1 = __ldg(w + (k + 1) * n_exp + e);
-        const float w2 = __ldg(w + (k + 2) * n_exp + e), w3 = __ldg(w + (k + 3) * n_exp + e);
-        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.x, s), w0));
-        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.y, s), w1));
-        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.z, s), w2));
-        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)c4.w, s), w3));
+    for (int64_t k0 = 0; k0 < d; k0 += rk) {
+        const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
+        __syncthreads();
+        for (int x = threadIdx.x; x < kn * n_exp; x += blockDim.x) ws[x] = __ldg(w + k0 * n_exp + x);
+        for (int x = threadIdx.x; x < tt_n * kn; x += blockDim.x) {
+            const int tl = x / kn, kk = x - tl * kn;
+            const int64_t tg = t0 + tl;
+            as[tl * rk + kk] = tg < n ? __fmul_rn((float)codes[tg * d + k0 + kk], __ldg(scales + tg)) : 0.0f;
+        }
+        __syncthreads();
+        if (live) {
+            const float *ar = as + t_loc * rk;
+#pragma unroll 8
+            for (int kk = 0; kk < kn; ++kk) acc = __fadd_rn(acc, __fmul_rn(ar[kk], ws[kk * n_exp + e]));
+        }
     }
-    for (; k < d; ++k) acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)q[k], s), __ldg(w + k * n_exp + e)));
-    logits[idx] = acc;
+    if (live) logits[t * n_exp + e] = acc;
 }
 
 // numpy's float32 sum of a short row: a plain loop below 8 elements, eight
@@ -171,7 +181,16 @@ __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *
 cq_status router_logits(const int8_t *codes, const float *scales, const float *w, int64_t n,
                         int64_t d, int64_t n_exp, float *logits, cudaStream_t st) {
     if (n * n_exp == 0) return CQ_OK;
-    router_logits_kernel<<<(unsigned)ceil_div(n * n_exp, 64), 64, 0, st>>>(codes, scales, w, n, d, n_exp, logits);
+    if (n_exp > 256) {
+        set_error("router: at most 256 experts");
+        return CQ_ERR_CONFIG;
+    }
+    const int tt = (int)(256 / n_exp);
+    // W chunk [rk][E] + inputs [tt][rk] in <= 48 KB of shared memory
+    const int rk = (int)std::max<int64_t>(16, std::min<int64_t>(256, (12288 / (n_exp + tt)) & ~15LL));
+    const size_t smem = ((size_t)rk * n_exp + (size_t)tt * rk) * sizeof(float);
+    router_logits_kernel<<<(unsigned)ceil_div(n, tt), (unsigned)(tt * n_exp), smem, st>>>(codes, scales, w, n, d,
+                                                                                         n_exp, rk, logits);
     return check_launch("router_logits");
 }
 

@@ -51,8 +51,7 @@ def test_fragment_ids_are_a_permutation_of_packed_ids():
     rng = np.random.default_rng(1)
     cent, ids, pw = _rand_pw(rng, 48, 384, 128)
     pw.prepare_tc(3)
-    frag = pw.tc["ids"].cpu().numpy().reshape(48 // 16, 384 // 128, 2, 32, 4).view(np.uint32)
-    frag = frag.reshape(48 // 16, 384 // 128, 2, 32, 4)
+    frag = pw.tc["ids"].cpu().numpy().reshape(-1).view(np.uint32).reshape(48 // 16, 384 // 128, 2, 32, 4)
     for tile in range(3):
         for chunk in range(3):
             for h in range(2):
