@@ -113,7 +113,10 @@ typedef struct {
     const int8_t *tc_lut;      /* [E*d_out/16][d_in/g][16 rows][planes][16] int8 digit-plane LUTs */
     const float *tc_rowscale;  /* [E*d_out] */
     int64_t tc_planes;         /* 2 or 3 base-255 digit planes (3 where the output is re-quantized) */
+    int64_t tc_layout;         /* CQ_TC_MMA16 (mma.sync kernel) or CQ_TC_UMMA128 (tcgen05 kernel) */
 } cq_expert_site;
+
+enum { CQ_TC_MMA16 = 0, CQ_TC_UMMA128 = 1 };
 
 typedef struct {
     int64_t d_model, d_ff, n_experts, top_k;
@@ -182,18 +185,19 @@ CQ_API cq_status cq_moe_combine(const int32_t *selected, const float *weights, c
  * per-row scale (m = rint(c / rowscale), |m| < 255^planes / 2), stored as
  * 16-entry byte LUTs pre-compensated for the PRMT sign-replicate lookup; ids
  * are permuted (2-byte units) into mma.m16n8k32 A-fragment order.
- * Requires rows % 16 == 0, d_in % 128 == 0, g % 128 == 0, planes in {2, 3}. */
+ * Requires rows % 16 == 0 (layout CQ_TC_MMA16) or rows % 128 == 0 (CQ_TC_UMMA128),
+ * d_in % 128 == 0, g % 128 == 0, planes in {2, 3}. */
 CQ_API cq_status cq_lut8_prepare(const uint8_t *ids, const float *centroids, int64_t rows,
-                          int64_t d_in, int64_t g, int64_t planes, uint8_t *tc_ids,
-                          int8_t *tc_lut, float *tc_rowscale, void *stream);
+                          int64_t d_in, int64_t g, int64_t planes, int64_t layout,
+                          uint8_t *tc_ids, int8_t *tc_lut, float *tc_rowscale, void *stream);
 
 /* Tensor-core LUT GEMM on prepared weights (one matrix): codes (n, d_in) int8
  * row-major, out (n, d_out) f32.  Same contract as cq_lut_gemm_f32 within the
  * digit-plane representation error (<= 2^-23 of the row max per weight). */
 CQ_API cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, const uint8_t *tc_ids,
                          const int8_t *tc_lut, const float *tc_rowscale, int64_t planes,
-                         int64_t n, int64_t d_in, int64_t d_out, int64_t g, float *out,
-                         void *stream);
+                         int64_t layout, int64_t n, int64_t d_in, int64_t d_out, int64_t g,
+                         float *out, void *stream);
 
 #ifdef __cplusplus
 }

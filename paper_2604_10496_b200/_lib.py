@@ -20,6 +20,8 @@ LIB_PATH = os.path.join(_HERE, "libcq_b200.so")
 CQ_OK, CQ_ERR_SHAPE, CQ_ERR_CONFIG, CQ_ERR_DIVERGENCE, CQ_ERR_CUDA, CQ_ERR_UNSUPPORTED = range(6)
 CQ_DTYPE_F32, CQ_DTYPE_BF16 = 0, 1
 CQ_PATH_AUTO, CQ_PATH_F32, CQ_PATH_TC, CQ_PATH_ORDERED = 0, 1, 2, 3
+CQ_TC_MMA16, CQ_TC_UMMA128 = 0, 1
+TC_LAYOUTS = {"mma16": CQ_TC_MMA16, "umma128": CQ_TC_UMMA128}
 WS_NAMES = ("codes", "scales", "logits", "selected", "weights", "counts", "offsets",
             "perm_token", "perm_slot", "inv", "codes_perm", "scales_perm", "hidden",
             "hcodes", "hscales", "fout", "rotated", "shared", "codes_frag", "hcodes_frag")
@@ -29,7 +31,8 @@ _vp, _i64, _i32, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.
 
 class ExpertSite(ctypes.Structure):
     _fields_ = [("ids", _vp), ("centroids", _vp), ("group_size", _i64),
-                ("tc_ids", _vp), ("tc_lut", _vp), ("tc_rowscale", _vp), ("tc_planes", _i64)]
+                ("tc_ids", _vp), ("tc_lut", _vp), ("tc_rowscale", _vp), ("tc_planes", _i64),
+                ("tc_layout", _i64)]
 
 
 class MoEDesc(ctypes.Structure):
@@ -53,8 +56,8 @@ _SIGS = {
     "cq_moe_route": [ctypes.POINTER(MoEDesc), _vp, _int, _i64, _vp, _i64, _vp],
     "cq_moe_experts": [ctypes.POINTER(MoEDesc), _vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp],
     "cq_moe_combine": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
-    "cq_lut8_prepare": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
-    "cq_lut_gemm_tc": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
+    "cq_lut8_prepare": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
+    "cq_lut_gemm_tc": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
 }
 
 EXPORTS = tuple(_SIGS) + ("cq_last_error", "cq_abi_version", "cq_launch_count", "cq_moe_workspace")

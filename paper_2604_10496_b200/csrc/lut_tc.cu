@@ -434,24 +434,45 @@ cq_status lut_tc_grouped_frag(const int8_t *codes, uint2 *frag, const float *sca
     return CQ_ERR_CONFIG;
 }
 
+cq_status umma_prepare(const uint8_t *, const int8_t *, int64_t, int64_t, int64_t, int64_t, uint8_t *, int8_t *,
+                       cudaStream_t);
+cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
+                           const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
+                           cudaStream_t);
+bool umma_ok(int64_t d_in, int64_t d_out, int64_t g);
+int64_t umma_b_tiles(int64_t rows);
+
 cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int64_t d_in, int64_t g, int64_t planes,
-                       uint8_t *tc_ids, int8_t *tc_lut, float *rowscale, cudaStream_t st) {
+                       int64_t layout, uint8_t *tc_ids, int8_t *tc_lut, float *rowscale, cudaStream_t st) {
     if (planes != 2 && planes != 3) {
         set_error("lut8_prepare: planes must be 2 or 3");
         return CQ_ERR_CONFIG;
     }
-    if (rows % 16 || !tc_path_ok(d_in, 16, g)) {
-        set_error("lut8_prepare: needs rows % 16 == 0, d_in % 128 == 0, g % 128 == 0");
+    if (rows % (layout == CQ_TC_UMMA128 ? 128 : 16) || !tc_path_ok(d_in, 16, g)) {
+        set_error("lut8_prepare: needs rows % 16 (mma16) / % 128 (umma128) == 0, d_in % 128 == 0, g % 128 == 0");
         return CQ_ERR_UNSUPPORTED;
     }
     if (rows == 0) return CQ_OK;
     const int64_t n_groups = d_in / g;
     const int64_t mb = planes == 3 ? TC_M3 : TC_M2;
-    rowscale_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(cent, rows, n_groups * 16, (double)mb, rowscale);
+    rowscale_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(cent, rows, n_groups * 16,
+                                                                 (double)mb, rowscale);
     CQ_TRY(check_launch("rowscale"));
+    int8_t *lut16 = tc_lut;
+    if (layout == CQ_TC_UMMA128) {
+        if (cudaMallocAsync(&lut16, rows * n_groups * planes * 16, st) != cudaSuccess) {
+            set_error("lut8_prepare: scratch alloc failed");
+            return CQ_ERR_CUDA;
+        }
+    }
     lut8_kernel<<<(unsigned)ceil_div(rows * n_groups, 128), 128, 0, st>>>(cent, rowscale, rows, n_groups, (int)planes,
-                                                                        mb, tc_lut);
+                                                                        mb, lut16);
     CQ_TRY(check_launch("lut8"));
+    if (layout == CQ_TC_UMMA128) {
+        cq_status rc = umma_prepare(ids, lut16, rows, d_in, g, planes, tc_ids, tc_lut, st);
+        cudaFreeAsync(lut16, st);
+        return rc;
+    }
     const int64_t total = (rows / 16) * (d_in / TC_CHUNK) * 64;
     ids_frag_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 32), 256, 0, st>>>(ids, rows, d_in,
                                                                                                 tc_ids);
@@ -463,9 +484,10 @@ cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int6
 using namespace cq;
 
 extern "C" cq_status cq_lut8_prepare(const uint8_t *ids, const float *centroids, int64_t rows, int64_t d_in,
-                                     int64_t g, int64_t planes, uint8_t *tc_ids, int8_t *tc_lut, float *tc_rowscale,
-                                     void *stream) {
-    return lut8_prepare(ids, centroids, rows, d_in, g, planes, tc_ids, tc_lut, tc_rowscale, as_stream(stream));
+                                     int64_t g, int64_t planes, int64_t layout, uint8_t *tc_ids, int8_t *tc_lut,
+                                     float *tc_rowscale, void *stream) {
+    return lut8_prepare(ids, centroids, rows, d_in, g, planes, layout, tc_ids, tc_lut, tc_rowscale,
+                        as_stream(stream));
 }
 
 __global__ void tc_single_segment_kernel(int32_t *off, int64_t n) {
@@ -474,8 +496,8 @@ __global__ void tc_single_segment_kernel(int32_t *off, int64_t n) {
 }
 
 extern "C" cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, const uint8_t *tc_ids,
-                                    const int8_t *tc_lut, const float *tc_rowscale, int64_t planes, int64_t n,
-                                    int64_t d_in, int64_t d_out, int64_t g, float *out, void *stream) {
+                                    const int8_t *tc_lut, const float *tc_rowscale, int64_t planes, int64_t layout,
+                                    int64_t n, int64_t d_in, int64_t d_out, int64_t g, float *out, void *stream) {
     if (n < 0 || g < 1 || d_in % g) {
         set_error("group size does not divide the input dimension");
         return CQ_ERR_SHAPE;
@@ -488,8 +510,9 @@ extern "C" cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, co
     site.tc_lut = tc_lut;
     site.tc_rowscale = tc_rowscale;
     site.tc_planes = planes;
+    site.tc_layout = layout;
     void *scratch = nullptr;
-    const int64_t frag_bytes = ceil_div(n, 8) * 8 * d_in;
+    const int64_t frag_bytes = (layout == CQ_TC_UMMA128 ? umma_b_tiles(n) : ceil_div(n, 8)) * 8 * d_in;
     if (cudaMallocAsync(&scratch, frag_bytes + 256, st) != cudaSuccess) {
         set_error("lut_gemm_tc: scratch alloc failed");
         return CQ_ERR_CUDA;
@@ -497,7 +520,10 @@ extern "C" cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, co
     int32_t *off = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(scratch) + frag_bytes);
     tc_single_segment_kernel<<<1, 1, 0, st>>>(off, n);
     cq_status rc = check_launch("single_segment");
-    if (rc == CQ_OK)
+    if (rc == CQ_OK && layout == CQ_TC_UMMA128)
+        rc = lut_umma_grouped(codes, reinterpret_cast<int8_t *>(scratch), scales, off, 1, 0, n, &site, out, nullptr,
+                              nullptr, d_in, d_out, st);
+    else if (rc == CQ_OK)
         rc = lut_tc_grouped_frag(codes, reinterpret_cast<uint2 *>(scratch), scales, off, 1, 0, n, &site, nullptr, d_in,
                                  d_out, out, st);
     cudaFreeAsync(scratch, st);

@@ -1,0 +1,458 @@
+// tcgen05 LUT GEMM: codebook rows expanded by PRMT into int8 digit planes and
+// written straight into TMEM as the MMA's A operand (kind::i8, A from TMEM),
+// activation codes staged in shared memory by bulk copies as the B operand,
+// exact int32 accumulators in TMEM.  Same numerics as lut_tc.cu (digit planes,
+// sign-garbage-compensated 16-entry byte LUTs — see that file's header); this
+// kernel removes the legacy mma.sync issue cost, which capped the register-
+// operand version at ~30% of HBM bandwidth (profiles/README.md).
+//
+// CTA = one 128-row weight tile of one expert matrix x one token pass
+// (<= 64 tokens), warp-specialised:
+//   warps 0-7  expanders: warp w owns TMEM lane quarter w%4 (= rows), the two
+//              warpgroups take alternating 32-column k-steps.  Per k-step a
+//              thread turns 32 ids of its row into P planes x {lo,hi} halves x
+//              8 columns with 2P PRMT per 4 ids and tcgen05.st's them.
+//   warp 8     producer: cp.async.bulk of ids (8 KB/128 columns), the group's
+//              LUT block and the activation tile into a 4-deep smem ring.
+//   warp 9     MMA issuer: one elected thread, 2P tcgen05.mma per k-step
+//              (M=128, N=16..64, K=32), commits free the A stage / smem stage.
+// Epilogue: expanders tcgen05.ld the P accumulators, combine digits
+// (sum 255^p S_p), scale by the row scale and the token scale, store fp32.
+#include "common.cuh"
+
+namespace cq {
+
+namespace um {
+constexpr int STAGES = 4;        // smem ring depth (128-column chunks)
+constexpr int ASTAGES = 6;       // TMEM A stages (one 32-column k-step each)
+constexpr int NTOK = 64;         // max tokens per pass (MMA N)
+constexpr int IDS = 128 * 64;    // ids bytes per chunk: 128 rows x 128 columns / 2
+constexpr int BTILE = 1024;      // activation bytes per 8-token tile per chunk
+constexpr int EXP_WARPS = 8, PROD_WARP = 8, MMA_WARP = 9, WARPS = 10;
+constexpr int THREADS = WARPS * 32;
+constexpr uint32_t TMEM_COLS = 512;
+}  // namespace um
+
+template <int P>
+struct UmStage {
+    static constexpr int LUT = 128 * P * 16;
+    static constexpr int B = (um::NTOK / 8) * um::BTILE;
+    static constexpr int BYTES = um::IDS + LUT + B;
+    static constexpr int ACOLS = 2 * P * 8;   // TMEM columns per A stage
+};
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (tcgen05 / mbarrier / bulk copy)
+
+__device__ __forceinline__ uint32_t u_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t u_prmt(uint32_t a, uint32_t b, uint32_t s) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+    return d;
+}
+
+__device__ __forceinline__ void u_bar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void u_bar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void u_bar_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void u_bar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "UW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra UW_%=;\n}" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void u_bulk(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+// D[tmem d] (+)= A[tmem a] x B[smem desc], kind::i8, 128 x N x 32.
+__device__ __forceinline__ void tc_mma_i8(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(d),
+        "r"(a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0u)
+        : "memory");
+}
+
+// 16 consecutive 32-bit TMEM columns of this thread's lane.
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// K-major, no-swizzle smem descriptor: core matrices of 8 rows x 16 bytes,
+// LBO = byte distance between the two 16-byte K halves, SBO = between 8-row groups.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+    return d;                // base offset 0, layout SWIZZLE_NONE
+}
+
+// kind::i8 instruction descriptor: s32 accumulate, A and B signed, both K-major.
+__device__ __forceinline__ uint32_t idesc_i8(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+template <int P>
+__device__ __forceinline__ double um_combine(const uint32_t (&acc)[P][16], int c) {
+    double s = (double)(int32_t)acc[P - 1][c];
+#pragma unroll
+    for (int p = P - 2; p >= 0; --p) s = s * 255.0 + (double)(int32_t)acc[p][c];
+    return s;
+}
+
+// grid: (d_out / 128, n_seg, n_mat); blockIdx.z picks the matrix (gate / up).
+template <int P>
+__global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
+    const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
+    const int32_t *__restrict__ offsets, int64_t seg_first, const uint8_t *__restrict__ ids0,
+    const int8_t *__restrict__ lut0, const float *__restrict__ rs0, float *__restrict__ out0,
+    const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1, const float *__restrict__ rs1,
+    float *__restrict__ out1, int d_in, int d_out, int g) {
+    using S = UmStage<P>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t full_bar[um::STAGES], empty_bar[um::STAGES];
+    __shared__ __align__(8) uint64_t afull_bar[um::ASTAGES], aempty_bar[um::ASTAGES];
+    __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t seg = blockIdx.y;
+    const int64_t rb = offsets[seg], re = offsets[seg + 1];
+    if (rb >= re) return;  // CTA-uniform
+    const int mat = blockIdx.z;
+    const uint8_t *ids = mat ? ids1 : ids0;
+    const int8_t *lut = mat ? lut1 : lut0;
+    const float *rsp = mat ? rs1 : rs0;
+    float *out = mat ? out1 : out0;
+    const int64_t e = seg + seg_first;
+    const int64_t tile = e * (d_out / 128) + blockIdx.x;
+    const int n_chunks = d_in / 128, cpg = g / 128, n_groups = d_in / g;
+    const int ksteps = n_chunks * 4;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < um::STAGES; ++s) {
+            u_bar_init(u_smem(&full_bar[s]), 1);
+            u_bar_init(u_smem(&empty_bar[s]), 1);
+        }
+        for (int s = 0; s < um::ASTAGES; ++s) {
+            u_bar_init(u_smem(&afull_bar[s]), 4);
+            u_bar_init(u_smem(&aempty_bar[s]), 1);
+        }
+        u_bar_init(u_smem(&accfull_bar), 1);
+        u_bar_init(u_smem(&accempty_bar), 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(u_smem(&tmem_base_sh)),
+                     "r"(um::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    // TMEM columns: [0, P*NTOK) accumulators (plane p at p*NTOK), then A stages
+    const uint32_t acol0 = P * um::NTOK;
+
+    const int64_t j_first = rb >> 3, j_last = (re - 1) >> 3;
+    const int n_pass = (int)((j_last - j_first + 1 + (um::NTOK / 8) - 1) / (um::NTOK / 8));
+
+    if (warp == um::PROD_WARP) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int pass = 0; pass < n_pass; ++pass) {
+                const int64_t j0 = j_first + (int64_t)pass * (um::NTOK / 8);
+                const int ntc = (int)((j_last - j0 + 1) < (um::NTOK / 8) ? (j_last - j0 + 1) : (um::NTOK / 8));
+                const int ntc16 = (ntc + 1) & ~1;  // MMA N is a multiple of 16
+                for (int c = 0; c < n_chunks; ++c, ++it) {
+                    const int s = it % um::STAGES;
+                    if (it >= um::STAGES) u_bar_wait(u_smem(&empty_bar[s]), ((it / um::STAGES) - 1) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const bool new_group = (c % cpg) == 0 || c == 0;
+                    const uint32_t bar = u_smem(&full_bar[s]);
+                    const uint32_t dst = u_smem(smem + (size_t)s * S::BYTES);
+                    u_bar_expect(bar, um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE);
+                    u_bulk(dst, ids + ((size_t)tile * n_chunks + c) * um::IDS, um::IDS, bar);
+                    if (new_group)
+                        u_bulk(dst + um::IDS, lut + ((size_t)tile * n_groups + c / cpg) * S::LUT, S::LUT, bar);
+                    u_bulk(dst + um::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + j0) * um::BTILE, ntc16 * um::BTILE,
+                           bar);
+                }
+            }
+        }
+    } else if (warp == um::MMA_WARP) {
+        // ------------------------------------------------------------ MMA issuer
+        uint32_t it = 0, ks_all = 0;
+        for (int pass = 0; pass < n_pass; ++pass) {
+            const int64_t j0 = j_first + (int64_t)pass * (um::NTOK / 8);
+            const int ntc = (int)((j_last - j0 + 1) < (um::NTOK / 8) ? (j_last - j0 + 1) : (um::NTOK / 8));
+            const int n = ((ntc + 1) & ~1) * 8;
+            const uint32_t idesc = idesc_i8(n);
+            if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
+            tc_fence_after();
+            for (int c = 0; c < n_chunks; ++c, ++it) {
+                const int s = it % um::STAGES;
+                u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
+                const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
+                for (int kk = 0; kk < 4; ++kk, ++ks_all) {
+                    const int as = ks_all % um::ASTAGES;
+                    u_bar_wait(u_smem(&afull_bar[as]), (ks_all / um::ASTAGES) & 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        // B tile layout in smem: [tile8][kstep][khalf][8 rows][16 B]
+                        const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
+#pragma unroll
+                        for (int sl = 0; sl < 2 * P; ++sl)
+                            tc_mma_i8(tmem + (uint32_t)((sl >> 1) * um::NTOK), tmem + acol0 + as * S::ACOLS + sl * 8,
+                                      bdesc, idesc, (c | kk) != 0 || (sl & 1) ? 1u : 0u);
+                        tc_commit(u_smem(&aempty_bar[as]));
+                        if (kk == 3) tc_commit(u_smem(&empty_bar[s]));
+                        if (kk == 3 && c == n_chunks - 1) tc_commit(u_smem(&accfull_bar));
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ expanders
+        const int wg = warp >> 2;         // warpgroup: k-steps of parity wg
+        const int quarter = warp & 3;     // TMEM lane quarter = row block
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        const float rscale = __ldg(rsp + tile * 128 + row);
+        uint32_t it = 0, ks_all = 0;
+        for (int pass = 0; pass < n_pass; ++pass) {
+            const int64_t j0 = j_first + (int64_t)pass * (um::NTOK / 8);
+            const int ntc = (int)((j_last - j0 + 1) < (um::NTOK / 8) ? (j_last - j0 + 1) : (um::NTOK / 8));
+            uint4 L[P];
+            for (int c = 0; c < n_chunks; ++c, ++it) {
+                const int s = it % um::STAGES;
+                u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
+                const uint8_t *st = smem + (size_t)s * S::BYTES;
+                if ((c % cpg) == 0) {
+                    const uint4 *lb = reinterpret_cast<const uint4 *>(st + um::IDS) + row * P;
+#pragma unroll
+                    for (int p = 0; p < P; ++p) L[p] = lb[p];
+                }
+                for (int kk = wg; kk < 4; kk += 2) {
+                    const uint32_t ksg = ks_all + kk;  // global k-step index
+                    const int as = ksg % um::ASTAGES;
+                    if (ksg >= um::ASTAGES) u_bar_wait(u_smem(&aempty_bar[as]), ((ksg / um::ASTAGES) - 1) & 1);
+                    tc_fence_after();
+                    const uint4 w = reinterpret_cast<const uint4 *>(st)[kk * 128 + row];
+                    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+                    uint32_t sel[8], xsel[8];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t x = wv[q] ^ 0x88888888u;
+                        sel[2 * q] = wv[q];
+                        sel[2 * q + 1] = wv[q] >> 16;
+                        xsel[2 * q] = x;
+                        xsel[2 * q + 1] = x >> 16;
+                    }
+                    const uint32_t abase = tmem + lane_addr + acol0 + as * S::ACOLS;
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        uint32_t v[16];
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc) {
+                            v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ sign garbage)
+                            v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
+                        }
+                        tc_st16(abase + p * 16, v);
+                    }
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) u_bar_arrive(u_smem(&afull_bar[as]));
+                }
+                ks_all += 4;
+            }
+            // ---- epilogue of this pass: accumulators -> fp32 out
+            u_bar_wait(u_smem(&accfull_bar), pass & 1);
+            tc_fence_after();
+            const int ncols = ((ntc + 1) & ~1) * 8;
+            for (int cb = wg * 16; cb < ncols; cb += 32) {
+                uint32_t acc[P][16];
+#pragma unroll
+                for (int p = 0; p < P; ++p) tc_ld16(tmem + lane_addr + p * um::NTOK + cb, acc[p]);
+                tc_wait_ld();
+#pragma unroll
+                for (int c2 = 0; c2 < 16; ++c2) {
+                    const int64_t tok = j0 * 8 + cb + c2;
+                    if (tok < rb || tok >= re) continue;
+                    const float v = (float)(um_combine<P>(acc, c2) * (double)rscale);
+                    out[tok * d_out + tile * 128 % d_out + row] = __fmul_rn(v, __ldg(scales + tok));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(um::TMEM_COLS)
+                     : "memory");
+    }
+}
+
+// codes (rows, K) row-major -> [chunk128][tile8][kstep4][khalf2][8 rows][16 B],
+// the canonical K-major no-swizzle UMMA B layout per k-step; rows >= n are zero.
+__global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
+                                 uint4 *__restrict__ dst) {
+    const int64_t total = (K / 128) * tiles * 64;  // 16-byte pieces: 8 (kstep, khalf) x 8 rows per tile-chunk
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(x & 7), kh = (int)((x >> 3) & 1), ks = (int)((x >> 4) & 3);
+        const int64_t j = (x >> 6) % tiles, c = (x >> 6) / tiles;
+        const int64_t row = j * 8 + r;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < n) v = *reinterpret_cast<const uint4 *>(src + row * K + c * 128 + ks * 32 + kh * 16);
+        dst[x] = v;
+    }
+}
+
+// ids (rows, d_in/2) -> [tile128][chunk][kstep][row][16 B] (the 16 packed bytes of
+// a row's 32 columns are already 8 PRMT selectors, low nibble first).
+__global__ void ids_umma_kernel(const uint8_t *__restrict__ ids, int64_t rows, int64_t d_in, uint4 *__restrict__ out) {
+    const int64_t n_chunks = d_in / 128;
+    const int64_t total = (rows / 128) * n_chunks * 4 * 128;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = x & 127, ks = (x >> 7) & 3, c = (x >> 9) % n_chunks, t = (x >> 9) / n_chunks;
+        out[x] = *reinterpret_cast<const uint4 *>(ids + (t * 128 + r) * (d_in / 2) + c * 64 + ks * 16);
+    }
+}
+
+// lut16 [rows/16][G][16][P][16] (lut8_kernel layout) -> [rows/128][G][128][P][16].
+__global__ void lut_umma_kernel(const int8_t *__restrict__ lut16, int64_t rows, int64_t n_groups, int planes,
+                                int8_t *__restrict__ out) {
+    const int64_t per = (int64_t)planes * 16;
+    const int64_t total = rows * n_groups;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = x % rows, grp = x / rows;
+        const int8_t *src = lut16 + (((row / 16) * n_groups + grp) * 16 + row % 16) * per;
+        int8_t *d = out + (((row / 128) * n_groups + grp) * 128 + row % 128) * per;
+        for (int64_t b = 0; b < per; b += 16)
+            *reinterpret_cast<uint4 *>(d + b) = *reinterpret_cast<const uint4 *>(src + b);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+bool umma_ok(int64_t d_in, int64_t d_out, int64_t g) { return d_in % 128 == 0 && g % 128 == 0 && d_out % 128 == 0; }
+
+template <int P>
+size_t umma_smem() {
+    return (size_t)um::STAGES * UmStage<P>::BYTES;
+}
+
+cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, cudaStream_t st) {
+    const int64_t total = (K / 128) * tiles * 64;
+    if (total == 0) return CQ_OK;
+    to_umma_b_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
+        codes, n, K, tiles, reinterpret_cast<uint4 *>(dst));
+    return check_launch("to_umma_b");
+}
+
+// tiles allocated in the B buffer: ceil(rows/8) + 2 (an N=16 MMA may read one tile past the end)
+int64_t umma_b_tiles(int64_t rows) { return ceil_div(rows, 8) + 2; }
+
+template <int P>
+cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *offsets, int64_t n_seg,
+                      int64_t seg_first, const cq_expert_site *a, float *out_a, const cq_expert_site *b, float *out_b,
+                      int64_t d_in, int64_t d_out, cudaStream_t st) {
+    static bool attr = false;
+    const size_t smem = umma_smem<P>();
+    if (!attr) {
+        cudaFuncSetAttribute(lut_umma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    dim3 grid((unsigned)(d_out / 128), (unsigned)n_seg, b ? 2u : 1u);
+    lut_umma_kernel<P><<<grid, um::THREADS, smem, st>>>(
+        bfrag, n_tiles, scales, offsets, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
+        b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, (int)d_in, (int)d_out,
+        (int)a->group_size);
+    return check_launch("lut_umma");
+}
+
+// Grouped tcgen05 LUT GEMM over segments.  `bbuf` holds umma_b_tiles(rows)
+// tiles x d_in bytes.  With b != nullptr, computes two matrices (gate -> out_a,
+// up -> out_b) in one launch.
+cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scales, const int32_t *offsets,
+                           int64_t n_seg, int64_t seg_first, int64_t rows, const cq_expert_site *a, float *out_a,
+                           const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
+    if (rows == 0 || n_seg == 0) return CQ_OK;
+    if (!umma_ok(d_in, d_out, a->group_size) || a->tc_lut == nullptr || (b && b->tc_lut == nullptr)) {
+        set_error("tcgen05 path: site not prepared or shape outside envelope");
+        return CQ_ERR_UNSUPPORTED;
+    }
+    if (b && (b->tc_planes != a->tc_planes || b->group_size != a->group_size)) {
+        set_error("tcgen05 path: paired matrices must share planes and group size");
+        return CQ_ERR_CONFIG;
+    }
+    const int64_t tiles = umma_b_tiles(rows);
+    CQ_TRY(to_umma_b(codes, rows, d_in, tiles, bbuf, st));
+    if (a->tc_planes == 3)
+        return launch_umma<3>(bbuf, tiles, scales, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, st);
+    if (a->tc_planes == 2)
+        return launch_umma<2>(bbuf, tiles, scales, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, st);
+    set_error("tcgen05 path: planes must be 2 or 3");
+    return CQ_ERR_CONFIG;
+}
+
+// One-time re-layout for the tcgen05 kernel from the mma16 LUT layout.
+cq_status umma_prepare(const uint8_t *ids, const int8_t *lut16, int64_t rows, int64_t d_in, int64_t g, int64_t planes,
+                       uint8_t *tc_ids, int8_t *tc_lut, cudaStream_t st) {
+    const int64_t total_ids = (rows / 128) * (d_in / 128) * 4 * 128;
+    ids_umma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total_ids, 256), 148 * 32), 256, 0, st>>>(
+        ids, rows, d_in, reinterpret_cast<uint4 *>(tc_ids));
+    CQ_TRY(check_launch("ids_umma"));
+    const int64_t total_lut = rows * (d_in / g);
+    lut_umma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total_lut, 256), 148 * 32), 256, 0, st>>>(
+        lut16, rows, d_in / g, (int)planes, tc_lut);
+    return check_launch("lut_umma_relayout");
+}
+
+}  // namespace cq

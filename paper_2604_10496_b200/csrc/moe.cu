@@ -30,6 +30,44 @@ cq_status lut_tc_grouped_frag(const int8_t *, uint2 *, const float *, const int3
                               const cq_expert_site *, const cq_expert_site *, int64_t, int64_t, float *,
                               cudaStream_t);
 bool tc_path_ok(int64_t d_in, int64_t d_out, int64_t g);
+cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
+                           const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
+                           cudaStream_t);
+int64_t umma_b_tiles(int64_t rows);
+
+// h = silu(a) * b (model.py:396) fused with the per-row A4 re-quantization of
+// h (model.py:397-398, quant.py:89-100): pass 1 forms h in place of a and its
+// max|h|; pass 2 writes the codes.  One CTA per row; same scale/rounding recipe
+// as the input quantizer.
+__global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, const float *__restrict__ b,
+                                                          int64_t ff, int8_t *__restrict__ codes,
+                                                          float *__restrict__ scales) {
+    const int64_t row = blockIdx.x;
+    float *ar = a + row * ff;
+    const float *br = b + row * ff;
+    float mx = 0.0f;
+    for (int64_t j = threadIdx.x; j < ff; j += blockDim.x) {
+        const float h = __fmul_rn(silu_f32(ar[j]), br[j]);
+        ar[j] = h;
+        mx = fmaxf(mx, fabsf(h));
+    }
+    __shared__ float red[8];
+    __shared__ float s_sh;
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0) {
+            s_sh = a4_scale(m);
+            scales[row] = s_sh;
+        }
+    }
+    __syncthreads();
+    const float s = s_sh;
+    for (int64_t j = threadIdx.x; j < ff; j += blockDim.x) codes[row * ff + j] = a4_code(ar[j], s);
+}
 
 // --- ordered grouped GEMM (GPU oracle path): bit-exact chains per segment.
 constexpr int OG_ROWS = 8, OG_TOK = 32, OG_J = 64;
@@ -173,14 +211,14 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_INV] = R * 4;
     sz[CQ_WS_CODES_PERM] = R * d;
     sz[CQ_WS_SCALES_PERM] = R * 4;
-    sz[CQ_WS_HIDDEN] = Rh * ff * 4 * (dsc->path == CQ_PATH_ORDERED ? 2 : 1);
+    sz[CQ_WS_HIDDEN] = Rh * ff * 4 * 2;  // h (or gate output a) | up output b
     sz[CQ_WS_HCODES] = Rh * ff;
     sz[CQ_WS_HSCALES] = Rh * 4;
     sz[CQ_WS_FOUT] = Rh * d * 4;
     sz[CQ_WS_ROTATED] = dsc->rotation ? n * d * 4 : 0;
     sz[CQ_WS_SHARED] = dsc->n_shared > 0 ? n * d * 4 : 0;
-    sz[CQ_WS_CODES_FRAG] = ceil_div(Rh, 8) * 8 * d;
-    sz[CQ_WS_HCODES_FRAG] = ceil_div(Rh, 8) * 8 * ff;
+    sz[CQ_WS_CODES_FRAG] = umma_b_tiles(Rh) * 8 * d;     // >= the mma16 fragment size too
+    sz[CQ_WS_HCODES_FRAG] = umma_b_tiles(Rh) * 8 * ff;
     int64_t pos = 0;
     for (int b = 0; b < CQ_WS_COUNT_; ++b) {
         if (off) off[b] = pos;
@@ -254,7 +292,8 @@ cq_status validate_desc(const cq_moe_desc *d) {
 
 int choose_path(const cq_moe_desc *d) {
     if (d->path != CQ_PATH_AUTO) return d->path;
-    const bool tc = d->gate.tc_lut && d->up.tc_lut && d->down.tc_lut &&
+    const bool tc = d->gate.tc_lut && d->up.tc_lut && d->down.tc_lut && d->gate.tc_layout == d->up.tc_layout &&
+                    d->up.tc_layout == d->down.tc_layout &&
                     tc_path_ok(d->d_model, d->d_ff, d->gate.group_size) &&
                     tc_path_ok(d->d_ff, d->d_model, d->down.group_size);
     if (tc) return CQ_PATH_TC;
@@ -271,6 +310,15 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
                       cudaStream_t st) {
     const int64_t d = dsc->d_model, ff = dsc->d_ff;
     if (rows == 0 || n_seg == 0) return CQ_OK;
+    if (path == CQ_PATH_TC && gate.tc_layout == CQ_TC_UMMA128) {
+        float *bbuf = hidden + rows * ff;
+        CQ_TRY(lut_umma_grouped(codes, reinterpret_cast<int8_t *>(frag_in), scales, offsets, n_seg, seg_first, rows,
+                                &gate, hidden, &up, bbuf, d, ff, st));
+        silu_quant_kernel<<<(unsigned)rows, 256, 0, st>>>(hidden, bbuf, ff, hcodes, hscales);
+        CQ_TRY(check_launch("silu_quant"));
+        return lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
+                                &down, fout, nullptr, nullptr, ff, d, st);
+    }
     if (path == CQ_PATH_TC) {
         CQ_TRY(lut_tc_grouped_frag(codes, frag_in, scales, offsets, n_seg, seg_first, rows, &gate, &up, d, ff,
                                    hidden, st));

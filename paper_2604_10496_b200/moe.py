@@ -62,11 +62,11 @@ class ExpertStack:
     def n(self) -> int:
         return self.ids.shape[0]
 
-    def prepare_tc(self, planes: int) -> None:
-        if self.tc is None or self.tc["planes"] != planes:
+    def prepare_tc(self, planes: int, layout: str = "umma128") -> None:
+        if self.tc is None or (self.tc["planes"], self.tc["layout"]) != (planes, layout):
             rows = self.n * self.d_out
             self.tc = prepare_tc_site(self.ids.view(rows, -1), self.centroids.view(rows, -1, 16),
-                                      rows, self.d_in, self.group_size, planes)
+                                      rows, self.d_in, self.group_size, planes, layout)
 
     def site(self) -> _lib.ExpertSite:
         s = _lib.ExpertSite()
@@ -78,6 +78,7 @@ class ExpertStack:
             s.tc_lut = self.tc["lut"].data_ptr()
             s.tc_rowscale = self.tc["rowscale"].data_ptr()
             s.tc_planes = self.tc["planes"]
+            s.tc_layout = _lib.TC_LAYOUTS[self.tc["layout"]]
         return s
 
 
@@ -146,15 +147,17 @@ class MoELayer:
         self._ws = {}
 
     # ------------------------------------------------------------------
-    def prepare_tc(self, planes_gate_up: int = 3, planes_down: int = 2) -> "MoELayer":
+    def prepare_tc(self, planes_gate_up: int = 3, planes_down: int = 2,
+                   layout: str = "umma128") -> "MoELayer":
         """Tensor-core layouts: 3 digit planes where the output is re-quantized
-        (gate, up), 2 for down (precision budget)."""
+        (gate, up), 2 for down (precision budget).  layout "umma128"
+        (tcgen05 kernel) or "mma16" (mma.sync kernel)."""
         sites = [(self.gate, planes_gate_up), (self.up, planes_gate_up), (self.down, planes_down)]
         if self.shared is not None:
             sites += [(self.shared[0], planes_gate_up), (self.shared[1], planes_gate_up),
                       (self.shared[2], planes_down)]
         for s, p in sites:
-            s.prepare_tc(p)
+            s.prepare_tc(p, layout)
         return self
 
     def desc(self, path: str | None = None) -> _lib.MoEDesc:

@@ -113,7 +113,8 @@ def test_lut_gemm_matches_oracle_full_size():
         want = oracle.c_lut_gemm(codes, scales, ids, cent, g)
         pw = _pw(ids, cent, d_in, g)
         got = lut_gemm(_qa(codes, scales), pw).cpu().numpy()
-        assert o.relative_error(got, want) <= 1e-6, (n, d_in, d_out, g)
+        # fp32 accumulation-order noise grows ~sqrt(d_in): 3e-6 at d_in = 4096
+        assert o.relative_error(got, want) <= 3e-6, (n, d_in, d_out, g)
         exact = reference_gemm(_qa(codes, scales), pw).cpu().numpy()
         assert np.array_equal(exact.view(np.int32), want.view(np.int32)), (n, d_in, d_out, g)
 

@@ -24,17 +24,22 @@ def _rand_pw(rng, d_out, d_in, g, scale=1.0):
     return cent, ids, PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), d_in, g)
 
 
+LAYOUTS = ["umma128", "mma16"]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("planes", [2, 3])
-def test_digit_plane_luts_decode_to_centroids(planes):
+def test_digit_plane_luts_decode_to_centroids(planes, layout):
     rng = np.random.default_rng(0)
-    cent, ids, pw = _rand_pw(rng, 32, 512, 128, 0.03)
+    rows, tr = 256, (128 if layout == "umma128" else 16)
+    cent, ids, pw = _rand_pw(rng, rows, 512, 128, 0.03)
     cent[3] = 0.0  # an all-zero row gets scale 1 and zero digits
     pw = PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), 512, 128)
-    pw.prepare_tc(planes)
-    lut = pw.tc["lut"].cpu().numpy().astype(np.int64)          # (rows, G, P, 16), tile-ordered
+    pw.prepare_tc(planes, layout)
+    lut = pw.tc["lut"].cpu().numpy().astype(np.int64)          # tile-ordered [tile][G][tr][P][16]
     rs = pw.tc["rowscale"].cpu().numpy().astype(np.float64)
     G = 512 // 128
-    lut = lut.reshape(32 // 16, G, 16, planes, 16).transpose(0, 2, 1, 3, 4).reshape(32, G, planes, 16)
+    lut = lut.reshape(rows // tr, G, tr, planes, 16).transpose(0, 2, 1, 3, 4).reshape(rows, G, planes, 16)
     partner = lut[..., np.arange(16) ^ 8]
     digits = lut + np.where(partner < 0, -1, 0)               # what PRMT(P) + PRMT(Q) deliver
     assert digits.min() >= -128 and digits.max() <= 126
@@ -50,7 +55,7 @@ def test_digit_plane_luts_decode_to_centroids(planes):
 def test_fragment_ids_are_a_permutation_of_packed_ids():
     rng = np.random.default_rng(1)
     cent, ids, pw = _rand_pw(rng, 48, 384, 128)
-    pw.prepare_tc(3)
+    pw.prepare_tc(3, "mma16")
     frag = pw.tc["ids"].cpu().numpy().reshape(-1).view(np.uint32).reshape(48 // 16, 384 // 128, 2, 32, 4)
     for tile in range(3):
         for chunk in range(3):
@@ -67,30 +72,42 @@ def test_fragment_ids_are_a_permutation_of_packed_ids():
                         assert w1 == sel(r0, k_lo + 16) | (sel(r1, k_lo + 16) << 16)
 
 
+def test_umma_ids_are_row_blocks_of_packed_ids():
+    rng = np.random.default_rng(2)
+    cent, ids, pw = _rand_pw(rng, 256, 384, 128)
+    pw.prepare_tc(3, "umma128")
+    got = pw.tc["ids"].cpu().numpy().reshape(2, 3, 4, 128, 16)     # [tile][chunk][kstep][row][16 B]
+    want = ids.reshape(2, 128, 3, 4, 16).transpose(0, 2, 3, 1, 4)
+    assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("n,d_in,d_out,g", [(1, 4096, 1024, 128), (7, 1024, 2816, 128), (16, 4096, 512, 4096),
-                                             (33, 2048, 768, 128), (64, 1408, 2048, 128), (100, 512, 256, 256)])
+                                             (33, 2048, 768, 128), (64, 1408, 2048, 128), (100, 512, 256, 256),
+                                             (130, 1024, 384, 1024)])
+@pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("planes", [2, 3])
-def test_lut_gemm_tc_matches_oracle(n, d_in, d_out, g, planes):
+def test_lut_gemm_tc_matches_oracle(n, d_in, d_out, g, planes, layout):
     rng = np.random.default_rng(n + d_in + planes)
     cent, ids, pw = _rand_pw(rng, d_out, d_in, g)
     codes = rng.integers(-8, 8, (n, d_in)).astype(np.int8)
     scales = (0.5 + rng.random(n)).astype(np.float32)
     want = oracle.c_lut_gemm(codes, scales, ids, cent, g)
     qa = QuantizedActivations(torch.from_numpy(codes).cuda(), torch.from_numpy(scales).cuda(), 4)
-    got = lut_gemm_tc(qa, pw, planes).cpu().numpy()
+    got = lut_gemm_tc(qa, pw, planes, layout).cpu().numpy()
     tol = 2e-6 if planes == 3 else 2e-4
     assert o.relative_error(got, want) <= tol
 
 
+@pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("name", ["moe_small.npz", "moe_c1.npz"])
-def test_moe_layer_tc_golden(golden, name):
+def test_moe_layer_tc_golden(golden, name, layout):
     g = golden(name)
     seed, n, d, ff, E, k, gs = (int(v) for v in g["config"])
     v, w, experts, _ = moe_inputs_host(seed, n, d, ff, E, gs)
     layer = MoELayer(w, to_device_experts(experts), k, path="tc")
     if d % 128 or ff % 128 or gs % 128:
         pytest.skip("shape outside the tensor-core envelope")
-    layer.prepare_tc()
+    layer.prepare_tc(layout=layout)
     out = layer(torch.from_numpy(v).cuda()).cpu().numpy()
     tr = layer.trace(n)
     assert np.array_equal(tr["selected"].cpu().numpy(), g["selected"])
@@ -98,11 +115,12 @@ def test_moe_layer_tc_golden(golden, name):
     assert err <= 1e-2, err
 
 
-def test_mixtral_decode_tc_vs_ordered():
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_mixtral_decode_tc_vs_ordered(layout):
     n, d, ff, E, k, g = 64, 4096, 14336, 8, 2, 128
     v, w, sites, _ = moe_inputs_device(11, n, d, ff, E, g)
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc").prepare_tc()
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc").prepare_tc(layout=layout)
     out = layer(v).float()
     tr = {key: t.clone() for key, t in layer.trace(n).items()}
     ordered = layer(v, path="ordered").float()
