@@ -6,29 +6,31 @@
 // kernel removes the legacy mma.sync issue cost, which capped the register-
 // operand version at ~30% of HBM bandwidth (profiles/README.md).
 //
-// CTA = one 128-row weight tile of one expert matrix x one token pass
-// (<= 64 tokens), warp-specialised:
+// CTA = one 128-row weight tile of one expert matrix x token passes of <= 32
+// tokens, warp-specialised:
 //   warps 0-7  expanders: warp w owns TMEM lane quarter w%4 (= rows), the two
 //              warpgroups take alternating 32-column k-steps.  Per k-step a
 //              thread turns 32 ids of its row into P planes x {lo,hi} halves x
-//              8 columns with 2P PRMT per 4 ids and tcgen05.st's them.
+//              8 columns with 2P PRMT per 4 ids and tcgen05.st's them; then the
+//              warpgroup's first thread issues that k-step's 2P tcgen05.mma
+//              (M=128, N=16|32, K=32) into the warpgroup's own accumulators
+//              and commits (frees the A stage / smem stage).  Two issuers, two
+//              accumulator sets: no cross-warp MMA hand-off on the critical path.
 //   warp 8     producer: cp.async.bulk of ids (8 KB/128 columns), the group's
 //              LUT block and the activation tile into a 4-deep smem ring.
-//   warp 9     MMA issuer: one elected thread, 2P tcgen05.mma per k-step
-//              (M=128, N=16..64, K=32), commits free the A stage / smem stage.
-// Epilogue: expanders tcgen05.ld the P accumulators, combine digits
-// (sum 255^p S_p), scale by the row scale and the token scale, store fp32.
+// Epilogue: expanders tcgen05.ld both warpgroups' P accumulators, add them
+// (exact int32), combine digits (sum 255^p S_p), scale by the row scale and
+// the token scale, store fp32.
 #include "common.cuh"
 
 namespace cq {
 
 namespace um {
 constexpr int STAGES = 4;        // smem ring depth (128-column chunks)
-constexpr int ASTAGES = 6;       // TMEM A stages (one 32-column k-step each)
-constexpr int NTOK = 64;         // max tokens per pass (MMA N)
+constexpr int NTOK = 32;         // max tokens per pass (MMA N)
 constexpr int IDS = 128 * 64;    // ids bytes per chunk: 128 rows x 128 columns / 2
 constexpr int BTILE = 1024;      // activation bytes per 8-token tile per chunk
-constexpr int EXP_WARPS = 8, PROD_WARP = 8, MMA_WARP = 9, WARPS = 10;
+constexpr int EXP_WARPS = 8, PROD_WARP = 8, WARPS = 9;
 constexpr int THREADS = WARPS * 32;
 constexpr uint32_t TMEM_COLS = 512;
 }  // namespace um
@@ -38,9 +40,10 @@ struct UmStage {
     static constexpr int LUT = 128 * P * 16;
     static constexpr int B = (um::NTOK / 8) * um::BTILE;
     static constexpr int BYTES = um::IDS + LUT + B;
-    static constexpr int ACOLS = 2 * P * 8;   // TMEM columns per A stage
+    static constexpr int ACOLS = 2 * P * 8;                   // TMEM columns per A stage (one k-step)
+    static constexpr int ACC = 2 * P * um::NTOK;              // accumulators: 2 warpgroups x P planes
+    static constexpr int AS = (um::TMEM_COLS - ACC) / ACOLS / 2;  // A stages per warpgroup
 };
-
 // ---------------------------------------------------------------------------
 // PTX wrappers (tcgen05 / mbarrier / bulk copy)
 
@@ -138,6 +141,10 @@ __device__ __forceinline__ double um_combine(const uint32_t (&acc)[P][16], int c
 }
 
 // grid: (d_out / 128, n_seg, n_mat); blockIdx.z picks the matrix (gate / up).
+// Warps 0-7 expand (warpgroup wg takes the k-steps of parity wg) and each
+// warpgroup's first thread issues the MMAs of its own k-steps into its own
+// accumulator set (exact int32, summed in the epilogue) — no cross-warp
+// MMA hand-off.  Warp 8 is the bulk-copy producer.
 template <int P>
 __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
@@ -146,9 +153,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1, const float *__restrict__ rs1,
     float *__restrict__ out1, int d_in, int d_out, int g) {
     using S = UmStage<P>;
+    constexpr int AS = S::AS;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full_bar[um::STAGES], empty_bar[um::STAGES];
-    __shared__ __align__(8) uint64_t afull_bar[um::ASTAGES], aempty_bar[um::ASTAGES];
+    __shared__ __align__(8) uint64_t aempty_bar[2][AS];
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
 
@@ -164,19 +172,16 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int64_t e = seg + seg_first;
     const int64_t tile = e * (d_out / 128) + blockIdx.x;
     const int n_chunks = d_in / 128, cpg = g / 128, n_groups = d_in / g;
-    const int ksteps = n_chunks * 4;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < um::STAGES; ++s) {
             u_bar_init(u_smem(&full_bar[s]), 1);
-            u_bar_init(u_smem(&empty_bar[s]), 1);
+            u_bar_init(u_smem(&empty_bar[s]), 2);   // one commit per warpgroup
         }
-        for (int s = 0; s < um::ASTAGES; ++s) {
-            u_bar_init(u_smem(&afull_bar[s]), 4);
-            u_bar_init(u_smem(&aempty_bar[s]), 1);
-        }
-        u_bar_init(u_smem(&accfull_bar), 1);
-        u_bar_init(u_smem(&accempty_bar), 8);
+        for (int w = 0; w < 2; ++w)
+            for (int s = 0; s < AS; ++s) u_bar_init(u_smem(&aempty_bar[w][s]), 1);
+        u_bar_init(u_smem(&accfull_bar), 2);
+        u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -189,25 +194,25 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
-    // TMEM columns: [0, P*NTOK) accumulators (plane p at p*NTOK), then A stages
-    const uint32_t acol0 = P * um::NTOK;
 
     const int64_t j_first = rb >> 3, j_last = (re - 1) >> 3;
-    const int n_pass = (int)((j_last - j_first + 1 + (um::NTOK / 8) - 1) / (um::NTOK / 8));
+    constexpr int TPP = um::NTOK / 8;  // token tiles per pass
+    const int n_pass = (int)((j_last - j_first + TPP) / TPP);
 
     if (warp == um::PROD_WARP) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             uint32_t it = 0;
             for (int pass = 0; pass < n_pass; ++pass) {
-                const int64_t j0 = j_first + (int64_t)pass * (um::NTOK / 8);
-                const int ntc = (int)((j_last - j0 + 1) < (um::NTOK / 8) ? (j_last - j0 + 1) : (um::NTOK / 8));
+                const int64_t j0 = j_first + (int64_t)pass * TPP;
+                const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
                 const int ntc16 = (ntc + 1) & ~1;  // MMA N is a multiple of 16
+                int gc = 0;  // chunk index within the current group
                 for (int c = 0; c < n_chunks; ++c, ++it) {
                     const int s = it % um::STAGES;
                     if (it >= um::STAGES) u_bar_wait(u_smem(&empty_bar[s]), ((it / um::STAGES) - 1) & 1);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    const bool new_group = (c % cpg) == 0 || c == 0;
+                    const bool new_group = gc == 0;
                     const uint32_t bar = u_smem(&full_bar[s]);
                     const uint32_t dst = u_smem(smem + (size_t)s * S::BYTES);
                     u_bar_expect(bar, um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE);
@@ -216,67 +221,45 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                         u_bulk(dst + um::IDS, lut + ((size_t)tile * n_groups + c / cpg) * S::LUT, S::LUT, bar);
                     u_bulk(dst + um::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + j0) * um::BTILE, ntc16 * um::BTILE,
                            bar);
-                }
-            }
-        }
-    } else if (warp == um::MMA_WARP) {
-        // ------------------------------------------------------------ MMA issuer
-        uint32_t it = 0, ks_all = 0;
-        for (int pass = 0; pass < n_pass; ++pass) {
-            const int64_t j0 = j_first + (int64_t)pass * (um::NTOK / 8);
-            const int ntc = (int)((j_last - j0 + 1) < (um::NTOK / 8) ? (j_last - j0 + 1) : (um::NTOK / 8));
-            const int n = ((ntc + 1) & ~1) * 8;
-            const uint32_t idesc = idesc_i8(n);
-            if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
-            tc_fence_after();
-            for (int c = 0; c < n_chunks; ++c, ++it) {
-                const int s = it % um::STAGES;
-                u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
-                const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
-                for (int kk = 0; kk < 4; ++kk, ++ks_all) {
-                    const int as = ks_all % um::ASTAGES;
-                    u_bar_wait(u_smem(&afull_bar[as]), (ks_all / um::ASTAGES) & 1);
-                    tc_fence_after();
-                    if (lane == 0) {
-                        // B tile layout in smem: [tile8][kstep][khalf][8 rows][16 B]
-                        const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
-#pragma unroll
-                        for (int sl = 0; sl < 2 * P; ++sl)
-                            tc_mma_i8(tmem + (uint32_t)((sl >> 1) * um::NTOK), tmem + acol0 + as * S::ACOLS + sl * 8,
-                                      bdesc, idesc, (c | kk) != 0 || (sl & 1) ? 1u : 0u);
-                        tc_commit(u_smem(&aempty_bar[as]));
-                        if (kk == 3) tc_commit(u_smem(&empty_bar[s]));
-                        if (kk == 3 && c == n_chunks - 1) tc_commit(u_smem(&accfull_bar));
-                    }
-                    __syncwarp();
+                    if (++gc == cpg) gc = 0;
                 }
             }
         }
     } else {
-        // ------------------------------------------------------------ expanders
+        // ------------------------------------------------------------ expanders (+ per-warpgroup MMA issue)
         const int wg = warp >> 2;         // warpgroup: k-steps of parity wg
         const int quarter = warp & 3;     // TMEM lane quarter = row block
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        const bool issuer = quarter == 0 && lane == 0;
         const float rscale = __ldg(rsp + tile * 128 + row);
-        uint32_t it = 0, ks_all = 0;
+        const uint32_t acc_base = tmem + (uint32_t)(wg * P * um::NTOK);
+        const uint32_t a_base = tmem + (uint32_t)S::ACC + (uint32_t)(wg * AS * S::ACOLS);
+        uint32_t it = 0, kq = 0;  // chunks consumed; k-steps of this warpgroup
         for (int pass = 0; pass < n_pass; ++pass) {
-            const int64_t j0 = j_first + (int64_t)pass * (um::NTOK / 8);
-            const int ntc = (int)((j_last - j0 + 1) < (um::NTOK / 8) ? (j_last - j0 + 1) : (um::NTOK / 8));
+            const int64_t j0 = j_first + (int64_t)pass * TPP;
+            const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
+            const int n = ((ntc + 1) & ~1) * 8;
+            const uint32_t idesc = idesc_i8(n);
+            if (pass > 0 && issuer) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
             uint4 L[P];
+            int gc = 0;
             for (int c = 0; c < n_chunks; ++c, ++it) {
                 const int s = it % um::STAGES;
                 u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
-                if ((c % cpg) == 0) {
+                if (gc == 0) {
                     const uint4 *lb = reinterpret_cast<const uint4 *>(st + um::IDS) + row * P;
 #pragma unroll
                     for (int p = 0; p < P; ++p) L[p] = lb[p];
                 }
-                for (int kk = wg; kk < 4; kk += 2) {
-                    const uint32_t ksg = ks_all + kk;  // global k-step index
-                    const int as = ksg % um::ASTAGES;
-                    if (ksg >= um::ASTAGES) u_bar_wait(u_smem(&aempty_bar[as]), ((ksg / um::ASTAGES) - 1) & 1);
+                if (++gc == cpg) gc = 0;
+                const uint32_t bbase = u_smem(st + um::IDS + S::LUT);
+#pragma unroll
+                for (int h = 0; h < 2; ++h, ++kq) {
+                    const int kk = 2 * h + wg;
+                    const int as = kq % AS;
+                    if (kq >= AS) u_bar_wait(u_smem(&aempty_bar[wg][as]), ((kq / AS) - 1) & 1);
                     tc_fence_after();
                     const uint4 w = reinterpret_cast<const uint4 *>(st)[kk * 128 + row];
                     const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
@@ -289,7 +272,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                         xsel[2 * q] = x;
                         xsel[2 * q + 1] = x >> 16;
                     }
-                    const uint32_t abase = tmem + lane_addr + acol0 + as * S::ACOLS;
+                    const uint32_t abase = a_base + lane_addr + as * S::ACOLS;
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
                         uint32_t v[16];
@@ -302,26 +285,43 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     }
                     tc_wait_st();
                     tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) u_bar_arrive(u_smem(&afull_bar[as]));
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");  // this warpgroup's stage is written
+                    if (issuer) {
+                        tc_fence_after();
+                        // B tile layout in smem: [tile8][kstep][khalf][8 rows][16 B]
+                        const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
+                        const bool first = (c == 0 && h == 0);
+#pragma unroll
+                        for (int sl = 0; sl < 2 * P; ++sl)
+                            tc_mma_i8(acc_base + (uint32_t)((sl >> 1) * um::NTOK), a_base + as * S::ACOLS + sl * 8,
+                                      bdesc, idesc, (!first || (sl & 1)) ? 1u : 0u);
+                        tc_commit(u_smem(&aempty_bar[wg][as]));
+                        if (h == 1) tc_commit(u_smem(&empty_bar[s]));
+                        if (h == 1 && c == n_chunks - 1) tc_commit(u_smem(&accfull_bar));
+                    }
                 }
-                ks_all += 4;
             }
-            // ---- epilogue of this pass: accumulators -> fp32 out
+            // ---- epilogue of this pass: (wg0 + wg1) accumulators -> fp32 out
             u_bar_wait(u_smem(&accfull_bar), pass & 1);
             tc_fence_after();
-            const int ncols = ((ntc + 1) & ~1) * 8;
-            for (int cb = wg * 16; cb < ncols; cb += 32) {
+            const int cb = wg * 16;  // each warpgroup converts 16 token columns
+            if (cb < n) {
                 uint32_t acc[P][16];
 #pragma unroll
-                for (int p = 0; p < P; ++p) tc_ld16(tmem + lane_addr + p * um::NTOK + cb, acc[p]);
-                tc_wait_ld();
+                for (int p = 0; p < P; ++p) {
+                    uint32_t t0[16], t1[16];
+                    tc_ld16(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), t0);
+                    tc_ld16(tmem + lane_addr + (uint32_t)((P + p) * um::NTOK + cb), t1);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int c2 = 0; c2 < 16; ++c2) acc[p][c2] = (uint32_t)((int32_t)t0[c2] + (int32_t)t1[c2]);
+                }
 #pragma unroll
                 for (int c2 = 0; c2 < 16; ++c2) {
                     const int64_t tok = j0 * 8 + cb + c2;
                     if (tok < rb || tok >= re) continue;
                     const float v = (float)(um_combine<P>(acc, c2) * (double)rscale);
-                    out[tok * d_out + tile * 128 % d_out + row] = __fmul_rn(v, __ldg(scales + tok));
+                    out[tok * d_out + (int64_t)blockIdx.x * 128 + row] = __fmul_rn(v, __ldg(scales + tok));
                 }
             }
             tc_fence_before();
@@ -365,7 +365,7 @@ __global__ void ids_umma_kernel(const uint8_t *__restrict__ ids, int64_t rows, i
 }
 
 // lut16 [rows/16][G][16][P][16] (lut8_kernel layout) -> [rows/128][G][128][P][16].
-__global__ void lut_umma_kernel(const int8_t *__restrict__ lut16, int64_t rows, int64_t n_groups, int planes,
+__global__ void lut_relayout_kernel(const int8_t *__restrict__ lut16, int64_t rows, int64_t n_groups, int planes,
                                 int8_t *__restrict__ out) {
     const int64_t per = (int64_t)planes * 16;
     const int64_t total = rows * n_groups;
@@ -450,7 +450,7 @@ cq_status umma_prepare(const uint8_t *ids, const int8_t *lut16, int64_t rows, in
         ids, rows, d_in, reinterpret_cast<uint4 *>(tc_ids));
     CQ_TRY(check_launch("ids_umma"));
     const int64_t total_lut = rows * (d_in / g);
-    lut_umma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total_lut, 256), 148 * 32), 256, 0, st>>>(
+    lut_relayout_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total_lut, 256), 148 * 32), 256, 0, st>>>(
         lut16, rows, d_in / g, (int)planes, tc_lut);
     return check_launch("lut_umma_relayout");
 }
