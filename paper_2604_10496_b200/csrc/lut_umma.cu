@@ -7,20 +7,22 @@
 // operand version at ~30% of HBM bandwidth (profiles/README.md).
 //
 // CTA = one 128-row weight tile of one expert matrix x token passes of <= 32
-// tokens, warp-specialised:
-//   warps 0-7  expanders: warp w owns TMEM lane quarter w%4 (= rows), the two
-//              warpgroups take alternating 32-column k-steps.  Per k-step a
-//              thread turns 32 ids of its row into P planes x {lo,hi} halves x
-//              8 columns with 2P PRMT per 4 ids and tcgen05.st's them; then the
-//              warpgroup's first thread issues that k-step's 2P tcgen05.mma
-//              (M=128, N=16|32, K=32) into the warpgroup's own accumulators
-//              and commits (frees the A stage / smem stage).  Two issuers, two
-//              accumulator sets: no cross-warp MMA hand-off on the critical path.
-//   warp 8     producer: cp.async.bulk of ids (8 KB/128 columns), the group's
-//              LUT block and the activation tile into a 4-deep smem ring.
-// Epilogue: expanders tcgen05.ld both warpgroups' P accumulators, add them
-// (exact int32), combine digits (sum 255^p S_p), scale by the row scale and
-// the token scale, store fp32.
+// tokens, warp-specialised (18 warps, one CTA per SM: it owns all 512 TMEM
+// columns):
+//   warps 0-15 expanders, 4 warpgroups: warp w owns TMEM lane quarter w%4
+//              (= 32 rows) and warpgroup w/4 expands k-step w/4 of every
+//              128-column chunk.  A thread turns the 32 ids of its row into
+//              P planes x {lo,hi} halves x 8 columns (2P PRMT per 4 ids) and
+//              tcgen05.st's them into its warpgroup's A stage; four warpgroups
+//              in flight hide the TMEM store latency (tcgen05.wait::st).
+//   warp 16    producer: cp.async.bulk of ids (8 KB per chunk), the group's LUT
+//              block and the activation tile into a 4-deep smem ring.
+//   warp 17    MMA issuer: one thread, 2P tcgen05.mma per k-step (M=128,
+//              N=16|32, K=32) into P int32 accumulators; commits free the A
+//              stage, the smem stage and finally signal the epilogue.
+// Epilogue: expanders tcgen05.ld the P accumulators (8 token columns per
+// warpgroup), combine digits (sum 255^p S_p), scale by the row scale and the
+// token scale, store fp32.
 #include "common.cuh"
 
 namespace cq {
@@ -30,7 +32,8 @@ constexpr int STAGES = 4;        // smem ring depth (128-column chunks)
 constexpr int NTOK = 32;         // max tokens per pass (MMA N)
 constexpr int IDS = 128 * 64;    // ids bytes per chunk: 128 rows x 128 columns / 2
 constexpr int BTILE = 1024;      // activation bytes per 8-token tile per chunk
-constexpr int EXP_WARPS = 8, PROD_WARP = 8, WARPS = 9;
+constexpr int WG = 4;            // expander warpgroups; warpgroup w expands k-step w of every chunk
+constexpr int EXP_WARPS = 4 * WG, PROD_WARP = EXP_WARPS, MMA_WARP = EXP_WARPS + 1, WARPS = EXP_WARPS + 2;
 constexpr int THREADS = WARPS * 32;
 constexpr uint32_t TMEM_COLS = 512;
 }  // namespace um
@@ -40,10 +43,11 @@ struct UmStage {
     static constexpr int LUT = 128 * P * 16;
     static constexpr int B = (um::NTOK / 8) * um::BTILE;
     static constexpr int BYTES = um::IDS + LUT + B;
-    static constexpr int ACOLS = 2 * P * 8;                   // TMEM columns per A stage (one k-step)
-    static constexpr int ACC = 2 * P * um::NTOK;              // accumulators: 2 warpgroups x P planes
-    static constexpr int AS = (um::TMEM_COLS - ACC) / ACOLS / 2;  // A stages per warpgroup
+    static constexpr int ACOLS = 2 * P * 8;                        // TMEM columns per A stage (one k-step)
+    static constexpr int ACC = P * um::NTOK;                       // accumulators: P planes x N
+    static constexpr int AS = (um::TMEM_COLS - ACC) / ACOLS / um::WG;  // A stages per warpgroup
 };
+
 // ---------------------------------------------------------------------------
 // PTX wrappers (tcgen05 / mbarrier / bulk copy)
 
@@ -113,6 +117,12 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "r"(taddr)
         : "memory");
 }
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -141,10 +151,6 @@ __device__ __forceinline__ double um_combine(const uint32_t (&acc)[P][16], int c
 }
 
 // grid: (d_out / 128, n_seg, n_mat); blockIdx.z picks the matrix (gate / up).
-// Warps 0-7 expand (warpgroup wg takes the k-steps of parity wg) and each
-// warpgroup's first thread issues the MMAs of its own k-steps into its own
-// accumulator set (exact int32, summed in the epilogue) — no cross-warp
-// MMA hand-off.  Warp 8 is the bulk-copy producer.
 template <int P>
 __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
@@ -154,9 +160,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     float *__restrict__ out1, int d_in, int d_out, int g) {
     using S = UmStage<P>;
     constexpr int AS = S::AS;
+    constexpr int NAS = AS * um::WG;  // A stages in total
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full_bar[um::STAGES], empty_bar[um::STAGES];
-    __shared__ __align__(8) uint64_t aempty_bar[2][AS];
+    __shared__ __align__(8) uint64_t afull_bar[NAS], aempty_bar[NAS];
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
 
@@ -176,11 +183,13 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     if (threadIdx.x == 0) {
         for (int s = 0; s < um::STAGES; ++s) {
             u_bar_init(u_smem(&full_bar[s]), 1);
-            u_bar_init(u_smem(&empty_bar[s]), 2);   // one commit per warpgroup
+            u_bar_init(u_smem(&empty_bar[s]), 1);
         }
-        for (int w = 0; w < 2; ++w)
-            for (int s = 0; s < AS; ++s) u_bar_init(u_smem(&aempty_bar[w][s]), 1);
-        u_bar_init(u_smem(&accfull_bar), 2);
+        for (int s = 0; s < NAS; ++s) {
+            u_bar_init(u_smem(&afull_bar[s]), 4);  // the 4 warps of the writing warpgroup
+            u_bar_init(u_smem(&aempty_bar[s]), 1);
+        }
+        u_bar_init(u_smem(&accfull_bar), 1);
         u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -194,6 +203,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    const uint32_t a_col0 = (uint32_t)S::ACC;  // A stages follow the accumulators
 
     const int64_t j_first = rb >> 3, j_last = (re - 1) >> 3;
     constexpr int TPP = um::NTOK / 8;  // token tiles per pass
@@ -225,28 +235,60 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 }
             }
         }
+    } else if (warp == um::MMA_WARP) {
+        // ------------------------------------------------------------ MMA issuer (one thread)
+        uint32_t it = 0, ks = 0;
+        for (int pass = 0; pass < n_pass; ++pass) {
+            const int64_t j0 = j_first + (int64_t)pass * TPP;
+            const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
+            const uint32_t idesc = idesc_i8(((ntc + 1) & ~1) * 8);
+            if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
+            for (int c = 0; c < n_chunks; ++c, ++it) {
+                const int s = it % um::STAGES;
+                u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
+                const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk, ++ks) {
+                    const int as = ks % NAS;
+                    u_bar_wait(u_smem(&afull_bar[as]), (ks / NAS) & 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
+                        const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
+                        const bool first = (c == 0 && kk == 0);
+#pragma unroll
+                        for (int sl = 0; sl < 2 * P; ++sl)
+                            tc_mma_i8(tmem + (uint32_t)((sl >> 1) * um::NTOK), tmem + a_col0 + as * S::ACOLS + sl * 8,
+                                      bdesc, idesc, (!first || (sl & 1)) ? 1u : 0u);
+                        tc_commit(u_smem(&aempty_bar[as]));
+                        if (kk == 3) tc_commit(u_smem(&empty_bar[s]));
+                        if (kk == 3 && c == n_chunks - 1) tc_commit(u_smem(&accfull_bar));
+                    }
+                    __syncwarp();
+                }
+            }
+        }
     } else {
-        // ------------------------------------------------------------ expanders (+ per-warpgroup MMA issue)
-        const int wg = warp >> 2;         // warpgroup: k-steps of parity wg
-        const int quarter = warp & 3;     // TMEM lane quarter = row block
+        // ------------------------------------------------------------ expanders
+        const int wg = warp >> 2;         // expands k-step wg of every chunk
+        const int quarter = warp & 3;     // TMEM lane quarter = rows
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        const bool issuer = quarter == 0 && lane == 0;
         const float rscale = __ldg(rsp + tile * 128 + row);
-        const uint32_t acc_base = tmem + (uint32_t)(wg * P * um::NTOK);
-        const uint32_t a_base = tmem + (uint32_t)S::ACC + (uint32_t)(wg * AS * S::ACOLS);
         uint32_t it = 0, kq = 0;  // chunks consumed; k-steps of this warpgroup
         for (int pass = 0; pass < n_pass; ++pass) {
             const int64_t j0 = j_first + (int64_t)pass * TPP;
             const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
             const int n = ((ntc + 1) & ~1) * 8;
-            const uint32_t idesc = idesc_i8(n);
-            if (pass > 0 && issuer) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
             uint4 L[P];
             int gc = 0;
-            for (int c = 0; c < n_chunks; ++c, ++it) {
+            for (int c = 0; c < n_chunks; ++c, ++it, ++kq) {
                 const int s = it % um::STAGES;
+                const int as_l = kq % AS;
+                const int as = as_l * um::WG + wg;  // global A stage = ks % NAS with ks = 4 * chunk + wg
+                if (kq >= AS) u_bar_wait(u_smem(&aempty_bar[as]), ((kq / AS) - 1) & 1);
                 u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
+                tc_fence_after();
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
                 if (gc == 0) {
                     const uint4 *lb = reinterpret_cast<const uint4 *>(st + um::IDS) + row * P;
@@ -254,70 +296,44 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     for (int p = 0; p < P; ++p) L[p] = lb[p];
                 }
                 if (++gc == cpg) gc = 0;
-                const uint32_t bbase = u_smem(st + um::IDS + S::LUT);
+                const uint4 w = reinterpret_cast<const uint4 *>(st)[wg * 128 + row];
+                const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+                uint32_t sel[8], xsel[8];
 #pragma unroll
-                for (int h = 0; h < 2; ++h, ++kq) {
-                    const int kk = 2 * h + wg;
-                    const int as = kq % AS;
-                    if (kq >= AS) u_bar_wait(u_smem(&aempty_bar[wg][as]), ((kq / AS) - 1) & 1);
-                    tc_fence_after();
-                    const uint4 w = reinterpret_cast<const uint4 *>(st)[kk * 128 + row];
-                    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-                    uint32_t sel[8], xsel[8];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t x = wv[q] ^ 0x88888888u;
-                        sel[2 * q] = wv[q];
-                        sel[2 * q + 1] = wv[q] >> 16;
-                        xsel[2 * q] = x;
-                        xsel[2 * q + 1] = x >> 16;
-                    }
-                    const uint32_t abase = a_base + lane_addr + as * S::ACOLS;
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        uint32_t v[16];
-#pragma unroll
-                        for (int cc = 0; cc < 8; ++cc) {
-                            v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ sign garbage)
-                            v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
-                        }
-                        tc_st16(abase + p * 16, v);
-                    }
-                    tc_wait_st();
-                    tc_fence_before();
-                    asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");  // this warpgroup's stage is written
-                    if (issuer) {
-                        tc_fence_after();
-                        // B tile layout in smem: [tile8][kstep][khalf][8 rows][16 B]
-                        const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
-                        const bool first = (c == 0 && h == 0);
-#pragma unroll
-                        for (int sl = 0; sl < 2 * P; ++sl)
-                            tc_mma_i8(acc_base + (uint32_t)((sl >> 1) * um::NTOK), a_base + as * S::ACOLS + sl * 8,
-                                      bdesc, idesc, (!first || (sl & 1)) ? 1u : 0u);
-                        tc_commit(u_smem(&aempty_bar[wg][as]));
-                        if (h == 1) tc_commit(u_smem(&empty_bar[s]));
-                        if (h == 1 && c == n_chunks - 1) tc_commit(u_smem(&accfull_bar));
-                    }
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t x = wv[q] ^ 0x88888888u;
+                    sel[2 * q] = wv[q];
+                    sel[2 * q + 1] = wv[q] >> 16;
+                    xsel[2 * q] = x;
+                    xsel[2 * q + 1] = x >> 16;
                 }
+                const uint32_t abase = tmem + lane_addr + a_col0 + as * S::ACOLS;
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    uint32_t v[16];
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc) {
+                        v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ sign garbage)
+                        v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
+                    }
+                    tc_st16(abase + p * 16, v);
+                }
+                tc_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) u_bar_arrive(u_smem(&afull_bar[as]));
             }
-            // ---- epilogue of this pass: (wg0 + wg1) accumulators -> fp32 out
+            // ---- epilogue of this pass: accumulators -> fp32 out (warpgroup wg: columns 8wg..8wg+7)
             u_bar_wait(u_smem(&accfull_bar), pass & 1);
             tc_fence_after();
-            const int cb = wg * 16;  // each warpgroup converts 16 token columns
+            const int cb = wg * 8;
             if (cb < n) {
                 uint32_t acc[P][16];
 #pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    uint32_t t0[16], t1[16];
-                    tc_ld16(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), t0);
-                    tc_ld16(tmem + lane_addr + (uint32_t)((P + p) * um::NTOK + cb), t1);
-                    tc_wait_ld();
+                for (int p = 0; p < P; ++p) tc_ld8(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), acc[p]);
+                tc_wait_ld();
 #pragma unroll
-                    for (int c2 = 0; c2 < 16; ++c2) acc[p][c2] = (uint32_t)((int32_t)t0[c2] + (int32_t)t1[c2]);
-                }
-#pragma unroll
-                for (int c2 = 0; c2 < 16; ++c2) {
+                for (int c2 = 0; c2 < 8; ++c2) {
                     const int64_t tok = j0 * 8 + cb + c2;
                     if (tok < rb || tok >= re) continue;
                     const float v = (float)(um_combine<P>(acc, c2) * (double)rscale);

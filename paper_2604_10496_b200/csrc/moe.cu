@@ -69,6 +69,71 @@ __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, 
     for (int64_t j = threadIdx.x; j < ff; j += blockDim.x) codes[row * ff + j] = a4_code(ar[j], s);
 }
 
+// Same, register-resident: 512 threads x V float4 cover the row (ff % 4 == 0,
+// ff <= 8192 V), so a and b are read once with 16-byte loads and h never
+// round-trips through memory before it is quantized.
+template <int V>
+__global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__ a, const float *__restrict__ b,
+                                                              int64_t ff, int8_t *__restrict__ codes,
+                                                              float *__restrict__ scales) {
+    const int64_t row = blockIdx.x;
+    float4 *ar = reinterpret_cast<float4 *>(a + row * ff);
+    const float4 *br = reinterpret_cast<const float4 *>(b + row * ff);
+    const int nv = (int)(ff >> 2);
+    float4 h[V];
+    float mx = 0.0f;
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+        const int j = threadIdx.x + u * 512;
+        if (j < nv) {
+            const float4 x = ar[j], y = br[j];
+            h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
+                               __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
+            ar[j] = h[u];
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
+        }
+    }
+    __shared__ float red[16];
+    __shared__ float s_sh;
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float m = threadIdx.x < 16 ? red[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0) {
+            s_sh = a4_scale(m);
+            scales[row] = s_sh;
+        }
+    }
+    __syncthreads();
+    const float s = s_sh;
+    char4 *cr = reinterpret_cast<char4 *>(codes + row * ff);
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+        const int j = threadIdx.x + u * 512;
+        if (j < nv) cr[j] = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+    }
+}
+
+cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
+                     cudaStream_t st) {
+    if (rows == 0) return CQ_OK;
+    const int64_t v = ceil_div(ff / 4, 512);
+    if (ff % 4 == 0 && v <= 8) {
+        switch (v) {
+            case 1: silu_quant_vec_kernel<1><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
+            case 2: silu_quant_vec_kernel<2><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
+            case 3:
+            case 4: silu_quant_vec_kernel<4><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
+            default: silu_quant_vec_kernel<8><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
+        }
+    } else {
+        silu_quant_kernel<<<(unsigned)rows, 256, 0, st>>>(a, b, ff, codes, scales);
+    }
+    return check_launch("silu_quant");
+}
+
 // --- ordered grouped GEMM (GPU oracle path): bit-exact chains per segment.
 constexpr int OG_ROWS = 8, OG_TOK = 32, OG_J = 64;
 
@@ -314,8 +379,7 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
         float *bbuf = hidden + rows * ff;
         CQ_TRY(lut_umma_grouped(codes, reinterpret_cast<int8_t *>(frag_in), scales, offsets, n_seg, seg_first, rows,
                                 &gate, hidden, &up, bbuf, d, ff, st));
-        silu_quant_kernel<<<(unsigned)rows, 256, 0, st>>>(hidden, bbuf, ff, hcodes, hscales);
-        CQ_TRY(check_launch("silu_quant"));
+        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, st));
         return lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
                                 &down, fout, nullptr, nullptr, ff, d, st);
     }

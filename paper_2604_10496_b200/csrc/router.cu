@@ -44,6 +44,66 @@ __global__ void router_logits_kernel(const int8_t *__restrict__ codes, const flo
     if (live) logits[t * n_exp + e] = acc;
 }
 
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+
+// Same chains, with the W / code chunks double-buffered by cp.async so the
+// next chunk lands while the current one is consumed (d % 16 == 0 and
+// rk * E % 4 == 0; the kernel above covers every other shape).
+__global__ void router_logits_async_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
+                                           const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp, int rk,
+                                           float *__restrict__ logits) {
+    extern __shared__ __align__(16) float rsm[];
+    const int tt_n = blockDim.x / (int)n_exp;
+    const int wsz = rk * (int)n_exp, csz = tt_n * rk;  // floats of W, bytes of codes per buffer
+    float *wbuf[2] = {rsm, rsm + wsz};
+    int8_t *cbuf[2] = {reinterpret_cast<int8_t *>(rsm + 2 * wsz), reinterpret_cast<int8_t *>(rsm + 2 * wsz) + csz};
+    const int t_loc = threadIdx.x / (int)n_exp, e = threadIdx.x % (int)n_exp;
+    const int64_t t0 = blockIdx.x * (int64_t)tt_n;
+    const int64_t t = t0 + t_loc;
+    const bool live = t_loc < tt_n && t < n;
+    const float s = live ? __ldg(scales + t) : 0.0f;
+    const int n_chunks = (int)((d + rk - 1) / rk);
+    auto load = [&](int ci, int b) {
+        const int64_t k0 = (int64_t)ci * rk;
+        const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
+        for (int x = threadIdx.x * 4; x < kn * n_exp; x += blockDim.x * 4) cp_async16(wbuf[b] + x, w + k0 * n_exp + x);
+        const int rowv = kn / 16;
+        for (int x = threadIdx.x; x < tt_n * rowv; x += blockDim.x) {
+            const int tl = x / rowv, v = x - tl * rowv;
+            const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // clamp: rows past n are never consumed
+            cp_async16(cbuf[b] + tl * rk + v * 16, codes + tg * d + k0 + v * 16);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    load(0, 0);
+    float acc = 0.0f;
+    for (int ci = 0; ci < n_chunks; ++ci) {
+        const int b = ci & 1;
+        if (ci + 1 < n_chunks) {
+            load(ci + 1, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const int64_t k0 = (int64_t)ci * rk;
+        const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
+        if (live) {
+            const int8_t *cr = cbuf[b] + t_loc * rk;
+            const float *wr = wbuf[b] + e;
+#pragma unroll 8
+            for (int kk = 0; kk < kn; ++kk)
+                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)cr[kk], s), wr[kk * n_exp]));
+        }
+        __syncthreads();  // buffer b is refilled by the next iteration's prefetch
+    }
+    if (live) logits[t * n_exp + e] = acc;
+}
+
 // numpy's float32 sum of a short row: a plain loop below 8 elements, eight
 // interleaved partial sums combined as a tree from 8 up (pairwise_sum).
 __device__ __forceinline__ float np_sum(const float *v, int n) {
@@ -186,6 +246,14 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *w
         return CQ_ERR_CONFIG;
     }
     const int tt = (int)(256 / n_exp);
+    if (d % 16 == 0) {
+        // double-buffered W chunk [rk][E] f32 + codes [tt][rk] i8 in <= 48 KB of shared memory
+        const int rk = (int)std::max<int64_t>(16, std::min<int64_t>(256, (24576 / (4 * n_exp + tt)) & ~15LL));
+        const size_t smem = 2 * ((size_t)rk * n_exp * sizeof(float) + (size_t)tt * rk);
+        router_logits_async_kernel<<<(unsigned)ceil_div(n, tt), (unsigned)(tt * n_exp), smem, st>>>(
+            codes, scales, w, n, d, n_exp, rk, logits);
+        return check_launch("router_logits");
+    }
     // W chunk [rk][E] + inputs [tt][rk] in <= 48 KB of shared memory
     const int rk = (int)std::max<int64_t>(16, std::min<int64_t>(256, (12288 / (n_exp + tt)) & ~15LL));
     const size_t smem = ((size_t)rk * n_exp + (size_t)tt * rk) * sizeof(float);
