@@ -340,6 +340,28 @@ __global__ void lut8_kernel(const float *__restrict__ cent, const float *__restr
     }
 }
 
+// Unsigned variant for the tcgen05 kernel: m = rint(c / rowscale) in
+// [-(2^(7P-1)-1), 2^(7P-1)-1] is stored biased, u = m + 2^(7P-1), as P base-128
+// digits in [0, 127].  Every table byte then has its sign bit clear, so the
+// sign-replicated half of each PRMT pair is exactly zero and the two halves
+// merge with one OR; the bias returns in the epilogue as 2^(7P-1) * sum_j q_j.
+__global__ void lut7_kernel(const float *__restrict__ cent, const float *__restrict__ rowscale, int64_t rows,
+                            int64_t n_groups, int planes, int8_t *__restrict__ lut) {
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (x >= rows * n_groups) return;
+    const int64_t row = x / n_groups, grp = x - row * n_groups;
+    const double s = (double)rowscale[row];
+    const long long bias = 1LL << (7 * planes - 1), mb = bias - 1;
+    const int64_t tile = row / 16, r16 = row % 16;
+    int8_t *dst = lut + ((tile * n_groups + grp) * 16 + r16) * planes * 16;
+    for (int c = 0; c < 16; ++c) {
+        long long m = llrint((double)cent[x * 16 + c] / s);
+        m = m > mb ? mb : (m < -mb ? -mb : m);
+        const long long u = m + bias;
+        for (int p = 0; p < planes; ++p) dst[p * 16 + c] = (int8_t)((u >> (7 * p)) & 127);
+    }
+}
+
 // ids (rows, d_in/2) -> [tile][chunk][h][lane][16 B]: lane (g, t), sub-chunk
 // s = 2h + {0,1}: w0 = sel(g, 32s+4t) | sel(g+8, 32s+4t) << 16,
 //                 w1 = sel(g, 32s+16+4t) | sel(g+8, 32s+16+4t) << 16,
@@ -440,7 +462,7 @@ cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_
                            const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
                            cudaStream_t);
 bool umma_ok(int64_t d_in, int64_t d_out, int64_t g);
-int64_t umma_b_tiles(int64_t rows);
+int64_t umma_b_bytes(int64_t rows, int64_t d_in);
 
 cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int64_t d_in, int64_t g, int64_t planes,
                        int64_t layout, uint8_t *tc_ids, int8_t *tc_lut, float *rowscale, cudaStream_t st) {
@@ -454,19 +476,23 @@ cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int6
     }
     if (rows == 0) return CQ_OK;
     const int64_t n_groups = d_in / g;
-    const int64_t mb = planes == 3 ? TC_M3 : TC_M2;
+    const bool um = layout == CQ_TC_UMMA128;  // unsigned base-128 digits (lut7_kernel)
+    const int64_t mb = um ? (1LL << (7 * planes - 1)) - 1 : (planes == 3 ? TC_M3 : TC_M2);
     rowscale_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(cent, rows, n_groups * 16,
                                                                  (double)mb, rowscale);
     CQ_TRY(check_launch("rowscale"));
     int8_t *lut16 = tc_lut;
-    if (layout == CQ_TC_UMMA128) {
+    if (um) {
         if (cudaMallocAsync(&lut16, rows * n_groups * planes * 16, st) != cudaSuccess) {
             set_error("lut8_prepare: scratch alloc failed");
             return CQ_ERR_CUDA;
         }
+        lut7_kernel<<<(unsigned)ceil_div(rows * n_groups, 128), 128, 0, st>>>(cent, rowscale, rows, n_groups,
+                                                                            (int)planes, lut16);
+    } else {
+        lut8_kernel<<<(unsigned)ceil_div(rows * n_groups, 128), 128, 0, st>>>(cent, rowscale, rows, n_groups,
+                                                                            (int)planes, mb, lut16);
     }
-    lut8_kernel<<<(unsigned)ceil_div(rows * n_groups, 128), 128, 0, st>>>(cent, rowscale, rows, n_groups, (int)planes,
-                                                                        mb, lut16);
     CQ_TRY(check_launch("lut8"));
     if (layout == CQ_TC_UMMA128) {
         cq_status rc = umma_prepare(ids, lut16, rows, d_in, g, planes, tc_ids, tc_lut, st);
@@ -512,7 +538,7 @@ extern "C" cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, co
     site.tc_planes = planes;
     site.tc_layout = layout;
     void *scratch = nullptr;
-    const int64_t frag_bytes = (layout == CQ_TC_UMMA128 ? umma_b_tiles(n) : ceil_div(n, 8)) * 8 * d_in;
+    const int64_t frag_bytes = layout == CQ_TC_UMMA128 ? umma_b_bytes(n, d_in) : ceil_div(n, 8) * 8 * d_in;
     if (cudaMallocAsync(&scratch, frag_bytes + 256, st) != cudaSuccess) {
         set_error("lut_gemm_tc: scratch alloc failed");
         return CQ_ERR_CUDA;

@@ -1,34 +1,44 @@
 // tcgen05 LUT GEMM: codebook rows expanded by PRMT into int8 digit planes and
 // written straight into TMEM as the MMA's A operand (kind::i8, A from TMEM),
 // activation codes staged in shared memory by bulk copies as the B operand,
-// exact int32 accumulators in TMEM.  Same numerics as lut_tc.cu (digit planes,
-// sign-garbage-compensated 16-entry byte LUTs — see that file's header); this
-// kernel removes the legacy mma.sync issue cost, which capped the register-
-// operand version at ~30% of HBM bandwidth (profiles/README.md).
+// exact int32 accumulators in TMEM.
+//
+// Numerics.  Each weight row's centroids are integers m = rint(c / rowscale),
+// |m| < 2^(7P-1), stored biased (u = m + 2^(7P-1)) as P unsigned base-128
+// digits (cq_lut8_prepare, lut7_kernel): 3 planes (21 bits of the row max)
+// where the GEMM output is re-quantized (gate, up), 2 (14 bits) for down.
+// Codes are exact int8, each plane's GEMM is an exact s8 x s8 -> s32 MMA, and
+//   y[t,i] = s_t * rowscale_i * (sum_p 128^p S_p[t,i] - 2^(7P-1) * sum_j q[t,j]).
+//
+// Lookup.  A (row, group) codebook plane is a 16-entry byte table in 4
+// registers.  Four consecutive packed ids are exactly a `prmt.b32` selector
+// (two ids per byte, low nibble first, lutgemm.py:111-116); ids 8..15 set the
+// selector's sign-replicate bit, so prmt(entries 0..7, sel) | prmt(entries
+// 8..15, sel ^ 0x8888) is the lookup: every table byte has its sign bit clear,
+// so the replicated "sign" of the other half is exactly zero.  3 ALU ops per
+// 4 weights per plane.
 //
 // CTA = one 128-row weight tile of one expert matrix x token passes of <= 32
-// tokens, warp-specialised (18 warps, one CTA per SM: it owns all 512 TMEM
-// columns):
+// tokens (MMA N = 16 or 32), warp-specialised, one CTA per SM (it owns all
+// 512 TMEM columns):
 //   warps 0-15 expanders, 4 warpgroups: warp w owns TMEM lane quarter w%4
-//              (= 32 rows) and warpgroup w/4 expands k-step w/4 of every
-//              128-column chunk.  A thread turns the 32 ids of its row into
-//              P planes x {lo,hi} halves x 8 columns (2P PRMT per 4 ids) and
-//              tcgen05.st's them into its warpgroup's A stage; four warpgroups
-//              in flight hide the TMEM store latency (tcgen05.wait::st).
+//              (= 32 rows); warpgroup w/4 expands k-step w/4 of every
+//              128-column chunk into its own A stages (tcgen05.st).  Four
+//              warpgroups in flight hide the TMEM store latency.
 //   warp 16    producer: cp.async.bulk of ids (8 KB per chunk), the group's LUT
-//              block and the activation tile into a 4-deep smem ring.
-//   warp 17    MMA issuer: one thread, 2P tcgen05.mma per k-step (M=128,
-//              N=16|32, K=32) into P int32 accumulators; commits free the A
-//              stage, the smem stage and finally signal the epilogue.
-// Epilogue: expanders tcgen05.ld the P accumulators (8 token columns per
-// warpgroup), combine digits (sum 255^p S_p), scale by the row scale and the
-// token scale, store fp32.
+//              block and the activation tile into an 8-deep smem ring.
+//   warp 17    MMA issuer: one thread, P tcgen05.mma per k-step (M=128, N,
+//              K=32).  Small-N MMAs into one accumulator serialise on the MMA
+//              latency, so k-step ks accumulates into set ks % SETS; the
+//              epilogue adds the sets (exact int32).
+// Epilogue: expanders tcgen05.ld, add sets, combine digits, remove the bias,
+// scale by the row scale and the token scale, store fp32.
 #include "common.cuh"
 
 namespace cq {
 
 namespace um {
-constexpr int STAGES = 4;        // smem ring depth (128-column chunks)
+constexpr int STAGES = 8;        // smem ring depth (128-column chunks)
 constexpr int NTOK = 32;         // max tokens per pass (MMA N)
 constexpr int IDS = 128 * 64;    // ids bytes per chunk: 128 rows x 128 columns / 2
 constexpr int BTILE = 1024;      // activation bytes per 8-token tile per chunk
@@ -43,9 +53,11 @@ struct UmStage {
     static constexpr int LUT = 128 * P * 16;
     static constexpr int B = (um::NTOK / 8) * um::BTILE;
     static constexpr int BYTES = um::IDS + LUT + B;
-    static constexpr int ACOLS = 2 * P * 8;                        // TMEM columns per A stage (one k-step)
-    static constexpr int ACC = P * um::NTOK;                       // accumulators: P planes x N
+    static constexpr int ACOLS = P * 8;                          // TMEM columns per A stage (one k-step)
+    static constexpr int SETS = P == 3 ? 3 : 4;                  // rotating accumulator sets
+    static constexpr int ACC = SETS * P * um::NTOK;              // accumulator columns
     static constexpr int AS = (um::TMEM_COLS - ACC) / ACOLS / um::WG;  // A stages per warpgroup
+    static_assert(AS >= 2, "TMEM budget");
 };
 
 // ---------------------------------------------------------------------------
@@ -100,8 +112,13 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d, uint32_t a, uint64_t bdesc
         : "memory");
 }
 
-// 16 consecutive 32-bit TMEM columns of this thread's lane.
-__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+// 8 consecutive 32-bit TMEM columns of this thread's lane.
+__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t *v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
             taddr),
@@ -109,15 +126,7 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16])
         "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
-__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr)
-        : "memory");
-}
-__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&v)[16]) {
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t *v) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                  : "r"(taddr)
@@ -142,22 +151,14 @@ __device__ __forceinline__ uint32_t idesc_i8(int n) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-template <int P>
-__device__ __forceinline__ double um_combine(const uint32_t (&acc)[P][16], int c) {
-    double s = (double)(int32_t)acc[P - 1][c];
-#pragma unroll
-    for (int p = P - 2; p >= 0; --p) s = s * 255.0 + (double)(int32_t)acc[p][c];
-    return s;
-}
-
 // grid: (d_out / 128, n_seg, n_mat); blockIdx.z picks the matrix (gate / up).
 template <int P>
 __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
-    const int32_t *__restrict__ offsets, int64_t seg_first, const uint8_t *__restrict__ ids0,
-    const int8_t *__restrict__ lut0, const float *__restrict__ rs0, float *__restrict__ out0,
-    const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1, const float *__restrict__ rs1,
-    float *__restrict__ out1, int d_in, int d_out, int g) {
+    const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int64_t seg_first,
+    const uint8_t *__restrict__ ids0, const int8_t *__restrict__ lut0, const float *__restrict__ rs0,
+    float *__restrict__ out0, const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1,
+    const float *__restrict__ rs1, float *__restrict__ out1, int d_in, int d_out, int g) {
     using S = UmStage<P>;
     constexpr int AS = S::AS;
     constexpr int NAS = AS * um::WG;  // A stages in total
@@ -243,23 +244,25 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
             const uint32_t idesc = idesc_i8(((ntc + 1) & ~1) * 8);
             if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
+            uint32_t kp = 0;  // k-step within this pass
             for (int c = 0; c < n_chunks; ++c, ++it) {
                 const int s = it % um::STAGES;
                 u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
                 const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk, ++ks) {
+                for (int kk = 0; kk < 4; ++kk, ++ks, ++kp) {
                     const int as = ks % NAS;
                     u_bar_wait(u_smem(&afull_bar[as]), (ks / NAS) & 1);
                     tc_fence_after();
                     if (lane == 0) {
                         // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
                         const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
-                        const bool first = (c == 0 && kk == 0);
+                        const uint32_t set = kp % S::SETS;
+                        const uint32_t accum = kp >= (uint32_t)S::SETS ? 1u : 0u;  // first use of a set zero-fills
 #pragma unroll
-                        for (int sl = 0; sl < 2 * P; ++sl)
-                            tc_mma_i8(tmem + (uint32_t)((sl >> 1) * um::NTOK), tmem + a_col0 + as * S::ACOLS + sl * 8,
-                                      bdesc, idesc, (!first || (sl & 1)) ? 1u : 0u);
+                        for (int p = 0; p < P; ++p)
+                            tc_mma_i8(tmem + (set * P + p) * um::NTOK, tmem + a_col0 + as * S::ACOLS + p * 8, bdesc,
+                                      idesc, accum);
                         tc_commit(u_smem(&aempty_bar[as]));
                         if (kk == 3) tc_commit(u_smem(&empty_bar[s]));
                         if (kk == 3 && c == n_chunks - 1) tc_commit(u_smem(&accfull_bar));
@@ -284,8 +287,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             int gc = 0;
             for (int c = 0; c < n_chunks; ++c, ++it, ++kq) {
                 const int s = it % um::STAGES;
-                const int as_l = kq % AS;
-                const int as = as_l * um::WG + wg;  // global A stage = ks % NAS with ks = 4 * chunk + wg
+                const int as = (kq % AS) * um::WG + wg;  // global A stage = ks % NAS, ks = 4 * chunk + wg
                 if (kq >= AS) u_bar_wait(u_smem(&aempty_bar[as]), ((kq / AS) - 1) & 1);
                 u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
                 tc_fence_after();
@@ -307,37 +309,51 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     xsel[2 * q] = x;
                     xsel[2 * q + 1] = x >> 16;
                 }
+                uint32_t v[P * 8];
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc)
+                        v[p * 8 + cc] = u_prmt(L[p].x, L[p].y, sel[cc]) | u_prmt(L[p].z, L[p].w, xsel[cc]);
                 const uint32_t abase = tmem + lane_addr + a_col0 + as * S::ACOLS;
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    uint32_t v[16];
-#pragma unroll
-                    for (int cc = 0; cc < 8; ++cc) {
-                        v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ sign garbage)
-                        v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
-                    }
-                    tc_st16(abase + p * 16, v);
-                }
+                tc_st16(abase, v);
+                if (P == 3) tc_st8(abase + 16, v + 16);
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(u_smem(&afull_bar[as]));
             }
-            // ---- epilogue of this pass: accumulators -> fp32 out (warpgroup wg: columns 8wg..8wg+7)
+            // ---- epilogue of this pass: accumulators -> fp32 out (warpgroup wg: token columns 8wg..8wg+7)
             u_bar_wait(u_smem(&accfull_bar), pass & 1);
             tc_fence_after();
             const int cb = wg * 8;
             if (cb < n) {
-                uint32_t acc[P][16];
+                int32_t acc[P][8];
 #pragma unroll
-                for (int p = 0; p < P; ++p) tc_ld8(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), acc[p]);
-                tc_wait_ld();
+                for (int p = 0; p < P; ++p)
+#pragma unroll
+                    for (int c2 = 0; c2 < 8; ++c2) acc[p][c2] = 0;
+                const int used = n_chunks * 4 < S::SETS ? n_chunks * 4 : S::SETS;
+                for (int set = 0; set < used; ++set) {
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        uint32_t t[8];
+                        tc_ld8(tmem + lane_addr + (uint32_t)((set * P + p) * um::NTOK + cb), t);
+                        tc_wait_ld();
+#pragma unroll
+                        for (int c2 = 0; c2 < 8; ++c2) acc[p][c2] += (int32_t)t[c2];
+                    }
+                }
 #pragma unroll
                 for (int c2 = 0; c2 < 8; ++c2) {
                     const int64_t tok = j0 * 8 + cb + c2;
                     if (tok < rb || tok >= re) continue;
-                    const float v = (float)(um_combine<P>(acc, c2) * (double)rscale);
-                    out[tok * d_out + (int64_t)blockIdx.x * 128 + row] = __fmul_rn(v, __ldg(scales + tok));
+                    double sum = (double)acc[P - 1][c2];
+#pragma unroll
+                    for (int p = P - 2; p >= 0; --p) sum = sum * 128.0 + (double)acc[p][c2];
+                    sum -= (double)(1LL << (7 * P - 1)) * (double)__ldg(qsums + tok);
+                    const float v2 = (float)(sum * (double)rscale);
+                    out[tok * d_out + (int64_t)blockIdx.x * 128 + row] = __fmul_rn(v2, __ldg(scales + tok));
                 }
             }
             tc_fence_before();
@@ -369,6 +385,27 @@ __global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int6
     }
 }
 
+// sums[r] = sum_j codes[r, j] (exact int32): the bias term of the unsigned digits.
+__global__ void row_sums_kernel(const int8_t *__restrict__ codes, int64_t n, int64_t K, int32_t *__restrict__ sums) {
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+    if (row >= n) return;
+    const int8_t *r = codes + row * K;
+    int32_t acc = 0;
+    if ((K & 15) == 0) {
+        for (int64_t j = (threadIdx.x & 31) * 16; j < K; j += 512) {
+            const int4 v = *reinterpret_cast<const int4 *>(r + j);
+            const int w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc = __dp4a(w4[u], 0x01010101, acc);
+        }
+    } else {
+        for (int64_t j = threadIdx.x & 31; j < K; j += 32) acc += r[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sums[row] = acc;
+}
+
 // ids (rows, d_in/2) -> [tile128][chunk][kstep][row][16 B] (the 16 packed bytes of
 // a row's 32 columns are already 8 PRMT selectors, low nibble first).
 __global__ void ids_umma_kernel(const uint8_t *__restrict__ ids, int64_t rows, int64_t d_in, uint4 *__restrict__ out) {
@@ -380,9 +417,9 @@ __global__ void ids_umma_kernel(const uint8_t *__restrict__ ids, int64_t rows, i
     }
 }
 
-// lut16 [rows/16][G][16][P][16] (lut8_kernel layout) -> [rows/128][G][128][P][16].
+// lut16 [rows/16][G][16][P][16] (lut7_kernel layout) -> [rows/128][G][128][P][16].
 __global__ void lut_relayout_kernel(const int8_t *__restrict__ lut16, int64_t rows, int64_t n_groups, int planes,
-                                int8_t *__restrict__ out) {
+                                    int8_t *__restrict__ out) {
     const int64_t per = (int64_t)planes * 16;
     const int64_t total = rows * n_groups;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
@@ -404,21 +441,28 @@ size_t umma_smem() {
     return (size_t)um::STAGES * UmStage<P>::BYTES;
 }
 
-cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, cudaStream_t st) {
+cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, int32_t *sums,
+                    cudaStream_t st) {
     const int64_t total = (K / 128) * tiles * 64;
     if (total == 0) return CQ_OK;
     to_umma_b_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
         codes, n, K, tiles, reinterpret_cast<uint4 *>(dst));
-    return check_launch("to_umma_b");
+    CQ_TRY(check_launch("to_umma_b"));
+    row_sums_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(codes, n, K, sums);
+    return check_launch("row_sums");
 }
 
-// tiles allocated in the B buffer: ceil(rows/8) + 2 (an N=16 MMA may read one tile past the end)
+// B buffer: umma_b_tiles(rows) tiles x d_in bytes (an N=16 MMA may read one
+// tile past the end), followed by the int32 row sums (256-byte aligned).
 int64_t umma_b_tiles(int64_t rows) { return ceil_div(rows, 8) + 2; }
+int64_t umma_b_bytes(int64_t rows, int64_t d_in) {
+    return umma_b_tiles(rows) * 8 * d_in + ceil_div(rows * 4, 256) * 256;
+}
 
 template <int P>
-cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *offsets, int64_t n_seg,
-                      int64_t seg_first, const cq_expert_site *a, float *out_a, const cq_expert_site *b, float *out_b,
-                      int64_t d_in, int64_t d_out, cudaStream_t st) {
+cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *sums,
+                      const int32_t *offsets, int64_t n_seg, int64_t seg_first, const cq_expert_site *a, float *out_a,
+                      const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
     static bool attr = false;
     const size_t smem = umma_smem<P>();
     if (!attr) {
@@ -427,14 +471,14 @@ cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales,
     }
     dim3 grid((unsigned)(d_out / 128), (unsigned)n_seg, b ? 2u : 1u);
     lut_umma_kernel<P><<<grid, um::THREADS, smem, st>>>(
-        bfrag, n_tiles, scales, offsets, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
+        bfrag, n_tiles, scales, sums, offsets, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
         b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, (int)d_in, (int)d_out,
         (int)a->group_size);
     return check_launch("lut_umma");
 }
 
-// Grouped tcgen05 LUT GEMM over segments.  `bbuf` holds umma_b_tiles(rows)
-// tiles x d_in bytes.  With b != nullptr, computes two matrices (gate -> out_a,
+// Grouped tcgen05 LUT GEMM over segments.  `bbuf` holds umma_b_bytes(rows,
+// d_in) bytes.  With b != nullptr, computes two matrices (gate -> out_a,
 // up -> out_b) in one launch.
 cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scales, const int32_t *offsets,
                            int64_t n_seg, int64_t seg_first, int64_t rows, const cq_expert_site *a, float *out_a,
@@ -449,16 +493,19 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         return CQ_ERR_CONFIG;
     }
     const int64_t tiles = umma_b_tiles(rows);
-    CQ_TRY(to_umma_b(codes, rows, d_in, tiles, bbuf, st));
+    int32_t *sums = reinterpret_cast<int32_t *>(bbuf + tiles * 8 * d_in);
+    CQ_TRY(to_umma_b(codes, rows, d_in, tiles, bbuf, sums, st));
     if (a->tc_planes == 3)
-        return launch_umma<3>(bbuf, tiles, scales, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, st);
+        return launch_umma<3>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out,
+                              st);
     if (a->tc_planes == 2)
-        return launch_umma<2>(bbuf, tiles, scales, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, st);
+        return launch_umma<2>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out,
+                              st);
     set_error("tcgen05 path: planes must be 2 or 3");
     return CQ_ERR_CONFIG;
 }
 
-// One-time re-layout for the tcgen05 kernel from the mma16 LUT layout.
+// One-time re-layout for the tcgen05 kernel from the 16-row LUT layout.
 cq_status umma_prepare(const uint8_t *ids, const int8_t *lut16, int64_t rows, int64_t d_in, int64_t g, int64_t planes,
                        uint8_t *tc_ids, int8_t *tc_lut, cudaStream_t st) {
     const int64_t total_ids = (rows / 128) * (d_in / 128) * 4 * 128;

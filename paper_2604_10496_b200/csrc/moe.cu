@@ -33,7 +33,7 @@ bool tc_path_ok(int64_t d_in, int64_t d_out, int64_t g);
 cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
                            const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
                            cudaStream_t);
-int64_t umma_b_tiles(int64_t rows);
+int64_t umma_b_bytes(int64_t rows, int64_t d_in);
 
 // h = silu(a) * b (model.py:396) fused with the per-row A4 re-quantization of
 // h (model.py:397-398, quant.py:89-100): pass 1 forms h in place of a and its
@@ -282,8 +282,8 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_FOUT] = Rh * d * 4;
     sz[CQ_WS_ROTATED] = dsc->rotation ? n * d * 4 : 0;
     sz[CQ_WS_SHARED] = dsc->n_shared > 0 ? n * d * 4 : 0;
-    sz[CQ_WS_CODES_FRAG] = umma_b_tiles(Rh) * 8 * d;     // >= the mma16 fragment size too
-    sz[CQ_WS_HCODES_FRAG] = umma_b_tiles(Rh) * 8 * ff;
+    sz[CQ_WS_CODES_FRAG] = umma_b_bytes(Rh, d);     // >= the mma16 fragment size too
+    sz[CQ_WS_HCODES_FRAG] = umma_b_bytes(Rh, ff);
     int64_t pos = 0;
     for (int b = 0; b < CQ_WS_COUNT_; ++b) {
         if (off) off[b] = pos;

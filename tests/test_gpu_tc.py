@@ -40,12 +40,20 @@ def test_digit_plane_luts_decode_to_centroids(planes, layout):
     rs = pw.tc["rowscale"].cpu().numpy().astype(np.float64)
     G = 512 // 128
     lut = lut.reshape(rows // tr, G, tr, planes, 16).transpose(0, 2, 1, 3, 4).reshape(rows, G, planes, 16)
-    partner = lut[..., np.arange(16) ^ 8]
-    digits = lut + np.where(partner < 0, -1, 0)               # what PRMT(P) + PRMT(Q) deliver
-    assert digits.min() >= -128 and digits.max() <= 126
-    m = np.zeros(digits.shape[:2] + (16,), np.int64)
-    for p in reversed(range(planes)):
-        m = m * 255 + digits[:, :, p, :]
+    m = np.zeros(lut.shape[:2] + (16,), np.int64)
+    if layout == "mma16":
+        # signed base-255 digits, sign garbage pre-compensated: PRMT(P) + PRMT(Q)
+        partner = lut[..., np.arange(16) ^ 8]
+        digits = lut + np.where(partner < 0, -1, 0)
+        assert digits.min() >= -128 and digits.max() <= 126
+        for p in reversed(range(planes)):
+            m = m * 255 + digits[:, :, p, :]
+    else:
+        # unsigned base-128 digits (sign bits clear, so PRMT(P) | PRMT(Q) is exact), biased
+        assert lut.min() >= 0 and lut.max() <= 127
+        for p in reversed(range(planes)):
+            m = m * 128 + lut[:, :, p, :]
+        m -= 1 << (7 * planes - 1)
     rec = m * rs[:, None, None]
     err = np.abs(rec - cent.astype(np.float64)).max(axis=(1, 2))
     assert np.all(err <= rs * 0.5 + 1e-30)
