@@ -113,10 +113,11 @@ typedef struct {
     const int8_t *tc_lut;      /* [E*d_out/16][d_in/g][16 rows][planes][16] int8 digit-plane LUTs */
     const float *tc_rowscale;  /* [E*d_out] */
     int64_t tc_planes;         /* 2 or 3 base-255 digit planes (3 where the output is re-quantized) */
-    int64_t tc_layout;         /* CQ_TC_MMA16 (mma.sync kernel) or CQ_TC_UMMA128 (tcgen05 kernel) */
+    int64_t tc_layout;         /* CQ_TC_MMA16 (mma.sync kernel), CQ_TC_UMMA128 / _UMMA128U (tcgen05
+                                  kernel; signed P/Q digit slices / unsigned OR-merged digits) */
 } cq_expert_site;
 
-enum { CQ_TC_MMA16 = 0, CQ_TC_UMMA128 = 1 };
+enum { CQ_TC_MMA16 = 0, CQ_TC_UMMA128 = 1, CQ_TC_UMMA128U = 2 };
 
 typedef struct {
     int64_t d_model, d_ff, n_experts, top_k;

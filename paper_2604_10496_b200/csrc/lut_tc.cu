@@ -470,23 +470,30 @@ cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int6
         set_error("lut8_prepare: planes must be 2 or 3");
         return CQ_ERR_CONFIG;
     }
-    if (rows % (layout == CQ_TC_UMMA128 ? 128 : 16) || !tc_path_ok(d_in, 16, g)) {
+    if (layout < CQ_TC_MMA16 || layout > CQ_TC_UMMA128U) {
+        set_error("lut8_prepare: unknown layout");
+        return CQ_ERR_CONFIG;
+    }
+    if (rows % (layout == CQ_TC_MMA16 ? 16 : 128) || !tc_path_ok(d_in, 16, g)) {
         set_error("lut8_prepare: needs rows % 16 (mma16) / % 128 (umma128) == 0, d_in % 128 == 0, g % 128 == 0");
         return CQ_ERR_UNSUPPORTED;
     }
     if (rows == 0) return CQ_OK;
     const int64_t n_groups = d_in / g;
-    const bool um = layout == CQ_TC_UMMA128;  // unsigned base-128 digits (lut7_kernel)
+    const bool um = layout == CQ_TC_UMMA128U;  // unsigned base-128 digits (lut7_kernel)
     const int64_t mb = um ? (1LL << (7 * planes - 1)) - 1 : (planes == 3 ? TC_M3 : TC_M2);
     rowscale_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(cent, rows, n_groups * 16,
                                                                  (double)mb, rowscale);
     CQ_TRY(check_launch("rowscale"));
     int8_t *lut16 = tc_lut;
-    if (um) {
+    const bool relayout = layout == CQ_TC_UMMA128 || layout == CQ_TC_UMMA128U;
+    if (relayout) {
         if (cudaMallocAsync(&lut16, rows * n_groups * planes * 16, st) != cudaSuccess) {
             set_error("lut8_prepare: scratch alloc failed");
             return CQ_ERR_CUDA;
         }
+    }
+    if (um) {
         lut7_kernel<<<(unsigned)ceil_div(rows * n_groups, 128), 128, 0, st>>>(cent, rowscale, rows, n_groups,
                                                                             (int)planes, lut16);
     } else {
@@ -494,7 +501,7 @@ cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int6
                                                                             (int)planes, mb, lut16);
     }
     CQ_TRY(check_launch("lut8"));
-    if (layout == CQ_TC_UMMA128) {
+    if (relayout) {
         cq_status rc = umma_prepare(ids, lut16, rows, d_in, g, planes, tc_ids, tc_lut, st);
         cudaFreeAsync(lut16, st);
         return rc;
@@ -538,7 +545,8 @@ extern "C" cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, co
     site.tc_planes = planes;
     site.tc_layout = layout;
     void *scratch = nullptr;
-    const int64_t frag_bytes = layout == CQ_TC_UMMA128 ? umma_b_bytes(n, d_in) : ceil_div(n, 8) * 8 * d_in;
+    const bool um = layout == CQ_TC_UMMA128 || layout == CQ_TC_UMMA128U;
+    const int64_t frag_bytes = um ? umma_b_bytes(n, d_in) : ceil_div(n, 8) * 8 * d_in;
     if (cudaMallocAsync(&scratch, frag_bytes + 256, st) != cudaSuccess) {
         set_error("lut_gemm_tc: scratch alloc failed");
         return CQ_ERR_CUDA;
@@ -546,7 +554,7 @@ extern "C" cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, co
     int32_t *off = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(scratch) + frag_bytes);
     tc_single_segment_kernel<<<1, 1, 0, st>>>(off, n);
     cq_status rc = check_launch("single_segment");
-    if (rc == CQ_OK && layout == CQ_TC_UMMA128)
+    if (rc == CQ_OK && um)
         rc = lut_umma_grouped(codes, reinterpret_cast<int8_t *>(scratch), scales, off, 1, 0, n, &site, out, nullptr,
                               nullptr, d_in, d_out, st);
     else if (rc == CQ_OK)

@@ -3,20 +3,25 @@
 // activation codes staged in shared memory by bulk copies as the B operand,
 // exact int32 accumulators in TMEM.
 //
-// Numerics.  Each weight row's centroids are integers m = rint(c / rowscale),
-// |m| < 2^(7P-1), stored biased (u = m + 2^(7P-1)) as P unsigned base-128
-// digits (cq_lut8_prepare, lut7_kernel): 3 planes (21 bits of the row max)
-// where the GEMM output is re-quantized (gate, up), 2 (14 bits) for down.
-// Codes are exact int8, each plane's GEMM is an exact s8 x s8 -> s32 MMA, and
-//   y[t,i] = s_t * rowscale_i * (sum_p 128^p S_p[t,i] - 2^(7P-1) * sum_j q[t,j]).
+// Numerics.  Each weight row's centroids are integers m = rint(c / rowscale)
+// written as P int8 digit planes: 3 planes where the GEMM output is
+// re-quantized (gate, up), 2 for down.  Codes are exact int8 and each plane's
+// GEMM is an exact s8 x s8 -> s32 MMA; planes are combined in the epilogue.
 //
 // Lookup.  A (row, group) codebook plane is a 16-entry byte table in 4
 // registers.  Four consecutive packed ids are exactly a `prmt.b32` selector
 // (two ids per byte, low nibble first, lutgemm.py:111-116); ids 8..15 set the
-// selector's sign-replicate bit, so prmt(entries 0..7, sel) | prmt(entries
-// 8..15, sel ^ 0x8888) is the lookup: every table byte has its sign bit clear,
-// so the replicated "sign" of the other half is exactly zero.  3 ALU ops per
-// 4 weights per plane.
+// selector's sign-replicate bit, so prmt(entries 0..7, sel) and prmt(entries
+// 8..15, sel ^ 0x8888) each give the right bytes for their half and a
+// replicated sign byte for the other.  Two digit formats (layouts):
+//   CQ_TC_UMMA128  (default) signed base-255 digits in [-128, 126], the sign
+//      garbage pre-compensated per (a, a+8) pair (lut8_kernel): both PRMT
+//      halves go through the MMA as separate K-slices whose sum is the lookup.
+//      2 ALU ops per 4 weights per plane; 2P MMAs per k-step.
+//   CQ_TC_UMMA128U unsigned base-128 digits, biased by 2^(7P-1) (lut7_kernel):
+//      sign bits clear, so the halves merge with one OR (3 ALU ops per 4
+//      weights per plane, P MMAs per k-step), and the bias returns in the
+//      epilogue as 2^(7P-1) * sum_j q[t,j].
 //
 // CTA = one 128-row weight tile of one expert matrix x token passes of <= 32
 // tokens (MMA N = 16 or 32), warp-specialised, one CTA per SM (it owns all
@@ -27,12 +32,13 @@
 //              warpgroups in flight hide the TMEM store latency.
 //   warp 16    producer: cp.async.bulk of ids (8 KB per chunk), the group's LUT
 //              block and the activation tile into an 8-deep smem ring.
-//   warp 17    MMA issuer: one thread, P tcgen05.mma per k-step (M=128, N,
-//              K=32).  Small-N MMAs into one accumulator serialise on the MMA
-//              latency, so k-step ks accumulates into set ks % SETS; the
-//              epilogue adds the sets (exact int32).
-// Epilogue: expanders tcgen05.ld, add sets, combine digits, remove the bias,
-// scale by the row scale and the token scale, store fp32.
+//   warp 17    MMA issuer: the whole warp runs the loop converged and
+//              elect.sync picks the issuing lane inside the asm (a divergent
+//              `if (lane == 0)` issue costs ~200 cycles per MMA, converged
+//              ~18: profiles/microbench/umma_probe.cu).  2P (or P) MMAs of
+//              M=128, N=16|32, K=32 per k-step into P int32 accumulators.
+// Epilogue: expanders tcgen05.ld the accumulators, combine the digits, scale
+// by the row scale and the token scale, store fp32.
 #include "common.cuh"
 
 namespace cq {
@@ -48,14 +54,14 @@ constexpr int THREADS = WARPS * 32;
 constexpr uint32_t TMEM_COLS = 512;
 }  // namespace um
 
-template <int P>
+template <int P, bool MERGED>
 struct UmStage {
     static constexpr int LUT = 128 * P * 16;
     static constexpr int B = (um::NTOK / 8) * um::BTILE;
     static constexpr int BYTES = um::IDS + LUT + B;
-    static constexpr int ACOLS = P * 8;                          // TMEM columns per A stage (one k-step)
-    static constexpr int SETS = P == 3 ? 3 : 4;                  // rotating accumulator sets
-    static constexpr int ACC = SETS * P * um::NTOK;              // accumulator columns
+    static constexpr int SLICES = MERGED ? P : 2 * P;            // MMA K-slices per k-step
+    static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per A stage (one k-step)
+    static constexpr int ACC = P * um::NTOK;                     // accumulator columns
     static constexpr int AS = (um::TMEM_COLS - ACC) / ACOLS / um::WG;  // A stages per warpgroup
     static_assert(AS >= 2, "TMEM budget");
 };
@@ -94,6 +100,22 @@ __device__ __forceinline__ void u_bulk(uint32_t dst, const void *src, uint32_t b
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// Warp-converged variants: every lane calls, one elected lane acts (a divergent
+// `if (lane == 0)` around async-proxy instructions costs ~200 cycles each).
+__device__ __forceinline__ void u_bar_expect_elect(uint32_t bar, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void u_bulk_elect(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -102,13 +124,21 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
                  : "memory");
 }
 
-// D[tmem d] (+)= A[tmem a] x B[smem desc], kind::i8, 128 x N x 32.
+// D[tmem d] (+)= A[tmem a] x B[smem desc], kind::i8, 128 x N x 32.  Called by a
+// whole converged warp; one elected lane issues.
 __device__ __forceinline__ void tc_mma_i8(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(d),
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(d),
         "r"(a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0u)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
         : "memory");
 }
 
@@ -152,14 +182,14 @@ __device__ __forceinline__ uint32_t idesc_i8(int n) {
 }
 
 // grid: (d_out / 128, n_seg, n_mat); blockIdx.z picks the matrix (gate / up).
-template <int P>
+template <int P, bool MERGED>
 __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
     const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int64_t seg_first,
     const uint8_t *__restrict__ ids0, const int8_t *__restrict__ lut0, const float *__restrict__ rs0,
     float *__restrict__ out0, const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1,
     const float *__restrict__ rs1, float *__restrict__ out1, int d_in, int d_out, int g) {
-    using S = UmStage<P>;
+    using S = UmStage<P, MERGED>;
     constexpr int AS = S::AS;
     constexpr int NAS = AS * um::WG;  // A stages in total
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -211,8 +241,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int n_pass = (int)((j_last - j_first + TPP) / TPP);
 
     if (warp == um::PROD_WARP) {
-        // ------------------------------------------------------------ producer
-        if (lane == 0) {
+        // ------------------------------------------------------------ producer (converged warp, elected lane)
+        {
             uint32_t it = 0;
             for (int pass = 0; pass < n_pass; ++pass) {
                 const int64_t j0 = j_first + (int64_t)pass * TPP;
@@ -226,48 +256,46 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     const bool new_group = gc == 0;
                     const uint32_t bar = u_smem(&full_bar[s]);
                     const uint32_t dst = u_smem(smem + (size_t)s * S::BYTES);
-                    u_bar_expect(bar, um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE);
-                    u_bulk(dst, ids + ((size_t)tile * n_chunks + c) * um::IDS, um::IDS, bar);
+                    u_bar_expect_elect(bar, um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE);
+                    u_bulk_elect(dst, ids + ((size_t)tile * n_chunks + c) * um::IDS, um::IDS, bar);
                     if (new_group)
-                        u_bulk(dst + um::IDS, lut + ((size_t)tile * n_groups + c / cpg) * S::LUT, S::LUT, bar);
-                    u_bulk(dst + um::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + j0) * um::BTILE, ntc16 * um::BTILE,
-                           bar);
+                        u_bulk_elect(dst + um::IDS, lut + ((size_t)tile * n_groups + c / cpg) * S::LUT, S::LUT, bar);
+                    u_bulk_elect(dst + um::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + j0) * um::BTILE,
+                                 ntc16 * um::BTILE, bar);
                     if (++gc == cpg) gc = 0;
                 }
             }
         }
     } else if (warp == um::MMA_WARP) {
-        // ------------------------------------------------------------ MMA issuer (one thread)
+        // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
         uint32_t it = 0, ks = 0;
         for (int pass = 0; pass < n_pass; ++pass) {
             const int64_t j0 = j_first + (int64_t)pass * TPP;
             const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
             const uint32_t idesc = idesc_i8(((ntc + 1) & ~1) * 8);
             if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
-            uint32_t kp = 0;  // k-step within this pass
             for (int c = 0; c < n_chunks; ++c, ++it) {
                 const int s = it % um::STAGES;
                 u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
                 const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk, ++ks, ++kp) {
+                for (int kk = 0; kk < 4; ++kk, ++ks) {
                     const int as = ks % NAS;
                     u_bar_wait(u_smem(&afull_bar[as]), (ks / NAS) & 1);
                     tc_fence_after();
-                    if (lane == 0) {
-                        // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
-                        const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
-                        const uint32_t set = kp % S::SETS;
-                        const uint32_t accum = kp >= (uint32_t)S::SETS ? 1u : 0u;  // first use of a set zero-fills
+                    // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
+                    const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
+                    const uint32_t abase = tmem + a_col0 + (uint32_t)(as * S::ACOLS);
+                    const uint32_t first = (c == 0 && kk == 0) ? 1u : 0u;
 #pragma unroll
-                        for (int p = 0; p < P; ++p)
-                            tc_mma_i8(tmem + (set * P + p) * um::NTOK, tmem + a_col0 + as * S::ACOLS + p * 8, bdesc,
-                                      idesc, accum);
-                        tc_commit(u_smem(&aempty_bar[as]));
-                        if (kk == 3) tc_commit(u_smem(&empty_bar[s]));
-                        if (kk == 3 && c == n_chunks - 1) tc_commit(u_smem(&accfull_bar));
+                    for (int sl = 0; sl < S::SLICES; ++sl) {
+                        const int p = MERGED ? sl : (sl >> 1);
+                        const uint32_t accum = (first && (MERGED || !(sl & 1))) ? 0u : 1u;
+                        tc_mma_i8(tmem + (uint32_t)(p * um::NTOK), abase + (uint32_t)(sl * 8), bdesc, idesc, accum);
                     }
-                    __syncwarp();
+                    tc_commit_elect(u_smem(&aempty_bar[as]));
+                    if (kk == 3) tc_commit_elect(u_smem(&empty_bar[s]));
+                    if (kk == 3 && c == n_chunks - 1) tc_commit_elect(u_smem(&accfull_bar));
                 }
             }
         }
@@ -309,15 +337,28 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     xsel[2 * q] = x;
                     xsel[2 * q + 1] = x >> 16;
                 }
-                uint32_t v[P * 8];
-#pragma unroll
-                for (int p = 0; p < P; ++p)
-#pragma unroll
-                    for (int cc = 0; cc < 8; ++cc)
-                        v[p * 8 + cc] = u_prmt(L[p].x, L[p].y, sel[cc]) | u_prmt(L[p].z, L[p].w, xsel[cc]);
                 const uint32_t abase = tmem + lane_addr + a_col0 + as * S::ACOLS;
-                tc_st16(abase, v);
-                if (P == 3) tc_st8(abase + 16, v + 16);
+                if (MERGED) {
+                    uint32_t v[P * 8];
+#pragma unroll
+                    for (int p = 0; p < P; ++p)
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc)
+                            v[p * 8 + cc] = u_prmt(L[p].x, L[p].y, sel[cc]) | u_prmt(L[p].z, L[p].w, xsel[cc]);
+                    tc_st16(abase, v);
+                    if (P == 3) tc_st8(abase + 16, v + 16);
+                } else {
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        uint32_t v[16];
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc) {
+                            v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ compensated sign byte)
+                            v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
+                        }
+                        tc_st16(abase + p * 16, v);
+                    }
+                }
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -328,30 +369,19 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             tc_fence_after();
             const int cb = wg * 8;
             if (cb < n) {
-                int32_t acc[P][8];
+                uint32_t acc[P][8];
 #pragma unroll
-                for (int p = 0; p < P; ++p)
-#pragma unroll
-                    for (int c2 = 0; c2 < 8; ++c2) acc[p][c2] = 0;
-                const int used = n_chunks * 4 < S::SETS ? n_chunks * 4 : S::SETS;
-                for (int set = 0; set < used; ++set) {
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        uint32_t t[8];
-                        tc_ld8(tmem + lane_addr + (uint32_t)((set * P + p) * um::NTOK + cb), t);
-                        tc_wait_ld();
-#pragma unroll
-                        for (int c2 = 0; c2 < 8; ++c2) acc[p][c2] += (int32_t)t[c2];
-                    }
-                }
+                for (int p = 0; p < P; ++p) tc_ld8(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), acc[p]);
+                tc_wait_ld();
 #pragma unroll
                 for (int c2 = 0; c2 < 8; ++c2) {
                     const int64_t tok = j0 * 8 + cb + c2;
                     if (tok < rb || tok >= re) continue;
-                    double sum = (double)acc[P - 1][c2];
+                    const double base = MERGED ? 128.0 : 255.0;
+                    double sum = (double)(int32_t)acc[P - 1][c2];
 #pragma unroll
-                    for (int p = P - 2; p >= 0; --p) sum = sum * 128.0 + (double)acc[p][c2];
-                    sum -= (double)(1LL << (7 * P - 1)) * (double)__ldg(qsums + tok);
+                    for (int p = P - 2; p >= 0; --p) sum = sum * base + (double)(int32_t)acc[p][c2];
+                    if (MERGED) sum -= (double)(1LL << (7 * P - 1)) * (double)__ldg(qsums + tok);
                     const float v2 = (float)(sum * (double)rscale);
                     out[tok * d_out + (int64_t)blockIdx.x * 128 + row] = __fmul_rn(v2, __ldg(scales + tok));
                 }
@@ -438,7 +468,7 @@ bool umma_ok(int64_t d_in, int64_t d_out, int64_t g) { return d_in % 128 == 0 &&
 
 template <int P>
 size_t umma_smem() {
-    return (size_t)um::STAGES * UmStage<P>::BYTES;
+    return (size_t)um::STAGES * UmStage<P, false>::BYTES;
 }
 
 cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, int32_t *sums,
@@ -448,6 +478,7 @@ cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, in
     to_umma_b_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
         codes, n, K, tiles, reinterpret_cast<uint4 *>(dst));
     CQ_TRY(check_launch("to_umma_b"));
+    if (sums == nullptr) return CQ_OK;
     row_sums_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(codes, n, K, sums);
     return check_launch("row_sums");
 }
@@ -459,18 +490,18 @@ int64_t umma_b_bytes(int64_t rows, int64_t d_in) {
     return umma_b_tiles(rows) * 8 * d_in + ceil_div(rows * 4, 256) * 256;
 }
 
-template <int P>
+template <int P, bool MERGED>
 cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *sums,
                       const int32_t *offsets, int64_t n_seg, int64_t seg_first, const cq_expert_site *a, float *out_a,
                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
     static bool attr = false;
     const size_t smem = umma_smem<P>();
     if (!attr) {
-        cudaFuncSetAttribute(lut_umma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lut_umma_kernel<P, MERGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     dim3 grid((unsigned)(d_out / 128), (unsigned)n_seg, b ? 2u : 1u);
-    lut_umma_kernel<P><<<grid, um::THREADS, smem, st>>>(
+    lut_umma_kernel<P, MERGED><<<grid, um::THREADS, smem, st>>>(
         bfrag, n_tiles, scales, sums, offsets, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
         b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, (int)d_in, (int)d_out,
         (int)a->group_size);
@@ -492,15 +523,19 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         set_error("tcgen05 path: paired matrices must share planes and group size");
         return CQ_ERR_CONFIG;
     }
+    if (b && b->tc_layout != a->tc_layout) {
+        set_error("tcgen05 path: paired matrices must share the layout");
+        return CQ_ERR_CONFIG;
+    }
+    const bool merged = a->tc_layout == CQ_TC_UMMA128U;
     const int64_t tiles = umma_b_tiles(rows);
-    int32_t *sums = reinterpret_cast<int32_t *>(bbuf + tiles * 8 * d_in);
+    int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + tiles * 8 * d_in) : nullptr;
     CQ_TRY(to_umma_b(codes, rows, d_in, tiles, bbuf, sums, st));
-    if (a->tc_planes == 3)
-        return launch_umma<3>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out,
-                              st);
-    if (a->tc_planes == 2)
-        return launch_umma<2>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out,
-                              st);
+#define CQ_UMMA(P_, M_) \
+    launch_umma<P_, M_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, st)
+    if (a->tc_planes == 3) return merged ? CQ_UMMA(3, true) : CQ_UMMA(3, false);
+    if (a->tc_planes == 2) return merged ? CQ_UMMA(2, true) : CQ_UMMA(2, false);
+#undef CQ_UMMA
     set_error("tcgen05 path: planes must be 2 or 3");
     return CQ_ERR_CONFIG;
 }

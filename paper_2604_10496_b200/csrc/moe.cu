@@ -375,7 +375,7 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
                       cudaStream_t st) {
     const int64_t d = dsc->d_model, ff = dsc->d_ff;
     if (rows == 0 || n_seg == 0) return CQ_OK;
-    if (path == CQ_PATH_TC && gate.tc_layout == CQ_TC_UMMA128) {
+    if (path == CQ_PATH_TC && gate.tc_layout != CQ_TC_MMA16) {
         float *bbuf = hidden + rows * ff;
         CQ_TRY(lut_umma_grouped(codes, reinterpret_cast<int8_t *>(frag_in), scales, offsets, n_seg, seg_first, rows,
                                 &gate, hidden, &up, bbuf, d, ff, st));

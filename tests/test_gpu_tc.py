@@ -24,14 +24,14 @@ def _rand_pw(rng, d_out, d_in, g, scale=1.0):
     return cent, ids, PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), d_in, g)
 
 
-LAYOUTS = ["umma128", "mma16"]
+LAYOUTS = ["umma128", "umma128u", "mma16"]
 
 
 @pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("planes", [2, 3])
 def test_digit_plane_luts_decode_to_centroids(planes, layout):
     rng = np.random.default_rng(0)
-    rows, tr = 256, (128 if layout == "umma128" else 16)
+    rows, tr = 256, (16 if layout == "mma16" else 128)
     cent, ids, pw = _rand_pw(rng, rows, 512, 128, 0.03)
     cent[3] = 0.0  # an all-zero row gets scale 1 and zero digits
     pw = PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), 512, 128)
@@ -41,7 +41,7 @@ def test_digit_plane_luts_decode_to_centroids(planes, layout):
     G = 512 // 128
     lut = lut.reshape(rows // tr, G, tr, planes, 16).transpose(0, 2, 1, 3, 4).reshape(rows, G, planes, 16)
     m = np.zeros(lut.shape[:2] + (16,), np.int64)
-    if layout == "mma16":
+    if layout in ("mma16", "umma128"):
         # signed base-255 digits, sign garbage pre-compensated: PRMT(P) + PRMT(Q)
         partner = lut[..., np.arange(16) ^ 8]
         digits = lut + np.where(partner < 0, -1, 0)
