@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--path", default="auto", choices=["auto", "tc", "f32", "ordered"])
+    p.add_argument("--layout", default="umma128", choices=["umma128", "umma128u", "mma16"],
+                   help="tensor-core weight layout / kernel")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=0)
     return p.parse_args()
@@ -228,7 +230,7 @@ def run_ours(args):
     layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=args.path)
     if args.path in ("auto", "tc"):
         try:
-            layer.prepare_tc()
+            layer.prepare_tc(layout=args.layout)
         except Exception as exc:  # tensor-core layout not available for this build
             if args.path == "tc":
                 raise
@@ -334,7 +336,7 @@ def run_ours(args):
             "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
             "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
                        "group_size": g, "batch": n, "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "path": path_used, "l2": "weights 1.41 GB > 126 MB L2, no flush needed",
+                       "path": path_used, "layout": args.layout, "l2": "weights 1.41 GB > 126 MB L2, no flush needed",
                        "cuda_graph": True, "active_experts": n_active},
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),

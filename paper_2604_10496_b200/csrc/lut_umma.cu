@@ -60,10 +60,11 @@ struct UmStage {
     static constexpr int B = (um::NTOK / 8) * um::BTILE;
     static constexpr int BYTES = um::IDS + LUT + B;
     static constexpr int SLICES = MERGED ? P : 2 * P;            // MMA K-slices per k-step
-    static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per A stage (one k-step)
+    static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per k-step
+    static constexpr int CCOLS = 4 * ACOLS;                      // TMEM columns per A stage (one chunk)
     static constexpr int ACC = P * um::NTOK;                     // accumulator columns
-    static constexpr int AS = (um::TMEM_COLS - ACC) / ACOLS / um::WG;  // A stages per warpgroup
-    static_assert(AS >= 2, "TMEM budget");
+    static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages (chunks in flight)
+    static_assert(NCS >= 2, "TMEM budget");
 };
 
 // ---------------------------------------------------------------------------
@@ -190,11 +191,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     float *__restrict__ out0, const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1,
     const float *__restrict__ rs1, float *__restrict__ out1, int d_in, int d_out, int g) {
     using S = UmStage<P, MERGED>;
-    constexpr int AS = S::AS;
-    constexpr int NAS = AS * um::WG;  // A stages in total
+    constexpr int NCS = S::NCS;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full_bar[um::STAGES], empty_bar[um::STAGES];
-    __shared__ __align__(8) uint64_t afull_bar[NAS], aempty_bar[NAS];
+    __shared__ __align__(8) uint64_t afull_bar[NCS], aempty_bar[NCS];
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
 
@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             u_bar_init(u_smem(&full_bar[s]), 1);
             u_bar_init(u_smem(&empty_bar[s]), 1);
         }
-        for (int s = 0; s < NAS; ++s) {
-            u_bar_init(u_smem(&afull_bar[s]), 4);  // the 4 warps of the writing warpgroup
+        for (int s = 0; s < NCS; ++s) {
+            u_bar_init(u_smem(&afull_bar[s]), um::EXP_WARPS);  // every expander warp writes its k-step
             u_bar_init(u_smem(&aempty_bar[s]), 1);
         }
         u_bar_init(u_smem(&accfull_bar), 1);
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         }
     } else if (warp == um::MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
-        uint32_t it = 0, ks = 0;
+        uint32_t it = 0;
         for (int pass = 0; pass < n_pass; ++pass) {
             const int64_t j0 = j_first + (int64_t)pass * TPP;
             const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
@@ -276,27 +276,27 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
             for (int c = 0; c < n_chunks; ++c, ++it) {
                 const int s = it % um::STAGES;
+                const int cs = it % NCS;
                 u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
+                u_bar_wait(u_smem(&afull_bar[cs]), (it / NCS) & 1);
+                tc_fence_after();
                 const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
+                const uint32_t abase = tmem + a_col0 + (uint32_t)(cs * S::CCOLS);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk, ++ks) {
-                    const int as = ks % NAS;
-                    u_bar_wait(u_smem(&afull_bar[as]), (ks / NAS) & 1);
-                    tc_fence_after();
+                for (int kk = 0; kk < 4; ++kk) {
                     // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
                     const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
-                    const uint32_t abase = tmem + a_col0 + (uint32_t)(as * S::ACOLS);
-                    const uint32_t first = (c == 0 && kk == 0) ? 1u : 0u;
 #pragma unroll
                     for (int sl = 0; sl < S::SLICES; ++sl) {
                         const int p = MERGED ? sl : (sl >> 1);
-                        const uint32_t accum = (first && (MERGED || !(sl & 1))) ? 0u : 1u;
-                        tc_mma_i8(tmem + (uint32_t)(p * um::NTOK), abase + (uint32_t)(sl * 8), bdesc, idesc, accum);
+                        const uint32_t accum = (c == 0 && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
+                        tc_mma_i8(tmem + (uint32_t)(p * um::NTOK), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
+                                  idesc, accum);
                     }
-                    tc_commit_elect(u_smem(&aempty_bar[as]));
-                    if (kk == 3) tc_commit_elect(u_smem(&empty_bar[s]));
-                    if (kk == 3 && c == n_chunks - 1) tc_commit_elect(u_smem(&accfull_bar));
                 }
+                tc_commit_elect(u_smem(&aempty_bar[cs]));
+                tc_commit_elect(u_smem(&empty_bar[s]));
+                if (c == n_chunks - 1) tc_commit_elect(u_smem(&accfull_bar));
             }
         }
     } else {
@@ -306,17 +306,17 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
         const float rscale = __ldg(rsp + tile * 128 + row);
-        uint32_t it = 0, kq = 0;  // chunks consumed; k-steps of this warpgroup
+        uint32_t it = 0;  // chunks consumed
         for (int pass = 0; pass < n_pass; ++pass) {
             const int64_t j0 = j_first + (int64_t)pass * TPP;
             const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
             const int n = ((ntc + 1) & ~1) * 8;
             uint4 L[P];
             int gc = 0;
-            for (int c = 0; c < n_chunks; ++c, ++it, ++kq) {
+            for (int c = 0; c < n_chunks; ++c, ++it) {
                 const int s = it % um::STAGES;
-                const int as = (kq % AS) * um::WG + wg;  // global A stage = ks % NAS, ks = 4 * chunk + wg
-                if (kq >= AS) u_bar_wait(u_smem(&aempty_bar[as]), ((kq / AS) - 1) & 1);
+                const int cs = it % NCS;
+                if (it >= (uint32_t)NCS) u_bar_wait(u_smem(&aempty_bar[cs]), ((it / NCS) - 1) & 1);
                 u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
                 tc_fence_after();
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     xsel[2 * q] = x;
                     xsel[2 * q + 1] = x >> 16;
                 }
-                const uint32_t abase = tmem + lane_addr + a_col0 + as * S::ACOLS;
+                const uint32_t abase = tmem + lane_addr + a_col0 + (uint32_t)(cs * S::CCOLS + wg * S::ACOLS);
                 if (MERGED) {
                     uint32_t v[P * 8];
 #pragma unroll
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) u_bar_arrive(u_smem(&afull_bar[as]));
+                if (lane == 0) u_bar_arrive(u_smem(&afull_bar[cs]));
             }
             // ---- epilogue of this pass: accumulators -> fp32 out (warpgroup wg: token columns 8wg..8wg+7)
             u_bar_wait(u_smem(&accfull_bar), pass & 1);
