@@ -104,6 +104,61 @@ __global__ void router_logits_async_kernel(const int8_t *__restrict__ codes, con
     if (live) logits[t * n_exp + e] = acc;
 }
 
+// Same chains, split so the serial part is only the additions: 128 producer
+// threads form the products p[k][j] = fl(fl(q[t,k] * s_t) * W[k,e]) for a
+// chunk of RK columns into shared memory while the chain threads (one per
+// (token, expert) pair, CH per CTA) add the previous chunk in k order.  Named
+// barriers double-buffer the product chunks.  The dependent fp32 adds are
+// the floor (~4 cycles each).
+constexpr int RC_PROD = 128;
+
+__global__ void router_chain_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
+                                    const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp, int tt, int ch,
+                                    int rk, float *__restrict__ logits) {
+    extern __shared__ __align__(16) float prod[];  // [2][rk][ch]
+    const int tid = threadIdx.x;
+    const int64_t t0 = blockIdx.x * (int64_t)tt;
+    const int n_chunks = (int)((d + rk - 1) / rk);
+    const int nthreads = ch + RC_PROD;
+    if (tid < ch) {
+        // ---- chain threads
+        const int t_loc = tid / (int)n_exp, e = tid % (int)n_exp;
+        const bool live = t_loc < tt && t0 + t_loc < n;
+        float acc = 0.0f;
+        for (int i = 0; i < n_chunks; ++i) {
+            const int b = i & 1;
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + b), "r"(nthreads) : "memory");
+            const int kn = (int)((d - (int64_t)i * rk) < rk ? (d - (int64_t)i * rk) : rk);
+            const float *pb = prod + (size_t)b * rk * ch + tid;
+#pragma unroll 8
+            for (int kk = 0; kk < kn; ++kk) acc = __fadd_rn(acc, pb[kk * ch]);
+            if (i + 2 < n_chunks) asm volatile("bar.arrive %0, %1;" ::"r"(3 + b), "r"(nthreads) : "memory");
+        }
+        if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
+    } else {
+        // ---- product threads
+        const int pt = tid - ch;
+        for (int i = 0; i < n_chunks; ++i) {
+            const int b = i & 1;
+            if (i >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + b), "r"(nthreads) : "memory");
+            const int64_t k0 = (int64_t)i * rk;
+            const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
+            float *pb = prod + (size_t)b * rk * ch;
+            for (int x = pt; x < kn * ch; x += RC_PROD) {
+                const int kk = x / ch, j = x - kk * ch;
+                const int t_loc = j / (int)n_exp, e = j - t_loc * (int)n_exp;
+                const int64_t t = t0 + t_loc;
+                float p = 0.0f;
+                if (t_loc < tt && t < n)
+                    p = __fmul_rn(__fmul_rn((float)codes[t * d + k0 + kk], __ldg(scales + t)),
+                                  __ldg(w + (k0 + kk) * n_exp + e));
+                pb[kk * ch + j] = p;
+            }
+            asm volatile("bar.arrive %0, %1;" ::"r"(1 + b), "r"(nthreads) : "memory");
+        }
+    }
+}
+
 // numpy's float32 sum of a short row: a plain loop below 8 elements, eight
 // interleaved partial sums combined as a tree from 8 up (pairwise_sum).
 __device__ __forceinline__ float np_sum(const float *v, int n) {
@@ -244,6 +299,16 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *w
     if (n_exp > 256) {
         set_error("router: at most 256 experts");
         return CQ_ERR_CONFIG;
+    }
+    if (n_exp <= 128) {
+        // chains per CTA: >= one warp; products double-buffered in <= 48 KB
+        const int tt2 = (int)std::max<int64_t>(1, 32 / n_exp);
+        const int ch = (int)(ceil_div(tt2 * n_exp, 32) * 32);
+        const int rk = (int)std::max<int64_t>(16, std::min<int64_t>(256, (6144 / ch) & ~15LL));
+        const size_t smem = 2 * (size_t)rk * ch * sizeof(float);
+        router_chain_kernel<<<(unsigned)ceil_div(n, tt2), (unsigned)(ch + RC_PROD), smem, st>>>(
+            codes, scales, w, n, d, n_exp, tt2, ch, rk, logits);
+        return check_launch("router_logits");
     }
     const int tt = (int)(256 / n_exp);
     if (d % 16 == 0) {
