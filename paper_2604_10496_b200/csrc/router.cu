@@ -112,16 +112,37 @@ __global__ void router_logits_async_kernel(const int8_t *__restrict__ codes, con
 // the floor (~4 cycles each).
 constexpr int RC_PROD = 128;
 
+// Shared-memory plan of router_chain_kernel for chunk size rk: double-buffered
+// codes [tt][rk] i8, W [rk][E] f32 and products [rk][ch] f32.
+struct RcPlan {
+    int rk;
+    size_t codes, wts, prod, total;
+};
+
+__host__ __device__ inline RcPlan rc_plan(int rk, int tt, int ch, int64_t n_exp) {
+    RcPlan p;
+    p.rk = rk;
+    p.codes = 0;
+    p.wts = (((size_t)2 * tt * rk + 15) / 16) * 16;
+    p.prod = p.wts + (size_t)2 * rk * n_exp * 4;
+    p.total = p.prod + (size_t)2 * rk * ch * 4;
+    return p;
+}
+
 __global__ void router_chain_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
                                     const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp, int tt, int ch,
                                     int rk, float *__restrict__ logits) {
-    extern __shared__ __align__(16) float prod[];  // [2][rk][ch]
+    extern __shared__ __align__(16) uint8_t rsm_raw[];
+    const RcPlan plan = rc_plan(rk, tt, ch, n_exp);
+    int8_t *cst = reinterpret_cast<int8_t *>(rsm_raw + plan.codes);   // [2][tt][rk]
+    float *wst = reinterpret_cast<float *>(rsm_raw + plan.wts);       // [2][rk][E]
+    float *prod = reinterpret_cast<float *>(rsm_raw + plan.prod);     // [2][rk][ch]
     const int tid = threadIdx.x;
     const int64_t t0 = blockIdx.x * (int64_t)tt;
     const int n_chunks = (int)((d + rk - 1) / rk);
     const int nthreads = ch + RC_PROD;
     if (tid < ch) {
-        // ---- chain threads
+        // ---- chain threads: the ordered adds only
         const int t_loc = tid / (int)n_exp, e = tid % (int)n_exp;
         const bool live = t_loc < tt && t0 + t_loc < n;
         float acc = 0.0f;
@@ -130,31 +151,67 @@ __global__ void router_chain_kernel(const int8_t *__restrict__ codes, const floa
             asm volatile("bar.sync %0, %1;" ::"r"(1 + b), "r"(nthreads) : "memory");
             const int kn = (int)((d - (int64_t)i * rk) < rk ? (d - (int64_t)i * rk) : rk);
             const float *pb = prod + (size_t)b * rk * ch + tid;
-#pragma unroll 8
-            for (int kk = 0; kk < kn; ++kk) acc = __fadd_rn(acc, pb[kk * ch]);
+            int kk = 0;
+            if (kn >= 16) {
+                float cur[16], nxt[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) cur[u] = pb[u * ch];
+                for (kk = 16; kk + 16 <= kn; kk += 16) {
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) nxt[u] = pb[(kk + u) * ch];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, cur[u]);
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, cur[u]);
+            }
+            for (; kk < kn; ++kk) acc = __fadd_rn(acc, pb[kk * ch]);
             if (i + 2 < n_chunks) asm volatile("bar.arrive %0, %1;" ::"r"(3 + b), "r"(nthreads) : "memory");
         }
         if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
     } else {
-        // ---- product threads
+        // ---- helpers: stage codes + W of chunk i+1 (cp.async) while forming
+        // the products of chunk i from shared memory
         const int pt = tid - ch;
-        for (int i = 0; i < n_chunks; ++i) {
+        auto stage = [&](int i) {
             const int b = i & 1;
-            if (i >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + b), "r"(nthreads) : "memory");
             const int64_t k0 = (int64_t)i * rk;
             const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
-            float *pb = prod + (size_t)b * rk * ch;
-            for (int x = pt; x < kn * ch; x += RC_PROD) {
-                const int kk = x / ch, j = x - kk * ch;
-                const int t_loc = j / (int)n_exp, e = j - t_loc * (int)n_exp;
-                const int64_t t = t0 + t_loc;
-                float p = 0.0f;
-                if (t_loc < tt && t < n)
-                    p = __fmul_rn(__fmul_rn((float)codes[t * d + k0 + kk], __ldg(scales + t)),
-                                  __ldg(w + (k0 + kk) * n_exp + e));
-                pb[kk * ch + j] = p;
+            for (int x = pt * 4; x < kn * (int)n_exp; x += RC_PROD * 4)
+                cp_async16(wst + (size_t)b * rk * n_exp + x, w + k0 * n_exp + x);
+            const int rowv = kn / 16;
+            for (int x = pt; x < tt * rowv; x += RC_PROD) {
+                const int tl = x / rowv, v = x - tl * rowv;
+                const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;
+                cp_async16(cst + (size_t)b * tt * rk + tl * rk + v * 16, codes + tg * d + k0 + v * 16);
             }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        const int j = pt % ch, kk0 = pt / ch, kstep = RC_PROD / ch;
+        const int t_loc = j / (int)n_exp, e = j - t_loc * (int)n_exp;
+        const bool live = t_loc < tt && t0 + t_loc < n;
+        const float s = live ? __ldg(scales + t0 + t_loc) : 0.0f;
+        stage(0);
+        for (int i = 0; i < n_chunks; ++i) {
+            const int b = i & 1;
+            if (i + 1 < n_chunks) {
+                stage(i + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            asm volatile("bar.sync 5, %0;" ::"r"(RC_PROD) : "memory");  // chunk i staged by every helper
+            if (i >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + b), "r"(nthreads) : "memory");
+            const int kn = (int)((d - (int64_t)i * rk) < rk ? (d - (int64_t)i * rk) : rk);
+            const int8_t *cr = cst + (size_t)b * tt * rk + (live ? t_loc : 0) * rk;
+            const float *wr = wst + (size_t)b * rk * n_exp + e;
+            float *pb = prod + (size_t)b * rk * ch + j;
+            for (int kk = kk0; kk < kn; kk += kstep)
+                pb[kk * ch] = live ? __fmul_rn(__fmul_rn((float)cr[kk], s), wr[kk * n_exp]) : 0.0f;
             asm volatile("bar.arrive %0, %1;" ::"r"(1 + b), "r"(nthreads) : "memory");
+            asm volatile("bar.sync 5, %0;" ::"r"(RC_PROD) : "memory");  // stage buffer b reusable
         }
     }
 }
@@ -300,12 +357,13 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *w
         set_error("router: at most 256 experts");
         return CQ_ERR_CONFIG;
     }
-    if (n_exp <= 128) {
-        // chains per CTA: >= one warp; products double-buffered in <= 48 KB
+    if (n_exp <= 128 && d % 16 == 0) {
+        // chains per CTA: >= one warp; staging + products double-buffered in <= 48 KB
         const int tt2 = (int)std::max<int64_t>(1, 32 / n_exp);
         const int ch = (int)(ceil_div(tt2 * n_exp, 32) * 32);
-        const int rk = (int)std::max<int64_t>(16, std::min<int64_t>(256, (6144 / ch) & ~15LL));
-        const size_t smem = 2 * (size_t)rk * ch * sizeof(float);
+        int rk = 256;
+        while (rk > 16 && rc_plan(rk, tt2, ch, n_exp).total > 48 * 1024) rk -= 16;
+        const size_t smem = rc_plan(rk, tt2, ch, n_exp).total;
         router_chain_kernel<<<(unsigned)ceil_div(n, tt2), (unsigned)(ch + RC_PROD), smem, st>>>(
             codes, scales, w, n, d, n_exp, tt2, ch, rk, logits);
         return check_launch("router_logits");
