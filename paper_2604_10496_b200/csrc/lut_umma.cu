@@ -72,6 +72,13 @@ struct UmStage {
 
 __device__ __forceinline__ uint32_t u_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// x >> 16 on the FMA pipe (IMAD.HI) — the ALU pipe is the expanders' bottleneck.
+__device__ __forceinline__ uint32_t hi16(uint32_t x) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, 65536;" : "=r"(r) : "r"(x));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t u_prmt(uint32_t a, uint32_t b, uint32_t s) {
     uint32_t d;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
@@ -333,9 +340,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t x = wv[q] ^ 0x88888888u;
                     sel[2 * q] = wv[q];
-                    sel[2 * q + 1] = wv[q] >> 16;
+                    sel[2 * q + 1] = hi16(wv[q]);
                     xsel[2 * q] = x;
-                    xsel[2 * q + 1] = x >> 16;
+                    xsel[2 * q + 1] = hi16(x);
                 }
                 const uint32_t abase = tmem + lane_addr + a_col0 + (uint32_t)(cs * S::CCOLS + wg * S::ACOLS);
                 if (MERGED) {
