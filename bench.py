@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--path", default="auto", choices=["auto", "tc", "f32", "ordered"])
-    p.add_argument("--layout", default="umma128", choices=["umma128", "umma128u", "mma16"],
+    p.add_argument("--layout", default="umma128u", choices=["umma128", "umma128u", "mma16"],
                    help="tensor-core weight layout / kernel")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=0)
@@ -301,7 +301,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
 
-    # dominant kernel: the grouped gate|up stage, timed alone with events on its stream
+    # dominant kernel: the grouped gate|up LUT GEMM, timed per stage with CUDA
+    # events on its stream (cq_moe_profile_experts records events between the
+    # expert-stage kernels: gate|up GEMM | silu*up + re-quantize | down GEMM)
     tr = layer.trace(n)
     offsets = tr["offsets"].cpu().numpy()
     n_active = int((np.diff(offsets) > 0).sum())
@@ -310,23 +312,22 @@ def run_ours(args):
     import ctypes
     desc = layer.desc()
     buf, _ = layer.workspace(n)
+    stage_ms = (ctypes.c_float * 3)()
     with torch.cuda.stream(stream):
-        args_e = (ctypes.byref(desc), tr["codes_perm"].data_ptr(), tr["scales_perm"].data_ptr(),
-                  tr["offsets"].data_ptr(), n * k)
-        ku = torch.cuda.Event(enable_timing=True)
-        kv = torch.cuda.Event(enable_timing=True)
         fexp = torch.empty((n * k, d), dtype=torch.float32, device="cuda")
-        L.check(L.lib().cq_moe_experts(*args_e, fexp.data_ptr(), buf.data_ptr(), buf.numel(), L.stream()))
-        reps = max(3, args.steps)
-        ku.record(stream)
-        for _ in range(reps):
-            L.check(L.lib().cq_moe_experts(*args_e, fexp.data_ptr(), buf.data_ptr(), buf.numel(), L.stream()))
-        kv.record(stream)
-        kv.synchronize()
-    experts_ms = ku.elapsed_time(kv) / reps
+        L.check(L.lib().cq_moe_profile_experts(ctypes.byref(desc), tr["codes_perm"].data_ptr(),
+                                                tr["scales_perm"].data_ptr(), tr["offsets"].data_ptr(), n * k,
+                                                fexp.data_ptr(), buf.data_ptr(), buf.numel(), max(3, args.steps),
+                                                stage_ms, L.stream()))
+    gu_ms, rq_ms, dn_ms = (float(x) for x in stage_ms)
     pk = peaks()
-    # expert stage = gate|up + requant + down: attribute by bytes of the two GEMM kernels
-    achieved = (byt["gate_up"] + byt["down"]) / (experts_ms * 1e-3) / 1e9
+    achieved = byt["gate_up"] / (gu_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.layout}:gate_up")
+    except (OSError, ValueError):
+        pass
 
     if rank == 0:
         res = {
@@ -341,11 +342,14 @@ def run_ours(args):
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),
                     "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},
-            "roofline": {"bound": "hbm", "kernel": "expert stage (grouped gate|up LUT GEMM + requant + down)",
+            "roofline": {"bound": "hbm",
+                         "kernel": "grouped gate|up LUT GEMM (lut_umma_kernel<3>, tcgen05 kind::i8, A from TMEM)",
                          "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "peak_src": pk["src"],
-                         "traffic": None, "algorithmic_bytes": byt["gate_up"] + byt["down"],
-                         "kernel_ms": experts_ms,
+                         "traffic": traffic, "algorithmic_bytes": byt["gate_up"], "kernel_ms": gu_ms,
+                         "bytes_def": "SURVEY 8(d): ids d_out*d_in/2 + fp32 centroids d_out*(d_in/g)*64 per active "
+                                      "expert and matrix, + codes/scales in + fp32 outputs",
+                         "stage_ms": {"gate_up": gu_ms, "silu_requant": rq_ms, "down": dn_ms},
                          "layer_frac": byt["layer"] / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
             "clocks": clk.summary(),
             "gpu_launches": int(launches_per_step * args.steps),

@@ -176,6 +176,13 @@ CQ_API cq_status cq_moe_route(const cq_moe_desc *desc, const void *x, int dtype,
 CQ_API cq_status cq_moe_experts(const cq_moe_desc *desc, const int8_t *codes_perm,
                          const float *scales_perm, const int32_t *offsets, int64_t rows,
                          float *fout, void *workspace, int64_t workspace_bytes, void *stream);
+/* Profiling: runs the expert stage `iters` times with CUDA events between its
+ * kernels on `stream`; stage_ms_host[3] (host memory) receives the mean device
+ * time of {gate|up GEMM (+ operand re-layout), silu*up + re-quantization, down GEMM}. */
+CQ_API cq_status cq_moe_profile_experts(const cq_moe_desc *desc, const int8_t *codes_perm,
+                                 const float *scales_perm, const int32_t *offsets, int64_t rows,
+                                 float *fout, void *workspace, int64_t workspace_bytes,
+                                 int32_t iters, float *stage_ms_host, void *stream);
 /* Weighted combine in ascending expert order (model.py:389-401). */
 CQ_API cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
                          const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,

@@ -56,6 +56,7 @@ _SIGS = {
     "cq_moe_route": [ctypes.POINTER(MoEDesc), _vp, _int, _i64, _vp, _i64, _vp],
     "cq_moe_experts": [ctypes.POINTER(MoEDesc), _vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp],
     "cq_moe_combine": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
+    "cq_moe_profile_experts": [ctypes.POINTER(MoEDesc), _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp],
     "cq_lut8_prepare": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "cq_lut_gemm_tc": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
 }

@@ -372,17 +372,23 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
                       const cq_expert_site &down, int64_t n_seg, int64_t seg_first, const int8_t *codes,
                       const float *scales, const int32_t *offsets, int64_t rows, float *hidden,
                       int8_t *hcodes, float *hscales, float *fout, uint2 *frag_in, uint2 *frag_h,
-                      cudaStream_t st) {
+                      cudaStream_t st, cudaEvent_t *ev = nullptr) {
     const int64_t d = dsc->d_model, ff = dsc->d_ff;
     if (rows == 0 || n_seg == 0) return CQ_OK;
     if (path == CQ_PATH_TC && gate.tc_layout != CQ_TC_MMA16) {
         float *bbuf = hidden + rows * ff;
+        if (ev) cudaEventRecord(ev[0], st);
         CQ_TRY(lut_umma_grouped(codes, reinterpret_cast<int8_t *>(frag_in), scales, offsets, n_seg, seg_first, rows,
                                 &gate, hidden, &up, bbuf, d, ff, st));
+        if (ev) cudaEventRecord(ev[1], st);
         CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, st));
-        return lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
-                                &down, fout, nullptr, nullptr, ff, d, st);
+        if (ev) cudaEventRecord(ev[2], st);
+        CQ_TRY(lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
+                                &down, fout, nullptr, nullptr, ff, d, st));
+        if (ev) cudaEventRecord(ev[3], st);
+        return CQ_OK;
     }
+    if (ev) cudaEventRecord(ev[0], st);
     if (path == CQ_PATH_TC) {
         CQ_TRY(lut_tc_grouped_frag(codes, frag_in, scales, offsets, n_seg, seg_first, rows, &gate, &up, d, ff,
                                    hidden, st));
@@ -399,7 +405,23 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
             hidden, bbuf, rows * ff);
         CQ_TRY(check_launch("silu_mul"));
     }
+    if (ev) cudaEventRecord(ev[1], st);
     CQ_TRY(quantize_a4(hidden, CQ_DTYPE_F32, rows, ff, hcodes, hscales, nullptr, st));
+    if (ev) cudaEventRecord(ev[2], st);
+    if (ev) {
+        cq_status rc;
+        if (path == CQ_PATH_TC)
+            rc = lut_tc_grouped_frag(hcodes, frag_h, hscales, offsets, n_seg, seg_first, rows, &down, nullptr, ff, d,
+                                     fout, st);
+        else if (path == CQ_PATH_F32)
+            rc = lut_f32_grouped(hcodes, hscales, offsets, n_seg, seg_first, down.ids, down.centroids, nullptr,
+                                 nullptr, ff, d, down.group_size, fout, st);
+        else
+            rc = ordered_grouped(hcodes, hscales, offsets, n_seg, seg_first, rows, down.ids, down.centroids, ff, d,
+                                 down.group_size, fout, st);
+        cudaEventRecord(ev[3], st);
+        return rc;
+    }
     if (path == CQ_PATH_TC)
         return lut_tc_grouped_frag(hcodes, frag_h, hscales, offsets, n_seg, seg_first, rows, &down, nullptr, ff, d,
                                    fout, st);
@@ -483,6 +505,40 @@ extern "C" cq_status cq_moe_experts(const cq_moe_desc *desc, const int8_t *codes
     return run_experts(desc, choose_path(desc), desc->gate, desc->up, desc->down, desc->n_local_experts, 0,
                        codes_perm, scales_perm, offsets, rows, w.hidden, w.hcodes, w.hscales, fout, w.codes_frag,
                        w.hcodes_frag, as_stream(stream));
+}
+
+extern "C" cq_status cq_moe_profile_experts(const cq_moe_desc *desc, const int8_t *codes_perm,
+                                            const float *scales_perm, const int32_t *offsets, int64_t rows, float *fout,
+                                            void *workspace, int64_t workspace_bytes, int32_t iters,
+                                            float *stage_ms_host, void *stream) {
+    CQ_TRY(validate_desc(desc));
+    const int64_t n_equiv = ceil_div(rows, desc->top_k);
+    int64_t off[CQ_WS_COUNT_];
+    if (workspace_layout(desc, n_equiv, off) > workspace_bytes) {
+        set_error("moe: workspace too small");
+        return CQ_ERR_SHAPE;
+    }
+    if (iters < 1) iters = 1;
+    Ws w = carve(workspace, off);
+    cudaStream_t st = as_stream(stream);
+    cudaEvent_t ev[4];
+    for (auto &e : ev) cudaEventCreate(&e);
+    double acc[3] = {0, 0, 0};
+    cq_status rc = CQ_OK;
+    for (int i = 0; i < iters && rc == CQ_OK; ++i) {
+        rc = run_experts(desc, choose_path(desc), desc->gate, desc->up, desc->down, desc->n_local_experts, 0,
+                         codes_perm, scales_perm, offsets, rows, w.hidden, w.hcodes, w.hscales, fout, w.codes_frag,
+                         w.hcodes_frag, st, ev);
+        cudaEventSynchronize(ev[3]);
+        for (int k = 0; k < 3; ++k) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+            acc[k] += ms;
+        }
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < 3; ++k) stage_ms_host[k] = (float)(acc[k] / iters);
+    return rc;
 }
 
 extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,

@@ -148,10 +148,11 @@ class MoELayer:
 
     # ------------------------------------------------------------------
     def prepare_tc(self, planes_gate_up: int = 3, planes_down: int = 2,
-                   layout: str = "umma128") -> "MoELayer":
+                   layout: str = "umma128u") -> "MoELayer":
         """Tensor-core layouts: 3 digit planes where the output is re-quantized
-        (gate, up), 2 for down (precision budget).  layout "umma128"
-        (tcgen05 kernel) or "mma16" (mma.sync kernel)."""
+        (gate, up), 2 for down.  layout "umma128u" (tcgen05,
+        unsigned merged digits), "umma128" (tcgen05, signed P/Q digit slices)
+        or "mma16" (mma.sync kernel)."""
         sites = [(self.gate, planes_gate_up), (self.up, planes_gate_up), (self.down, planes_down)]
         if self.shared is not None:
             sites += [(self.shared[0], planes_gate_up), (self.shared[1], planes_gate_up),
