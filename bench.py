@@ -11,9 +11,10 @@ grouped gate|up LUT GEMM + silu -> re-quantize -> grouped down -> combine.
     python bench.py [--gpus N --steps K --warmup W --batch B --path auto|tc|f32]
     python bench.py --impl reference ...   # the reference CPU kernel (oracle/_ref)
 
-N > 1 (torchrun): one independent replica per GPU over its own batch (the
-single-GPU layer fits in HBM; the expert-parallel path is ep.py), reported as
-weak scaling; time = max over ranks.
+N > 1 (torchrun): expert parallelism (ep.py; `run_ep`): E/N experts and a
+batch of B tokens per rank, NCCL all_to_all dispatch/return, reported as weak
+scaling; time = max over ranks.  `--replicas` runs N independent full layers
+instead; `--ep` forces the EP driver at N = 1 (torchrun --nproc-per-node 1).
 """
 
 from __future__ import annotations
@@ -39,7 +40,7 @@ CFG = dict(name="mixtral-8x7b-moe-layer-decode", d_model=4096, d_ff=14336, n_exp
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -47,62 +48,74 @@ def parse():
     p.add_argument("--layout", default="umma128u", choices=["umma128", "umma128u", "mma16"],
                    help="tensor-core weight layout / kernel")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--replicas", action="store_true",
+                   help="N > 1: independent full replicas instead of expert parallelism")
+    p.add_argument("--ep", action="store_true", help="expert-parallel driver even at N = 1 (under torchrun)")
     p.add_argument("--seed", type=int, default=0)
     return p.parse_args()
 
 
-def layer_bytes(n_active: int, n: int, k: int) -> dict:
-    """Algorithmic HBM bytes: reference-format weights of the
-    active experts + activations, per layer and for the gate|up kernel."""
+def layer_bytes(n_active: int, R: int) -> dict:
+    """Algorithmic HBM bytes for R routed rows: reference-format
+    weights of the active experts + activations, per layer and for the gate|up
+    kernel."""
     d, ff, g = CFG["d_model"], CFG["d_ff"], CFG["group_size"]
     w_gu = 2 * (ff * d // 2 + ff * (d // g) * 16 * 4)        # gate + up ids + centroids
     w_dn = d * ff // 2 + d * (ff // g) * 16 * 4
-    R = n * k
     gu = n_active * w_gu + R * d + R * 4 + R * ff * 4         # + codes, scales in; hidden out
     dn = n_active * w_dn + R * ff + R * 4 + R * d * 4
     return dict(gate_up=gu, down=dn, layer=gu + dn + d * CFG["n_experts"] * 4)
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled during the timed region.
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NVML polled from a thread every ~2 ms (nvidia-smi's 100 ms loop is too slow
+    for a millisecond-scale region); falls back to nvidia-smi if NVML is absent.
+    """
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop, self.thread = index, [], threading.Event(), None
+
+    def _poll_nvml(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        names = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                 nv.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
+        while not self.stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((sm, mx, [v for k, v in names.items() if bits & k]))
+            time.sleep(0.002)
+        nv.nvmlShutdown()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
-        except OSError:
-            self.proc = None
+            import pynvml  # noqa: F401
+            self.thread = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.thread.start()
+            time.sleep(0.01)
+        except ImportError:
+            self.thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        self.stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self) -> dict:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[2]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.rows[0][1]),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
 def peaks() -> dict:
@@ -133,11 +146,17 @@ def host_layer(seed: int, n: int):
     return v, w, experts
 
 
-def cpu_reference_step(v, w, experts, k, threads, expert_sample):
-    """The composed MoE block on the reference's native kernels
-    (oracle/_ref: _core.matmul_f32 for the router, _core.lut_gemm_f32 with the
-    reference's token-block threading for the experts), restricted to one
-    sampled expert; returns seconds scaled to the whole layer."""
+ROW_FRAC = 8  # each reference step times 1/ROW_FRAC of one expert's output rows
+
+
+def cpu_reference_step(v, w, experts, k, threads, e, part):
+    """One bounded sample of the composed MoE block on the
+    reference's native kernels (oracle/_ref): the router for every token
+    (_core.matmul_f32 + select_top_k), then expert e's gate, up and down LUT
+    GEMMs (_core.lut_gemm_f32 with the reference's token-block threading,
+    BASELINE.md §3 settings) restricted to output-row slice `part` of
+    ROW_FRAC.  Returns seconds scaled to the whole layer: expert work is
+    additive over experts and over output rows."""
     import oracle
     from oracle import oracle as o
     t0 = time.perf_counter()
@@ -148,20 +167,24 @@ def cpu_reference_step(v, w, experts, k, threads, expert_sample):
     sel, wts = o.select_top_k(logits, k)
     t_route = time.perf_counter() - t0
     E = len(experts)
-    t_exp = 0.0
-    for e in expert_sample:
-        rows = np.nonzero((sel == e).any(axis=1))[0]
-        if rows.size == 0:
-            continue
-        t1 = time.perf_counter()
-        bt = max(1, -(-rows.size // threads))
-        (cg, ig, gg), (cu, iu, gu), (cd, idn, gd) = experts[e]
-        a = oracle.ref_lut_gemm(codes[rows], scales[rows], ig, cg, gg, bt, threads)
-        b = oracle.ref_lut_gemm(codes[rows], scales[rows], iu, cu, gu, bt, threads)
-        hc, hs = o.quantize((o.silu(a) * b).astype(np.float32), 4)
-        oracle.ref_lut_gemm(hc, hs, idn, cd, gd, bt, threads)
-        t_exp += time.perf_counter() - t1
-    return t_route + t_exp * E / len(expert_sample)
+    rows = np.nonzero((sel == e).any(axis=1))[0]
+    if rows.size == 0:
+        return t_route
+    bt = max(1, -(-rows.size // threads))
+    (cg, ig, gg), (cu, iu, gu), (cd, idn, gd) = experts[e]
+
+    def sl(a):
+        m = a.shape[0] // ROW_FRAC
+        return np.ascontiguousarray(a[part * m:(part + 1) * m])
+
+    hc = np.random.default_rng(part).integers(-7, 8, (rows.size, cd.shape[1] * gd)).astype(np.int8)
+    hs = np.ones(rows.size, np.float32)
+    t1 = time.perf_counter()
+    oracle.ref_lut_gemm(codes[rows], scales[rows], sl(ig), sl(cg), gg, bt, threads)
+    oracle.ref_lut_gemm(codes[rows], scales[rows], sl(iu), sl(cu), gu, bt, threads)
+    oracle.ref_lut_gemm(hc, hs, sl(idn), sl(cd), gd, bt, threads)
+    t_exp = time.perf_counter() - t1
+    return t_route + t_exp * E * ROW_FRAC
 
 
 def run_reference(args):
@@ -175,13 +198,13 @@ def run_reference(args):
     v, w, experts = host_layer(args.seed, n)
     times = []
     for i in range(args.warmup + args.steps):
-        t = cpu_reference_step(v, w, experts, k, threads, [i % E])
+        t = cpu_reference_step(v, w, experts, k, threads, i % E, (i // E) % ROW_FRAC)
         if i >= args.warmup:
             times.append(t)
     sec = float(np.mean(times))
     value = n / sec
-    sample = (f"batch {n}: router for all tokens, 1 of {E} experts per step (rotating), "
-              f"expert time x{E} (per-expert work is additive)")
+    sample = (f"batch {n}: router for all tokens + 1 of {E} experts x 1/{ROW_FRAC} of its output rows per "
+              f"step (rotating), expert time x{E * ROW_FRAC} (work is additive over experts and rows)")
     print(json.dumps({
         "impl": "reference", "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
@@ -200,15 +223,144 @@ def cpu_baseline(n, k, threads) -> dict:
     oracle.ref_core()
     v, w, experts = host_layer(1, n)
     E = CFG["n_experts"]
-    times = [cpu_reference_step(v, w, experts, k, threads, [e]) for e in (0, 3, 6)]
+    times = [cpu_reference_step(v, w, experts, k, threads, i % E, (3 * i) % ROW_FRAC) for i in range(16)]
     sec = float(np.mean(times))
     return {"value": n / sec, "unit": "tokens/s", "cores": threads, "kind": "reference",
-            "sample": f"batch {n}, experts 0/3/6 timed one per step, expert time x{E}; "
-                      f"reference _core.lut_gemm_f32 + _core.matmul_f32 (oracle/_ref)"}
+            "sample": f"batch {n}, 16 samples of (router + 1 expert x 1/{ROW_FRAC} of its rows), scaled "
+                      f"x{E * ROW_FRAC}; reference _core.lut_gemm_f32 + _core.matmul_f32 (oracle/_ref)"}
 
 
 # ---------------------------------------------------------------------------
 # GPU side.
+
+
+def profile_expert_stage(layer, codes_perm, scales_perm, offsets, R, iters):
+    """Per-stage device times of the grouped expert stage on the current
+    stream (cq_moe_profile_experts records CUDA events between the kernels:
+    gate|up GEMM | silu*up + re-quantize | down GEMM), averaged over iters.
+    Returns (active experts, algorithmic bytes, (gu_ms, rq_ms, dn_ms))."""
+    import ctypes
+    import torch
+    from paper_2604_10496_b200 import _lib as L
+    off = offsets.cpu().numpy()
+    n_active = int((np.diff(off) > 0).sum())
+    desc = layer.desc()
+    buf, _ = layer.workspace(max(1, -(-R // layer.top_k)))
+    stage_ms = (ctypes.c_float * 3)()
+    fexp = torch.empty((max(R, 1), layer.d_model), dtype=torch.float32, device="cuda")
+    L.check(L.lib().cq_moe_profile_experts(ctypes.byref(desc), codes_perm.data_ptr(), scales_perm.data_ptr(),
+                                            offsets.data_ptr(), R, fexp.data_ptr(), buf.data_ptr(), buf.numel(),
+                                            iters, stage_ms, L.stream()))
+    return n_active, layer_bytes(n_active, R), tuple(float(x) for x in stage_ms)
+
+
+def traffic_for(layout):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(f"{layout}:gate_up")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ep(args, rank, world, local):
+    """N > 1: expert parallelism.  Every rank holds E/N experts
+    (identical seeded weights on all ranks, sliced) and its own batch of
+    tokens; a step is EPMoE.forward: route -> counts all_to_all -> codes /
+    scales / expert-id all_to_all -> grouped local experts -> inverse
+    all_to_all -> ascending-expert combine.  The counts exchange makes the
+    step host-synchronous, so it runs eagerly (no CUDA graph)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_10496_b200 import _lib as L
+    from paper_2604_10496_b200.ep import CudaBackend, EPMoE, expert_range
+    from paper_2604_10496_b200.moe import ExpertStack, MoELayer
+    from paper_2604_10496_b200.synthetic import moe_inputs_device
+
+    n, d, ff, E, k, g = args.batch, CFG["d_model"], CFG["d_ff"], CFG["n_experts"], CFG["top_k"], CFG["group_size"]
+    _, w, sites, _ = moe_inputs_device(args.seed, 1, d, ff, E, g)
+    begin, per = expert_range(E, world, rank)
+    stacks = [ExpertStack(sites[s][0][begin:begin + per].contiguous(), sites[s][1][begin:begin + per].contiguous(),
+                          sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    del sites
+    torch.cuda.empty_cache()
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=args.path, expert_begin=begin, n_experts=E)
+    if args.path in ("auto", "tc"):
+        layer.prepare_tc(layout=args.layout)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(args.seed + 1000 + rank)
+    v = torch.randn((n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    backend = CudaBackend(layer)
+    ep = EPMoE(backend, E, k, rank, world)
+    stream = torch.cuda.Stream()
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        c0 = L.launch_count()
+        ep(v)
+        launches_per_step = L.launch_count() - c0
+        for _ in range(args.warmup):
+            ep(v)
+    torch.cuda.synchronize()
+
+    def timed(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            barrier()
+            e0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local) as clk:
+        ms = timed(lambda: ep(v))
+
+    x_host = v.cpu().pin_memory()
+    y_host = torch.empty((n, d), dtype=torch.float32).pin_memory()
+    x_dev = torch.empty_like(v)
+
+    def e2e_step():
+        x_dev.copy_(x_host, non_blocking=True)
+        y_host.copy_(ep(x_dev), non_blocking=True)
+
+    e2e_ms = timed(e2e_step)
+
+    gc, gs, goff, R = backend.last
+    with torch.cuda.stream(stream):
+        n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, gc, gs, goff, R, max(3, args.steps))
+    pk = peaks()
+    achieved = byt["gate_up"] / (gu_ms * 1e-3) / 1e9 if gu_ms > 0 else None
+    if rank == 0:
+        res = {
+            "metric": "MoE-layer tokens/s", "value": n * world / (ms * 1e-3), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32",
+            "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
+            "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
+                       "group_size": g, "batch_per_rank": n, "parallelism": f"ep{world}",
+                       "experts_per_rank": per, "path": args.path, "layout": args.layout,
+                       "l2": "weights > L2, no flush needed", "cuda_graph": False},
+            "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),
+                    "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},
+            "roofline": {"bound": "hbm", "kernel": "rank 0's grouped gate|up LUT GEMM (lut_umma_kernel)",
+                         "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm_gbs"] if achieved else None, "peak_src": pk["src"],
+                         "traffic": None, "algorithmic_bytes": byt["gate_up"], "kernel_ms": gu_ms,
+                         "rows_received": R, "active_local_experts": n_active,
+                         "stage_ms": {"gate_up": gu_ms, "silu_requant": rq_ms, "down": dn_ms}},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches_per_step * args.steps),
+        }
+        print(json.dumps(res), flush=True)
+    dist.destroy_process_group()
 
 
 def run_ours(args):
@@ -218,11 +370,19 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.ep:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2604_10496_b200 import _lib
     from paper_2604_10496_b200.moe import ExpertStack, MoELayer
     from paper_2604_10496_b200.synthetic import moe_inputs_device
+
+    if (world > 1 and not args.replicas) or args.ep:
+        try:
+            return run_ep(args, rank, world, local)
+        except Exception as exc:  # report replicas rather than nothing, and say why
+            print(f"[bench] expert-parallel path failed ({exc!r}); running replicas", file=sys.stderr)
+            args.ep_error = repr(exc)
+            torch.cuda.empty_cache()
 
     n, d, ff, E, k, g = args.batch, CFG["d_model"], CFG["d_ff"], CFG["n_experts"], CFG["top_k"], CFG["group_size"]
     v, w, sites, _ = moe_inputs_device(args.seed + 17 * rank, n, d, ff, E, g)
@@ -305,29 +465,12 @@ def run_ours(args):
     # events on its stream (cq_moe_profile_experts records events between the
     # expert-stage kernels: gate|up GEMM | silu*up + re-quantize | down GEMM)
     tr = layer.trace(n)
-    offsets = tr["offsets"].cpu().numpy()
-    n_active = int((np.diff(offsets) > 0).sum())
-    byt = layer_bytes(n_active, n, k)
-    from paper_2604_10496_b200 import _lib as L
-    import ctypes
-    desc = layer.desc()
-    buf, _ = layer.workspace(n)
-    stage_ms = (ctypes.c_float * 3)()
     with torch.cuda.stream(stream):
-        fexp = torch.empty((n * k, d), dtype=torch.float32, device="cuda")
-        L.check(L.lib().cq_moe_profile_experts(ctypes.byref(desc), tr["codes_perm"].data_ptr(),
-                                                tr["scales_perm"].data_ptr(), tr["offsets"].data_ptr(), n * k,
-                                                fexp.data_ptr(), buf.data_ptr(), buf.numel(), max(3, args.steps),
-                                                stage_ms, L.stream()))
-    gu_ms, rq_ms, dn_ms = (float(x) for x in stage_ms)
+        n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, tr["codes_perm"], tr["scales_perm"],
+                                                                    tr["offsets"], n * k, max(3, args.steps))
     pk = peaks()
     achieved = byt["gate_up"] / (gu_ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(f"{args.layout}:gate_up")
-    except (OSError, ValueError):
-        pass
+    traffic = traffic_for(args.layout)
 
     if rank == 0:
         res = {
@@ -336,7 +479,10 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32",
             "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
             "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
-                       "group_size": g, "batch": n, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "group_size": g, "batch": n,
+                       "parallelism": (f"replicas{world}" + (f" (ep failed: {args.ep_error})"
+                                                             if getattr(args, "ep_error", None) else ""))
+                       if world > 1 else "single",
                        "path": path_used, "layout": args.layout, "l2": "weights 1.41 GB > 126 MB L2, no flush needed",
                        "cuda_graph": True, "active_experts": n_active},
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "tokens/s",

@@ -1,0 +1,164 @@
+"""Expert parallelism for the MoE layer: experts sharded
+over the ranks of one node, tokens data-parallel at the input, one exchange
+each way over NCCL.
+
+Per rank, one forward pass:
+  1. route its own tokens: A4 codes + scales, ordered router logits, top-k
+     (bit-exact; `cq_moe_route`);
+  2. dispatch: every (token, slot) route goes to the rank owning its expert
+     (experts [r*E/G, (r+1)*E/G) live on rank r).  Counts go first
+     (all_to_all of G ints), then the payload: the token's int8 codes (exact —
+     quantization is per token and happens before routing, model.py:379), its
+     fp32 scale and the local expert id (all_to_all_single with the counts as
+     split sizes);
+  3. the owner regroups the received rows by local expert (stable) and runs the
+     grouped gate|up -> silu*up -> re-quantize -> down stage (`cq_moe_experts`);
+  4. return: the per-route fp32 outputs travel back by the inverse split;
+  5. combine on the source rank in ascending expert order (`cq_moe_combine`),
+     so the result is identical to the single-GPU layer.
+
+The compute steps are pluggable: `CudaBackend` (libcq_b200.so) or
+`OracleBackend` (the CPU oracle, used by the world_size-2 gloo tests of this
+host logic).  Deduplication of a token routed to two experts of one rank is
+not done yet: each route carries its own copy of the codes (d bytes + 8).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+def expert_range(n_experts: int, world: int, rank: int) -> tuple[int, int]:
+    if n_experts % world:
+        raise ValueError(f"{n_experts} experts do not split over {world} ranks")
+    per = n_experts // world
+    return rank * per, per
+
+
+def plan_dispatch(selected: torch.Tensor, n_experts: int, world: int):
+    """Route -> destination bookkeeping (pure index work, any device).
+
+    Returns order (routes sorted by destination rank, stable in (t, slot)
+    order), the destination of each sorted route, and per-rank send counts."""
+    per = n_experts // world
+    flat_e = selected.reshape(-1).long()
+    dest = flat_e // per
+    order = torch.sort(dest, stable=True).indices
+    counts = torch.bincount(dest, minlength=world)
+    return order, dest[order], counts
+
+
+def all_to_all_counts(send_counts: torch.Tensor, group=None) -> torch.Tensor:
+    recv = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv, send_counts, group=group)
+    return recv
+
+
+def exchange(t: torch.Tensor, send_counts: list, recv_counts: list, group=None) -> torch.Tensor:
+    out = torch.empty((sum(recv_counts),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_to_all_single(out, t.contiguous(), output_split_sizes=recv_counts, input_split_sizes=send_counts,
+                           group=group)
+    return out
+
+
+class EPMoE:
+    """One rank's share of an expert-parallel MoE layer."""
+
+    def __init__(self, backend, n_experts: int, top_k: int, rank: int, world: int, group=None):
+        self.be, self.E, self.k, self.rank, self.world, self.group = backend, n_experts, top_k, rank, world, group
+        self.begin, self.per = expert_range(n_experts, world, rank)
+
+    # The three local phases; `forward` puts the two exchanges between them.
+    def dispatch(self, x: torch.Tensor) -> dict:
+        """Route the rank's tokens and build the send buffers, ordered by
+        destination rank (stable in (token, slot) order)."""
+        codes, scales, selected, weights = self.be.route(x)
+        order, _, send = plan_dispatch(selected, self.E, self.world)
+        tok = order // self.k
+        eid = (selected.reshape(-1).long()[order] % self.per).to(torch.int32)
+        return {"selected": selected, "weights": weights, "order": order, "send": send,
+                "codes": codes[tok], "scales": scales[tok], "eid": eid}
+
+    def compute(self, r_codes, r_scales, r_eid) -> torch.Tensor:
+        """Received routes -> per-route fp32 expert outputs, in received order."""
+        return self.be.experts(r_codes, r_scales, r_eid, self.per)
+
+    def finish(self, st: dict, f_back: torch.Tensor) -> torch.Tensor:
+        """Returned outputs (rows in send order) -> combined moe_sum."""
+        f_routes = torch.empty_like(f_back)
+        f_routes[st["order"]] = f_back                                    # (t, slot) order
+        return self.be.combine(st["selected"], st["weights"], f_routes)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        st = self.dispatch(x)
+        recv = all_to_all_counts(st["send"], self.group)
+        send_l, recv_l = st["send"].tolist(), recv.tolist()
+        r_codes = exchange(st["codes"], send_l, recv_l, self.group)
+        r_scales = exchange(st["scales"], send_l, recv_l, self.group)
+        r_eid = exchange(st["eid"], send_l, recv_l, self.group)
+        f_recv = self.compute(r_codes, r_scales, r_eid)                   # (rows_recv, d) f32
+        f_back = exchange(f_recv, recv_l, send_l, self.group)             # rows in send order
+        return self.finish(st, f_back)
+
+    __call__ = forward
+
+
+# ---------------------------------------------------------------------------
+# Backends
+
+
+class CudaBackend:
+    """The B200 kernels.  `local` is a MoELayer built from this rank's experts
+    with expert_begin/n_experts set (router weight replicated)."""
+
+    def __init__(self, local):
+        self.layer = local
+
+    def route(self, x):
+        lay = self.layer
+        n = x.shape[0]
+        buf, _ = lay.workspace(n)
+        d = lay.desc()
+        _lib.check(_lib.lib().cq_moe_route(ctypes.byref(d), x.data_ptr(), _lib.dtype_code(x), n, buf.data_ptr(),
+                                           buf.numel(), _lib.stream()))
+        tr = lay.trace(n)
+        return tr["codes"], tr["scales"], tr["selected"], tr["weights"]
+
+    def experts(self, codes, scales, eid, n_local):
+        lay = self.layer
+        rows = codes.shape[0]
+        out = torch.zeros((rows, lay.d_model), dtype=torch.float32, device="cuda")
+        offsets = torch.zeros(n_local + 1, dtype=torch.int32, device="cuda")
+        if rows == 0:
+            self.last = (codes, scales, offsets, 0)
+            return out
+        order = torch.sort(eid.long(), stable=True).indices
+        counts = torch.bincount(eid.long(), minlength=n_local)
+        offsets[1:] = torch.cumsum(counts, 0).to(torch.int32)
+        g_codes, g_scales = codes[order].contiguous(), scales[order].contiguous()
+        self.last = (g_codes, g_scales, offsets, rows)   # grouped inputs of the last call (profiling)
+        f = torch.empty_like(out)
+        # received row counts vary per step: size the workspace by the next power of two
+        buf, _ = lay.workspace(1 << max(0, (-(-rows // lay.top_k) - 1).bit_length()))
+        d = lay.desc()
+        _lib.check(_lib.lib().cq_moe_experts(ctypes.byref(d), g_codes.data_ptr(), g_scales.data_ptr(),
+                                             offsets.data_ptr(), rows, f.data_ptr(), buf.data_ptr(), buf.numel(),
+                                             _lib.stream()))
+        out[order] = f
+        return out
+
+    def combine(self, selected, weights, f_routes):
+        n, k = selected.shape
+        d = f_routes.shape[1]
+        inv = torch.arange(n * k, dtype=torch.int32, device="cuda").view(n, k)
+        out = torch.empty((n, d), dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().cq_moe_combine(selected.data_ptr(), weights.data_ptr(), inv.data_ptr(),
+                                             f_routes.contiguous().data_ptr(), n, k, d, None, out.data_ptr(),
+                                             _lib.stream()))
+        return out

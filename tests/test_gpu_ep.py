@@ -1,0 +1,93 @@
+"""The expert-parallel driver on the CUDA backend (NCCL, world_size 1 on the
+single GPU this run has; the multi-rank exchange logic is covered by the gloo
+tests).  Routing, segment order and per-row arithmetic are the same as the
+single-GPU layer, so the outputs must be bitwise equal."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+pytestmark = pytest.mark.gpu
+
+from paper_2604_10496_b200.ep import CudaBackend, EPMoE  # noqa: E402
+from paper_2604_10496_b200.moe import ExpertStack, MoELayer  # noqa: E402
+from paper_2604_10496_b200.synthetic import moe_inputs_device  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def nccl_world1():
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("path", ["tc", "f32"])
+def test_ep_world1_equals_single_gpu_layer(nccl_world1, path):
+    n, d, ff, E, k, g = 48, 1024, 1536, 8, 2, 128
+    v, w, sites, _ = moe_inputs_device(5, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=path)
+    if path == "tc":
+        layer.prepare_tc()
+    want = layer(v).clone()
+    ep = EPMoE(CudaBackend(layer), E, k, rank=0, world=1)
+    got = ep(v)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
+def _shard(stack, begin, per):
+    return ExpertStack(stack.ids[begin:begin + per].contiguous(), stack.centroids[begin:begin + per].contiguous(),
+                       stack.d_in, stack.d_out, stack.group_size)
+
+
+@pytest.mark.parametrize("world,n_tok,E,k", [(2, 40, 8, 2), (4, 33, 8, 2), (2, 21, 6, 3)])
+def test_ep_sharded_ranks_in_one_process(world, n_tok, E, k):
+    """`world` ranks with E/world experts each, driven in one process: the
+    all_to_all exchanges are done here by concatenating the send segments.
+    Each rank's layer holds only its experts (expert_begin/n_local < E), so
+    this runs the sharded route/expert/combine kernels exactly as a real
+    multi-GPU run would."""
+    d, ff, g = 1024, 1536, 128
+    v, w, sites, _ = moe_inputs_device(11, n_tok, d, ff, E, g)
+    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
+    ref.prepare_tc()
+    want = ref(v).clone()
+    per = E // world
+    ranks = []
+    for r in range(world):
+        loc = MoELayer.from_stacks(w, *(_shard(s, r * per, per) for s in full), top_k=k, path="tc",
+                                   expert_begin=r * per, n_experts=E)
+        loc.prepare_tc()
+        ranks.append(EPMoE(CudaBackend(loc), E, k, rank=r, world=world))
+    bounds = [(r * n_tok // world, (r + 1) * n_tok // world) for r in range(world)]
+    states = [ep.dispatch(v[lo:hi]) for ep, (lo, hi) in zip(ranks, bounds)]
+    cuts = [np.concatenate([[0], np.cumsum(st["send"].tolist())]) for st in states]
+
+    def seg(st, c, key, q):
+        return st[key][int(c[q]):int(c[q + 1])]
+
+    back = [[None] * world for _ in range(world)]
+    for q, ep in enumerate(ranks):
+        parts = {key: torch.cat([seg(st, c, key, q) for st, c in zip(states, cuts)]) for key in ("codes", "scales",
+                                                                                                 "eid")}
+        f = ep.compute(parts["codes"], parts["scales"], parts["eid"])
+        off = 0
+        for r, (st, c) in enumerate(zip(states, cuts)):
+            cnt = int(c[q + 1] - c[q])
+            back[r][q] = f[off:off + cnt]
+            off += cnt
+    got = torch.cat([ep.finish(st, torch.cat(back[r])) for r, (ep, st) in enumerate(zip(ranks, states))])
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
