@@ -76,6 +76,7 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.rows, self.stop, self.thread = index, [], threading.Event(), None
+        self.ready = threading.Event()
 
     def _poll_nvml(self):
         import pynvml as nv
@@ -91,6 +92,7 @@ class ClockSampler:
             sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
             bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             self.rows.append((sm, mx, [v for k, v in names.items() if bits & k]))
+            self.ready.set()
             time.sleep(0.002)
         nv.nvmlShutdown()
 
@@ -99,7 +101,8 @@ class ClockSampler:
             import pynvml  # noqa: F401
             self.thread = threading.Thread(target=self._poll_nvml, daemon=True)
             self.thread.start()
-            time.sleep(0.01)
+            self.ready.wait(timeout=5.0)   # NVML init can take longer than a short timed region
+            self.rows.clear()
         except ImportError:
             self.thread = None
         return self
@@ -244,6 +247,7 @@ def profile_expert_stage(layer, codes_perm, scales_perm, offsets, R, iters):
     from paper_2604_10496_b200 import _lib as L
     off = offsets.cpu().numpy()
     n_active = int((np.diff(off) > 0).sum())
+    live = int(off[-1])                     # R is the row bound; bytes count the live rows
     desc = layer.desc()
     buf, _ = layer.workspace(max(1, -(-R // layer.top_k)))
     stage_ms = (ctypes.c_float * 3)()
@@ -251,7 +255,7 @@ def profile_expert_stage(layer, codes_perm, scales_perm, offsets, R, iters):
     L.check(L.lib().cq_moe_profile_experts(ctypes.byref(desc), codes_perm.data_ptr(), scales_perm.data_ptr(),
                                             offsets.data_ptr(), R, fexp.data_ptr(), buf.data_ptr(), buf.numel(),
                                             iters, stage_ms, L.stream()))
-    return n_active, layer_bytes(n_active, R), tuple(float(x) for x in stage_ms)
+    return n_active, layer_bytes(n_active, live), tuple(float(x) for x in stage_ms)
 
 
 def traffic_for(layout):
@@ -265,14 +269,14 @@ def traffic_for(layout):
 def run_ep(args, rank, world, local):
     """N > 1: expert parallelism.  Every rank holds E/N experts
     (identical seeded weights on all ranks, sliced) and its own batch of
-    tokens; a step is EPMoE.forward: route -> counts all_to_all -> codes /
-    scales / expert-id all_to_all -> grouped local experts -> inverse
-    all_to_all -> ascending-expert combine.  The counts exchange makes the
-    step host-synchronous, so it runs eagerly (no CUDA graph)."""
+    tokens; a step is EPStep: route -> device-side dispatch into fixed-capacity
+    slots -> all_to_all -> group by local expert -> grouped experts -> scatter
+    -> all_to_all back -> ascending-expert combine.  No host synchronisation,
+    so the step is captured in one CUDA graph."""
     import torch
     import torch.distributed as dist
     from paper_2604_10496_b200 import _lib as L
-    from paper_2604_10496_b200.ep import CudaBackend, EPMoE, expert_range
+    from paper_2604_10496_b200.ep import EPStep, expert_range
     from paper_2604_10496_b200.moe import ExpertStack, MoELayer
     from paper_2604_10496_b200.synthetic import moe_inputs_device
 
@@ -289,8 +293,7 @@ def run_ep(args, rank, world, local):
     gen = torch.Generator(device="cuda")
     gen.manual_seed(args.seed + 1000 + rank)
     v = torch.randn((n, d), generator=gen, device="cuda").to(torch.bfloat16)
-    backend = CudaBackend(layer)
-    ep = EPMoE(backend, E, k, rank, world)
+    step = EPStep(layer, n, rank, world)
     stream = torch.cuda.Stream()
 
     def barrier():
@@ -299,10 +302,25 @@ def run_ep(args, rank, world, local):
 
     with torch.cuda.stream(stream):
         c0 = L.launch_count()
-        ep(v)
+        step(v)
         launches_per_step = L.launch_count() - c0
+        for _ in range(2):
+            step(v)
+    torch.cuda.synchronize()
+    # one step (both NCCL exchanges included) in a CUDA graph; eager if capture is refused
+    graph, capture_err = None, None
+    try:
+        g_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_, stream=stream):
+            step(v)
+        graph = g_
+    except Exception as exc:
+        capture_err = repr(exc)[:200]
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else (lambda: step(v))
+    with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            ep(v)
+            run()
     torch.cuda.synchronize()
 
     def timed(fn):
@@ -320,21 +338,24 @@ def run_ep(args, rank, world, local):
         return float(t.item())
 
     with ClockSampler(local) as clk:
-        ms = timed(lambda: ep(v))
+        ms = timed(run)
 
+    # end to end through the public step: pinned host input -> device -> step -> host output
     x_host = v.cpu().pin_memory()
     y_host = torch.empty((n, d), dtype=torch.float32).pin_memory()
     x_dev = torch.empty_like(v)
 
     def e2e_step():
         x_dev.copy_(x_host, non_blocking=True)
-        y_host.copy_(ep(x_dev), non_blocking=True)
+        y_host.copy_(step(x_dev), non_blocking=True)
 
     e2e_ms = timed(e2e_step)
 
-    gc, gs, goff, R = backend.last
     with torch.cuda.stream(stream):
-        n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, gc, gs, goff, R, max(3, args.steps))
+        step(v)
+        n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, step.codes_perm, step.scales_perm,
+                                                                    step.offsets, step.slots, max(3, args.steps))
+    R = int(step.offsets[-1].item())
     pk = peaks()
     achieved = byt["gate_up"] / (gu_ms * 1e-3) / 1e9 if gu_ms > 0 else None
     if rank == 0:
@@ -346,7 +367,8 @@ def run_ep(args, rank, world, local):
             "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
                        "group_size": g, "batch_per_rank": n, "parallelism": f"ep{world}",
                        "experts_per_rank": per, "path": args.path, "layout": args.layout,
-                       "l2": "weights > L2, no flush needed", "cuda_graph": False},
+                       "l2": "weights > L2, no flush needed", "cuda_graph": graph is not None,
+                       "capacity_per_peer": step.cap, **({"capture_error": capture_err} if capture_err else {})},
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),
                     "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},

@@ -188,6 +188,40 @@ CQ_API cq_status cq_moe_combine(const int32_t *selected, const float *weights, c
                          const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
                          const float *add, float *out, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Expert parallelism, device-side planning (the reference has
+ * no multi-GPU path — these serve the EP driver paper_2604_10496_b200/ep.py).
+ * No host synchronisation: a whole EP step (route, dispatch, exchange, group,
+ * experts, scatter, exchange, combine) can be captured in one CUDA graph.
+ *
+ * Every rank sends each peer `capacity` slots of cq_ep_row_bytes(d_model)
+ * bytes ([codes][f32 scale][i32 local expert id][pad]; id -1 = empty), so both
+ * exchanges are equal-split all_to_alls.  capacity >= n_tokens *
+ * min(top_k, experts_per_rank).  Experts [r*per, (r+1)*per) live on rank r. */
+CQ_API int64_t cq_ep_row_bytes(int64_t d_model);
+/* Scratch bytes for cq_ep_dispatch / cq_ep_group with these sizes. */
+CQ_API int64_t cq_ep_scratch_bytes(int64_t n_tokens, int64_t top_k, int32_t world, int64_t capacity,
+                                   int64_t n_local);
+/* codes (n, d) int8, scales (n,), selected (n, k) global expert ids (cq_moe_route)
+ * -> send [world][capacity] rows, and inv (n, k) = slot of each route, i.e. the
+ * row of the returned [world][capacity][d] f32 buffer its output arrives in
+ * (feed to cq_moe_combine).  Slots are filled in (token, slot) order per peer. */
+CQ_API cq_status cq_ep_dispatch(const int8_t *codes, const float *scales, const int32_t *selected,
+                                int64_t n_tokens, int64_t top_k, int64_t d_model, int64_t experts_per_rank,
+                                int32_t world, int64_t capacity, uint8_t *send, int32_t *inv, void *scratch,
+                                void *stream);
+/* Received rows recv [slots] -> codes_perm (slots, d) / scales_perm grouped by
+ * local expert (stable in slot order), offsets (n_local+1), slot_of_row
+ * (grouped row -> slot).  Rows past offsets[n_local] are left untouched; pass
+ * `slots` as the row bound of cq_moe_experts. */
+CQ_API cq_status cq_ep_group(const uint8_t *recv, int64_t slots, int64_t d_model, int64_t n_local,
+                             int8_t *codes_perm, float *scales_perm, int32_t *offsets, int32_t *slot_of_row,
+                             void *scratch, void *stream);
+/* Grouped expert outputs fout (rows, d) -> back [slot] rows (slot order) for
+ * the return exchange; only the offsets[n_local] live rows are moved. */
+CQ_API cq_status cq_ep_scatter(const float *fout, const int32_t *offsets, const int32_t *slot_of_row,
+                               int64_t n_local, int64_t rows_bound, int64_t d_model, float *back, void *stream);
+
 /* One-time re-layout of one stacked site (rows = E*d_out) for the tensor-core path:
  * every row's centroids become `planes` int8 base-255 digit planes at one
  * per-row scale (m = rint(c / rowscale), |m| < 255^planes / 2), stored as

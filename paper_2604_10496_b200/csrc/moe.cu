@@ -41,8 +41,10 @@ int64_t umma_b_bytes(int64_t rows, int64_t d_in);
 // as the input quantizer.
 __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, const float *__restrict__ b,
                                                           int64_t ff, int8_t *__restrict__ codes,
-                                                          float *__restrict__ scales) {
+                                                          float *__restrict__ scales,
+                                                          const int32_t *__restrict__ live) {
     const int64_t row = blockIdx.x;
+    if (live != nullptr && row >= *live) return;
     float *ar = a + row * ff;
     const float *br = b + row * ff;
     float mx = 0.0f;
@@ -75,8 +77,10 @@ __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, 
 template <int V>
 __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__ a, const float *__restrict__ b,
                                                               int64_t ff, int8_t *__restrict__ codes,
-                                                              float *__restrict__ scales) {
+                                                              float *__restrict__ scales,
+                                                              const int32_t *__restrict__ live) {
     const int64_t row = blockIdx.x;
+    if (live != nullptr && row >= *live) return;
     float4 *ar = reinterpret_cast<float4 *>(a + row * ff);
     const float4 *br = reinterpret_cast<const float4 *>(b + row * ff);
     const int nv = (int)(ff >> 2);
@@ -116,20 +120,21 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     }
 }
 
+// `live` (device, nullable): rows at or past *live are skipped (EP slot bounds).
 cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                     cudaStream_t st) {
+                     const int32_t *live, cudaStream_t st) {
     if (rows == 0) return CQ_OK;
     const int64_t v = ceil_div(ff / 4, 512);
     if (ff % 4 == 0 && v <= 8) {
         switch (v) {
-            case 1: silu_quant_vec_kernel<1><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
-            case 2: silu_quant_vec_kernel<2><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
+            case 1: silu_quant_vec_kernel<1><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
+            case 2: silu_quant_vec_kernel<2><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
             case 3:
-            case 4: silu_quant_vec_kernel<4><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
-            default: silu_quant_vec_kernel<8><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales); break;
+            case 4: silu_quant_vec_kernel<4><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
+            default: silu_quant_vec_kernel<8><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
         }
     } else {
-        silu_quant_kernel<<<(unsigned)rows, 256, 0, st>>>(a, b, ff, codes, scales);
+        silu_quant_kernel<<<(unsigned)rows, 256, 0, st>>>(a, b, ff, codes, scales, live);
     }
     return check_launch("silu_quant");
 }
@@ -381,7 +386,7 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
         CQ_TRY(lut_umma_grouped(codes, reinterpret_cast<int8_t *>(frag_in), scales, offsets, n_seg, seg_first, rows,
                                 &gate, hidden, &up, bbuf, d, ff, st));
         if (ev) cudaEventRecord(ev[1], st);
-        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, st));
+        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, offsets + n_seg, st));
         if (ev) cudaEventRecord(ev[2], st);
         CQ_TRY(lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
                                 &down, fout, nullptr, nullptr, ff, d, st));

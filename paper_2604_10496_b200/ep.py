@@ -109,6 +109,90 @@ class EPMoE:
     __call__ = forward
 
 
+class EPStep:
+    """One rank's EP MoE step over fixed-capacity slots (csrc/ep.cu): no host
+    synchronisation, fixed buffers, so the whole step — including the two
+    equal-split all_to_alls — can be captured in a CUDA graph.
+
+    Same arithmetic and the same combine order as EPMoE / the single-GPU layer
+    (bitwise equal); slot padding costs exchange bytes, not compute (the
+    expert kernels read the live row count from the device offsets).
+
+    `layer` is this rank's MoELayer (expert_begin / n_local set), `n_tokens`
+    the fixed batch per rank.  `all_to_all(out, inp)` defaults to
+    dist.all_to_all_single over `group`."""
+
+    def __init__(self, layer, n_tokens: int, rank: int, world: int, group=None, all_to_all=None):
+        L = _lib.lib()
+        self.layer, self.n, self.rank, self.world = layer, int(n_tokens), rank, world
+        self.k, self.per, self.d = layer.top_k, layer.n_local, layer.d_model
+        if layer.n_experts != self.per * world or layer.expert_begin != rank * self.per:
+            raise ValueError("layer must hold experts [rank*per, (rank+1)*per) of n_experts = per*world")
+        self.cap = self.n * min(self.k, self.per)
+        self.slots = world * self.cap
+        rb = L.cq_ep_row_bytes(self.d)
+        dev = torch.device("cuda")
+        self.send = torch.empty((self.slots, rb), dtype=torch.uint8, device=dev)
+        self.recv = torch.empty_like(self.send)
+        self.inv = torch.empty((self.n, self.k), dtype=torch.int32, device=dev)
+        self.scratch = torch.empty(L.cq_ep_scratch_bytes(self.n, self.k, world, self.cap, self.per),
+                                   dtype=torch.uint8, device=dev)
+        self.codes_perm = torch.empty((self.slots, self.d), dtype=torch.int8, device=dev)
+        self.scales_perm = torch.empty(self.slots, dtype=torch.float32, device=dev)
+        self.offsets = torch.zeros(self.per + 1, dtype=torch.int32, device=dev)
+        self.slot_of_row = torch.empty(self.slots, dtype=torch.int32, device=dev)
+        self.fout = torch.empty((self.slots, self.d), dtype=torch.float32, device=dev)
+        self.back = torch.empty_like(self.fout)
+        self.ret = torch.empty_like(self.fout)
+        self.out = torch.empty((self.n, self.d), dtype=torch.float32, device=dev)
+        self.ws_route, _ = layer.workspace(self.n)
+        self.tr = layer.trace(self.n)
+        self.desc = layer.desc()
+        offs = (ctypes.c_int64 * len(_lib.WS_NAMES))()   # expert-stage scratch, separate from routing's
+        size = L.cq_moe_workspace(ctypes.byref(self.desc), -(-self.slots // self.k), offs)
+        self.ws_exp = torch.empty(max(size, 256), dtype=torch.uint8, device=dev)
+        if all_to_all is None:
+            def all_to_all(out, inp):
+                dist.all_to_all_single(out, inp, group=group)
+        self.a2a = all_to_all
+
+    def route_and_pack(self, x: torch.Tensor) -> None:
+        L, tr = _lib.lib(), self.tr
+        if x.shape != (self.n, self.d):
+            raise ValueError(f"EPStep is built for ({self.n}, {self.d}) inputs, got {tuple(x.shape)}")
+        _lib.check(L.cq_moe_route(ctypes.byref(self.desc), x.data_ptr(), _lib.dtype_code(x), self.n,
+                                  self.ws_route.data_ptr(), self.ws_route.numel(), _lib.stream()))
+        _lib.check(L.cq_ep_dispatch(tr["codes"].data_ptr(), tr["scales"].data_ptr(), tr["selected"].data_ptr(),
+                                    self.n, self.k, self.d, self.per, self.world, self.cap, self.send.data_ptr(),
+                                    self.inv.data_ptr(), self.scratch.data_ptr(), _lib.stream()))
+
+    def run_experts(self) -> None:
+        """recv -> grouped experts -> back (slot order)."""
+        L = _lib.lib()
+        _lib.check(L.cq_ep_group(self.recv.data_ptr(), self.slots, self.d, self.per, self.codes_perm.data_ptr(),
+                                 self.scales_perm.data_ptr(), self.offsets.data_ptr(), self.slot_of_row.data_ptr(),
+                                 self.scratch.data_ptr(), _lib.stream()))
+        _lib.check(L.cq_moe_experts(ctypes.byref(self.desc), self.codes_perm.data_ptr(), self.scales_perm.data_ptr(),
+                                    self.offsets.data_ptr(), self.slots, self.fout.data_ptr(),
+                                    self.ws_exp.data_ptr(), self.ws_exp.numel(), _lib.stream()))
+        _lib.check(L.cq_ep_scatter(self.fout.data_ptr(), self.offsets.data_ptr(), self.slot_of_row.data_ptr(),
+                                   self.per, self.slots, self.d, self.back.data_ptr(), _lib.stream()))
+
+    def combine(self) -> torch.Tensor:
+        tr = self.tr
+        _lib.check(_lib.lib().cq_moe_combine(tr["selected"].data_ptr(), tr["weights"].data_ptr(),
+                                             self.inv.data_ptr(), self.ret.data_ptr(), self.n, self.k, self.d,
+                                             None, self.out.data_ptr(), _lib.stream()))
+        return self.out
+
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        self.route_and_pack(x)
+        self.a2a(self.recv, self.send)
+        self.run_experts()
+        self.a2a(self.ret, self.back)
+        return self.combine()
+
+
 # ---------------------------------------------------------------------------
 # Backends
 

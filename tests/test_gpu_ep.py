@@ -13,7 +13,7 @@ import torch.distributed as dist
 
 pytestmark = pytest.mark.gpu
 
-from paper_2604_10496_b200.ep import CudaBackend, EPMoE  # noqa: E402
+from paper_2604_10496_b200.ep import CudaBackend, EPMoE, EPStep  # noqa: E402
 from paper_2604_10496_b200.moe import ExpertStack, MoELayer  # noqa: E402
 from paper_2604_10496_b200.synthetic import moe_inputs_device  # noqa: E402
 
@@ -91,3 +91,98 @@ def test_ep_sharded_ranks_in_one_process(world, n_tok, E, k):
     got = torch.cat([ep.finish(st, torch.cat(back[r])) for r, (ep, st) in enumerate(zip(ranks, states))])
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+def _sharded_layers(w, full, E, k, world, path="tc"):
+    per = E // world
+    out = []
+    for r in range(world):
+        loc = MoELayer.from_stacks(w, *(_shard(s, r * per, per) for s in full), top_k=k, path=path,
+                                   expert_begin=r * per, n_experts=E)
+        if path == "tc":
+            loc.prepare_tc()
+        out.append(loc)
+    return out
+
+
+def _run_ranks_in_process(steps, xs):
+    """Drive EPStep phases of all ranks, doing the two equal-split exchanges
+    by slicing: recv_q[src block] = send_src[q block]."""
+    world, cap = len(steps), steps[0].cap
+    for st, x in zip(steps, xs):
+        st.route_and_pack(x)
+    for q, st in enumerate(steps):
+        for src, other in enumerate(steps):
+            st.recv[src * cap:(src + 1) * cap].copy_(other.send[q * cap:(q + 1) * cap])
+    for st in steps:
+        st.run_experts()
+    for r, st in enumerate(steps):
+        for q, other in enumerate(steps):
+            st.ret[q * cap:(q + 1) * cap].copy_(other.back[r * cap:(r + 1) * cap])
+    return [st.combine().clone() for st in steps]
+
+
+@pytest.mark.parametrize("world,n_tok,E,k,path", [(2, 40, 8, 2, "tc"), (4, 32, 8, 2, "tc"), (8, 16, 8, 2, "tc"),
+                                                  (2, 21, 6, 3, "tc"), (2, 24, 8, 2, "f32")])
+def test_ep_step_slots_match_single_gpu_layer(world, n_tok, E, k, path):
+    """Fixed-capacity EP step (device-side dispatch / group / scatter): every
+    rank's combined output equals the single-GPU layer's rows bit for bit."""
+    d, ff, g = 1024, 1536, 128
+    v, w, sites, _ = moe_inputs_device(13, n_tok * world, d, ff, E, g)
+    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    ref = MoELayer.from_stacks(w, *full, top_k=k, path=path)
+    if path == "tc":
+        ref.prepare_tc()
+    want = ref(v).clone()
+    layers = _sharded_layers(w, full, E, k, world, path)
+    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
+    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
+def test_ep_step_skewed_routing_fills_one_rank():
+    """All tokens routed to the experts of rank 0 (router columns of the other
+    ranks pushed to -inf-like values): rank 0's slots fill to capacity, the
+    other ranks receive nothing and run no expert rows."""
+    world, n_tok, E, k, d, ff, g = 4, 16, 8, 2, 1024, 1536, 128
+    v, w, sites, _ = moe_inputs_device(17, n_tok * world, d, ff, E, g)
+    w = w.clone()
+    w[:, 2:] = -1e3 * w[:, 2:].abs() - 1.0   # experts 0, 1 (rank 0) always win
+    v = v.abs() + 0.01                        # positive inputs keep the margin
+    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
+    ref.prepare_tc()
+    want = ref(v).clone()
+    assert set(ref.trace(n_tok * world)["selected"].unique().tolist()) <= {0, 1}
+    layers = _sharded_layers(w, full, E, k, world)
+    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
+    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert steps[0].offsets[-1].item() == n_tok * world * k
+    assert all(st.offsets[-1].item() == 0 for st in steps[1:])
+
+
+def test_ep_step_world1_nccl_graph_capture(nccl_world1):
+    """The whole EP step (NCCL all_to_all included) captured in a CUDA graph
+    and replayed equals the eager single-GPU layer."""
+    n, d, ff, E, k, g = 32, 1024, 1536, 8, 2, 128
+    v, w, sites, _ = moe_inputs_device(23, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
+    layer.prepare_tc()
+    want = layer(v).clone()
+    step = EPStep(layer, n, 0, 1)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        eager = step(v).clone()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            step(v)
+        step.out.zero_()
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(eager, want)
+    assert torch.equal(step.out, want)
