@@ -13,9 +13,9 @@
 namespace cq {
 
 // --- stage kernels defined in other units
-cq_status quantize_a4(const void *, int, int64_t, int64_t, int8_t *, float *, int *, cudaStream_t);
-cq_status router_logits(const int8_t *, const float *, const float *, int64_t, int64_t, int64_t, float *,
-                        cudaStream_t);
+cq_status quantize_a4(const void *, int, int64_t, int64_t, int8_t *, float *, int *, float *, cudaStream_t);
+cq_status router_logits(const int8_t *, const float *, const float *, const float *, int64_t, int64_t, int64_t,
+                        float *, cudaStream_t);
 cq_status topk(const float *, int64_t, int64_t, int64_t, int32_t *, float *, int32_t *, int64_t, int64_t,
                cudaStream_t);
 cq_status permute(const int32_t *, const int32_t *, int64_t, int64_t, int64_t, int64_t, int32_t *,
@@ -411,7 +411,7 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
         CQ_TRY(check_launch("silu_mul"));
     }
     if (ev) cudaEventRecord(ev[1], st);
-    CQ_TRY(quantize_a4(hidden, CQ_DTYPE_F32, rows, ff, hcodes, hscales, nullptr, st));
+    CQ_TRY(quantize_a4(hidden, CQ_DTYPE_F32, rows, ff, hcodes, hscales, nullptr, nullptr, st));
     if (ev) cudaEventRecord(ev[2], st);
     if (ev) {
         cq_status rc;
@@ -460,8 +460,9 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
         qin = w.rotated;
         qdt = CQ_DTYPE_F32;
     }
-    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, st));
-    CQ_TRY(router_logits(w.codes, w.scales, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
+    // the dequantized rows (router input) go to the fout buffer, unused until the down GEMM
+    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, w.fout, st));
+    CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
     if (cudaMemsetAsync(w.counts, 0, (dsc->n_experts + 1) * 4, st) != cudaSuccess) {
         set_error("moe: memset counts failed");
         return CQ_ERR_CUDA;

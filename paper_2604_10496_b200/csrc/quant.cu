@@ -16,7 +16,8 @@ template <int DT>
 __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict__ x, int64_t d,
                                                           int8_t *__restrict__ codes,
                                                           float *__restrict__ scales,
-                                                          int *__restrict__ nonfinite) {
+                                                          int *__restrict__ nonfinite,
+                                                          float *__restrict__ deq) {
     const int64_t row = blockIdx.x;
     const int64_t base = row * d;
     float mx = 0.0f;
@@ -43,7 +44,12 @@ __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict
     }
     __syncthreads();
     const float s = s_sh;
-    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) codes[base + j] = a4_code(load_x<DT>(x, base + j), s);
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+        const int8_t c = a4_code(load_x<DT>(x, base + j), s);
+        codes[base + j] = c;
+        // dequantized value, rounded exactly as codes.astype(f32) * scales (model.py:379-381)
+        if (deq != nullptr) deq[base + j] = __fmul_rn((float)c, s);
+    }
 }
 
 __global__ void unpack_ids_kernel(const uint8_t *__restrict__ packed, int64_t rows, int64_t d_in,
@@ -58,13 +64,14 @@ __global__ void unpack_ids_kernel(const uint8_t *__restrict__ packed, int64_t ro
     }
 }
 
+// deq (nullable): also write code * scale as f32 (the router's input).
 cq_status quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes, float *scales,
-                      int *nonfinite_dev, cudaStream_t st) {
+                      int *nonfinite_dev, float *deq, cudaStream_t st) {
     if (n == 0) return CQ_OK;
     if (dtype == CQ_DTYPE_F32)
-        quantize_a4_kernel<CQ_DTYPE_F32><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev);
+        quantize_a4_kernel<CQ_DTYPE_F32><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev, deq);
     else
-        quantize_a4_kernel<CQ_DTYPE_BF16><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev);
+        quantize_a4_kernel<CQ_DTYPE_BF16><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev, deq);
     return check_launch("quantize_a4");
 }
 
@@ -96,7 +103,7 @@ extern "C" cq_status cq_quantize_a4(const void *x, int dtype, int64_t n, int64_t
             return CQ_ERR_CUDA;
         }
     }
-    cq_status rc = quantize_a4(x, dtype, n, d, codes, scales, flag, st);
+    cq_status rc = quantize_a4(x, dtype, n, d, codes, scales, flag, nullptr, st);
     if (check_finite) {
         int host = 0;
         cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);

@@ -50,170 +50,90 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
                  : "memory");
 }
 
-// Same chains, with the W / code chunks double-buffered by cp.async so the
-// next chunk lands while the current one is consumed (d % 16 == 0 and
-// rk * E % 4 == 0; the kernel above covers every other shape).
-__global__ void router_logits_async_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
-                                           const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp, int rk,
-                                           float *__restrict__ logits) {
-    extern __shared__ __align__(16) float rsm[];
-    const int tt_n = blockDim.x / (int)n_exp;
-    const int wsz = rk * (int)n_exp, csz = tt_n * rk;  // floats of W, bytes of codes per buffer
-    float *wbuf[2] = {rsm, rsm + wsz};
-    int8_t *cbuf[2] = {reinterpret_cast<int8_t *>(rsm + 2 * wsz), reinterpret_cast<int8_t *>(rsm + 2 * wsz) + csz};
-    const int t_loc = threadIdx.x / (int)n_exp, e = threadIdx.x % (int)n_exp;
-    const int64_t t0 = blockIdx.x * (int64_t)tt_n;
-    const int64_t t = t0 + t_loc;
-    const bool live = t_loc < tt_n && t < n;
-    const float s = live ? __ldg(scales + t) : 0.0f;
+// Same chains on the dequantized rows x = fl(q * s) that the quantizer writes
+// alongside the codes (quant.cu), so a chain step is one FMUL (off the
+// critical path) and one dependent FADD.  CTA = TT tokens x E experts <= 128
+// chains = 4 warps, one per SMSP; x rows and W rows are staged RK columns at a
+// time by cp.async, double-buffered.  Per element and lane: a quarter of a
+// broadcast LDS.128 (x), one LDS (w), FMUL, FADD — under the 4-cycle FADD
+// latency, which is the floor (d dependent adds per chain).
+constexpr int RD_THREADS = 128;
+
+// EC: n_exp as a compile-time constant (w offsets become immediates), 0 = runtime.
+template <int EC>
+__global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__restrict__ xdeq,
+                                                                const float *__restrict__ w, int64_t n, int64_t d,
+                                                                int64_t n_exp, int tt, int rk,
+                                                                float *__restrict__ logits) {
+    extern __shared__ __align__(16) float rds[];
+    const int E = EC ? EC : (int)n_exp;
+    float *xs = rds;                         // [2][tt][rk]
+    float *ws = rds + (size_t)2 * tt * rk;   // [2][rk][E]
+    const int tid = threadIdx.x;
+    const int64_t t0 = blockIdx.x * (int64_t)tt;
+    const int t_loc = tid / E, e = tid - t_loc * E;
+    const bool chain = t_loc < tt;
+    const bool live = chain && t0 + t_loc < n;
     const int n_chunks = (int)((d + rk - 1) / rk);
-    auto load = [&](int ci, int b) {
-        const int64_t k0 = (int64_t)ci * rk;
+    auto stage = [&](int i) {
+        const int b = i & 1;
+        const int64_t k0 = (int64_t)i * rk;
         const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
-        for (int x = threadIdx.x * 4; x < kn * n_exp; x += blockDim.x * 4) cp_async16(wbuf[b] + x, w + k0 * n_exp + x);
-        const int rowv = kn / 16;
-        for (int x = threadIdx.x; x < tt_n * rowv; x += blockDim.x) {
+        float *wsb = ws + (size_t)b * rk * E;
+        for (int x = tid; x < kn * E / 4; x += RD_THREADS) cp_async16(wsb + 4 * x, w + k0 * E + 4 * x);
+        const int rowv = kn / 4;
+        float *xsb = xs + (size_t)b * tt * rk;
+        for (int x = tid; x < tt * rowv; x += RD_THREADS) {
             const int tl = x / rowv, v = x - tl * rowv;
             const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // clamp: rows past n are never consumed
-            cp_async16(cbuf[b] + tl * rk + v * 16, codes + tg * d + k0 + v * 16);
+            cp_async16(xsb + tl * rk + 4 * v, xdeq + tg * d + k0 + 4 * v);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    load(0, 0);
+    stage(0);
     float acc = 0.0f;
-    for (int ci = 0; ci < n_chunks; ++ci) {
-        const int b = ci & 1;
-        if (ci + 1 < n_chunks) {
-            load(ci + 1, b ^ 1);
+    for (int i = 0; i < n_chunks; ++i) {
+        const int b = i & 1;
+        if (i + 1 < n_chunks) {
+            stage(i + 1);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        const int64_t k0 = (int64_t)ci * rk;
-        const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
-        if (live) {
-            const int8_t *cr = cbuf[b] + t_loc * rk;
-            const float *wr = wbuf[b] + e;
-#pragma unroll 8
-            for (int kk = 0; kk < kn; ++kk)
-                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn((float)cr[kk], s), wr[kk * n_exp]));
+        const int kn = (int)((d - (int64_t)i * rk) < rk ? (d - (int64_t)i * rk) : rk);  // multiple of 16
+        if (chain) {
+            const float4 *xr = reinterpret_cast<const float4 *>(xs + (size_t)b * tt * rk + t_loc * rk);
+            const float *wr = ws + (size_t)b * rk * E + e;
+            // register double buffer: the next 16 (x, w) pairs load while the
+            // current 16 dependent adds run
+            float xc[16], wc[16], xn[16], wn[16];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float4 v = xr[u];
+                xc[4 * u] = v.x, xc[4 * u + 1] = v.y, xc[4 * u + 2] = v.z, xc[4 * u + 3] = v.w;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) wc[u] = wr[u * E];
+            for (int j = 16; j < kn; j += 16) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float4 v = xr[(j >> 2) + u];
+                    xn[4 * u] = v.x, xn[4 * u + 1] = v.y, xn[4 * u + 2] = v.z, xn[4 * u + 3] = v.w;
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) wn[u] = wr[(j + u) * E];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, __fmul_rn(xc[u], wc[u]));
+#pragma unroll
+                for (int u = 0; u < 16; ++u) xc[u] = xn[u], wc[u] = wn[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, __fmul_rn(xc[u], wc[u]));
         }
         __syncthreads();  // buffer b is refilled by the next iteration's prefetch
     }
-    if (live) logits[t * n_exp + e] = acc;
-}
-
-// Same chains, split so the serial part is only the additions: 128 producer
-// threads form the products p[k][j] = fl(fl(q[t,k] * s_t) * W[k,e]) for a
-// chunk of RK columns into shared memory while the chain threads (one per
-// (token, expert) pair, CH per CTA) add the previous chunk in k order.  Named
-// barriers double-buffer the product chunks.  The dependent fp32 adds are
-// the floor (~4 cycles each).
-constexpr int RC_PROD = 128;
-
-// Shared-memory plan of router_chain_kernel for chunk size rk: double-buffered
-// codes [tt][rk] i8, W [rk][E] f32 and products [rk][ch] f32.
-struct RcPlan {
-    int rk;
-    size_t codes, wts, prod, total;
-};
-
-__host__ __device__ inline RcPlan rc_plan(int rk, int tt, int ch, int64_t n_exp) {
-    RcPlan p;
-    p.rk = rk;
-    p.codes = 0;
-    p.wts = (((size_t)2 * tt * rk + 15) / 16) * 16;
-    p.prod = p.wts + (size_t)2 * rk * n_exp * 4;
-    p.total = p.prod + (size_t)2 * rk * ch * 4;
-    return p;
-}
-
-__global__ void router_chain_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
-                                    const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp, int tt, int ch,
-                                    int rk, float *__restrict__ logits) {
-    extern __shared__ __align__(16) uint8_t rsm_raw[];
-    const RcPlan plan = rc_plan(rk, tt, ch, n_exp);
-    int8_t *cst = reinterpret_cast<int8_t *>(rsm_raw + plan.codes);   // [2][tt][rk]
-    float *wst = reinterpret_cast<float *>(rsm_raw + plan.wts);       // [2][rk][E]
-    float *prod = reinterpret_cast<float *>(rsm_raw + plan.prod);     // [2][rk][ch]
-    const int tid = threadIdx.x;
-    const int64_t t0 = blockIdx.x * (int64_t)tt;
-    const int n_chunks = (int)((d + rk - 1) / rk);
-    const int nthreads = ch + RC_PROD;
-    if (tid < ch) {
-        // ---- chain threads: the ordered adds only
-        const int t_loc = tid / (int)n_exp, e = tid % (int)n_exp;
-        const bool live = t_loc < tt && t0 + t_loc < n;
-        float acc = 0.0f;
-        for (int i = 0; i < n_chunks; ++i) {
-            const int b = i & 1;
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + b), "r"(nthreads) : "memory");
-            const int kn = (int)((d - (int64_t)i * rk) < rk ? (d - (int64_t)i * rk) : rk);
-            const float *pb = prod + (size_t)b * rk * ch + tid;
-            int kk = 0;
-            if (kn >= 16) {
-                float cur[16], nxt[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) cur[u] = pb[u * ch];
-                for (kk = 16; kk + 16 <= kn; kk += 16) {
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) nxt[u] = pb[(kk + u) * ch];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, cur[u]);
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
-                }
-#pragma unroll
-                for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, cur[u]);
-            }
-            for (; kk < kn; ++kk) acc = __fadd_rn(acc, pb[kk * ch]);
-            if (i + 2 < n_chunks) asm volatile("bar.arrive %0, %1;" ::"r"(3 + b), "r"(nthreads) : "memory");
-        }
-        if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
-    } else {
-        // ---- helpers: stage codes + W of chunk i+1 (cp.async) while forming
-        // the products of chunk i from shared memory
-        const int pt = tid - ch;
-        auto stage = [&](int i) {
-            const int b = i & 1;
-            const int64_t k0 = (int64_t)i * rk;
-            const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
-            for (int x = pt * 4; x < kn * (int)n_exp; x += RC_PROD * 4)
-                cp_async16(wst + (size_t)b * rk * n_exp + x, w + k0 * n_exp + x);
-            const int rowv = kn / 16;
-            for (int x = pt; x < tt * rowv; x += RC_PROD) {
-                const int tl = x / rowv, v = x - tl * rowv;
-                const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;
-                cp_async16(cst + (size_t)b * tt * rk + tl * rk + v * 16, codes + tg * d + k0 + v * 16);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        const int j = pt % ch, kk0 = pt / ch, kstep = RC_PROD / ch;
-        const int t_loc = j / (int)n_exp, e = j - t_loc * (int)n_exp;
-        const bool live = t_loc < tt && t0 + t_loc < n;
-        const float s = live ? __ldg(scales + t0 + t_loc) : 0.0f;
-        stage(0);
-        for (int i = 0; i < n_chunks; ++i) {
-            const int b = i & 1;
-            if (i + 1 < n_chunks) {
-                stage(i + 1);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
-            asm volatile("bar.sync 5, %0;" ::"r"(RC_PROD) : "memory");  // chunk i staged by every helper
-            if (i >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + b), "r"(nthreads) : "memory");
-            const int kn = (int)((d - (int64_t)i * rk) < rk ? (d - (int64_t)i * rk) : rk);
-            const int8_t *cr = cst + (size_t)b * tt * rk + (live ? t_loc : 0) * rk;
-            const float *wr = wst + (size_t)b * rk * n_exp + e;
-            float *pb = prod + (size_t)b * rk * ch + j;
-            for (int kk = kk0; kk < kn; kk += kstep)
-                pb[kk * ch] = live ? __fmul_rn(__fmul_rn((float)cr[kk], s), wr[kk * n_exp]) : 0.0f;
-            asm volatile("bar.arrive %0, %1;" ::"r"(1 + b), "r"(nthreads) : "memory");
-            asm volatile("bar.sync 5, %0;" ::"r"(RC_PROD) : "memory");  // stage buffer b reusable
-        }
-    }
+    if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
 }
 
 // numpy's float32 sum of a short row: a plain loop below 8 elements, eight
@@ -350,33 +270,42 @@ __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *
     }
 }
 
-cq_status router_logits(const int8_t *codes, const float *scales, const float *w, int64_t n,
+// xdeq (nullable): the dequantized rows code * scale from the quantizer.
+cq_status router_logits(const int8_t *codes, const float *scales, const float *xdeq, const float *w, int64_t n,
                         int64_t d, int64_t n_exp, float *logits, cudaStream_t st) {
     if (n * n_exp == 0) return CQ_OK;
     if (n_exp > 256) {
         set_error("router: at most 256 experts");
         return CQ_ERR_CONFIG;
     }
-    if (n_exp <= 128 && d % 16 == 0) {
-        // chains per CTA: >= one warp; staging + products double-buffered in <= 48 KB
-        const int tt2 = (int)std::max<int64_t>(1, 32 / n_exp);
-        const int ch = (int)(ceil_div(tt2 * n_exp, 32) * 32);
-        int rk = 256;
-        while (rk > 16 && rc_plan(rk, tt2, ch, n_exp).total > 48 * 1024) rk -= 16;
-        const size_t smem = rc_plan(rk, tt2, ch, n_exp).total;
-        router_chain_kernel<<<(unsigned)ceil_div(n, tt2), (unsigned)(ch + RC_PROD), smem, st>>>(
-            codes, scales, w, n, d, n_exp, tt2, ch, rk, logits);
+    if (xdeq != nullptr && n_exp <= RD_THREADS && d % 16 == 0) {
+        const int tt = RD_THREADS / (int)n_exp;
+        // double-buffered x [tt][rk] + W [rk][E] f32 in <= 96 KB; rk a multiple of 16, <= 512
+        int rk = (int)std::min<int64_t>(512, ((96 * 1024) / (8 * (tt + n_exp))) & ~15LL);
+        if (rk < 16) rk = 16;
+        const size_t smem = (size_t)8 * rk * (tt + n_exp);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(router_deq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(router_deq_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(router_deq_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(router_deq_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(router_deq_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            attr = true;
+        }
+        const dim3 grid((unsigned)ceil_div(n, tt));
+        switch (n_exp) {
+            case 8: router_deq_kernel<8><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 16: router_deq_kernel<16><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 64: router_deq_kernel<64><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 128:
+                router_deq_kernel<128><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
+                break;
+            default: router_deq_kernel<0><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
+        }
         return check_launch("router_logits");
     }
     const int tt = (int)(256 / n_exp);
-    if (d % 16 == 0) {
-        // double-buffered W chunk [rk][E] f32 + codes [tt][rk] i8 in <= 48 KB of shared memory
-        const int rk = (int)std::max<int64_t>(16, std::min<int64_t>(256, (24576 / (4 * n_exp + tt)) & ~15LL));
-        const size_t smem = 2 * ((size_t)rk * n_exp * sizeof(float) + (size_t)tt * rk);
-        router_logits_async_kernel<<<(unsigned)ceil_div(n, tt), (unsigned)(tt * n_exp), smem, st>>>(
-            codes, scales, w, n, d, n_exp, rk, logits);
-        return check_launch("router_logits");
-    }
     // W chunk [rk][E] + inputs [tt][rk] in <= 48 KB of shared memory
     const int rk = (int)std::max<int64_t>(16, std::min<int64_t>(256, (12288 / (n_exp + tt)) & ~15LL));
     const size_t smem = ((size_t)rk * n_exp + (size_t)tt * rk) * sizeof(float);
