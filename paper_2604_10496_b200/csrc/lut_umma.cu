@@ -79,6 +79,14 @@ __device__ __forceinline__ uint32_t hi16(uint32_t x) {
     return r;
 }
 
+// a | b for halves with disjoint non-zero bytes (== a + b, no carries), as an
+// integer multiply-add so it issues on the FMA pipe instead of the saturated ALU pipe.
+__device__ __forceinline__ uint32_t u_merge(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t u_prmt(uint32_t a, uint32_t b, uint32_t s) {
     uint32_t d;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     for (int p = 0; p < P; ++p)
 #pragma unroll
                         for (int cc = 0; cc < 8; ++cc)
-                            v[p * 8 + cc] = u_prmt(L[p].x, L[p].y, sel[cc]) | u_prmt(L[p].z, L[p].w, xsel[cc]);
+                            v[p * 8 + cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
                     tc_st16(abase, v);
                     if (P == 3) tc_st8(abase + 16, v + 16);
                 } else {
