@@ -63,8 +63,13 @@ struct UmStage {
     static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per k-step
     static constexpr int CCOLS = 4 * ACOLS;                      // TMEM columns per A stage (one chunk)
     static constexpr int ACC = P * um::NTOK;                     // accumulator columns
-    static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages (chunks in flight)
+    static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages that fit in TMEM
     static_assert(NCS >= 2, "TMEM budget");
+    // One ring for the smem stages and the TMEM A stages (chunk c uses slot
+    // c % RING of both).  full[s] for chunk c means the producer refilled slot s,
+    // which it does only after the MMAs of chunk c - RING completed (empty[s]),
+    // so the A stage is free too: expanders wait on one barrier per chunk.
+    static constexpr int RING = NCS < um::STAGES ? NCS : um::STAGES;
 };
 
 // ---------------------------------------------------------------------------
@@ -206,10 +211,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     float *__restrict__ out0, const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1,
     const float *__restrict__ rs1, float *__restrict__ out1, int d_in, int d_out, int g) {
     using S = UmStage<P, MERGED>;
-    constexpr int NCS = S::NCS;
+    constexpr int RING = S::RING;
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t full_bar[um::STAGES], empty_bar[um::STAGES];
-    __shared__ __align__(8) uint64_t afull_bar[NCS], aempty_bar[NCS];
+    __shared__ __align__(8) uint64_t full_bar[RING], empty_bar[RING], afull_bar[RING];
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
 
@@ -227,13 +231,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int n_chunks = d_in / 128, cpg = g / 128, n_groups = d_in / g;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < um::STAGES; ++s) {
+        for (int s = 0; s < RING; ++s) {
             u_bar_init(u_smem(&full_bar[s]), 1);
             u_bar_init(u_smem(&empty_bar[s]), 1);
-        }
-        for (int s = 0; s < NCS; ++s) {
             u_bar_init(u_smem(&afull_bar[s]), um::EXP_WARPS);  // every expander warp writes its k-step
-            u_bar_init(u_smem(&aempty_bar[s]), 1);
         }
         u_bar_init(u_smem(&accfull_bar), 1);
         u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
@@ -265,8 +266,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 const int ntc16 = (ntc + 1) & ~1;  // MMA N is a multiple of 16
                 int gc = 0;  // chunk index within the current group
                 for (int c = 0; c < n_chunks; ++c, ++it) {
-                    const int s = it % um::STAGES;
-                    if (it >= um::STAGES) u_bar_wait(u_smem(&empty_bar[s]), ((it / um::STAGES) - 1) & 1);
+                    const int s = it % RING;
+                    if (it >= RING) u_bar_wait(u_smem(&empty_bar[s]), ((it / RING) - 1) & 1);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     const bool new_group = gc == 0;
                     const uint32_t bar = u_smem(&full_bar[s]);
@@ -290,13 +291,12 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             const uint32_t idesc = idesc_i8(((ntc + 1) & ~1) * 8);
             if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
             for (int c = 0; c < n_chunks; ++c, ++it) {
-                const int s = it % um::STAGES;
-                const int cs = it % NCS;
-                u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
-                u_bar_wait(u_smem(&afull_bar[cs]), (it / NCS) & 1);
+                const int s = it % RING;
+                // afull[s] implies full[s]: every expander waited for the chunk's data
+                u_bar_wait(u_smem(&afull_bar[s]), (it / RING) & 1);
                 tc_fence_after();
                 const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
-                const uint32_t abase = tmem + a_col0 + (uint32_t)(cs * S::CCOLS);
+                const uint32_t abase = tmem + a_col0 + (uint32_t)(s * S::CCOLS);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                     // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
@@ -309,8 +309,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                                   idesc, accum);
                     }
                 }
-                tc_commit_elect(u_smem(&aempty_bar[cs]));
-                tc_commit_elect(u_smem(&empty_bar[s]));
+                tc_commit_elect(u_smem(&empty_bar[s]));  // frees the smem stage and the A stage
                 if (c == n_chunks - 1) tc_commit_elect(u_smem(&accfull_bar));
             }
         }
@@ -329,10 +328,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             uint4 L[P];
             int gc = 0;
             for (int c = 0; c < n_chunks; ++c, ++it) {
-                const int s = it % um::STAGES;
-                const int cs = it % NCS;
-                if (it >= (uint32_t)NCS) u_bar_wait(u_smem(&aempty_bar[cs]), ((it / NCS) - 1) & 1);
-                u_bar_wait(u_smem(&full_bar[s]), (it / um::STAGES) & 1);
+                const int s = it % RING;
+                u_bar_wait(u_smem(&full_bar[s]), (it / RING) & 1);
                 tc_fence_after();
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
                 if (gc == 0) {
@@ -352,7 +349,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     xsel[2 * q] = x;
                     xsel[2 * q + 1] = hi16(x);
                 }
-                const uint32_t abase = tmem + lane_addr + a_col0 + (uint32_t)(cs * S::CCOLS + wg * S::ACOLS);
+                const uint32_t abase = tmem + lane_addr + a_col0 + (uint32_t)(s * S::CCOLS + wg * S::ACOLS);
                 if (MERGED) {
                     uint32_t v[P * 8];
 #pragma unroll
@@ -377,7 +374,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) u_bar_arrive(u_smem(&afull_bar[cs]));
+                if (lane == 0) u_bar_arrive(u_smem(&afull_bar[s]));
             }
             // ---- epilogue of this pass: accumulators -> fp32 out (warpgroup wg: token columns 8wg..8wg+7)
             u_bar_wait(u_smem(&accfull_bar), pass & 1);
@@ -481,9 +478,9 @@ __global__ void lut_relayout_kernel(const int8_t *__restrict__ lut16, int64_t ro
 
 bool umma_ok(int64_t d_in, int64_t d_out, int64_t g) { return d_in % 128 == 0 && g % 128 == 0 && d_out % 128 == 0; }
 
-template <int P>
+template <int P, bool MERGED>
 size_t umma_smem() {
-    return (size_t)um::STAGES * UmStage<P, false>::BYTES;
+    return (size_t)UmStage<P, MERGED>::RING * UmStage<P, MERGED>::BYTES;
 }
 
 cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, int32_t *sums,
@@ -510,7 +507,7 @@ cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales,
                       const int32_t *offsets, int64_t n_seg, int64_t seg_first, const cq_expert_site *a, float *out_a,
                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
     static bool attr = false;
-    const size_t smem = umma_smem<P>();
+    const size_t smem = umma_smem<P, MERGED>();
     if (!attr) {
         cudaFuncSetAttribute(lut_umma_kernel<P, MERGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
