@@ -15,7 +15,8 @@ import torch
 from .errors import ConfigError, DivergenceError, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcq_b200.so")
+# CQ_B200_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("CQ_B200_LIB") or os.path.join(_HERE, "libcq_b200.so")
 
 CQ_OK, CQ_ERR_SHAPE, CQ_ERR_CONFIG, CQ_ERR_DIVERGENCE, CQ_ERR_CUDA, CQ_ERR_UNSUPPORTED = range(6)
 CQ_DTYPE_F32, CQ_DTYPE_BF16 = 0, 1

@@ -41,6 +41,8 @@
 // by the row scale and the token scale, store fp32.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace cq {
 
 namespace um {
@@ -65,11 +67,17 @@ struct UmStage {
     static constexpr int ACC = P * um::NTOK;                     // accumulator columns
     static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages that fit in TMEM
     static_assert(NCS >= 2, "TMEM budget");
-    // One ring for the smem stages and the TMEM A stages (chunk c uses slot
-    // c % RING of both).  full[s] for chunk c means the producer refilled slot s,
-    // which it does only after the MMAs of chunk c - RING completed (empty[s]),
-    // so the A stage is free too: expanders wait on one barrier per chunk.
-    static constexpr int RING = NCS < um::STAGES ? NCS : um::STAGES;
+    // Chunk c uses TMEM A stage c % NA and smem stage c % NS, NS = NA + LAG.
+    // The producer issues chunk c's copies once the MMAs of chunk c - NS are
+    // done (empty[c % NS]) — NS chunks of data in flight — but makes full[c % NS]
+    // completable (its arrive.expect_tx) only LAG iterations later, after the
+    // empty wait for chunk c + LAG, i.e. once the MMAs of chunk c - NA are done
+    // and A stage c % NA is free.  So full[] alone tells an expander that both
+    // the data and the A stage are ready: one barrier wait per chunk.
+    static constexpr int NA = NCS < um::STAGES ? NCS : um::STAGES;
+    static constexpr int LAG = 0;  // > 0: issue copies LAG chunks before arming them (measured slower)
+    static constexpr int NS = NA + LAG;
+    static_assert(NS * BYTES <= 200 * 1024, "smem budget");
 };
 
 // ---------------------------------------------------------------------------
@@ -137,6 +145,21 @@ __device__ __forceinline__ void u_bulk_elect(uint32_t dst, const void *src, uint
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ uint32_t u_pin(uint32_t x) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+__device__ __forceinline__ void cp_async4(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(u_smem(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void u_prefetch_elect(const void *src, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(src),
+        "r"(bytes)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -202,40 +225,164 @@ __device__ __forceinline__ uint32_t idesc_i8(int n) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-// grid: (d_out / 128, n_seg, n_mat); blockIdx.z picks the matrix (gate / up).
+// ---------------------------------------------------------------------------
+// Work decomposition: persistent, data-parallel rounds + a stream-K tail.  A
+// unit is one 128-row tile of one matrix for one pass of <= NTOK tokens of one
+// segment; its d_in/128 chunks are iterations.  With G CTAs (one per SM),
+// CTA b first runs whole units b, b+G, b+2G, ... (the order of a plain grid,
+// so concurrent CTAs stream neighbouring tiles) for the full rounds; the R < G
+// leftover units, which would otherwise form a mostly idle last wave, are
+// split by iterations into equal contiguous ranges over the first G_t CTAs
+// (>= MIN_ITERS chunks each).  A unit cut by a range boundary is finished by
+// whichever of its CTAs arrives last on a per-unit counter: the others leave
+// their int32 partial accumulators in `part`, the last one adds them before
+// the epilogue.  Integer sums are exact, so the result does not depend on the
+// split.  Every CTA pays the prologue and the pipeline fill once.
+namespace um {
+constexpr int MAX_SEG = 1024;  // segments (experts) per launch, prefix table in smem
+constexpr int MIN_ITERS = 8;   // fewest chunk iterations per CTA in the tail
+constexpr int PART_WORDS = 3 * NTOK * 128;  // int32 partial accumulators per slot (P <= 3)
+}  // namespace um
+
+struct UmWork {
+    const int32_t *unit_pre;  // [n_seg + 1] units before segment s (smem)
+    const int32_t *seg_off;   // [n_seg + 1] segment row offsets (smem copy of `offsets`)
+    int n_rt, n_mat, n_chunks, G, Gt;
+    int64_t n_units, full_rounds;
+    int64_t T0, T;            // tail: iterations [T0, T0 + T)
+    __device__ __forceinline__ int64_t tstart(int b) const { return T0 + (int64_t)b * T / Gt; }
+    __device__ int owner(int64_t x) const {  // tail CTA whose range holds iteration x
+        int b = (int)((x - T0) * Gt / T);
+        while (b + 1 < Gt && tstart(b + 1) <= x) ++b;
+        while (b > 0 && tstart(b) > x) --b;
+        return b;
+    }
+};
+
+// A CTA's sequence of (unit, first chunk, end chunk).
+struct UmSeq {  // 32-bit: unit and iteration counts stay far below 2^31
+    int u_next, full_left, t, te;
+    __device__ __forceinline__ bool next(const UmWork &w, int &u, int &c0, int &c1) {
+        if (full_left > 0) {
+            u = u_next;
+            u_next += w.G;
+            --full_left;
+            c0 = 0;
+            c1 = w.n_chunks;
+            return true;
+        }
+        if (t >= te) return false;
+        u = t / w.n_chunks;
+        c0 = t - u * w.n_chunks;
+        c1 = (te - u * w.n_chunks) < w.n_chunks ? (te - u * w.n_chunks) : w.n_chunks;
+        t = u * w.n_chunks + c1;
+        return true;
+    }
+};
+
+struct UmUnit {
+    int64_t rb, re, j0, tile;
+    int ntc, mat;
+    int rt;
+};
+
+// unit u -> (segment, pass, matrix, row tile); `seg` walks forward (units are visited in order)
+__device__ __forceinline__ UmUnit um_unit(const UmWork &w, int64_t seg_first, int u, int &seg) {
+    while (w.unit_pre[seg + 1] <= u) ++seg;
+    UmUnit x;
+    x.rb = w.seg_off[seg];
+    x.re = w.seg_off[seg + 1];
+    const int local = u - w.unit_pre[seg];
+    const int per_pass = w.n_rt * w.n_mat;
+    const int pass = local / per_pass, r = local - pass * per_pass;
+    x.mat = r / w.n_rt;
+    x.rt = r - x.mat * w.n_rt;
+    const int64_t j_last = (x.re - 1) >> 3;
+    x.j0 = (x.rb >> 3) + (int64_t)pass * (um::NTOK / 8);
+    const int64_t left = j_last - x.j0 + 1;
+    x.ntc = (int)(left < um::NTOK / 8 ? left : um::NTOK / 8);
+    x.tile = (seg + seg_first) * w.n_rt + x.rt;
+    return x;
+}
+
+// grid: (#SMs); n_mat = 2 computes gate (ids0 ... out0) and up (ids1 ... out1).
 template <int P, bool MERGED>
 __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
-    const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int64_t seg_first,
+    const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int n_seg, int64_t seg_first,
     const uint8_t *__restrict__ ids0, const int8_t *__restrict__ lut0, const float *__restrict__ rs0,
     float *__restrict__ out0, const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1,
-    const float *__restrict__ rs1, float *__restrict__ out1, int d_in, int d_out, int g) {
+    const float *__restrict__ rs1, float *__restrict__ out1, int n_mat, int d_in, int d_out, int g,
+    int32_t *__restrict__ part, int32_t *__restrict__ cnt) {
     using S = UmStage<P, MERGED>;
-    constexpr int RING = S::RING;
+    constexpr int NA = S::NA, NS = S::NS, LAG = S::LAG;
+    constexpr int TPP = um::NTOK / 8;  // token tiles per pass
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t full_bar[RING], empty_bar[RING], afull_bar[RING];
+    __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA];
+    __shared__ uint32_t tx_bytes[NS];  // producer: bytes of the chunk in each smem stage
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
+    __shared__ int32_t unit_pre[um::MAX_SEG + 1], seg_off[um::MAX_SEG + 1];
+    __shared__ __align__(16) uint32_t tok_sh[um::EXP_WARPS][16];  // per expander warp: 8 token scales, 8 row sums
+    __shared__ int last_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t seg = blockIdx.y;
-    const int64_t rb = offsets[seg], re = offsets[seg + 1];
-    if (rb >= re) return;  // CTA-uniform
-    const int mat = blockIdx.z;
-    const uint8_t *ids = mat ? ids1 : ids0;
-    const int8_t *lut = mat ? lut1 : lut0;
-    const float *rsp = mat ? rs1 : rs0;
-    float *out = mat ? out1 : out0;
-    const int64_t e = seg + seg_first;
-    const int64_t tile = e * (d_out / 128) + blockIdx.x;
     const int n_chunks = d_in / 128, cpg = g / 128, n_groups = d_in / g;
 
+    // units per segment -> prefix table (warp 0: a serial run per lane + shuffle scan)
+    if (warp == 0) {
+        const int per = (n_seg + 31) / 32;
+        const int s0 = lane * per, s1 = min(n_seg, s0 + per);
+        int run = 0;
+        for (int s = s0; s < s1; ++s) {
+            const int64_t rb = offsets[s], re = offsets[s + 1];
+            const int np = rb < re ? (int)((((re - 1) >> 3) - (rb >> 3) + TPP) / TPP) : 0;
+            run += np * (d_out / 128) * n_mat;
+            unit_pre[s + 1] = run;
+            seg_off[s] = (int32_t)rb;
+            if (s == n_seg - 1) seg_off[n_seg] = (int32_t)re;
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        for (int s = s0; s < s1; ++s) unit_pre[s + 1] += incl - run;
+        if (lane == 0) unit_pre[0] = 0;
+    }
+    __syncthreads();
+    __shared__ UmWork W_sh;  // in smem: keeps the expanders' chunk loop clear of live descriptor registers
+    UmWork &W = W_sh;
+    W.unit_pre = unit_pre;
+    W.seg_off = seg_off;
+    W.n_rt = d_out / 128;
+    W.n_mat = n_mat;
+    W.n_chunks = n_chunks;
+    W.G = gridDim.x;
+    W.n_units = unit_pre[n_seg];
+    W.full_rounds = W.n_units / W.G;
+    W.T0 = W.full_rounds * W.G * n_chunks;
+    W.T = (W.n_units - W.full_rounds * W.G) * n_chunks;
+    {
+        const int64_t gt = W.T / um::MIN_ITERS > 0 ? W.T / um::MIN_ITERS : 1;
+        W.Gt = (int)(gt < W.G ? gt : W.G);
+    }
+    const int cta = blockIdx.x;
+    UmSeq seq0;
+    seq0.u_next = cta;
+    seq0.full_left = (int)W.full_rounds;
+    seq0.t = W.T > 0 && cta < W.Gt ? (int)W.tstart(cta) : 0;
+    seq0.te = W.T > 0 && cta < W.Gt ? (int)W.tstart(cta + 1) : 0;
+    if (seq0.full_left == 0 && seq0.t >= seq0.te) return;  // CTA-uniform: no work
+    const int first_tail_unit = seq0.t / n_chunks;
+
     if (threadIdx.x == 0) {
-        for (int s = 0; s < RING; ++s) {
+        for (int s = 0; s < NS; ++s) {
             u_bar_init(u_smem(&full_bar[s]), 1);
             u_bar_init(u_smem(&empty_bar[s]), 1);
-            u_bar_init(u_smem(&afull_bar[s]), um::EXP_WARPS);  // every expander warp writes its k-step
         }
+        for (int s = 0; s < NA; ++s) u_bar_init(u_smem(&afull_bar[s]), um::EXP_WARPS);  // every expander warp
         u_bar_init(u_smem(&accfull_bar), 1);
         u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -251,52 +398,80 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
     const uint32_t a_col0 = (uint32_t)S::ACC;  // A stages follow the accumulators
-
-    const int64_t j_first = rb >> 3, j_last = (re - 1) >> 3;
-    constexpr int TPP = um::NTOK / 8;  // token tiles per pass
-    const int n_pass = (int)((j_last - j_first + TPP) / TPP);
+    // shared-window addresses, computed once (slot s adds 8 * s / s * S::BYTES)
+    // (volatile moves: ptxas would otherwise re-derive them from SR_CgaCtaId in every loop iteration)
+    const uint32_t full_a = u_pin(u_smem(&full_bar[0])), empty_a = u_pin(u_smem(&empty_bar[0]));
+    const uint32_t afull_a = u_pin(u_smem(&afull_bar[0])), stage_a = u_pin(u_smem(smem));
 
     if (warp == um::PROD_WARP) {
         // ------------------------------------------------------------ producer (converged warp, elected lane)
-        {
-            uint32_t it = 0;
-            for (int pass = 0; pass < n_pass; ++pass) {
-                const int64_t j0 = j_first + (int64_t)pass * TPP;
-                const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
-                const int ntc16 = (ntc + 1) & ~1;  // MMA N is a multiple of 16
-                int gc = 0;  // chunk index within the current group
-                for (int c = 0; c < n_chunks; ++c, ++it) {
-                    const int s = it % RING;
-                    if (it >= RING) u_bar_wait(u_smem(&empty_bar[s]), ((it / RING) - 1) & 1);
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    const bool new_group = gc == 0;
-                    const uint32_t bar = u_smem(&full_bar[s]);
-                    const uint32_t dst = u_smem(smem + (size_t)s * S::BYTES);
-                    u_bar_expect_elect(bar, um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE);
-                    u_bulk_elect(dst, ids + ((size_t)tile * n_chunks + c) * um::IDS, um::IDS, bar);
-                    if (new_group)
-                        u_bulk_elect(dst + um::IDS, lut + ((size_t)tile * n_groups + c / cpg) * S::LUT, S::LUT, bar);
-                    u_bulk_elect(dst + um::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + j0) * um::BTILE,
-                                 ntc16 * um::BTILE, bar);
-                    if (++gc == cpg) gc = 0;
+        uint32_t k = 0;
+        int seg = 0;
+        UmSeq q = seq0;
+        int u, c0, c1;
+        while (q.next(W, u, c0, c1)) {
+            const UmUnit x = um_unit(W, seg_first, u, seg);
+            const uint8_t *ids = x.mat ? ids1 : ids0;
+            const int8_t *lut = x.mat ? lut1 : lut0;
+            const int ntc16 = (x.ntc + 1) & ~1;  // MMA N is a multiple of 16
+            int grp = c0 / cpg, gc = c0 - grp * cpg;  // group and chunk-in-group, stepped without division
+            for (int c = c0; c < c1; ++c, ++k) {
+                const int s = k % NS;
+                if (k >= NS) u_bar_wait(empty_a + 8 * s, ((k / NS) - 1) & 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const bool new_group = gc == 0 || c == c0;
+                const uint32_t bar = full_a + 8 * s;
+                const uint32_t dst = stage_a + s * S::BYTES;
+                const uint32_t bytes = um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE;
+                if (LAG == 0) {
+                    u_bar_expect_elect(bar, bytes);
+                } else if (lane == 0) {
+                    tx_bytes[s] = bytes;
+                }
+                u_bulk_elect(dst, ids + ((size_t)x.tile * n_chunks + c) * um::IDS, um::IDS, bar);
+                if (new_group)
+                    u_bulk_elect(dst + um::IDS, lut + ((size_t)x.tile * n_groups + grp) * S::LUT, S::LUT, bar);
+                u_bulk_elect(dst + um::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + x.j0) * um::BTILE,
+                             ntc16 * um::BTILE, bar);
+                if (++gc == cpg) {
+                    gc = 0;
+                    ++grp;
+                }
+                // chunk k - LAG: its A stage is free now (the empty wait above covered chunk k - NS)
+                if (LAG > 0) {
+                    __syncwarp();
+                    if (k >= (uint32_t)LAG) {
+                        const int sj = (k - LAG) % NS;
+                        u_bar_expect_elect(full_a + 8 * sj, tx_bytes[sj]);
+                    }
                 }
             }
         }
+        // the last LAG chunks: wait as if their successors were issued, then arm them
+        for (uint32_t kv = k; kv < k + LAG; ++kv) {
+            if (kv < (uint32_t)LAG) continue;
+            const int s = kv % NS;
+            if (kv >= NS) u_bar_wait(empty_a + 8 * s, ((kv / NS) - 1) & 1);
+            const int sj = (kv - LAG) % NS;
+            u_bar_expect_elect(full_a + 8 * sj, tx_bytes[sj]);
+        }
     } else if (warp == um::MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
-        uint32_t it = 0;
-        for (int pass = 0; pass < n_pass; ++pass) {
-            const int64_t j0 = j_first + (int64_t)pass * TPP;
-            const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
-            const uint32_t idesc = idesc_i8(((ntc + 1) & ~1) * 8);
-            if (pass > 0) u_bar_wait(u_smem(&accempty_bar), (pass - 1) & 1);
-            for (int c = 0; c < n_chunks; ++c, ++it) {
-                const int s = it % RING;
-                // afull[s] implies full[s]: every expander waited for the chunk's data
-                u_bar_wait(u_smem(&afull_bar[s]), (it / RING) & 1);
+        uint32_t k = 0, nu = 0;
+        int seg = 0;
+        UmSeq q = seq0;
+        int u, c0, c1;
+        for (; q.next(W, u, c0, c1); ++nu) {
+            const UmUnit x = um_unit(W, seg_first, u, seg);
+            const uint32_t idesc = idesc_i8(((x.ntc + 1) & ~1) * 8);
+            if (nu > 0) u_bar_wait(u_smem(&accempty_bar), (nu - 1) & 1);
+            for (int c = c0; c < c1; ++c, ++k) {
+                const int s = k % NS, sa = k % NA;
+                // afull implies full: every expander waited for the chunk's data
+                u_bar_wait(afull_a + 8 * sa, (k / NA) & 1);
                 tc_fence_after();
-                const uint32_t bbase = u_smem(smem + (size_t)s * S::BYTES + um::IDS + S::LUT);
-                const uint32_t abase = tmem + a_col0 + (uint32_t)(s * S::CCOLS);
+                const uint32_t bbase = stage_a + s * S::BYTES + um::IDS + S::LUT;
+                const uint32_t abase = tmem + a_col0 + (uint32_t)(sa * S::CCOLS);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                     // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
@@ -304,13 +479,13 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 #pragma unroll
                     for (int sl = 0; sl < S::SLICES; ++sl) {
                         const int p = MERGED ? sl : (sl >> 1);
-                        const uint32_t accum = (c == 0 && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
+                        const uint32_t accum = (c == c0 && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
                         tc_mma_i8(tmem + (uint32_t)(p * um::NTOK), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
                                   idesc, accum);
                     }
                 }
-                tc_commit_elect(u_smem(&empty_bar[s]));  // frees the smem stage and the A stage
-                if (c == n_chunks - 1) tc_commit_elect(u_smem(&accfull_bar));
+                tc_commit_elect(empty_a + 8 * s);  // frees the smem stage (and, LAG chunks on, the A stage)
+                if (c == c1 - 1) tc_commit_elect(u_smem(&accfull_bar));
             }
         }
     } else {
@@ -319,20 +494,34 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         const int quarter = warp & 3;     // TMEM lane quarter = rows
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        const float rscale = __ldg(rsp + tile * 128 + row);
-        uint32_t it = 0;  // chunks consumed
-        for (int pass = 0; pass < n_pass; ++pass) {
-            const int64_t j0 = j_first + (int64_t)pass * TPP;
-            const int ntc = (int)((j_last - j0 + 1) < TPP ? (j_last - j0 + 1) : TPP);
-            const int n = ((ntc + 1) & ~1) * 8;
+        const int cb = wg * 8;            // epilogue: token columns cb..cb+7
+        uint32_t k = 0, nu = 0;
+        int seg = 0;
+        UmSeq q = seq0;
+        int u, c0, c1;
+        for (; q.next(W, u, c0, c1); ++nu) {
+            float rscale;
+            {
+                const UmUnit x = um_unit(W, seg_first, u, seg);
+                rscale = __ldg((x.mat ? rs1 : rs0) + x.tile * 128 + row);
+                // per-token epilogue operands: async copies into this warp's smem slot now, so their
+                // latency hides under the unit's chunks (lanes 0-7 scales, 8-15 row sums)
+                if (lane < 16 && cb < ((x.ntc + 1) & ~1) * 8) {
+                    const int64_t tok = x.j0 * 8 + cb + (lane & 7);
+                    if (tok >= x.rb && tok < x.re && (lane < 8 || MERGED))
+                        cp_async4(&tok_sh[warp][lane],
+                                  lane < 8 ? (const void *)(scales + tok) : (const void *)(qsums + tok));
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
             uint4 L[P];
-            int gc = 0;
-            for (int c = 0; c < n_chunks; ++c, ++it) {
-                const int s = it % RING;
-                u_bar_wait(u_smem(&full_bar[s]), (it / RING) & 1);
+            int gc = c0 % cpg;  // chunk within its codebook group
+            for (int c = c0; c < c1; ++c, ++k) {
+                const int s = k % NS, sa = k % NA;
+                u_bar_wait(full_a + 8 * s, (k / NS) & 1);
                 tc_fence_after();
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
-                if (gc == 0) {
+                if (gc == 0 || c == c0) {
                     const uint4 *lb = reinterpret_cast<const uint4 *>(st + um::IDS) + row * P;
 #pragma unroll
                     for (int p = 0; p < P; ++p) L[p] = lb[p];
@@ -343,22 +532,23 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 uint32_t sel[8], xsel[8];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint32_t x = wv[q] ^ 0x88888888u;
+                    const uint32_t xx = wv[q] ^ 0x88888888u;
                     sel[2 * q] = wv[q];
                     sel[2 * q + 1] = hi16(wv[q]);
-                    xsel[2 * q] = x;
-                    xsel[2 * q + 1] = hi16(x);
+                    xsel[2 * q] = xx;
+                    xsel[2 * q + 1] = hi16(xx);
                 }
-                const uint32_t abase = tmem + lane_addr + a_col0 + (uint32_t)(s * S::CCOLS + wg * S::ACOLS);
+                const uint32_t abase = tmem + lane_addr + a_col0 + (uint32_t)(sa * S::CCOLS + wg * S::ACOLS);
                 if (MERGED) {
-                    uint32_t v[P * 8];
+                    // one 8-column store per plane as soon as it is expanded (keeps the register peak low)
 #pragma unroll
-                    for (int p = 0; p < P; ++p)
+                    for (int p = 0; p < P; ++p) {
+                        uint32_t v[8];
 #pragma unroll
                         for (int cc = 0; cc < 8; ++cc)
-                            v[p * 8 + cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
-                    tc_st16(abase, v);
-                    if (P == 3) tc_st8(abase + 16, v + 16);
+                            v[cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
+                        tc_st8(abase + p * 8, v);
+                    }
                 } else {
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
@@ -374,33 +564,76 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) u_bar_arrive(u_smem(&afull_bar[s]));
+                if (lane == 0) u_bar_arrive(afull_a + 8 * sa);
             }
-            // ---- epilogue of this pass: accumulators -> fp32 out (warpgroup wg: token columns 8wg..8wg+7)
-            u_bar_wait(u_smem(&accfull_bar), pass & 1);
+            // ---- epilogue of this unit: accumulators -> registers, release TMEM, then finish
+            u_bar_wait(u_smem(&accfull_bar), nu & 1);
             tc_fence_after();
-            const int cb = wg * 8;
+            const UmUnit x = um_unit(W, seg_first, u, seg);  // re-decoded (smem) rather than kept live
+            const int n = ((x.ntc + 1) & ~1) * 8;
+            int32_t acc[P][8];
             if (cb < n) {
-                uint32_t acc[P][8];
 #pragma unroll
-                for (int p = 0; p < P; ++p) tc_ld8(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), acc[p]);
+                for (int p = 0; p < P; ++p)
+                    tc_ld8(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), reinterpret_cast<uint32_t *>(acc[p]));
                 tc_wait_ld();
-#pragma unroll
-                for (int c2 = 0; c2 < 8; ++c2) {
-                    const int64_t tok = j0 * 8 + cb + c2;
-                    if (tok < rb || tok >= re) continue;
-                    const double base = MERGED ? 128.0 : 255.0;
-                    double sum = (double)(int32_t)acc[P - 1][c2];
-#pragma unroll
-                    for (int p = P - 2; p >= 0; --p) sum = sum * base + (double)(int32_t)acc[p][c2];
-                    if (MERGED) sum -= (double)(1LL << (7 * P - 1)) * (double)__ldg(qsums + tok);
-                    const float v2 = (float)(sum * (double)rscale);
-                    out[tok * d_out + (int64_t)blockIdx.x * 128 + row] = __fmul_rn(v2, __ldg(scales + tok));
-                }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
+            if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));  // the MMA may start the next unit
+            bool finish = true;
+            if (c0 > 0 || c1 < n_chunks) {
+                // unit shared with neighbouring CTAs: publish the partial, the last arriver finishes
+                const int64_t ustart = (int64_t)u * n_chunks;
+                const int bf = W.owner(ustart), bl = W.owner(ustart + n_chunks - 1);
+                int32_t *mine = part + (size_t)(2 * cta + (u != first_tail_unit ? 1 : 0)) * um::PART_WORDS;
+                if (cb < n) {
+#pragma unroll
+                    for (int p = 0; p < P; ++p)
+#pragma unroll
+                        for (int c2 = 0; c2 < 8; ++c2) mine[(p * um::NTOK + cb + c2) * 128 + row] = acc[p][c2];
+                }
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"r"(um::EXP_WARPS * 32) : "memory");
+                if (threadIdx.x == 0) {
+                    const int last = atomicAdd(cnt + bf, 1) == bl - bf;
+                    if (last) cnt[bf] = 0;  // ready for the next launch
+                    last_sh = last;
+                }
+                asm volatile("bar.sync 1, %0;" ::"r"(um::EXP_WARPS * 32) : "memory");
+                finish = last_sh != 0;
+                if (finish && cb < n) {
+                    __threadfence();
+                    for (int b2 = bf; b2 <= bl; ++b2) {
+                        if (b2 == cta) continue;
+                        const int64_t fu = W.tstart(b2) / n_chunks;
+                        const int32_t *src = part + (size_t)(2 * b2 + (u != fu ? 1 : 0)) * um::PART_WORDS;
+#pragma unroll
+                        for (int p = 0; p < P; ++p)
+#pragma unroll
+                            for (int c2 = 0; c2 < 8; ++c2) acc[p][c2] += __ldcg(src + (p * um::NTOK + cb + c2) * 128 + row);
+                    }
+                }
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            if (finish && cb < n) {
+                float *out = x.mat ? out1 : out0;
+                const float *tscale = reinterpret_cast<const float *>(tok_sh[warp]);
+                const int32_t *tqsum = reinterpret_cast<const int32_t *>(tok_sh[warp]) + 8;
+#pragma unroll
+                for (int c2 = 0; c2 < 8; ++c2) {
+                    const int64_t tok = x.j0 * 8 + cb + c2;
+                    if (tok < x.rb || tok >= x.re) continue;
+                    const double base = MERGED ? 128.0 : 255.0;
+                    double sum = (double)acc[P - 1][c2];
+#pragma unroll
+                    for (int p = P - 2; p >= 0; --p) sum = sum * base + (double)acc[p][c2];
+                    if (MERGED) sum -= (double)(1LL << (7 * P - 1)) * (double)tqsum[c2];
+                    const float v2 = (float)(sum * (double)rscale);
+                    out[tok * d_out + (int64_t)x.rt * 128 + row] = __fmul_rn(v2, tscale[c2]);
+                }
+            }
         }
     }
     tc_fence_before();
@@ -414,9 +647,12 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 
 // codes (rows, K) row-major -> [chunk128][tile8][kstep4][khalf2][8 rows][16 B],
 // the canonical K-major no-swizzle UMMA B layout per k-step; rows >= n are zero.
+// Also zeroes the GEMM's split-unit counters (zero[0..n_zero)).
 __global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
-                                 uint4 *__restrict__ dst) {
+                                 uint4 *__restrict__ dst, int32_t *__restrict__ zero, int n_zero) {
     const int64_t total = (K / 128) * tiles * 64;  // 16-byte pieces: 8 (kstep, khalf) x 8 rows per tile-chunk
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(x & 7), kh = (int)((x >> 3) & 1), ks = (int)((x >> 4) & 3);
         const int64_t j = (x >> 6) % tiles, c = (x >> 6) / tiles;
@@ -480,43 +716,65 @@ bool umma_ok(int64_t d_in, int64_t d_out, int64_t g) { return d_in % 128 == 0 &&
 
 template <int P, bool MERGED>
 size_t umma_smem() {
-    return (size_t)UmStage<P, MERGED>::RING * UmStage<P, MERGED>::BYTES;
+    return (size_t)UmStage<P, MERGED>::NS * UmStage<P, MERGED>::BYTES;
 }
 
 cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, int32_t *sums,
-                    cudaStream_t st) {
+                    int32_t *zero, int n_zero, cudaStream_t st) {
     const int64_t total = (K / 128) * tiles * 64;
     if (total == 0) return CQ_OK;
     to_umma_b_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
-        codes, n, K, tiles, reinterpret_cast<uint4 *>(dst));
+        codes, n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero);
     CQ_TRY(check_launch("to_umma_b"));
     if (sums == nullptr) return CQ_OK;
     row_sums_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(codes, n, K, sums);
     return check_launch("row_sums");
 }
 
+// Persistent grid: one CTA per SM (CQ_UMMA_GRID overrides, for experiments).
+int umma_grid() {
+    static int sms = 0;
+    if (sms == 0) {
+        const char *env = getenv("CQ_UMMA_GRID");
+        if (env != nullptr) sms = atoi(env);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (sms <= 0 && (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0))
+            sms = 148;
+    }
+    return sms;
+}
+
 // B buffer: umma_b_tiles(rows) tiles x d_in bytes (an N=16 MMA may read one
-// tile past the end), followed by the int32 row sums (256-byte aligned).
+// tile past the end), then the int32 row sums, then the split-unit scratch:
+// 2 partial-accumulator slots per CTA and one counter per CTA (256-byte aligned).
 int64_t umma_b_tiles(int64_t rows) { return ceil_div(rows, 8) + 2; }
+static int64_t umma_sums_off(int64_t rows, int64_t d_in) { return umma_b_tiles(rows) * 8 * d_in; }
+static int64_t umma_part_off(int64_t rows, int64_t d_in) {
+    return umma_sums_off(rows, d_in) + ceil_div(rows * 4, 256) * 256;
+}
+static int64_t umma_cnt_off(int64_t rows, int64_t d_in) {
+    return umma_part_off(rows, d_in) + (int64_t)2 * umma_grid() * um::PART_WORDS * 4;
+}
 int64_t umma_b_bytes(int64_t rows, int64_t d_in) {
-    return umma_b_tiles(rows) * 8 * d_in + ceil_div(rows * 4, 256) * 256;
+    return umma_cnt_off(rows, d_in) + ceil_div((int64_t)umma_grid() * 4, 256) * 256;
 }
 
 template <int P, bool MERGED>
 cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *sums,
                       const int32_t *offsets, int64_t n_seg, int64_t seg_first, const cq_expert_site *a, float *out_a,
-                      const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
+                      const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, int32_t *part,
+                      int32_t *cnt, cudaStream_t st) {
     static bool attr = false;
     const size_t smem = umma_smem<P, MERGED>();
     if (!attr) {
         cudaFuncSetAttribute(lut_umma_kernel<P, MERGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    dim3 grid((unsigned)(d_out / 128), (unsigned)n_seg, b ? 2u : 1u);
-    lut_umma_kernel<P, MERGED><<<grid, um::THREADS, smem, st>>>(
-        bfrag, n_tiles, scales, sums, offsets, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
-        b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, (int)d_in, (int)d_out,
-        (int)a->group_size);
+    lut_umma_kernel<P, MERGED><<<umma_grid(), um::THREADS, smem, st>>>(
+        bfrag, n_tiles, scales, sums, offsets, (int)n_seg, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
+        b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, b ? 2 : 1, (int)d_in,
+        (int)d_out, (int)a->group_size, part, cnt);
     return check_launch("lut_umma");
 }
 
@@ -539,12 +797,19 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         set_error("tcgen05 path: paired matrices must share the layout");
         return CQ_ERR_CONFIG;
     }
+    if (n_seg > um::MAX_SEG) {
+        set_error("tcgen05 path: at most 1024 segments (experts) per launch");
+        return CQ_ERR_UNSUPPORTED;
+    }
     const bool merged = a->tc_layout == CQ_TC_UMMA128U;
     const int64_t tiles = umma_b_tiles(rows);
-    int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + tiles * 8 * d_in) : nullptr;
-    CQ_TRY(to_umma_b(codes, rows, d_in, tiles, bbuf, sums, st));
-#define CQ_UMMA(P_, M_) \
-    launch_umma<P_, M_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, st)
+    int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in)) : nullptr;
+    int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
+    int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
+    CQ_TRY(to_umma_b(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), st));
+#define CQ_UMMA(P_, M_)                                                                                             \
+    launch_umma<P_, M_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, part, \
+                        cnt, st)
     if (a->tc_planes == 3) return merged ? CQ_UMMA(3, true) : CQ_UMMA(3, false);
     if (a->tc_planes == 2) return merged ? CQ_UMMA(2, true) : CQ_UMMA(2, false);
 #undef CQ_UMMA
