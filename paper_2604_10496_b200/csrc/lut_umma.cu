@@ -45,6 +45,12 @@
 
 namespace cq {
 
+#ifndef LAG_P2
+#define LAG_P2 1
+#endif
+#ifndef LAG_P3
+#define LAG_P3 1
+#endif
 namespace um {
 constexpr int STAGES = 8;        // smem ring depth (128-column chunks)
 constexpr int NTOK = 32;         // max tokens per pass (MMA N)
@@ -67,17 +73,22 @@ struct UmStage {
     static constexpr int ACC = P * um::NTOK;                     // accumulator columns
     static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages that fit in TMEM
     static_assert(NCS >= 2, "TMEM budget");
-    // Chunk c uses TMEM A stage c % NA and smem stage c % NS, NS = NA + LAG.
-    // The producer issues chunk c's copies once the MMAs of chunk c - NS are
-    // done (empty[c % NS]) — NS chunks of data in flight — but makes full[c % NS]
-    // completable (its arrive.expect_tx) only LAG iterations later, after the
-    // empty wait for chunk c + LAG, i.e. once the MMAs of chunk c - NA are done
-    // and A stage c % NA is free.  So full[] alone tells an expander that both
-    // the data and the A stage are ready: one barrier wait per chunk.
-    static constexpr int NA = NCS < um::STAGES ? NCS : um::STAGES;
-    static constexpr int LAG = 0;  // > 0: issue copies LAG chunks before arming them (measured slower)
+    // Chunk c uses smem stage and TMEM A stage c % NS (one ring).  full[s] for
+    // chunk c means the producer refilled stage s, which it does only after the
+    // MMAs of chunk c - NS completed (empty[s]), so the A stage is free too:
+    // expanders wait on one barrier per chunk.  Chunk c is expanded by
+    // warpgroup c % WGS; NS is a multiple of WGS so every stage belongs to one
+    // warpgroup, which consumes its phases in order (a stage shared by two
+    // warpgroups would let one pass try_wait.parity on the other's older phase).
+    static constexpr int WGS = NCS < um::WG ? NCS : um::WG;  // expanding warpgroups
+    static constexpr int NA = ((NCS < um::STAGES ? NCS : um::STAGES) / WGS) * WGS;
+    // LAG > 0: the producer issues chunk c's copies LAG chunks before it arms
+    // full[c % NS] (arrive.expect_tx, after the empty wait that proves the MMAs
+    // of chunk c - NA done), so NS = NA + LAG chunks of data are in flight
+    // while full[] alone still means "data and A stage ready".
+    static constexpr int LAG = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? WGS : 0;
     static constexpr int NS = NA + LAG;
-    static_assert(NS * BYTES <= 200 * 1024, "smem budget");
+    static_assert(NS % WGS == 0 && NS * BYTES <= 200 * 1024, "smem ring");
 };
 
 // ---------------------------------------------------------------------------
@@ -315,13 +326,13 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const float *__restrict__ rs1, float *__restrict__ out1, int n_mat, int d_in, int d_out, int g,
     int32_t *__restrict__ part, int32_t *__restrict__ cnt) {
     using S = UmStage<P, MERGED>;
-    constexpr int NA = S::NA, NS = S::NS, LAG = S::LAG;
+    constexpr int NA = S::NA, NS = S::NS, WGS = S::WGS, LAG = S::LAG;
     constexpr int TPP = um::NTOK / 8;  // token tiles per pass
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA];
-    __shared__ uint32_t tx_bytes[NS];  // producer: bytes of the chunk in each smem stage
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
+    __shared__ uint32_t tx_bytes[NS];  // producer: bytes of the chunk in each smem stage (LAG > 0)
     __shared__ int32_t unit_pre[um::MAX_SEG + 1], seg_off[um::MAX_SEG + 1];
     __shared__ __align__(16) uint32_t tok_sh[um::EXP_WARPS][16];  // per expander warp: 8 token scales, 8 row sums
     __shared__ int last_sh;
@@ -382,7 +393,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             u_bar_init(u_smem(&full_bar[s]), 1);
             u_bar_init(u_smem(&empty_bar[s]), 1);
         }
-        for (int s = 0; s < NA; ++s) u_bar_init(u_smem(&afull_bar[s]), um::EXP_WARPS);  // every expander warp
+        for (int s = 0; s < NA; ++s) u_bar_init(u_smem(&afull_bar[s]), 4);  // the 4 warps of one warpgroup
         u_bar_init(u_smem(&accfull_bar), 1);
         u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -419,14 +430,14 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 const int s = k % NS;
                 if (k >= NS) u_bar_wait(empty_a + 8 * s, ((k / NS) - 1) & 1);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const bool new_group = gc == 0 || c == c0;
+                const bool new_group = true;  // every chunk carries its LUT block: warpgroups take alternate chunks
                 const uint32_t bar = full_a + 8 * s;
                 const uint32_t dst = stage_a + s * S::BYTES;
                 const uint32_t bytes = um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE;
                 if (LAG == 0) {
                     u_bar_expect_elect(bar, bytes);
                 } else if (lane == 0) {
-                    tx_bytes[s] = bytes;
+                    tx_bytes[s] = bytes;  // complete_tx may land before the arm: tx-count goes transiently negative
                 }
                 u_bulk_elect(dst, ids + ((size_t)x.tile * n_chunks + c) * um::IDS, um::IDS, bar);
                 if (new_group)
@@ -437,10 +448,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     gc = 0;
                     ++grp;
                 }
-                // chunk k - LAG: its A stage is free now (the empty wait above covered chunk k - NS)
-                if (LAG > 0) {
+                if (LAG > 0) {  // arm chunk k - LAG: the empty wait above covered its A stage
                     __syncwarp();
-                    if (k >= (uint32_t)LAG) {
+                    if ((int)k >= LAG) {
                         const int sj = (k - LAG) % NS;
                         u_bar_expect_elect(full_a + 8 * sj, tx_bytes[sj]);
                     }
@@ -448,8 +458,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             }
         }
         // the last LAG chunks: wait as if their successors were issued, then arm them
-        for (uint32_t kv = k; kv < k + LAG; ++kv) {
-            if (kv < (uint32_t)LAG) continue;
+        for (uint32_t kv = k; LAG > 0 && kv < k + LAG; ++kv) {
+            if ((int)kv < LAG) continue;
             const int s = kv % NS;
             if (kv >= NS) u_bar_wait(empty_a + 8 * s, ((kv / NS) - 1) & 1);
             const int sj = (kv - LAG) % NS;
@@ -484,13 +494,13 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                                   idesc, accum);
                     }
                 }
-                tc_commit_elect(empty_a + 8 * s);  // frees the smem stage (and, LAG chunks on, the A stage)
+                tc_commit_elect(empty_a + 8 * s);  // frees the smem stage and the A stage
                 if (c == c1 - 1) tc_commit_elect(u_smem(&accfull_bar));
             }
         }
     } else {
         // ------------------------------------------------------------ expanders
-        const int wg = warp >> 2;         // expands k-step wg of every chunk
+        const int wg = warp >> 2;         // expands chunks k = wg (mod WGS)
         const int quarter = warp & 3;     // TMEM lane quarter = rows
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
@@ -514,51 +524,57 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
-            uint4 L[P];
-            int gc = c0 % cpg;  // chunk within its codebook group
+            // warpgroup wg expands the chunks k = wg (mod WGS), all four k-steps: the warpgroups
+            // work on different chunks, so their barrier waits are staggered, and the per-chunk
+            // bookkeeping is paid once per 128 columns
             for (int c = c0; c < c1; ++c, ++k) {
+                if ((int)(k % WGS) != wg) continue;  // warpgroup-uniform
                 const int s = k % NS, sa = k % NA;
                 u_bar_wait(full_a + 8 * s, (k / NS) & 1);
                 tc_fence_after();
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
-                if (gc == 0 || c == c0) {
+                uint4 L[P];
+                {
                     const uint4 *lb = reinterpret_cast<const uint4 *>(st + um::IDS) + row * P;
 #pragma unroll
                     for (int p = 0; p < P; ++p) L[p] = lb[p];
                 }
-                if (++gc == cpg) gc = 0;
-                const uint4 w = reinterpret_cast<const uint4 *>(st)[wg * 128 + row];
-                const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-                uint32_t sel[8], xsel[8];
+                const uint32_t abase0 = tmem + lane_addr + a_col0 + (uint32_t)(sa * S::CCOLS);
+#pragma unroll 1
+                for (int ks = 0; ks < 4; ++ks) {
+                    const uint4 w = reinterpret_cast<const uint4 *>(st)[ks * 128 + row];
+                    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+                    uint32_t sel[8], xsel[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t xx = wv[q] ^ 0x88888888u;
-                    sel[2 * q] = wv[q];
-                    sel[2 * q + 1] = hi16(wv[q]);
-                    xsel[2 * q] = xx;
-                    xsel[2 * q + 1] = hi16(xx);
-                }
-                const uint32_t abase = tmem + lane_addr + a_col0 + (uint32_t)(sa * S::CCOLS + wg * S::ACOLS);
-                if (MERGED) {
-                    // one 8-column store per plane as soon as it is expanded (keeps the register peak low)
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        uint32_t v[8];
-#pragma unroll
-                        for (int cc = 0; cc < 8; ++cc)
-                            v[cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
-                        tc_st8(abase + p * 8, v);
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t xx = wv[q] ^ 0x88888888u;
+                        sel[2 * q] = wv[q];
+                        sel[2 * q + 1] = hi16(wv[q]);
+                        xsel[2 * q] = xx;
+                        xsel[2 * q + 1] = hi16(xx);
                     }
-                } else {
+                    const uint32_t abase = abase0 + (uint32_t)(ks * S::ACOLS);
+                    if (MERGED) {
+                        // one 8-column store per plane as soon as it is expanded (keeps the register peak low)
 #pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        uint32_t v[16];
+                        for (int p = 0; p < P; ++p) {
+                            uint32_t v[8];
 #pragma unroll
-                        for (int cc = 0; cc < 8; ++cc) {
-                            v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ compensated sign byte)
-                            v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
+                            for (int cc = 0; cc < 8; ++cc)
+                                v[cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
+                            tc_st8(abase + p * 8, v);
                         }
-                        tc_st16(abase + p * 16, v);
+                    } else {
+#pragma unroll
+                        for (int p = 0; p < P; ++p) {
+                            uint32_t v[16];
+#pragma unroll
+                            for (int cc = 0; cc < 8; ++cc) {
+                                v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ compensated sign byte)
+                                v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
+                            }
+                            tc_st16(abase + p * 16, v);
+                        }
                     }
                 }
                 tc_wait_st();
