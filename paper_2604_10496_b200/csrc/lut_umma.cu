@@ -45,6 +45,9 @@
 
 namespace cq {
 
+#ifndef UM_GS4  // chunk streams when >= 4 A stages fit (measured: 4 beats 2 double-buffered)
+#define UM_GS4 4
+#endif
 #ifndef LAG_P2
 #define LAG_P2 1
 #endif
@@ -77,18 +80,23 @@ struct UmStage {
     // chunk c means the producer refilled stage s, which it does only after the
     // MMAs of chunk c - NS completed (empty[s]), so the A stage is free too:
     // expanders wait on one barrier per chunk.  Chunk c is expanded by
-    // warpgroup c % WGS; NS is a multiple of WGS so every stage belongs to one
+    // stream c % GS; NS is a multiple of GS so every stage belongs to one
     // warpgroup, which consumes its phases in order (a stage shared by two
     // warpgroups would let one pass try_wait.parity on the other's older phase).
-    static constexpr int WGS = NCS < um::WG ? NCS : um::WG;  // expanding warpgroups
-    static constexpr int NA = ((NCS < um::STAGES ? NCS : um::STAGES) / WGS) * WGS;
+    // GS chunk streams: stream g expands the chunks c = g (mod GS); its WG / GS
+    // warpgroups split each chunk's 4 k-steps.  Streams work on different
+    // chunks (staggered waits, bookkeeping paid per GS k-steps) and each owns
+    // NA / GS >= 2 A stages, so it expands chunk c + GS while the MMAs of c run.
+    static constexpr int NA0 = NCS < um::STAGES ? NCS : um::STAGES;
+    static constexpr int GS = NA0 >= 4 ? UM_GS4 : (NA0 >= 2 ? 2 : 1);
+    static constexpr int NA = (NA0 / GS) * GS;
     // LAG > 0: the producer issues chunk c's copies LAG chunks before it arms
     // full[c % NS] (arrive.expect_tx, after the empty wait that proves the MMAs
     // of chunk c - NA done), so NS = NA + LAG chunks of data are in flight
     // while full[] alone still means "data and A stage ready".
-    static constexpr int LAG = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? WGS : 0;
+    static constexpr int LAG = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? 4 : 0;
     static constexpr int NS = NA + LAG;
-    static_assert(NS % WGS == 0 && NS * BYTES <= 200 * 1024, "smem ring");
+    static_assert(NS % GS == 0 && NA % GS == 0 && NS * BYTES <= 200 * 1024, "smem ring");
 };
 
 // ---------------------------------------------------------------------------
@@ -326,7 +334,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const float *__restrict__ rs1, float *__restrict__ out1, int n_mat, int d_in, int d_out, int g,
     int32_t *__restrict__ part, int32_t *__restrict__ cnt) {
     using S = UmStage<P, MERGED>;
-    constexpr int NA = S::NA, NS = S::NS, WGS = S::WGS, LAG = S::LAG;
+    constexpr int NA = S::NA, NS = S::NS, GS = S::GS, LAG = S::LAG;
+    constexpr int WPS = um::WG / GS;  // warpgroups per stream
     constexpr int TPP = um::NTOK / 8;  // token tiles per pass
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA];
@@ -393,7 +402,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             u_bar_init(u_smem(&full_bar[s]), 1);
             u_bar_init(u_smem(&empty_bar[s]), 1);
         }
-        for (int s = 0; s < NA; ++s) u_bar_init(u_smem(&afull_bar[s]), 4);  // the 4 warps of one warpgroup
+        for (int s = 0; s < NA; ++s) u_bar_init(u_smem(&afull_bar[s]), 4 * WPS);  // the warps of one stream
+        // (splitting afull per chunk half, so the MMAs start earlier, measured slower: the extra
+        //  tcgen05.wait::st mid-chunk costs more than the overlap gains)
         u_bar_init(u_smem(&accfull_bar), 1);
         u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -477,11 +488,11 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             if (nu > 0) u_bar_wait(u_smem(&accempty_bar), (nu - 1) & 1);
             for (int c = c0; c < c1; ++c, ++k) {
                 const int s = k % NS, sa = k % NA;
+                const uint32_t bbase = stage_a + s * S::BYTES + um::IDS + S::LUT;
+                const uint32_t abase = tmem + a_col0 + (uint32_t)(sa * S::CCOLS);
                 // afull implies full: every expander waited for the chunk's data
                 u_bar_wait(afull_a + 8 * sa, (k / NA) & 1);
                 tc_fence_after();
-                const uint32_t bbase = stage_a + s * S::BYTES + um::IDS + S::LUT;
-                const uint32_t abase = tmem + a_col0 + (uint32_t)(sa * S::CCOLS);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                     // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
@@ -490,8 +501,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     for (int sl = 0; sl < S::SLICES; ++sl) {
                         const int p = MERGED ? sl : (sl >> 1);
                         const uint32_t accum = (c == c0 && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
+#ifndef UM_EXP_NO_MMA
                         tc_mma_i8(tmem + (uint32_t)(p * um::NTOK), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
                                   idesc, accum);
+#endif
                     }
                 }
                 tc_commit_elect(empty_a + 8 * s);  // frees the smem stage and the A stage
@@ -500,7 +513,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         }
     } else {
         // ------------------------------------------------------------ expanders
-        const int wg = warp >> 2;         // expands chunks k = wg (mod WGS)
+        const int wg = warp >> 2;
+        const int stream = wg / WPS, ks0 = (wg % WPS) * GS;  // chunks k = stream (mod GS), k-steps ks0..
         const int quarter = warp & 3;     // TMEM lane quarter = rows
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
@@ -524,11 +538,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
-            // warpgroup wg expands the chunks k = wg (mod WGS), all four k-steps: the warpgroups
-            // work on different chunks, so their barrier waits are staggered, and the per-chunk
-            // bookkeeping is paid once per 128 columns
+            // stream wg / WPS expands the chunks k = stream (mod GS); this warpgroup does k-steps
+            // ks0 .. ks0 + GS - 1 of each (see UmStage)
             for (int c = c0; c < c1; ++c, ++k) {
-                if ((int)(k % WGS) != wg) continue;  // warpgroup-uniform
+                if ((int)(k % GS) != stream) continue;  // warpgroup-uniform
                 const int s = k % NS, sa = k % NA;
                 u_bar_wait(full_a + 8 * s, (k / NS) & 1);
                 tc_fence_after();
@@ -540,8 +553,11 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     for (int p = 0; p < P; ++p) L[p] = lb[p];
                 }
                 const uint32_t abase0 = tmem + lane_addr + a_col0 + (uint32_t)(sa * S::CCOLS);
-#pragma unroll 1
-                for (int ks = 0; ks < 4; ++ks) {
+#ifdef UM_EXP_NO_EXPAND
+                if (false)
+#endif
+#pragma unroll
+                for (int ks = ks0; ks < ks0 + GS; ++ks) {
                     const uint4 w = reinterpret_cast<const uint4 *>(st)[ks * 128 + row];
                     const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
                     uint32_t sel[8], xsel[8];
