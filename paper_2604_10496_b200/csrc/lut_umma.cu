@@ -45,8 +45,14 @@
 
 namespace cq {
 
+#ifndef UM_CK
+#define UM_CK 128  // measured: 64 (8 A stages, 2 per stream) loses to the per-chunk handshake cost
+#endif
 #ifndef UM_GS4  // chunk streams when >= 4 A stages fit (measured: 4 beats 2 double-buffered)
 #define UM_GS4 4
+#endif
+#ifndef UM_LAG  // chunks of data issued ahead of arming (smem ring = A stages + UM_LAG)
+#define UM_LAG 4
 #endif
 #ifndef LAG_P2
 #define LAG_P2 1
@@ -57,8 +63,10 @@ namespace cq {
 namespace um {
 constexpr int STAGES = 8;        // smem ring depth (128-column chunks)
 constexpr int NTOK = 32;         // max tokens per pass (MMA N)
-constexpr int IDS = 128 * 64;    // ids bytes per chunk: 128 rows x 128 columns / 2
-constexpr int BTILE = 1024;      // activation bytes per 8-token tile per chunk
+constexpr int CK = UM_CK;        // chunk width (input columns): 64 -> 8 A stages of 2 k-steps fit in TMEM
+constexpr int KS = CK / 32;      // MMA k-steps per chunk
+constexpr int IDS = 128 * CK / 2;  // ids bytes per chunk: 128 rows x CK columns / 2
+constexpr int BTILE = 8 * CK;    // activation bytes per 8-token tile per chunk
 constexpr int WG = 4;            // expander warpgroups; warpgroup w expands k-step w of every chunk
 constexpr int EXP_WARPS = 4 * WG, PROD_WARP = EXP_WARPS, MMA_WARP = EXP_WARPS + 1, WARPS = EXP_WARPS + 2;
 constexpr int THREADS = WARPS * 32;
@@ -72,7 +80,7 @@ struct UmStage {
     static constexpr int BYTES = um::IDS + LUT + B;
     static constexpr int SLICES = MERGED ? P : 2 * P;            // MMA K-slices per k-step
     static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per k-step
-    static constexpr int CCOLS = 4 * ACOLS;                      // TMEM columns per A stage (one chunk)
+    static constexpr int CCOLS = um::KS * ACOLS;                 // TMEM columns per A stage (one chunk)
     static constexpr int ACC = P * um::NTOK;                     // accumulator columns
     static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages that fit in TMEM
     static_assert(NCS >= 2, "TMEM budget");
@@ -90,11 +98,14 @@ struct UmStage {
     static constexpr int NA0 = NCS < um::STAGES ? NCS : um::STAGES;
     static constexpr int GS = NA0 >= 4 ? UM_GS4 : (NA0 >= 2 ? 2 : 1);
     static constexpr int NA = (NA0 / GS) * GS;
-    // LAG > 0: the producer issues chunk c's copies LAG chunks before it arms
-    // full[c % NS] (arrive.expect_tx, after the empty wait that proves the MMAs
-    // of chunk c - NA done), so NS = NA + LAG chunks of data are in flight
-    // while full[] alone still means "data and A stage ready".
-    static constexpr int LAG = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? 4 : 0;
+    // LAG > 0: NS = NA + LAG smem stages, so the producer issues chunk c's
+    // copies as soon as the MMAs of chunk c - NS are done, LAG chunks before
+    // A stage c % NA frees.  full[c % NS] then expects two arrivals: the
+    // producer's arrive.expect_tx with the copies, and a tcgen05.commit the MMA
+    // warp issues after chunk c - NA (fires when those MMAs, the last readers
+    // of the A stage, complete).  full[] alone still means "data and A stage
+    // ready", and the producer is out of the expanders' round trip.
+    static constexpr int LAG = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? UM_LAG : 0;
     static constexpr int NS = NA + LAG;
     static_assert(NS % GS == 0 && NA % GS == 0 && NS * BYTES <= 200 * 1024, "smem ring");
 };
@@ -155,6 +166,12 @@ __device__ __forceinline__ void u_bar_expect_elect(uint32_t bar, uint32_t bytes)
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
         "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
         "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void u_bar_arrive_elect(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar)
         : "memory");
 }
 __device__ __forceinline__ void u_bulk_elect(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
@@ -341,13 +358,12 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA];
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
-    __shared__ uint32_t tx_bytes[NS];  // producer: bytes of the chunk in each smem stage (LAG > 0)
     __shared__ int32_t unit_pre[um::MAX_SEG + 1], seg_off[um::MAX_SEG + 1];
     __shared__ __align__(16) uint32_t tok_sh[um::EXP_WARPS][16];  // per expander warp: 8 token scales, 8 row sums
     __shared__ int last_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_chunks = d_in / 128, cpg = g / 128, n_groups = d_in / g;
+    const int n_chunks = d_in / um::CK, cpg = g / um::CK, n_groups = d_in / g;
 
     // units per segment -> prefix table (warp 0: a serial run per lane + shuffle scan)
     if (warp == 0) {
@@ -399,7 +415,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
-            u_bar_init(u_smem(&full_bar[s]), 1);
+            u_bar_init(u_smem(&full_bar[s]), LAG > 0 ? 2 : 1);
             u_bar_init(u_smem(&empty_bar[s]), 1);
         }
         for (int s = 0; s < NA; ++s) u_bar_init(u_smem(&afull_bar[s]), 4 * WPS);  // the warps of one stream
@@ -444,12 +460,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 const bool new_group = true;  // every chunk carries its LUT block: warpgroups take alternate chunks
                 const uint32_t bar = full_a + 8 * s;
                 const uint32_t dst = stage_a + s * S::BYTES;
-                const uint32_t bytes = um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE;
-                if (LAG == 0) {
-                    u_bar_expect_elect(bar, bytes);
-                } else if (lane == 0) {
-                    tx_bytes[s] = bytes;  // complete_tx may land before the arm: tx-count goes transiently negative
-                }
+                u_bar_expect_elect(bar, um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE);
+                if (LAG > 0 && (int)k < NA) u_bar_arrive_elect(bar);  // no chunk k - NA: A stage already free
                 u_bulk_elect(dst, ids + ((size_t)x.tile * n_chunks + c) * um::IDS, um::IDS, bar);
                 if (new_group)
                     u_bulk_elect(dst + um::IDS, lut + ((size_t)x.tile * n_groups + grp) * S::LUT, S::LUT, bar);
@@ -459,22 +471,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     gc = 0;
                     ++grp;
                 }
-                if (LAG > 0) {  // arm chunk k - LAG: the empty wait above covered its A stage
-                    __syncwarp();
-                    if ((int)k >= LAG) {
-                        const int sj = (k - LAG) % NS;
-                        u_bar_expect_elect(full_a + 8 * sj, tx_bytes[sj]);
-                    }
-                }
             }
-        }
-        // the last LAG chunks: wait as if their successors were issued, then arm them
-        for (uint32_t kv = k; LAG > 0 && kv < k + LAG; ++kv) {
-            if ((int)kv < LAG) continue;
-            const int s = kv % NS;
-            if (kv >= NS) u_bar_wait(empty_a + 8 * s, ((kv / NS) - 1) & 1);
-            const int sj = (kv - LAG) % NS;
-            u_bar_expect_elect(full_a + 8 * sj, tx_bytes[sj]);
         }
     } else if (warp == um::MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
@@ -494,9 +491,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 u_bar_wait(afull_a + 8 * sa, (k / NA) & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
+                for (int kk = 0; kk < um::KS; ++kk) {
                     // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
-                    const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, 1024);
+                    const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, um::BTILE);
 #pragma unroll
                     for (int sl = 0; sl < S::SLICES; ++sl) {
                         const int p = MERGED ? sl : (sl >> 1);
@@ -507,14 +504,17 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 #endif
                     }
                 }
-                tc_commit_elect(empty_a + 8 * s);  // frees the smem stage and the A stage
+                tc_commit_elect(empty_a + 8 * s);  // frees the smem stage (and with LAG == 0 the A stage)
+                if (LAG > 0) tc_commit_elect(full_a + 8 * ((k + NA) % NS));  // A stage free for chunk k + NA
                 if (c == c1 - 1) tc_commit_elect(u_smem(&accfull_bar));
             }
         }
     } else {
         // ------------------------------------------------------------ expanders
         const int wg = warp >> 2;
-        const int stream = wg / WPS, ks0 = (wg % WPS) * GS;  // chunks k = stream (mod GS), k-steps ks0..
+        constexpr int KSW = um::KS / WPS;  // k-steps per warpgroup and chunk
+        static_assert(um::KS % WPS == 0, "a chunk's k-steps split evenly over its stream's warpgroups");
+        const int stream = wg / WPS, ks0 = (wg % WPS) * KSW;  // chunks k = stream (mod GS), k-steps ks0..
         const int quarter = warp & 3;     // TMEM lane quarter = rows
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
             // stream wg / WPS expands the chunks k = stream (mod GS); this warpgroup does k-steps
-            // ks0 .. ks0 + GS - 1 of each (see UmStage)
+            // ks0 .. ks0 + KSW - 1 of each (see UmStage)
             for (int c = c0; c < c1; ++c, ++k) {
                 if ((int)(k % GS) != stream) continue;  // warpgroup-uniform
                 const int s = k % NS, sa = k % NA;
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 if (false)
 #endif
 #pragma unroll
-                for (int ks = ks0; ks < ks0 + GS; ++ks) {
+                for (int ks = ks0; ks < ks0 + KSW; ++ks) {
                     const uint4 w = reinterpret_cast<const uint4 *>(st)[ks * 128 + row];
                     const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
                     uint32_t sel[8], xsel[8];
@@ -677,20 +677,21 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     }
 }
 
-// codes (rows, K) row-major -> [chunk128][tile8][kstep4][khalf2][8 rows][16 B],
+// codes (rows, K) row-major -> [chunk CK][tile8][kstep KS][khalf2][8 rows][16 B],
 // the canonical K-major no-swizzle UMMA B layout per k-step; rows >= n are zero.
 // Also zeroes the GEMM's split-unit counters (zero[0..n_zero)).
 __global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
                                  uint4 *__restrict__ dst, int32_t *__restrict__ zero, int n_zero) {
-    const int64_t total = (K / 128) * tiles * 64;  // 16-byte pieces: 8 (kstep, khalf) x 8 rows per tile-chunk
+    constexpr int PIECES = 16 * um::KS;  // 16-byte pieces per tile-chunk: KS x 2 khalf x 8 rows
+    const int64_t total = (K / um::CK) * tiles * PIECES;
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(x & 7), kh = (int)((x >> 3) & 1), ks = (int)((x >> 4) & 3);
-        const int64_t j = (x >> 6) % tiles, c = (x >> 6) / tiles;
+        const int r = (int)(x & 7), kh = (int)((x >> 3) & 1), ks = (int)((x >> 4) % um::KS);
+        const int64_t j = (x / PIECES) % tiles, c = (x / PIECES) / tiles;
         const int64_t row = j * 8 + r;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (row < n) v = *reinterpret_cast<const uint4 *>(src + row * K + c * 128 + ks * 32 + kh * 16);
+        if (row < n) v = *reinterpret_cast<const uint4 *>(src + row * K + c * um::CK + ks * 32 + kh * 16);
         dst[x] = v;
     }
 }
@@ -753,7 +754,7 @@ size_t umma_smem() {
 
 cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, int32_t *sums,
                     int32_t *zero, int n_zero, cudaStream_t st) {
-    const int64_t total = (K / 128) * tiles * 64;
+    const int64_t total = (K / um::CK) * tiles * 16 * um::KS;
     if (total == 0) return CQ_OK;
     to_umma_b_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
         codes, n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero);
