@@ -33,8 +33,22 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(name="mixtral-8x7b-moe-layer-decode", d_model=4096, d_ff=14336, n_experts=8, top_k=2,
-           group_size=128)
+# SURVEY.md §8(d) configurations.  The headline (default) is MX: the Mixtral-8x7B
+# layer at decode batch 64 (BASELINE.json configs[1]); the others are for the
+# per-config table in DESIGN.md and are selected with --config.
+CONFIGS = {
+    "mx": dict(name="mixtral-8x7b-moe-layer-decode", d_model=4096, d_ff=14336, n_experts=8, top_k=2, batch=64),
+    "mx1": dict(name="mixtral-8x7b-moe-layer-decode-b1", d_model=4096, d_ff=14336, n_experts=8, top_k=2, batch=1),
+    "mx8": dict(name="mixtral-8x7b-moe-layer-decode-b8", d_model=4096, d_ff=14336, n_experts=8, top_k=2, batch=8),
+    "c1": dict(name="c1-moe-layer-cpu-parity", d_model=1024, d_ff=2816, n_experts=8, top_k=2, batch=64),
+    "ph": dict(name="phi-3.5-moe-layer-prefill-rotation", d_model=4096, d_ff=6400, n_experts=16, top_k=2,
+               batch=4096, rotation=True),
+    "qw": dict(name="qwen3-30b-a3b-moe-layer-prefill", d_model=2048, d_ff=768, n_experts=128, top_k=8, batch=4096),
+    "qw64": dict(name="qwen3-30b-a3b-moe-layer-decode", d_model=2048, d_ff=768, n_experts=128, top_k=8, batch=64),
+    "ds": dict(name="deepseek-v2-lite-moe-block-prefill", d_model=2048, d_ff=1408, n_experts=64, top_k=6,
+               batch=8192, n_shared=2),
+}
+CFG = dict(CONFIGS["mx"], group_size=128)
 
 
 def parse():
@@ -42,7 +56,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--batch", type=int, default=64)
+    p.add_argument("--config", default="mx", choices=sorted(CONFIGS))
+    p.add_argument("--batch", type=int, default=None, help="tokens per step (per rank); default: the config's")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--path", default="auto", choices=["auto", "tc", "f32", "ordered"])
     p.add_argument("--layout", default="umma128u", choices=["umma128", "umma128u", "mma16"],
@@ -125,9 +140,10 @@ def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return {"hbm_gbs": p["hbm_gbs"], "src": "measured"}
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                "src": "measured"}
     except (OSError, KeyError, ValueError):
-        return {"hbm_gbs": 6650.0, "src": "fallback"}
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 2250.0, "src": "fallback"}
 
 
 # ---------------------------------------------------------------------------
@@ -407,9 +423,17 @@ def run_ours(args):
             torch.cuda.empty_cache()
 
     n, d, ff, E, k, g = args.batch, CFG["d_model"], CFG["d_ff"], CFG["n_experts"], CFG["top_k"], CFG["group_size"]
-    v, w, sites, _ = moe_inputs_device(args.seed + 17 * rank, n, d, ff, E, g)
+    n_sh = CFG.get("n_shared", 0)
+    v, w, sites, sh_sites = moe_inputs_device(args.seed + 17 * rank, n, d, ff, E, g, n_shared=n_sh)
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=args.path)
+    shared = (tuple(ExpertStack(sh_sites[s][0], sh_sites[s][1], sh_sites[s][2], sh_sites[s][3], g)
+                    for s in ("gate", "up", "down")) if n_sh else None)
+    rotation = None
+    if CFG.get("rotation"):  # random orthogonal R (rotation.py:38-44 draws a QR of a Gaussian)
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(args.seed + 99)
+        rotation = torch.linalg.qr(torch.randn((d, d), generator=gen, device="cuda"))[0].contiguous()
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, rotation=rotation, shared=shared, path=args.path)
     if args.path in ("auto", "tc"):
         try:
             layer.prepare_tc(layout=args.layout)
@@ -491,8 +515,15 @@ def run_ours(args):
         n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, tr["codes_perm"], tr["scales_perm"],
                                                                     tr["offsets"], n * k, max(3, args.steps))
     pk = peaks()
-    achieved = byt["gate_up"] / (gu_ms * 1e-3) / 1e9
-    traffic = traffic_for(args.layout)
+    R = n * k
+    # prefill (>= 128 routes per active expert) is tensor-bound: report the gate|up
+    # kernel's algorithmic flops (2*R*2*d*ff, digit planes not counted) against the dense bf16 peak
+    tensor_bound = R >= 128 * max(n_active, 1)
+    if tensor_bound:
+        achieved, peak_v, unit = 4.0 * R * d * ff / (gu_ms * 1e-3) / 1e12, pk["bf16_tflops"], "TFLOP/s"
+    else:
+        achieved, peak_v, unit = byt["gate_up"] / (gu_ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+    traffic = traffic_for(args.layout) if args.config == "mx" else None
 
     if rank == 0:
         res = {
@@ -505,15 +536,16 @@ def run_ours(args):
                        "parallelism": (f"replicas{world}" + (f" (ep failed: {args.ep_error})"
                                                              if getattr(args, "ep_error", None) else ""))
                        if world > 1 else "single",
-                       "path": path_used, "layout": args.layout, "l2": "weights 1.41 GB > 126 MB L2, no flush needed",
+                       "path": path_used, "layout": args.layout,
+                       "l2": "weights > 126 MB L2, no flush needed",
                        "cuda_graph": True, "active_experts": n_active},
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),
                     "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},
-            "roofline": {"bound": "hbm",
+            "roofline": {"bound": "tensor" if tensor_bound else "hbm",
                          "kernel": "grouped gate|up LUT GEMM (lut_umma_kernel<3>, tcgen05 kind::i8, A from TMEM)",
-                         "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "peak_src": pk["src"],
+                         "achieved": achieved, "peak": peak_v, "unit": unit,
+                         "frac": achieved / peak_v, "peak_src": pk["src"],
                          "traffic": traffic, "algorithmic_bytes": byt["gate_up"], "kernel_ms": gu_ms,
                          "bytes_def": "SURVEY 8(d): ids d_out*d_in/2 + fp32 centroids d_out*(d_in/g)*64 per active "
                                       "expert and matrix, + codes/scales in + fp32 outputs",
@@ -535,6 +567,12 @@ def run_ours(args):
 
 def main():
     args = parse()
+    CFG.clear()
+    CFG.update(CONFIGS[args.config], group_size=128)
+    if args.batch is None:
+        args.batch = CFG["batch"]
+    if args.config != "mx":
+        args.no_cpu_baseline = True  # the bounded CPU sample is calibrated for the headline config
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     float mx = 0.0f;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
-        const int j = threadIdx.x + u * 512;
+        const int j = threadIdx.x + u * (int)blockDim.x;
         if (j < nv) {
             const float4 x = ar[j], y = br[j];
             h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x < 32) {
-        float m = threadIdx.x < 16 ? red[threadIdx.x] : 0.0f;
+        float m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
         m = warp_max(m);
         if (threadIdx.x == 0) {
             s_sh = a4_scale(m);
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     char4 *cr = reinterpret_cast<char4 *>(codes + row * ff);
 #pragma unroll
     for (int u = 0; u < V; ++u) {
-        const int j = threadIdx.x + u * 512;
+        const int j = threadIdx.x + u * (int)blockDim.x;
         if (j < nv) cr[j] = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
     }
 }
@@ -127,7 +127,11 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
     const int64_t v = ceil_div(ff / 4, 512);
     if (ff % 4 == 0 && v <= 8) {
         switch (v) {
-            case 1: silu_quant_vec_kernel<1><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
+            case 1: {  // short rows: one float4 per thread, CTA sized to the row
+                const int thr = (int)std::max<int64_t>(64, ceil_div(ff / 4, 32) * 32);
+                silu_quant_vec_kernel<1><<<(unsigned)rows, thr, 0, st>>>(a, b, ff, codes, scales, live);
+                break;
+            }
             case 2: silu_quant_vec_kernel<2><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
             case 3:
             case 4: silu_quant_vec_kernel<4><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
@@ -201,22 +205,56 @@ __global__ void combine_kernel(const int32_t *__restrict__ selected, const float
                                const int32_t *__restrict__ inv, const float *__restrict__ fout, int64_t k,
                                int64_t d, const float *__restrict__ add, float *__restrict__ out) {
     const int64_t t = blockIdx.x;
-    int32_t ex[16], pos[16];
-    float w[16];
-    for (int s = 0; s < k; ++s) {
-        ex[s] = __ldg(selected + t * k + s);
-        pos[s] = __ldg(inv + t * k + s);
-        w[s] = __ldg(weights + t * k + s);
-    }
-    for (int a = 1; a < k; ++a)  // insertion sort by expert id (ids are distinct)
-        for (int b = a; b > 0 && ex[b - 1] > ex[b]; --b) {
-            int32_t te = ex[b]; ex[b] = ex[b - 1]; ex[b - 1] = te;
-            int32_t tp = pos[b]; pos[b] = pos[b - 1]; pos[b - 1] = tp;
-            float tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
+    __shared__ int32_t pos_sh[16];
+    __shared__ float w_sh[16];
+    if (threadIdx.x == 0) {  // this token's routes in ascending expert order (ids are distinct)
+        int32_t ex[16], pos[16];
+        float w[16];
+        for (int s = 0; s < k; ++s) {
+            ex[s] = __ldg(selected + t * k + s);
+            pos[s] = __ldg(inv + t * k + s);
+            w[s] = __ldg(weights + t * k + s);
         }
+        for (int a = 1; a < k; ++a)
+            for (int b = a; b > 0 && ex[b - 1] > ex[b]; --b) {
+                int32_t te = ex[b]; ex[b] = ex[b - 1]; ex[b - 1] = te;
+                int32_t tp = pos[b]; pos[b] = pos[b - 1]; pos[b - 1] = tp;
+                float tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
+            }
+        for (int s = 0; s < k; ++s) {
+            pos_sh[s] = pos[s];
+            w_sh[s] = w[s];
+        }
+    }
+    __syncthreads();
+    const int kk = (int)k;
+    if ((d & 3) == 0) {  // 16-byte rows: float4 per thread
+        const int64_t d4 = d >> 2;
+        const float4 *f4 = reinterpret_cast<const float4 *>(fout);
+        for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < d4; j += (int64_t)gridDim.y * blockDim.x) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s = 0; s < kk; ++s) {
+                const float ws = w_sh[s];
+                const float4 f = __ldg(f4 + (int64_t)pos_sh[s] * d4 + j);
+                acc.x = __fadd_rn(acc.x, __fmul_rn(ws, f.x));
+                acc.y = __fadd_rn(acc.y, __fmul_rn(ws, f.y));
+                acc.z = __fadd_rn(acc.z, __fmul_rn(ws, f.z));
+                acc.w = __fadd_rn(acc.w, __fmul_rn(ws, f.w));
+            }
+            if (add != nullptr) {
+                const float4 a4 = reinterpret_cast<const float4 *>(add)[t * d4 + j];
+                acc.x = __fadd_rn(acc.x, a4.x);
+                acc.y = __fadd_rn(acc.y, a4.y);
+                acc.z = __fadd_rn(acc.z, a4.z);
+                acc.w = __fadd_rn(acc.w, a4.w);
+            }
+            reinterpret_cast<float4 *>(out)[t * d4 + j] = acc;
+        }
+        return;
+    }
     for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < d; j += (int64_t)gridDim.y * blockDim.x) {
         float acc = 0.0f;
-        for (int s = 0; s < k; ++s) acc = __fadd_rn(acc, __fmul_rn(w[s], __ldg(fout + (int64_t)pos[s] * d + j)));
+        for (int s = 0; s < kk; ++s) acc = __fadd_rn(acc, __fmul_rn(w_sh[s], __ldg(fout + (int64_t)pos_sh[s] * d + j)));
         if (add != nullptr) acc = __fadd_rn(acc, add[t * d + j]);
         out[t * d + j] = acc;
     }
@@ -555,8 +593,10 @@ extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weight
         set_error("combine: top_k out of range");
         return CQ_ERR_CONFIG;
     }
-    dim3 grid((unsigned)n_tokens, (unsigned)std::max<int64_t>(1, std::min<int64_t>(16, ceil_div(d_model, 256))));
-    combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(selected, weights, inv, fout, top_k, d_model, add, out);
+    const int64_t cols = (d_model & 3) == 0 ? d_model / 4 : d_model;  // work items per token
+    const int threads = (int)std::min<int64_t>(256, ceil_div(cols, 32) * 32);
+    dim3 grid((unsigned)n_tokens, (unsigned)std::max<int64_t>(1, std::min<int64_t>(16, ceil_div(cols, threads))));
+    combine_kernel<<<grid, threads, 0, as_stream(stream)>>>(selected, weights, inv, fout, top_k, d_model, add, out);
     return check_launch("combine");
 }
 

@@ -136,6 +136,73 @@ __global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__r
     if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
 }
 
+// Many experts (E in {32, 64, 128}): thread = (token group, expert), TPT
+// independent token chains per thread, so a staged W element is reused TPT
+// times instead of once (with one chain per thread every CTA streams all of W
+// for a single token).  Each chain is still one ordered fp32 add per column.
+template <int EC, int TPT>
+__global__ void __launch_bounds__(RD_THREADS) router_multi_kernel(const float *__restrict__ xdeq,
+                                                                  const float *__restrict__ w, int64_t n, int64_t d,
+                                                                  int rk, float *__restrict__ logits) {
+    constexpr int TG = RD_THREADS / EC;  // token groups per CTA
+    constexpr int TT = TG * TPT;         // tokens per CTA
+    extern __shared__ __align__(16) float rds[];
+    float *xs = rds;                          // [2][TT][rk]
+    float *ws = rds + (size_t)2 * TT * rk;    // [2][rk][EC]
+    const int tid = threadIdx.x, e = tid % EC, tg = tid / EC;
+    const int64_t t0 = blockIdx.x * (int64_t)TT;
+    const int n_chunks = (int)((d + rk - 1) / rk);
+    auto stage = [&](int i) {
+        const int b = i & 1;
+        const int64_t k0 = (int64_t)i * rk;
+        const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
+        float *wsb = ws + (size_t)b * rk * EC;
+        for (int x = tid; x < kn * EC / 4; x += RD_THREADS) cp_async16(wsb + 4 * x, w + k0 * EC + 4 * x);
+        const int rowv = kn / 4;
+        float *xsb = xs + (size_t)b * TT * rk;
+        for (int x = tid; x < TT * rowv; x += RD_THREADS) {
+            const int tl = x / rowv, v = x - tl * rowv;
+            const int64_t tg2 = t0 + tl < n ? t0 + tl : n - 1;  // clamp: rows past n are never stored
+            cp_async16(xsb + tl * rk + 4 * v, xdeq + tg2 * d + k0 + 4 * v);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage(0);
+    float acc[TPT];
+#pragma unroll
+    for (int i = 0; i < TPT; ++i) acc[i] = 0.0f;
+    for (int c = 0; c < n_chunks; ++c) {
+        const int b = c & 1;
+        if (c + 1 < n_chunks) {
+            stage(c + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const int kn = (int)((d - (int64_t)c * rk) < rk ? (d - (int64_t)c * rk) : rk);  // multiple of 16
+        const float *wr = ws + (size_t)b * rk * EC + e;
+        const float *xr = xs + (size_t)b * TT * rk + (size_t)tg * TPT * rk;
+        for (int j = 0; j < kn; j += 4) {
+            const float w0 = wr[(j + 0) * EC], w1 = wr[(j + 1) * EC], w2 = wr[(j + 2) * EC], w3 = wr[(j + 3) * EC];
+#pragma unroll
+            for (int i = 0; i < TPT; ++i) {
+                const float4 xv = *reinterpret_cast<const float4 *>(xr + i * rk + j);
+                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.x, w0));
+                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.y, w1));
+                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.z, w2));
+                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.w, w3));
+            }
+        }
+        __syncthreads();  // buffer b is refilled by the next iteration's prefetch
+    }
+#pragma unroll
+    for (int i = 0; i < TPT; ++i) {
+        const int64_t t = t0 + tg * TPT + i;
+        if (t < n) logits[t * EC + e] = acc[i];
+    }
+}
+
 // numpy's float32 sum of a short row: a plain loop below 8 elements, eight
 // interleaved partial sums combined as a tree from 8 up (pairwise_sum).
 __device__ __forceinline__ float np_sum(const float *v, int n) {
@@ -157,33 +224,55 @@ __device__ __forceinline__ float np_sum(const float *v, int n) {
 
 constexpr int MAX_TOPK = 16;
 
-// One thread per token: stable descending selection (ties -> lower id; +0 and
-// -0 compare equal like numpy's sort), softmax over the selected logits, and
-// per-expert route counts for the local expert range.
-__global__ void topk_kernel(const float *__restrict__ logits, int64_t n, int64_t n_exp, int64_t k,
-                            int32_t *__restrict__ selected, float *__restrict__ weights,
-                            int32_t *__restrict__ counts, int64_t local_begin, int64_t n_local) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n) return;
+// One warp per token: the lanes hold the token's logits (expert e in lane e % 32),
+// and each of the k rounds is a warp argmax (larger logit first, ties -> lower
+// expert id, +0 and -0 equal like numpy's sort): the stable descending
+// selection of model.py:324-330.  Lane 0 then forms the softmax over the
+// selected logits and counts the routes of the local expert range.
+constexpr int TOPK_WARPS = 4;
+
+__global__ void __launch_bounds__(TOPK_WARPS * 32) topk_kernel(const float *__restrict__ logits, int64_t n,
+                                                               int64_t n_exp, int64_t k, int32_t *__restrict__ selected,
+                                                               float *__restrict__ weights, int32_t *__restrict__ counts,
+                                                               int64_t local_begin, int64_t n_local) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = blockIdx.x * (int64_t)TOPK_WARPS + (threadIdx.x >> 5);
+    if (t >= n) return;  // warp-uniform
     const float *row = logits + t * n_exp;
+    constexpr int PER = 256 / 32;  // <= 256 experts
+    float lv[PER];
+    uint32_t taken = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int64_t e = lane + 32 * i;
+        lv[i] = e < n_exp ? __ldg(row + e) : 0.0f;
+        if (e >= n_exp) taken |= 1u << i;
+    }
     int sel[MAX_TOPK];
     float val[MAX_TOPK];
     for (int s = 0; s < k; ++s) {
         int best = -1;
         float bv = 0.0f;
-        for (int e = 0; e < n_exp; ++e) {
-            bool taken = false;
-            for (int p = 0; p < s; ++p) taken |= (sel[p] == e);
-            if (taken) continue;
-            const float v = row[e];
-            if (best < 0 || v > bv) {
-                best = e;
-                bv = v;
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            if (!(taken >> i & 1) && (best < 0 || lv[i] > bv)) {  // lane-local: ids ascending with i
+                best = lane + 32 * i;
+                bv = lv[i];
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            if (ob >= 0 && (best < 0 || ov > bv || (!(bv > ov) && ob < best))) {
+                best = ob;
+                bv = ov;
             }
         }
         sel[s] = best;
         val[s] = bv;
+        if ((best & 31) == lane) taken |= 1u << (best >> 5);
     }
+    if (lane != 0) return;
     const float m = val[0];  // max of the selected logits
     float ex[MAX_TOPK];
     for (int s = 0; s < k; ++s) ex[s] = expf(__fsub_rn(val[s], m));
@@ -278,6 +367,29 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         set_error("router: at most 256 experts");
         return CQ_ERR_CONFIG;
     }
+    if (xdeq != nullptr && d % 16 == 0 && (n_exp == 32 || n_exp == 64 || n_exp == 128) && n >= 64) {
+        constexpr int TPT = 16;
+        const int tt = (RD_THREADS / (int)n_exp) * TPT;
+        int rk = (int)std::min<int64_t>(512, ((96 * 1024) / (8 * (tt + n_exp))) & ~15LL);
+        if (rk < 16) rk = 16;
+        const size_t smem = (size_t)8 * rk * (tt + n_exp);
+        static bool attr_m = false;
+        if (!attr_m) {
+            cudaFuncSetAttribute(router_multi_kernel<32, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(router_multi_kernel<64, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(router_multi_kernel<128, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 96 * 1024);
+            attr_m = true;
+        }
+        const dim3 grid((unsigned)ceil_div(n, tt));
+        if (n_exp == 32)
+            router_multi_kernel<32, TPT><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, rk, logits);
+        else if (n_exp == 64)
+            router_multi_kernel<64, TPT><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, rk, logits);
+        else
+            router_multi_kernel<128, TPT><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, rk, logits);
+        return check_launch("router_logits");
+    }
     if (xdeq != nullptr && n_exp <= RD_THREADS && d % 16 == 0) {
         const int tt = RD_THREADS / (int)n_exp;
         // double-buffered x [tt][rk] + W [rk][E] f32 in <= 96 KB; rk a multiple of 16, <= 512
@@ -321,8 +433,8 @@ cq_status topk(const float *logits, int64_t n, int64_t n_exp, int64_t k, int32_t
         return CQ_ERR_CONFIG;
     }
     if (n == 0) return CQ_OK;
-    topk_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(logits, n, n_exp, k, sel, wts, counts,
-                                                            local_begin, n_local);
+    topk_kernel<<<(unsigned)ceil_div(n, TOPK_WARPS), TOPK_WARPS * 32, 0, st>>>(logits, n, n_exp, k, sel, wts,
+                                                                             counts, local_begin, n_local);
     return check_launch("topk");
 }
 

@@ -119,3 +119,72 @@ def test_mixtral_decode_vs_oracle_subsample_and_ordered():
     want = oracle.moe_layer_fast(v[:sub].float().cpu().numpy(), w.cpu().numpy(), host_experts, k)
     assert o.relative_error(ordered[:sub].cpu().numpy(), want) <= LAYER_TOL
     assert o.relative_error(out[:sub].cpu().numpy(), want) <= LAYER_TOL
+
+
+def _host_experts(sites, n_exp, g):
+    out = []
+    for e in range(n_exp):
+        out.append([(sites[s][1][e].cpu().numpy(), sites[s][0][e].cpu().numpy(), g) for s in ("gate", "up", "down")])
+    return out
+
+
+@pytest.mark.parametrize("E,k", [(32, 6), (64, 6), (128, 8), (16, 2)])
+def test_router_many_experts_bit_exact(E, k):
+    """Routing at the QW / DS / PH expert counts (the multi-chain router kernel
+    for E in {32, 64, 128}): logits and the selected experts bit-exact with the
+    ordered chain of _core.matmul_f32 + select_top_k; weights ulp-bounded."""
+    n, d, ff, g = 300, 1024, 128, 128
+    v, w, sites, _ = moe_inputs_device(23 + E, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="f32")
+    layer(v)
+    tr = layer.trace(n)
+    vh = v.float().cpu().numpy()
+    codes, scales = oracle.c_quantize(vh)
+    logits = oracle.c_matmul(codes.astype(np.float32) * scales[:, None], w.cpu().numpy())
+    sel, wts = o.select_top_k(logits, k)
+    assert np.array_equal(tr["logits"].cpu().numpy().view(np.int32), logits.view(np.int32))
+    assert np.array_equal(tr["selected"].cpu().numpy(), sel)
+    ulp = np.abs(tr["weights"].cpu().numpy().view(np.int32) - wts.astype(np.float32).view(np.int32))
+    assert ulp.max() <= 8
+    tok, slot, off, inv = o.route_permutation(sel, E)
+    assert np.array_equal(tr["offsets"].cpu().numpy(), off)
+    assert np.array_equal(tr["inv"].cpu().numpy(), inv)
+
+
+@pytest.mark.parametrize("cfg", ["qw", "ds"])
+def test_many_expert_layers_tc_vs_oracle(cfg):
+    """QW (d2048/ff768/E128/top-8) and DS (d2048/ff1408/E64+2 shared/top-6)
+    layer shapes on the tensor-core path vs the composed CPU oracle."""
+    d, ff, E, k, n_sh = {"qw": (2048, 768, 128, 8, 0), "ds": (2048, 1408, 64, 6, 2)}[cfg]
+    n, g = 80, 128
+    v, w, sites, sh = moe_inputs_device(31, n, d, ff, E, g, n_shared=n_sh)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    shared = (tuple(ExpertStack(sh[s][0], sh[s][1], sh[s][2], sh[s][3], g) for s in ("gate", "up", "down"))
+              if n_sh else None)
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, shared=shared, path="tc")
+    layer.prepare_tc()
+    out = layer(v).cpu().numpy()
+    ordered = layer(v, path="ordered").cpu().numpy()
+    want = oracle.moe_layer_fast(v.float().cpu().numpy(), w.cpu().numpy(), _host_experts(sites, E, g), k,
+                                 shared=_host_experts(sh, n_sh, g) if n_sh else ())
+    assert o.relative_error(ordered, want) <= 1e-6
+    assert o.relative_error(out, want) <= LAYER_TOL
+
+
+def test_phi_prefill_rotation_tc_vs_oracle():
+    """PH shape (d4096/ff6400/E16/top-2) with the online rotation v = x @ R,
+    prefill-sized batch: the tensor-core path vs the oracle on a token subsample."""
+    n, d, ff, E, k, g = 256, 4096, 6400, 16, 2, 128
+    x, w, sites, _ = moe_inputs_device(37, n, d, ff, E, g)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    R = torch.linalg.qr(torch.randn((d, d), generator=gen, device="cuda"))[0].contiguous()
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, rotation=R, path="tc")
+    layer.prepare_tc()
+    out = layer(x).cpu().numpy()
+    sub = 8
+    vr = oracle.c_matmul(x[:sub].float().cpu().numpy(), R.cpu().numpy())
+    want = oracle.moe_layer_fast(vr, w.cpu().numpy(), _host_experts(sites, E, g), k)
+    assert o.relative_error(out[:sub], want) <= LAYER_TOL
