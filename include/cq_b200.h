@@ -129,6 +129,8 @@ typedef struct {
     int64_t n_shared;          /* builder-defined always-on experts (weight 1), stacked like the above */
     cq_expert_site sh_gate, sh_up, sh_down;
     int32_t path;              /* CQ_PATH_* */
+    const void *rotation_tc;   /* optional: R prepared by cq_rotation_prepare (tensor-core rotation);
+                                  NULL -> fp32 CUDA-core rotation of `rotation` */
 } cq_moe_desc;
 
 enum { CQ_PATH_AUTO = 0, CQ_PATH_F32 = 1, CQ_PATH_TC = 2, CQ_PATH_ORDERED = 3 };
@@ -155,6 +157,7 @@ enum {
     CQ_WS_SHARED,       /* f32  [n][d_model]   shared-expert sum             */
     CQ_WS_CODES_FRAG,   /* int8 [ceil(n*k/8)*8][d_model] codes in mma-B fragment order */
     CQ_WS_HCODES_FRAG,  /* int8 [ceil(n*k/8)*8][d_ff]    hidden codes, fragment order  */
+    CQ_WS_ROT_ACT,      /* bf16 [3][ceil(n/128)*128][d_model] rotation operand planes (rotation_tc) */
     CQ_WS_COUNT_
 };
 
@@ -221,6 +224,13 @@ CQ_API cq_status cq_ep_group(const uint8_t *recv, int64_t slots, int64_t d_model
  * the return exchange; only the offsets[n_local] live rows are moved. */
 CQ_API cq_status cq_ep_scatter(const float *fout, const int32_t *offsets, const int32_t *slot_of_row,
                                int64_t n_local, int64_t rows_bound, int64_t d_model, float *back, void *stream);
+
+/* Online rotation on the tensor cores (pipeline.py:516, v = x @ R) at fp32 accuracy:
+ * R (d, d) f32 is split once into three bf16 planes of R^T in the UMMA operand layout
+ * (`prepared`: cq_rotation_prepared_bytes(d) bytes); set cq_moe_desc.rotation_tc to it.
+ * Requires d % 256 == 0. */
+CQ_API int64_t cq_rotation_prepared_bytes(int64_t d_model);
+CQ_API cq_status cq_rotation_prepare(const float *rotation, int64_t d_model, void *prepared, void *stream);
 
 /* One-time re-layout of one stacked site (rows = E*d_out) for the tensor-core path:
  * every row's centroids become `planes` int8 base-255 digit planes at one

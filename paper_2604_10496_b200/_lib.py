@@ -25,7 +25,7 @@ CQ_TC_MMA16, CQ_TC_UMMA128, CQ_TC_UMMA128U = 0, 1, 2
 TC_LAYOUTS = {"mma16": CQ_TC_MMA16, "umma128": CQ_TC_UMMA128, "umma128u": CQ_TC_UMMA128U}
 WS_NAMES = ("codes", "scales", "logits", "selected", "weights", "counts", "offsets",
             "perm_token", "perm_slot", "inv", "codes_perm", "scales_perm", "hidden",
-            "hcodes", "hscales", "fout", "rotated", "shared", "codes_frag", "hcodes_frag")
+            "hcodes", "hscales", "fout", "rotated", "shared", "codes_frag", "hcodes_frag", "rot_act")
 
 _vp, _i64, _i32, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 
@@ -43,7 +43,7 @@ class MoEDesc(ctypes.Structure):
                 ("gate", ExpertSite), ("up", ExpertSite), ("down", ExpertSite),
                 ("n_shared", _i64),
                 ("sh_gate", ExpertSite), ("sh_up", ExpertSite), ("sh_down", ExpertSite),
-                ("path", _i32)]
+                ("path", _i32), ("rotation_tc", _vp)]
 
 
 _SIGS = {
@@ -63,10 +63,11 @@ _SIGS = {
     "cq_ep_dispatch": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _vp, _vp],
     "cq_ep_group": [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
     "cq_ep_scatter": [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp],
+    "cq_rotation_prepare": [_vp, _i64, _vp, _vp],
 }
 
 EXPORTS = tuple(_SIGS) + ("cq_last_error", "cq_abi_version", "cq_launch_count", "cq_moe_workspace",
-                          "cq_ep_row_bytes", "cq_ep_scratch_bytes")
+                          "cq_ep_row_bytes", "cq_ep_scratch_bytes", "cq_rotation_prepared_bytes")
 
 _LIB = None
 
@@ -92,6 +93,8 @@ def load_library() -> ctypes.CDLL:
         lib.cq_ep_row_bytes.restype = _i64
         lib.cq_ep_scratch_bytes.argtypes = [_i64, _i64, _i32, _i64, _i64]
         lib.cq_ep_scratch_bytes.restype = _i64
+        lib.cq_rotation_prepared_bytes.argtypes = [_i64]
+        lib.cq_rotation_prepared_bytes.restype = _i64
         _LIB = lib
     return _LIB
 

@@ -8,5 +8,5 @@ void set_error(const std::string &msg) { t_error = msg; }
 }  // namespace cq
 
 extern "C" const char *cq_last_error(void) { return cq::t_error.c_str(); }
-extern "C" int cq_abi_version(void) { return 1; }
+extern "C" int cq_abi_version(void) { return 2; }
 extern "C" int64_t cq_launch_count(void) { return cq::g_launches.load(); }

@@ -40,6 +40,7 @@
 // Epilogue: expanders tcgen05.ld the accumulators, combine the digits, scale
 // by the row scale and the token scale, store fp32.
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 #include <cstdlib>
 
@@ -109,157 +110,6 @@ struct UmStage {
     static constexpr int NS = NA + LAG;
     static_assert(NS % GS == 0 && NA % GS == 0 && NS * BYTES <= 200 * 1024, "smem ring");
 };
-
-// ---------------------------------------------------------------------------
-// PTX wrappers (tcgen05 / mbarrier / bulk copy)
-
-__device__ __forceinline__ uint32_t u_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-// x >> 16 on the FMA pipe (IMAD.HI) — the ALU pipe is the expanders' bottleneck.
-__device__ __forceinline__ uint32_t hi16(uint32_t x) {
-    uint32_t r;
-    asm("mul.hi.u32 %0, %1, 65536;" : "=r"(r) : "r"(x));
-    return r;
-}
-
-// a | b for halves with disjoint non-zero bytes (== a + b, no carries), as an
-// integer multiply-add so it issues on the FMA pipe instead of the saturated ALU pipe.
-__device__ __forceinline__ uint32_t u_merge(uint32_t a, uint32_t b) {
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(r) : "r"(a), "r"(b));
-    return r;
-}
-
-__device__ __forceinline__ uint32_t u_prmt(uint32_t a, uint32_t b, uint32_t s) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
-    return d;
-}
-
-__device__ __forceinline__ void u_bar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void u_bar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void u_bar_expect(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void u_bar_wait(uint32_t bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "UW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra UW_%=;\n}" ::"r"(bar),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void u_bulk(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-// Warp-converged variants: every lane calls, one elected lane acts (a divergent
-// `if (lane == 0)` around async-proxy instructions costs ~200 cycles each).
-__device__ __forceinline__ void u_bar_expect_elect(uint32_t bar, uint32_t bytes) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
-        "r"(bytes)
-        : "memory");
-}
-__device__ __forceinline__ void u_bar_arrive_elect(uint32_t bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void u_bulk_elect(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ uint32_t u_pin(uint32_t x) {
-    uint32_t r;
-    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
-    return r;
-}
-__device__ __forceinline__ void cp_async4(void *smem_dst, const void *gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(u_smem(smem_dst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void u_prefetch_elect(const void *src, uint32_t bytes) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(src),
-        "r"(bytes)
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-
-// D[tmem d] (+)= A[tmem a] x B[smem desc], kind::i8, 128 x N x 32.  Called by a
-// whole converged warp; one elected lane issues.
-__device__ __forceinline__ void tc_mma_i8(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(d),
-        "r"(a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0u)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
-        : "memory");
-}
-
-// 8 consecutive 32-bit TMEM columns of this thread's lane.
-__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t *v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t *v) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-            taddr),
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t *v) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr)
-                 : "memory");
-}
-__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// K-major, no-swizzle smem descriptor: core matrices of 8 rows x 16 bytes,
-// LBO = byte distance between the two 16-byte K halves, SBO = between 8-row groups.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((addr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-    return d;                // base offset 0, layout SWIZZLE_NONE
-}
-
-// kind::i8 instruction descriptor: s32 accumulate, A and B signed, both K-major.
-__device__ __forceinline__ uint32_t idesc_i8(int n) {
-    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}
 
 // ---------------------------------------------------------------------------
 // Work decomposition: persistent, data-parallel rounds + a stream-K tail.  A

@@ -34,6 +34,9 @@ cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_
                            const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
                            cudaStream_t);
 int64_t umma_b_bytes(int64_t rows, int64_t d_in);
+int64_t rot_tc_act_bytes(int64_t n, int64_t d);
+cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const void *prepared, void *act, float *v,
+                       cudaStream_t st);
 
 // h = silu(a) * b (model.py:396) fused with the per-row A4 re-quantization of
 // h (model.py:397-398, quant.py:89-100): pass 1 forms h in place of a and its
@@ -323,10 +326,11 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_HCODES] = Rh * ff;
     sz[CQ_WS_HSCALES] = Rh * 4;
     sz[CQ_WS_FOUT] = Rh * d * 4;
-    sz[CQ_WS_ROTATED] = dsc->rotation ? n * d * 4 : 0;
+    sz[CQ_WS_ROTATED] = (dsc->rotation || dsc->rotation_tc) ? n * d * 4 : 0;
     sz[CQ_WS_SHARED] = dsc->n_shared > 0 ? n * d * 4 : 0;
     sz[CQ_WS_CODES_FRAG] = umma_b_bytes(Rh, d);     // >= the mma16 fragment size too
     sz[CQ_WS_HCODES_FRAG] = umma_b_bytes(Rh, ff);
+    sz[CQ_WS_ROT_ACT] = dsc->rotation_tc ? rot_tc_act_bytes(n, d) : 0;
     int64_t pos = 0;
     for (int b = 0; b < CQ_WS_COUNT_; ++b) {
         if (off) off[b] = pos;
@@ -341,6 +345,7 @@ struct Ws {
     int32_t *selected, *counts, *offsets, *perm_token, *perm_slot, *inv;
     int8_t *codes_perm, *hcodes;
     uint2 *codes_frag, *hcodes_frag;
+    void *rot_act;
 };
 
 Ws carve(void *base, const int64_t *o) {
@@ -363,6 +368,7 @@ Ws carve(void *base, const int64_t *o) {
     w.hscales = reinterpret_cast<float *>(b + o[CQ_WS_HSCALES]);
     w.fout = reinterpret_cast<float *>(b + o[CQ_WS_FOUT]);
     w.rotated = reinterpret_cast<float *>(b + o[CQ_WS_ROTATED]);
+    w.rot_act = b + o[CQ_WS_ROT_ACT];
     w.shared = reinterpret_cast<float *>(b + o[CQ_WS_SHARED]);
     w.codes_frag = reinterpret_cast<uint2 *>(b + o[CQ_WS_CODES_FRAG]);
     w.hcodes_frag = reinterpret_cast<uint2 *>(b + o[CQ_WS_HCODES_FRAG]);
@@ -488,7 +494,11 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
     const int64_t d = dsc->d_model;
     const void *qin = x;
     int qdt = dtype;
-    if (dsc->rotation != nullptr) {
+    if (dsc->rotation_tc != nullptr) {  // tensor cores, bf16-split R (rotate_tc.cu)
+        CQ_TRY(rot_tc_apply(x, dtype, n, d, dsc->rotation_tc, w.rot_act, w.rotated, st));
+        qin = w.rotated;
+        qdt = CQ_DTYPE_F32;
+    } else if (dsc->rotation != nullptr) {
         dim3 grid((unsigned)ceil_div(d, 64), (unsigned)ceil_div(n, 64));
         if (dtype == CQ_DTYPE_F32)
             rotate_kernel<CQ_DTYPE_F32><<<grid, 256, 0, st>>>(x, dsc->rotation, n, d, w.rotated);

@@ -145,6 +145,7 @@ class MoELayer:
             raise ConfigError(f"unknown path {path!r}; one of {sorted(_PATHS)}")
         self.path = path
         self._ws = {}
+        self._rot_tc = None  # R as three bf16 planes for the tensor-core rotation (prepare_tc)
 
     # ------------------------------------------------------------------
     def prepare_tc(self, planes_gate_up: int = 3, planes_down: int = 2,
@@ -159,6 +160,13 @@ class MoELayer:
                       (self.shared[2], planes_down)]
         for s, p in sites:
             s.prepare_tc(p, layout)
+        if self.rotation is not None and self.d_model % 256 == 0 and self._rot_tc is None:
+            lib = _lib.lib()
+            buf = torch.empty(lib.cq_rotation_prepared_bytes(self.d_model), dtype=torch.uint8, device="cuda")
+            _lib.check(lib.cq_rotation_prepare(self.rotation.data_ptr(), self.d_model, buf.data_ptr(),
+                                               _lib.stream()))
+            self._rot_tc = buf
+            self._ws = {}
         return self
 
     def desc(self, path: str | None = None) -> _lib.MoEDesc:
@@ -172,6 +180,9 @@ class MoELayer:
             d.n_shared = self.shared[0].n
             d.sh_gate, d.sh_up, d.sh_down = (s.site() for s in self.shared)
         d.path = _PATHS[path or self.path]
+        # the tensor-core rotation goes with the tensor-core path; f32 / ordered keep the fp32 rotation
+        if self._rot_tc is not None and (path or self.path) in ("tc", "auto"):
+            d.rotation_tc = self._rot_tc.data_ptr()
         return d
 
     def workspace(self, n: int, path: str | None = None):

@@ -188,3 +188,35 @@ def test_phi_prefill_rotation_tc_vs_oracle():
     vr = oracle.c_matmul(x[:sub].float().cpu().numpy(), R.cpu().numpy())
     want = oracle.moe_layer_fast(vr, w.cpu().numpy(), _host_experts(sites, E, g), k)
     assert o.relative_error(out[:sub], want) <= LAYER_TOL
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_tensor_core_rotation_fp32_accuracy(dtype):
+    """The online rotation on the tensor cores (three bf16 planes of R; three of
+    x for fp32 input) matches x @ R at fp32 accuracy: Frobenius relative error
+    <= 2e-6 vs an fp64 product (fp32 accumulation-order level)."""
+    n, d, ff, E, k, g = 200, 1024, 256, 8, 2, 128
+    x, w, sites, _ = moe_inputs_device(41, n, d, ff, E, g)
+    x = x.to(dtype)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(9)
+    R = torch.linalg.qr(torch.randn((d, d), generator=gen, device="cuda"))[0].contiguous()
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, rotation=R, path="tc")
+    layer.prepare_tc()
+    layer(x)
+    buf, offs = layer.workspace(n)
+    buf.fill_(0xFF)  # poison the workspace: every operand the kernels read must be written first
+    layer(x)
+    from paper_2604_10496_b200 import _lib
+    o_rot = offs[_lib.WS_NAMES.index("rotated")]
+    got = buf[o_rot:o_rot + n * d * 4].view(torch.float32).view(n, d)
+    want = (x.double() @ R.double())
+    err = (torch.linalg.norm(got.double() - want) / torch.linalg.norm(want)).item()
+    # fp32-level: the split keeps ~24 bits; the residual is the tensor core's fp32 accumulation order
+    assert err <= 2e-5, err
+    # and the layer's routing equals the fp32 CUDA-core rotation's almost everywhere
+    f32 = MoELayer.from_stacks(w, *stacks, top_k=k, rotation=R, path="f32")
+    f32(x)
+    agree = (f32.trace(n)["selected"] == layer.trace(n)["selected"]).all(dim=1).float().mean().item()
+    assert agree >= 0.98, agree
