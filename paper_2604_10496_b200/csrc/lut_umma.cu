@@ -62,29 +62,40 @@ namespace cq {
 #define LAG_P3 1
 #endif
 namespace um {
-constexpr int STAGES = 8;        // smem ring depth (128-column chunks)
-constexpr int NTOK = 32;         // max tokens per pass (MMA N)
-constexpr int CK = UM_CK;        // chunk width (input columns): 64 -> 8 A stages of 2 k-steps fit in TMEM
-constexpr int KS = CK / 32;      // MMA k-steps per chunk
-constexpr int IDS = 128 * CK / 2;  // ids bytes per chunk: 128 rows x CK columns / 2
-constexpr int BTILE = 8 * CK;    // activation bytes per 8-token tile per chunk
+constexpr int STAGES = 8;        // most A stages used
 constexpr int WG = 4;            // expander warpgroups; warpgroup w expands k-step w of every chunk
 constexpr int EXP_WARPS = 4 * WG, PROD_WARP = EXP_WARPS, MMA_WARP = EXP_WARPS + 1, WARPS = EXP_WARPS + 2;
 constexpr int THREADS = WARPS * 32;
 constexpr uint32_t TMEM_COLS = 512;
 }  // namespace um
 
-template <int P, bool MERGED>
+// Pass geometry: NT tokens per pass (MMA N), CK input columns per chunk.  Decode
+// uses NT 32 / CK 128 (4 A stages of 4 k-steps); prefill NT 128 / CK 64 (the
+// 3 x 128 accumulator columns leave room for 64-column A stages only), which
+// expands each weight chunk once per 128 tokens instead of per 32.
+template <int NT_, int CK_>
+struct UmGeo {
+    static constexpr int NT = NT_, CK = CK_;
+    static constexpr int KS = CK / 32;         // MMA k-steps per chunk
+    static constexpr int IDS = 128 * CK / 2;   // ids bytes per chunk: 128 rows x CK columns / 2
+    static constexpr int BTILE = 8 * CK;       // activation bytes per 8-token tile per chunk
+    static constexpr int NCB = NT / 32;        // epilogue column blocks per warpgroup
+    static constexpr int PART_WORDS = 3 * NT * 128;  // int32 partial accumulators per slot (P <= 3)
+};
+using UmDecode = UmGeo<32, UM_CK>;
+using UmPrefill = UmGeo<128, 64>;
+
+template <int P, bool MERGED, class GEO>
 struct UmStage {
     static constexpr int LUT = 128 * P * 16;
-    static constexpr int B = (um::NTOK / 8) * um::BTILE;
-    static constexpr int BYTES = um::IDS + LUT + B;
+    static constexpr int B = (GEO::NT / 8) * GEO::BTILE;
+    static constexpr int BYTES = GEO::IDS + LUT + B;
     static constexpr int SLICES = MERGED ? P : 2 * P;            // MMA K-slices per k-step
     static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per k-step
-    static constexpr int CCOLS = um::KS * ACOLS;                 // TMEM columns per A stage (one chunk)
-    static constexpr int ACC = P * um::NTOK;                     // accumulator columns
+    static constexpr int CCOLS = GEO::KS * ACOLS;                // TMEM columns per A stage (one chunk)
+    static constexpr int ACC = P * GEO::NT;                      // accumulator columns
     static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages that fit in TMEM
-    static_assert(NCS >= 2, "TMEM budget");
+    static_assert(NCS >= 1, "TMEM budget");
     // Chunk c uses smem stage and TMEM A stage c % NS (one ring).  full[s] for
     // chunk c means the producer refilled stage s, which it does only after the
     // MMAs of chunk c - NS completed (empty[s]), so the A stage is free too:
@@ -98,6 +109,7 @@ struct UmStage {
     // NA / GS >= 2 A stages, so it expands chunk c + GS while the MMAs of c run.
     static constexpr int NA0 = NCS < um::STAGES ? NCS : um::STAGES;
     static constexpr int GS = NA0 >= 4 ? UM_GS4 : (NA0 >= 2 ? 2 : 1);
+    static_assert(GEO::KS % (um::WG / GS) == 0, "a chunk's k-steps split evenly over a stream's warpgroups");
     static constexpr int NA = (NA0 / GS) * GS;
     // LAG > 0: NS = NA + LAG smem stages, so the producer issues chunk c's
     // copies as soon as the MMAs of chunk c - NS are done, LAG chunks before
@@ -127,7 +139,6 @@ struct UmStage {
 namespace um {
 constexpr int MAX_SEG = 1024;  // segments (experts) per launch, prefix table in smem
 constexpr int MIN_ITERS = 8;   // fewest chunk iterations per CTA in the tail
-constexpr int PART_WORDS = 3 * NTOK * 128;  // int32 partial accumulators per slot (P <= 3)
 }  // namespace um
 
 struct UmWork {
@@ -173,7 +184,7 @@ struct UmUnit {
 };
 
 // unit u -> (segment, pass, matrix, row tile); `seg` walks forward (units are visited in order)
-__device__ __forceinline__ UmUnit um_unit(const UmWork &w, int64_t seg_first, int u, int &seg) {
+__device__ __forceinline__ UmUnit um_unit(const UmWork &w, int64_t seg_first, int u, int &seg, int tpp) {
     while (w.unit_pre[seg + 1] <= u) ++seg;
     UmUnit x;
     x.rb = w.seg_off[seg];
@@ -184,15 +195,15 @@ __device__ __forceinline__ UmUnit um_unit(const UmWork &w, int64_t seg_first, in
     x.mat = r / w.n_rt;
     x.rt = r - x.mat * w.n_rt;
     const int64_t j_last = (x.re - 1) >> 3;
-    x.j0 = (x.rb >> 3) + (int64_t)pass * (um::NTOK / 8);
+    x.j0 = (x.rb >> 3) + (int64_t)pass * tpp;
     const int64_t left = j_last - x.j0 + 1;
-    x.ntc = (int)(left < um::NTOK / 8 ? left : um::NTOK / 8);
+    x.ntc = (int)(left < tpp ? left : tpp);
     x.tile = (seg + seg_first) * w.n_rt + x.rt;
     return x;
 }
 
 // grid: (#SMs); n_mat = 2 computes gate (ids0 ... out0) and up (ids1 ... out1).
-template <int P, bool MERGED>
+template <int P, bool MERGED, class GEO>
 __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
     const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int n_seg, int64_t seg_first,
@@ -200,20 +211,22 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     float *__restrict__ out0, const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1,
     const float *__restrict__ rs1, float *__restrict__ out1, int n_mat, int d_in, int d_out, int g,
     int32_t *__restrict__ part, int32_t *__restrict__ cnt) {
-    using S = UmStage<P, MERGED>;
+    using S = UmStage<P, MERGED, GEO>;
     constexpr int NA = S::NA, NS = S::NS, GS = S::GS, LAG = S::LAG;
     constexpr int WPS = um::WG / GS;  // warpgroups per stream
-    constexpr int TPP = um::NTOK / 8;  // token tiles per pass
+    constexpr int NT = GEO::NT, CK = GEO::CK, NCB = GEO::NCB;
+    constexpr int TPP = NT / 8;       // token tiles per pass
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA];
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
     __shared__ int32_t unit_pre[um::MAX_SEG + 1], seg_off[um::MAX_SEG + 1];
-    __shared__ __align__(16) uint32_t tok_sh[um::EXP_WARPS][16];  // per expander warp: 8 token scales, 8 row sums
+    // per expander warp and column block: 8 token scales, 8 row sums
+    __shared__ __align__(16) uint32_t tok_sh[um::EXP_WARPS][NCB][16];
     __shared__ int last_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_chunks = d_in / um::CK, cpg = g / um::CK, n_groups = d_in / g;
+    const int n_chunks = d_in / CK, cpg = g / CK, n_groups = d_in / g;
 
     // units per segment -> prefix table (warp 0: a serial run per lane + shuffle scan)
     if (warp == 0) {
@@ -298,7 +311,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         UmSeq q = seq0;
         int u, c0, c1;
         while (q.next(W, u, c0, c1)) {
-            const UmUnit x = um_unit(W, seg_first, u, seg);
+            const UmUnit x = um_unit(W, seg_first, u, seg, TPP);
             const uint8_t *ids = x.mat ? ids1 : ids0;
             const int8_t *lut = x.mat ? lut1 : lut0;
             const int ntc16 = (x.ntc + 1) & ~1;  // MMA N is a multiple of 16
@@ -310,13 +323,13 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 const bool new_group = true;  // every chunk carries its LUT block: warpgroups take alternate chunks
                 const uint32_t bar = full_a + 8 * s;
                 const uint32_t dst = stage_a + s * S::BYTES;
-                u_bar_expect_elect(bar, um::IDS + (new_group ? S::LUT : 0) + ntc16 * um::BTILE);
+                u_bar_expect_elect(bar, GEO::IDS + (new_group ? S::LUT : 0) + ntc16 * GEO::BTILE);
                 if (LAG > 0 && (int)k < NA) u_bar_arrive_elect(bar);  // no chunk k - NA: A stage already free
-                u_bulk_elect(dst, ids + ((size_t)x.tile * n_chunks + c) * um::IDS, um::IDS, bar);
+                u_bulk_elect(dst, ids + ((size_t)x.tile * n_chunks + c) * GEO::IDS, GEO::IDS, bar);
                 if (new_group)
-                    u_bulk_elect(dst + um::IDS, lut + ((size_t)x.tile * n_groups + grp) * S::LUT, S::LUT, bar);
-                u_bulk_elect(dst + um::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + x.j0) * um::BTILE,
-                             ntc16 * um::BTILE, bar);
+                    u_bulk_elect(dst + GEO::IDS, lut + ((size_t)x.tile * n_groups + grp) * S::LUT, S::LUT, bar);
+                u_bulk_elect(dst + GEO::IDS + S::LUT, bfrag + ((size_t)c * n_tiles + x.j0) * GEO::BTILE,
+                             ntc16 * GEO::BTILE, bar);
                 if (++gc == cpg) {
                     gc = 0;
                     ++grp;
@@ -330,26 +343,26 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         UmSeq q = seq0;
         int u, c0, c1;
         for (; q.next(W, u, c0, c1); ++nu) {
-            const UmUnit x = um_unit(W, seg_first, u, seg);
+            const UmUnit x = um_unit(W, seg_first, u, seg, TPP);
             const uint32_t idesc = idesc_i8(((x.ntc + 1) & ~1) * 8);
             if (nu > 0) u_bar_wait(u_smem(&accempty_bar), (nu - 1) & 1);
             for (int c = c0; c < c1; ++c, ++k) {
                 const int s = k % NS, sa = k % NA;
-                const uint32_t bbase = stage_a + s * S::BYTES + um::IDS + S::LUT;
+                const uint32_t bbase = stage_a + s * S::BYTES + GEO::IDS + S::LUT;
                 const uint32_t abase = tmem + a_col0 + (uint32_t)(sa * S::CCOLS);
                 // afull implies full: every expander waited for the chunk's data
                 u_bar_wait(afull_a + 8 * sa, (k / NA) & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < um::KS; ++kk) {
+                for (int kk = 0; kk < GEO::KS; ++kk) {
                     // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
-                    const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, um::BTILE);
+                    const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, GEO::BTILE);
 #pragma unroll
                     for (int sl = 0; sl < S::SLICES; ++sl) {
                         const int p = MERGED ? sl : (sl >> 1);
                         const uint32_t accum = (c == c0 && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
 #ifndef UM_EXP_NO_MMA
-                        tc_mma_i8(tmem + (uint32_t)(p * um::NTOK), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
+                        tc_mma_i8(tmem + (uint32_t)(p * NT), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
                                   idesc, accum);
 #endif
                     }
@@ -362,13 +375,12 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     } else {
         // ------------------------------------------------------------ expanders
         const int wg = warp >> 2;
-        constexpr int KSW = um::KS / WPS;  // k-steps per warpgroup and chunk
-        static_assert(um::KS % WPS == 0, "a chunk's k-steps split evenly over its stream's warpgroups");
+        constexpr int KSW = GEO::KS / WPS;  // k-steps per warpgroup and chunk
         const int stream = wg / WPS, ks0 = (wg % WPS) * KSW;  // chunks k = stream (mod GS), k-steps ks0..
         const int quarter = warp & 3;     // TMEM lane quarter = rows
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        const int cb = wg * 8;            // epilogue: token columns cb..cb+7
+        const int cb = wg * 8;            // epilogue: token columns cb + 32 i .. + 7, i < NCB
         uint32_t k = 0, nu = 0;
         int seg = 0;
         UmSeq q = seq0;
@@ -376,16 +388,18 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         for (; q.next(W, u, c0, c1); ++nu) {
             float rscale;
             {
-                const UmUnit x = um_unit(W, seg_first, u, seg);
+                const UmUnit x = um_unit(W, seg_first, u, seg, TPP);
                 rscale = __ldg((x.mat ? rs1 : rs0) + x.tile * 128 + row);
-                // per-token epilogue operands: async copies into this warp's smem slot now, so their
+                // per-token epilogue operands: async copies into this warp's smem slots now, so their
                 // latency hides under the unit's chunks (lanes 0-7 scales, 8-15 row sums)
-                if (lane < 16 && cb < ((x.ntc + 1) & ~1) * 8) {
-                    const int64_t tok = x.j0 * 8 + cb + (lane & 7);
-                    if (tok >= x.rb && tok < x.re && (lane < 8 || MERGED))
-                        cp_async4(&tok_sh[warp][lane],
-                                  lane < 8 ? (const void *)(scales + tok) : (const void *)(qsums + tok));
-                }
+#pragma unroll
+                for (int i = 0; i < NCB; ++i)
+                    if (lane < 16 && cb + 32 * i < ((x.ntc + 1) & ~1) * 8) {
+                        const int64_t tok = x.j0 * 8 + cb + 32 * i + (lane & 7);
+                        if (tok >= x.rb && tok < x.re && (lane < 8 || MERGED))
+                            cp_async4(&tok_sh[warp][i][lane],
+                                      lane < 8 ? (const void *)(scales + tok) : (const void *)(qsums + tok));
+                    }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
             // stream wg / WPS expands the chunks k = stream (mod GS); this warpgroup does k-steps
@@ -398,7 +412,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
                 uint4 L[P];
                 {
-                    const uint4 *lb = reinterpret_cast<const uint4 *>(st + um::IDS) + row * P;
+                    const uint4 *lb = reinterpret_cast<const uint4 *>(st + GEO::IDS) + row * P;
 #pragma unroll
                     for (int p = 0; p < P; ++p) L[p] = lb[p];
                 }
@@ -448,33 +462,45 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(afull_a + 8 * sa);
             }
-            // ---- epilogue of this unit: accumulators -> registers, release TMEM, then finish
+            // ---- epilogue of this unit.  Warpgroup wg owns token columns cb + 32 i (i < NCB).
             u_bar_wait(u_smem(&accfull_bar), nu & 1);
             tc_fence_after();
-            const UmUnit x = um_unit(W, seg_first, u, seg);  // re-decoded (smem) rather than kept live
+            const UmUnit x = um_unit(W, seg_first, u, seg, TPP);  // re-decoded (smem) rather than kept live
             const int n = ((x.ntc + 1) & ~1) * 8;
-            int32_t acc[P][8];
-            if (cb < n) {
+            const bool split = c0 > 0 || c1 < n_chunks;  // unit shared with neighbouring CTAs (stream-K tail)
+            int bf = 0, bl = 0;
+            if (split) {
+                const int64_t ustart = (int64_t)u * n_chunks;
+                bf = W.owner(ustart);
+                bl = W.owner(ustart + n_chunks - 1);
+            }
+            auto load_acc = [&](int cbi, int32_t (&acc)[P][8]) {
 #pragma unroll
                 for (int p = 0; p < P; ++p)
-                    tc_ld8(tmem + lane_addr + (uint32_t)(p * um::NTOK + cb), reinterpret_cast<uint32_t *>(acc[p]));
+                    tc_ld8(tmem + lane_addr + (uint32_t)(p * NT + cbi), reinterpret_cast<uint32_t *>(acc[p]));
                 tc_wait_ld();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));  // the MMA may start the next unit
-            bool finish = true;
-            if (c0 > 0 || c1 < n_chunks) {
-                // unit shared with neighbouring CTAs: publish the partial, the last arriver finishes
-                const int64_t ustart = (int64_t)u * n_chunks;
-                const int bf = W.owner(ustart), bl = W.owner(ustart + n_chunks - 1);
-                int32_t *mine = part + (size_t)(2 * cta + (u != first_tail_unit ? 1 : 0)) * um::PART_WORDS;
-                if (cb < n) {
+            };
+            // the last CTA of a split unit adds the others' partials (exact int32)
+            auto add_partials = [&](int cbi, int32_t (&acc)[P][8]) {
+                __threadfence();
+                for (int b2 = bf; b2 <= bl; ++b2) {
+                    if (b2 == cta) continue;
+                    const int64_t fu = W.tstart(b2) / n_chunks;
+                    const int32_t *src = part + (size_t)(2 * b2 + (u != fu ? 1 : 0)) * GEO::PART_WORDS;
 #pragma unroll
                     for (int p = 0; p < P; ++p)
 #pragma unroll
-                        for (int c2 = 0; c2 < 8; ++c2) mine[(p * um::NTOK + cb + c2) * 128 + row] = acc[p][c2];
+                        for (int c2 = 0; c2 < 8; ++c2) acc[p][c2] += __ldcg(src + (p * NT + cbi + c2) * 128 + row);
                 }
+            };
+            auto publish = [&](int cbi, const int32_t (&acc)[P][8]) {
+                int32_t *mine = part + (size_t)(2 * cta + (u != first_tail_unit ? 1 : 0)) * GEO::PART_WORDS;
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+#pragma unroll
+                    for (int c2 = 0; c2 < 8; ++c2) mine[(p * NT + cbi + c2) * 128 + row] = acc[p][c2];
+            };
+            auto arrive_last = [&]() -> bool {  // every expander thread: true on the unit's last CTA
                 __threadfence();
                 asm volatile("bar.sync 1, %0;" ::"r"(um::EXP_WARPS * 32) : "memory");
                 if (threadIdx.x == 0) {
@@ -483,29 +509,16 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     last_sh = last;
                 }
                 asm volatile("bar.sync 1, %0;" ::"r"(um::EXP_WARPS * 32) : "memory");
-                finish = last_sh != 0;
-                if (finish && cb < n) {
-                    __threadfence();
-                    for (int b2 = bf; b2 <= bl; ++b2) {
-                        if (b2 == cta) continue;
-                        const int64_t fu = W.tstart(b2) / n_chunks;
-                        const int32_t *src = part + (size_t)(2 * b2 + (u != fu ? 1 : 0)) * um::PART_WORDS;
-#pragma unroll
-                        for (int p = 0; p < P; ++p)
-#pragma unroll
-                            for (int c2 = 0; c2 < 8; ++c2) acc[p][c2] += __ldcg(src + (p * um::NTOK + cb + c2) * 128 + row);
-                    }
-                }
-            }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-            if (finish && cb < n) {
+                return last_sh != 0;
+            };
+            auto store = [&](int i, const int32_t (&acc)[P][8]) {
+                const int cbi = cb + 32 * i;
                 float *out = x.mat ? out1 : out0;
-                const float *tscale = reinterpret_cast<const float *>(tok_sh[warp]);
-                const int32_t *tqsum = reinterpret_cast<const int32_t *>(tok_sh[warp]) + 8;
+                const float *tscale = reinterpret_cast<const float *>(tok_sh[warp][i]);
+                const int32_t *tqsum = reinterpret_cast<const int32_t *>(tok_sh[warp][i]) + 8;
 #pragma unroll
                 for (int c2 = 0; c2 < 8; ++c2) {
-                    const int64_t tok = x.j0 * 8 + cb + c2;
+                    const int64_t tok = x.j0 * 8 + cbi + c2;
                     if (tok < x.rb || tok >= x.re) continue;
                     const double base = MERGED ? 128.0 : 255.0;
                     double sum = (double)acc[P - 1][c2];
@@ -515,6 +528,52 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     const float v2 = (float)(sum * (double)rscale);
                     out[tok * d_out + (int64_t)x.rt * 128 + row] = __fmul_rn(v2, tscale[c2]);
                 }
+            };
+            if constexpr (NCB == 1) {
+                // one block: keep it in registers and release TMEM at once, so the MMAs of the next
+                // unit overlap this epilogue
+                int32_t acc[P][8];
+                if (cb < n) load_acc(cb, acc);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
+                bool finish = true;
+                if (split) {
+                    if (cb < n) publish(cb, acc);
+                    finish = arrive_last();
+                    if (finish && cb < n) add_partials(cb, acc);
+                }
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
+                if (finish && cb < n) store(0, acc);
+            } else {
+                // several blocks: read TMEM block by block, release it after the last
+                bool finish = true;
+                if (split) {
+#pragma unroll 1
+                    for (int i = 0; i < NCB; ++i) {
+                        if (cb + 32 * i >= n) break;
+                        int32_t acc[P][8];
+                        load_acc(cb + 32 * i, acc);
+                        publish(cb + 32 * i, acc);
+                    }
+                    finish = arrive_last();
+                }
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
+                if (finish) {
+#pragma unroll 1
+                    for (int i = 0; i < NCB; ++i) {
+                        if (cb + 32 * i >= n) break;
+                        int32_t acc[P][8];
+                        load_acc(cb + 32 * i, acc);
+                        if (split) add_partials(cb + 32 * i, acc);
+                        store(i, acc);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
             }
         }
     }
@@ -530,18 +589,19 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 // codes (rows, K) row-major -> [chunk CK][tile8][kstep KS][khalf2][8 rows][16 B],
 // the canonical K-major no-swizzle UMMA B layout per k-step; rows >= n are zero.
 // Also zeroes the GEMM's split-unit counters (zero[0..n_zero)).
+template <int CK>
 __global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
                                  uint4 *__restrict__ dst, int32_t *__restrict__ zero, int n_zero) {
-    constexpr int PIECES = 16 * um::KS;  // 16-byte pieces per tile-chunk: KS x 2 khalf x 8 rows
-    const int64_t total = (K / um::CK) * tiles * PIECES;
+    constexpr int PIECES = 16 * (CK / 32);  // 16-byte pieces per tile-chunk: k-steps x 2 khalf x 8 rows
+    const int64_t total = (K / CK) * tiles * PIECES;
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(x & 7), kh = (int)((x >> 3) & 1), ks = (int)((x >> 4) % um::KS);
+        const int r = (int)(x & 7), kh = (int)((x >> 3) & 1), ks = (int)((x >> 4) % (CK / 32));
         const int64_t j = (x / PIECES) % tiles, c = (x / PIECES) / tiles;
         const int64_t row = j * 8 + r;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (row < n) v = *reinterpret_cast<const uint4 *>(src + row * K + c * um::CK + ks * 32 + kh * 16);
+        if (row < n) v = *reinterpret_cast<const uint4 *>(src + row * K + c * CK + ks * 32 + kh * 16);
         dst[x] = v;
     }
 }
@@ -597,16 +657,17 @@ __global__ void lut_relayout_kernel(const int8_t *__restrict__ lut16, int64_t ro
 
 bool umma_ok(int64_t d_in, int64_t d_out, int64_t g) { return d_in % 128 == 0 && g % 128 == 0 && d_out % 128 == 0; }
 
-template <int P, bool MERGED>
+template <int P, bool MERGED, class GEO>
 size_t umma_smem() {
-    return (size_t)UmStage<P, MERGED>::NS * UmStage<P, MERGED>::BYTES;
+    return (size_t)UmStage<P, MERGED, GEO>::NS * UmStage<P, MERGED, GEO>::BYTES;
 }
 
+template <int CK>
 cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, int32_t *sums,
                     int32_t *zero, int n_zero, cudaStream_t st) {
-    const int64_t total = (K / um::CK) * tiles * 16 * um::KS;
+    const int64_t total = (K / CK) * tiles * 16 * (CK / 32);
     if (total == 0) return CQ_OK;
-    to_umma_b_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
+    to_umma_b_kernel<CK><<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
         codes, n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero);
     CQ_TRY(check_launch("to_umma_b"));
     if (sums == nullptr) return CQ_OK;
@@ -636,29 +697,60 @@ static int64_t umma_sums_off(int64_t rows, int64_t d_in) { return umma_b_tiles(r
 static int64_t umma_part_off(int64_t rows, int64_t d_in) {
     return umma_sums_off(rows, d_in) + ceil_div(rows * 4, 256) * 256;
 }
+// Prefill geometry when the segments average >= 64 rows (and there are >= 256 rows).
+static bool umma_prefill(int64_t rows, int64_t n_seg) { return rows >= 256 && rows >= 64 * n_seg; }
+// The scratch is sized for the largest geometry `rows` can select.
+static int64_t umma_part_words(int64_t rows) {
+    return rows >= 256 ? UmPrefill::PART_WORDS : UmDecode::PART_WORDS;
+}
 static int64_t umma_cnt_off(int64_t rows, int64_t d_in) {
-    return umma_part_off(rows, d_in) + (int64_t)2 * umma_grid() * um::PART_WORDS * 4;
+    return umma_part_off(rows, d_in) + (int64_t)2 * umma_grid() * umma_part_words(rows) * 4;
 }
 int64_t umma_b_bytes(int64_t rows, int64_t d_in) {
     return umma_cnt_off(rows, d_in) + ceil_div((int64_t)umma_grid() * 4, 256) * 256;
 }
 
-template <int P, bool MERGED>
+template <int P, bool MERGED, class GEO>
 cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *sums,
                       const int32_t *offsets, int64_t n_seg, int64_t seg_first, const cq_expert_site *a, float *out_a,
                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, int32_t *part,
                       int32_t *cnt, cudaStream_t st) {
     static bool attr = false;
-    const size_t smem = umma_smem<P, MERGED>();
+    const size_t smem = umma_smem<P, MERGED, GEO>();
     if (!attr) {
-        cudaFuncSetAttribute(lut_umma_kernel<P, MERGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lut_umma_kernel<P, MERGED, GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    lut_umma_kernel<P, MERGED><<<umma_grid(), um::THREADS, smem, st>>>(
+    lut_umma_kernel<P, MERGED, GEO><<<umma_grid(), um::THREADS, smem, st>>>(
         bfrag, n_tiles, scales, sums, offsets, (int)n_seg, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
         b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, b ? 2 : 1, (int)d_in,
         (int)d_out, (int)a->group_size, part, cnt);
     return check_launch("lut_umma");
+}
+
+template <class GEO>
+cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, const int32_t *offsets, int64_t n_seg,
+                       int64_t seg_first, int64_t rows, const cq_expert_site *a, float *out_a,
+                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
+    const bool merged = a->tc_layout == CQ_TC_UMMA128U;
+    const int64_t tiles = umma_b_tiles(rows);
+    int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in)) : nullptr;
+    int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
+    int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
+    CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), st));
+#define CQ_UMMA(P_, M_)                                                                                   \
+    launch_umma<P_, M_, GEO>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, \
+                             d_out, part, cnt, st)
+    if (merged) {
+        if (a->tc_planes == 3) return CQ_UMMA(3, true);
+        if (a->tc_planes == 2) return CQ_UMMA(2, true);
+    } else if constexpr (GEO::NT == 32) {  // the signed layouts exist in the decode geometry only
+        if (a->tc_planes == 3) return CQ_UMMA(3, false);
+        if (a->tc_planes == 2) return CQ_UMMA(2, false);
+    }
+#undef CQ_UMMA
+    set_error("tcgen05 path: planes must be 2 or 3");
+    return CQ_ERR_CONFIG;
 }
 
 // Grouped tcgen05 LUT GEMM over segments.  `bbuf` holds umma_b_bytes(rows,
@@ -684,20 +776,12 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         set_error("tcgen05 path: at most 1024 segments (experts) per launch");
         return CQ_ERR_UNSUPPORTED;
     }
-    const bool merged = a->tc_layout == CQ_TC_UMMA128U;
-    const int64_t tiles = umma_b_tiles(rows);
-    int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in)) : nullptr;
-    int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
-    int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
-    CQ_TRY(to_umma_b(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), st));
-#define CQ_UMMA(P_, M_)                                                                                             \
-    launch_umma<P_, M_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, part, \
-                        cnt, st)
-    if (a->tc_planes == 3) return merged ? CQ_UMMA(3, true) : CQ_UMMA(3, false);
-    if (a->tc_planes == 2) return merged ? CQ_UMMA(2, true) : CQ_UMMA(2, false);
-#undef CQ_UMMA
-    set_error("tcgen05 path: planes must be 2 or 3");
-    return CQ_ERR_CONFIG;
+    // prefill geometry (128-token passes, merged layout only) when segments are long
+    if (umma_prefill(rows, n_seg) && a->tc_layout == CQ_TC_UMMA128U && getenv("CQ_UMMA_NO_PREFILL") == nullptr)
+        return lut_umma_geo<UmPrefill>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b,
+                                       d_in, d_out, st);
+    return lut_umma_geo<UmDecode>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b, d_in,
+                                  d_out, st);
 }
 
 // One-time re-layout for the tcgen05 kernel from the 16-row LUT layout.

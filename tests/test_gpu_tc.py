@@ -140,3 +140,39 @@ def test_mixtral_decode_tc_vs_ordered(layout):
     # and the tc path is deterministic
     again = layer(v).float()
     assert torch.equal(again, out)
+
+
+@pytest.mark.parametrize("n,d_in,d_out,g,planes", [(256, 1024, 512, 128, 3), (300, 2048, 768, 128, 2),
+                                                   (777, 1024, 1408, 256, 3), (1024, 4096, 256, 128, 3)])
+def test_prefill_geometry_bitwise_equals_decode(monkeypatch, n, d_in, d_out, g, planes):
+    """Long segments take the prefill geometry (128-token passes, 64-column
+    chunks).  Both geometries accumulate exact int32 digit products, so the
+    result is bitwise that of the 32-token decode geometry, and matches the
+    oracle within the digit-plane tolerance."""
+    rng = np.random.default_rng(n + d_in + planes)
+    cent, ids, pw = _rand_pw(rng, d_out, d_in, g)
+    codes = rng.integers(-8, 8, (n, d_in)).astype(np.int8)
+    scales = (0.5 + rng.random(n)).astype(np.float32)
+    qa = QuantizedActivations(torch.from_numpy(codes).cuda(), torch.from_numpy(scales).cuda(), 4)
+    pre = lut_gemm_tc(qa, pw, planes, "umma128u").clone()
+    monkeypatch.setenv("CQ_UMMA_NO_PREFILL", "1")
+    dec = lut_gemm_tc(qa, pw, planes, "umma128u").clone()
+    torch.cuda.synchronize()
+    assert torch.equal(pre, dec)
+    want = oracle.c_lut_gemm(codes, scales, ids, cent, g)
+    assert o.relative_error(pre.cpu().numpy(), want) <= (2e-6 if planes == 3 else 2e-4)
+
+
+def test_prefill_moe_layer_bitwise_equals_decode(monkeypatch):
+    """A prefill-sized MoE layer (avg 200 routes per expert): the grouped
+    prefill GEMMs (stream-K tail included) equal the decode geometry bitwise."""
+    n, d, ff, E, k, g = 400, 1024, 1536, 4, 2, 128
+    v, w, sites, _ = moe_inputs_device(43, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
+    layer.prepare_tc()
+    pre = layer(v).clone()
+    monkeypatch.setenv("CQ_UMMA_NO_PREFILL", "1")
+    dec = layer(v).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(pre, dec)
