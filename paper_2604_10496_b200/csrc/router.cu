@@ -7,6 +7,8 @@
 // are therefore bit-exact.  Route weights use CUDA expf (ulp-bounded vs numpy).
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace cq {
 
 // logits[t, e] = sum_k (q[t,k] * s_t) * W[k, e], k ascending, one rounding per
@@ -80,10 +82,10 @@ __global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__r
         const int64_t k0 = (int64_t)i * rk;
         const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
         float *wsb = ws + (size_t)b * rk * E;
-        for (int x = tid; x < kn * E / 4; x += RD_THREADS) cp_async16(wsb + 4 * x, w + k0 * E + 4 * x);
+        for (int x = tid; x < kn * E / 4; x += (int)blockDim.x) cp_async16(wsb + 4 * x, w + k0 * E + 4 * x);
         const int rowv = kn / 4;
         float *xsb = xs + (size_t)b * tt * rk;
-        for (int x = tid; x < tt * rowv; x += RD_THREADS) {
+        for (int x = tid; x < tt * rowv; x += (int)blockDim.x) {
             const int tl = x / rowv, v = x - tl * rowv;
             const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // clamp: rows past n are never consumed
             cp_async16(xsb + tl * rk + 4 * v, xdeq + tg * d + k0 + 4 * v);
@@ -391,7 +393,17 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         return check_launch("router_logits");
     }
     if (xdeq != nullptr && n_exp <= RD_THREADS && d % 16 == 0) {
-        const int tt = RD_THREADS / (int)n_exp;
+        // tokens per CTA: fewer, smaller CTAs stage less per chunk (CQ_ROUTER_TT overrides, experiments)
+        static int tt_env = -1;
+        if (tt_env < 0) {
+            const char *e = getenv("CQ_ROUTER_TT");
+            tt_env = e ? atoi(e) : 0;
+        }
+        // about one CTA per SM: a decode batch gets one token per CTA (the chains run on many SMs
+        // and each stages little), a large batch up to 128 / E tokens per CTA (W reused across them)
+        int tt = (int)std::min<int64_t>(RD_THREADS / n_exp, std::max<int64_t>(1, ceil_div(n, 148)));
+        if (tt_env > 0 && tt_env * n_exp <= RD_THREADS) tt = tt_env;
+        const int threads = (int)ceil_div(tt * n_exp, 32) * 32;
         // double-buffered x [tt][rk] + W [rk][E] f32 in <= 96 KB; rk a multiple of 16, <= 512
         int rk = (int)std::min<int64_t>(512, ((96 * 1024) / (8 * (tt + n_exp))) & ~15LL);
         if (rk < 16) rk = 16;
@@ -407,13 +419,13 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         }
         const dim3 grid((unsigned)ceil_div(n, tt));
         switch (n_exp) {
-            case 8: router_deq_kernel<8><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
-            case 16: router_deq_kernel<16><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
-            case 64: router_deq_kernel<64><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 8: router_deq_kernel<8><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 16: router_deq_kernel<16><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 64: router_deq_kernel<64><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
             case 128:
-                router_deq_kernel<128><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
+                router_deq_kernel<128><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
                 break;
-            default: router_deq_kernel<0><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
+            default: router_deq_kernel<0><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
         }
         return check_launch("router_logits");
     }
