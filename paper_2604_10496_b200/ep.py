@@ -178,19 +178,20 @@ class EPStep:
         _lib.check(L.cq_ep_scatter(self.fout.data_ptr(), self.offsets.data_ptr(), self.slot_of_row.data_ptr(),
                                    self.per, self.slots, self.d, self.back.data_ptr(), _lib.stream()))
 
-    def combine(self) -> torch.Tensor:
+    def combine(self, out: torch.Tensor | None = None) -> torch.Tensor:
         tr = self.tr
+        out = self.out if out is None else out
         _lib.check(_lib.lib().cq_moe_combine(tr["selected"].data_ptr(), tr["weights"].data_ptr(),
                                              self.inv.data_ptr(), self.ret.data_ptr(), self.n, self.k, self.d,
-                                             None, self.out.data_ptr(), _lib.stream()))
-        return self.out
+                                             None, out.data_ptr(), _lib.stream()))
+        return out
 
-    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         self.route_and_pack(x)
         self.a2a(self.recv, self.send)
         self.run_experts()
         self.a2a(self.ret, self.back)
-        return self.combine()
+        return self.combine(out)
 
 
 # ---------------------------------------------------------------------------
