@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/cq_b200.h"
 
@@ -83,6 +84,40 @@ __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+}
+
+}  // namespace cq
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// (and run its prologue) while the previous kernel in the stream drains; it
+// must call griddep_wait() before touching anything the previous kernel
+// writes.  Under a normal launch griddep_wait() returns at once.  Disabled with
+// CQ_PDL=0.
+namespace cq {
+
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+    if (!pdl_enabled()) {
+        kernel<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+        return cudaSuccess;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace cq

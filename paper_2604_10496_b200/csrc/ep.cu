@@ -46,6 +46,7 @@ __device__ __forceinline__ int bucket_of(const KeySrc &k, int64_t i) {
 __global__ void __launch_bounds__(EP_THREADS) bucket_rank_kernel(KeySrc ks, int64_t n, int nb, int32_t *rank,
                                                                  int32_t *counts, int32_t *offsets,
                                                                  int32_t *slot_item, int64_t cap) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     extern __shared__ int32_t sm[];
     int32_t *carry = sm;        // [nb]
     int32_t *wtab = sm + nb;    // [32][nb]
@@ -102,6 +103,7 @@ __global__ void ep_pack_kernel(const int8_t *__restrict__ codes, const float *__
                                int64_t k, int64_t d, int32_t per, const int32_t *__restrict__ counts,
                                const int32_t *__restrict__ slot_route, int64_t cap, int64_t slots,
                                uint8_t *__restrict__ send, int32_t *__restrict__ inv) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t pieces = d / 16 + 1, total = slots * pieces;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += stride) {
@@ -128,6 +130,7 @@ __global__ void ep_group_kernel(const uint8_t *__restrict__ recv, int64_t slots,
                                 const int32_t *__restrict__ rank, const int32_t *__restrict__ offsets,
                                 int8_t *__restrict__ codes_perm, float *__restrict__ scales_perm,
                                 int32_t *__restrict__ slot_of_row) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t pieces = d / 16, total = slots * pieces;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = x / pieces, pc = x - s * pieces;
@@ -146,6 +149,7 @@ __global__ void ep_group_kernel(const uint8_t *__restrict__ recv, int64_t slots,
 __global__ void ep_scatter_kernel(const float4 *__restrict__ fout, const int32_t *__restrict__ live,
                                   const int32_t *__restrict__ slot_of_row, int64_t rows_bound, int64_t d4,
                                   float4 *__restrict__ back) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t n = *live, total = (n < rows_bound ? n : rows_bound) * d4;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t pos = x / d4, c = x - pos * d4;

@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(F32_WARPS * 32) lut_f32_grouped_kernel(
     const uint8_t *__restrict__ ids_a, const float *__restrict__ cent_a,
     const uint8_t *__restrict__ ids_b, const float *__restrict__ cent_b,
     int64_t d_in, int64_t d_out, int64_t g, float *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t seg = blockIdx.y;
     const int64_t i = blockIdx.x * (int64_t)F32_WARPS + warp;
@@ -105,6 +106,7 @@ cq_status reference_gemm(const int8_t *, const float *, const uint8_t *, const f
 cq_status validate_gemm(int64_t, int64_t, int64_t, int64_t);
 
 __global__ void single_segment_kernel(int32_t *off, int64_t n) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     off[0] = 0;
     off[1] = (int32_t)n;
 }

@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(256) reference_gemm_kernel(
     const int8_t *__restrict__ codes, const float *__restrict__ scales,
     const uint8_t *__restrict__ ids, const float *__restrict__ cent, int64_t n, int64_t d_in,
     int64_t d_out, int64_t g, float *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     __shared__ int8_t tile[REF_J][REF_TOK];
     const int lane = threadIdx.x, wy = threadIdx.y;
     const int64_t t = blockIdx.x * (int64_t)REF_TOK + lane;
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(256) reference_gemm_kernel(
 // out[m, c] = sum_k a[m,k] * b[k,c], k ascending, one rounding per op.
 __global__ void matmul_ordered_kernel(const float *__restrict__ a, const float *__restrict__ b,
                                       float *__restrict__ out, int64_t m, int64_t k, int64_t nc) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= m * nc) return;
     const int64_t r = idx / nc, c = idx - r * nc;

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
     const int32_t *__restrict__ offsets, int64_t seg_first, const uint8_t *__restrict__ ids_a, const int8_t *__restrict__ lut_a,
     const float *__restrict__ rs_a, const uint8_t *__restrict__ ids_b, const int8_t *__restrict__ lut_b,
     const float *__restrict__ rs_b, int d_in, int d_out, int g, float *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int SB = TcStage<P>::BYTES;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32) lut_tc_kernel(
 // contiguous bulk copy.  Rows >= n are zero.
 __global__ void to_frag_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
                                uint2 *__restrict__ dst) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t total = (K / 128) * tiles * 128;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
         const int lane = (int)(x & 31), sub = (int)((x >> 5) & 3);
@@ -294,6 +296,7 @@ __global__ void to_frag_kernel(const int8_t *__restrict__ src, int64_t n, int64_
 
 __global__ void rowscale_kernel(const float *__restrict__ cent, int64_t rows, int64_t per_row, double mbound,
                                 float *__restrict__ rowscale) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
     if (row >= rows) return;
     const float *c = cent + row * per_row;
@@ -307,6 +310,7 @@ __global__ void rowscale_kernel(const float *__restrict__ cent, int64_t rows, in
 // sign-garbage compensation of every (a, a + 8) pair, per plane.
 __global__ void lut8_kernel(const float *__restrict__ cent, const float *__restrict__ rowscale, int64_t rows,
                             int64_t n_groups, int planes, int64_t mbound, int8_t *__restrict__ lut) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (x >= rows * n_groups) return;
     const int64_t row = x / n_groups, grp = x - row * n_groups;
@@ -347,6 +351,7 @@ __global__ void lut8_kernel(const float *__restrict__ cent, const float *__restr
 // merge with one OR; the bias returns in the epilogue as 2^(7P-1) * sum_j q_j.
 __global__ void lut7_kernel(const float *__restrict__ cent, const float *__restrict__ rowscale, int64_t rows,
                             int64_t n_groups, int planes, int8_t *__restrict__ lut) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (x >= rows * n_groups) return;
     const int64_t row = x / n_groups, grp = x - row * n_groups;
@@ -368,6 +373,7 @@ __global__ void lut7_kernel(const float *__restrict__ cent, const float *__restr
 // sel(r, k) = the 16-bit little-endian word at packed byte k/2 of row r.
 __global__ void ids_frag_kernel(const uint8_t *__restrict__ ids, int64_t rows, int64_t d_in,
                                 uint8_t *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t n_chunks = d_in / TC_CHUNK, row_bytes = d_in / 2;
     const int64_t total = (rows / 16) * n_chunks * 64;  // (h, lane) pairs
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
@@ -524,6 +530,7 @@ extern "C" cq_status cq_lut8_prepare(const uint8_t *ids, const float *centroids,
 }
 
 __global__ void tc_single_segment_kernel(int32_t *off, int64_t n) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     off[0] = 0;
     off[1] = (int32_t)n;
 }

@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     float *__restrict__ out0, const uint8_t *__restrict__ ids1, const int8_t *__restrict__ lut1,
     const float *__restrict__ rs1, float *__restrict__ out1, int n_mat, int d_in, int d_out, int g,
     int32_t *__restrict__ part, int32_t *__restrict__ cnt) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     using S = UmStage<P, MERGED, GEO>;
     constexpr int NA = S::NA, NS = S::NS, GS = S::GS, LAG = S::LAG;
     constexpr int WPS = um::WG / GS;  // warpgroups per stream
@@ -592,6 +593,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 template <int CK>
 __global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
                                  uint4 *__restrict__ dst, int32_t *__restrict__ zero, int n_zero) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     constexpr int PIECES = 16 * (CK / 32);  // 16-byte pieces per tile-chunk: k-steps x 2 khalf x 8 rows
     const int64_t total = (K / CK) * tiles * PIECES;
     if (blockIdx.x == 0)
@@ -608,6 +610,7 @@ __global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int6
 
 // sums[r] = sum_j codes[r, j] (exact int32): the bias term of the unsigned digits.
 __global__ void row_sums_kernel(const int8_t *__restrict__ codes, int64_t n, int64_t K, int32_t *__restrict__ sums) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
     if (row >= n) return;
     const int8_t *r = codes + row * K;
@@ -630,6 +633,7 @@ __global__ void row_sums_kernel(const int8_t *__restrict__ codes, int64_t n, int
 // ids (rows, d_in/2) -> [tile128][chunk][kstep][row][16 B] (the 16 packed bytes of
 // a row's 32 columns are already 8 PRMT selectors, low nibble first).
 __global__ void ids_umma_kernel(const uint8_t *__restrict__ ids, int64_t rows, int64_t d_in, uint4 *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t n_chunks = d_in / 128;
     const int64_t total = (rows / 128) * n_chunks * 4 * 128;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
@@ -641,6 +645,7 @@ __global__ void ids_umma_kernel(const uint8_t *__restrict__ ids, int64_t rows, i
 // lut16 [rows/16][G][16][P][16] (lut7_kernel layout) -> [rows/128][G][128][P][16].
 __global__ void lut_relayout_kernel(const int8_t *__restrict__ lut16, int64_t rows, int64_t n_groups, int planes,
                                     int8_t *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t per = (int64_t)planes * 16;
     const int64_t total = rows * n_groups;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
@@ -667,11 +672,11 @@ cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, in
                     int32_t *zero, int n_zero, cudaStream_t st) {
     const int64_t total = (K / CK) * tiles * 16 * (CK / 32);
     if (total == 0) return CQ_OK;
-    to_umma_b_kernel<CK><<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st>>>(
-        codes, n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero);
+    launch_pdl(to_umma_b_kernel<CK>, (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st, codes,
+               n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero);
     CQ_TRY(check_launch("to_umma_b"));
     if (sums == nullptr) return CQ_OK;
-    row_sums_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(codes, n, K, sums);
+    launch_pdl(row_sums_kernel, (unsigned)ceil_div(n, 8), 256, 0, st, codes, n, K, sums);
     return check_launch("row_sums");
 }
 
@@ -721,7 +726,7 @@ cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales,
         cudaFuncSetAttribute(lut_umma_kernel<P, MERGED, GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    lut_umma_kernel<P, MERGED, GEO><<<umma_grid(), um::THREADS, smem, st>>>(
+    launch_pdl(lut_umma_kernel<P, MERGED, GEO>, umma_grid(), um::THREADS, smem, st, 
         bfrag, n_tiles, scales, sums, offsets, (int)n_seg, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
         b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, b ? 2 : 1, (int)d_in,
         (int)d_out, (int)a->group_size, part, cnt);

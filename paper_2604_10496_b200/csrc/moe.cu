@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, 
                                                           int64_t ff, int8_t *__restrict__ codes,
                                                           float *__restrict__ scales,
                                                           const int32_t *__restrict__ live) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
     float *ar = a + row * ff;
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
                                                               int64_t ff, int8_t *__restrict__ codes,
                                                               float *__restrict__ scales,
                                                               const int32_t *__restrict__ live) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
     float4 *ar = reinterpret_cast<float4 *>(a + row * ff);
@@ -132,16 +134,16 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
         switch (v) {
             case 1: {  // short rows: one float4 per thread, CTA sized to the row
                 const int thr = (int)std::max<int64_t>(64, ceil_div(ff / 4, 32) * 32);
-                silu_quant_vec_kernel<1><<<(unsigned)rows, thr, 0, st>>>(a, b, ff, codes, scales, live);
+                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live);
                 break;
             }
-            case 2: silu_quant_vec_kernel<2><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
+            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live); break;
             case 3:
-            case 4: silu_quant_vec_kernel<4><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
-            default: silu_quant_vec_kernel<8><<<(unsigned)rows, 512, 0, st>>>(a, b, ff, codes, scales, live); break;
+            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live); break;
+            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live); break;
         }
     } else {
-        silu_quant_kernel<<<(unsigned)rows, 256, 0, st>>>(a, b, ff, codes, scales, live);
+        launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live);
     }
     return check_launch("silu_quant");
 }
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(256) ordered_grouped_kernel(
     const int8_t *__restrict__ codes, const float *__restrict__ scales, const int32_t *__restrict__ offsets,
     int64_t seg_first, const uint8_t *__restrict__ ids, const float *__restrict__ cent, int64_t d_in,
     int64_t d_out, int64_t g, float *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     __shared__ int8_t tile[OG_J][OG_TOK];
     const int lane = threadIdx.x, wy = threadIdx.y;
     const int64_t seg = blockIdx.z;
@@ -198,6 +201,7 @@ cq_status ordered_grouped(const int8_t *codes, const float *scales, const int32_
 
 // h = silu(a) * b elementwise (model.py:396), in place into a.
 __global__ void silu_mul_kernel(float *__restrict__ a, const float *__restrict__ b, int64_t count) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count; x += (int64_t)gridDim.x * blockDim.x)
         a[x] = __fmul_rn(silu_f32(a[x]), b[x]);
 }
@@ -207,6 +211,7 @@ __global__ void silu_mul_kernel(float *__restrict__ a, const float *__restrict__
 __global__ void combine_kernel(const int32_t *__restrict__ selected, const float *__restrict__ weights,
                                const int32_t *__restrict__ inv, const float *__restrict__ fout, int64_t k,
                                int64_t d, const float *__restrict__ add, float *__restrict__ out) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t t = blockIdx.x;
     __shared__ int32_t pos_sh[16];
     __shared__ float w_sh[16];
@@ -267,6 +272,7 @@ __global__ void combine_kernel(const int32_t *__restrict__ selected, const float
 template <int DT>
 __global__ void __launch_bounds__(256) rotate_kernel(const void *__restrict__ x, const float *__restrict__ r,
                                                      int64_t n, int64_t d, float *__restrict__ v) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     __shared__ float xs[16][64 + 1];
     __shared__ float rs[16][64 + 1];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -482,11 +488,13 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
 }
 
 __global__ void add_inplace_kernel(float *__restrict__ a, const float *__restrict__ b, int64_t count) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count; x += (int64_t)gridDim.x * blockDim.x)
         a[x] = __fadd_rn(a[x], b[x]);
 }
 
 __global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     for (int64_t s = 0; s <= n_shared; ++s) off[s] = (int32_t)(s * n);
 }
 
@@ -606,7 +614,7 @@ extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weight
     const int64_t cols = (d_model & 3) == 0 ? d_model / 4 : d_model;  // work items per token
     const int threads = (int)std::min<int64_t>(256, ceil_div(cols, 32) * 32);
     dim3 grid((unsigned)n_tokens, (unsigned)std::max<int64_t>(1, std::min<int64_t>(16, ceil_div(cols, threads))));
-    combine_kernel<<<grid, threads, 0, as_stream(stream)>>>(selected, weights, inv, fout, top_k, d_model, add, out);
+    launch_pdl(combine_kernel, grid, threads, 0, as_stream(stream), selected, weights, inv, fout, top_k, d_model, add, out);
     return check_launch("combine");
 }
 

@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict
                                                           float *__restrict__ scales,
                                                           int *__restrict__ nonfinite,
                                                           float *__restrict__ deq) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     const int64_t base = row * d;
     float mx = 0.0f;
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict
 
 __global__ void unpack_ids_kernel(const uint8_t *__restrict__ packed, int64_t rows, int64_t d_in,
                                   uint8_t *__restrict__ ids) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row_bytes = (d_in + 1) >> 1;
     const int64_t total = rows * d_in;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -69,9 +71,9 @@ cq_status quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *co
                       int *nonfinite_dev, float *deq, cudaStream_t st) {
     if (n == 0) return CQ_OK;
     if (dtype == CQ_DTYPE_F32)
-        quantize_a4_kernel<CQ_DTYPE_F32><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev, deq);
+        launch_pdl(quantize_a4_kernel<CQ_DTYPE_F32>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq);
     else
-        quantize_a4_kernel<CQ_DTYPE_BF16><<<(unsigned)n, 256, 0, st>>>(x, d, codes, scales, nonfinite_dev, deq);
+        launch_pdl(quantize_a4_kernel<CQ_DTYPE_BF16>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq);
     return check_launch("quantize_a4");
 }
 

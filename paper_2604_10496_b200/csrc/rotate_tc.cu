@@ -52,6 +52,7 @@ __device__ __forceinline__ void piece_coords(int64_t x, int64_t tiles, int64_t &
 
 // R (d x d, row k, column n) -> three bf16 planes of R^T (rows n) in the UMMA layout.
 __global__ void rot_split_r_kernel(const float *__restrict__ R, int64_t d, uint4 *__restrict__ planes) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t tiles = d / 8, per_plane = d * d / 8;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < per_plane; x += (int64_t)gridDim.x * blockDim.x) {
         int64_t n, k0;
@@ -80,6 +81,7 @@ __global__ void rot_split_r_kernel(const float *__restrict__ R, int64_t d, uint4
 template <int DT, int NP>
 __global__ void rot_split_x_kernel(const void *__restrict__ x, int64_t n, int64_t d, int64_t tiles,
                                    uint4 *__restrict__ planes) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t per_plane = tiles * 8 * d / 8;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_plane; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t row, k0;
@@ -139,6 +141,7 @@ template <int NPA>
 __global__ void __launch_bounds__(rt::THREADS, 1) rot_gemm_kernel(const uint8_t *__restrict__ xa, int64_t a_tiles,
                                                                    const uint8_t *__restrict__ rb, int64_t d,
                                                                    int64_t n, float *__restrict__ v) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     // (activation plane, R plane) products, largest first: x R0, x R1, x R2 for a bf16 x; for an
     // fp32 x the six terms of relative size >= 2^-16 (x0R0, x0R1, x1R0, x0R2, x1R1, x2R0)
     constexpr int NPAIR = NPA == 1 ? 3 : 6;
@@ -254,9 +257,9 @@ cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const voi
     const int64_t pieces = tiles * 8 * d / 8;
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(pieces, 256), 148 * 16);
     if (dtype == CQ_DTYPE_BF16)
-        rot_split_x_kernel<CQ_DTYPE_BF16, 1><<<blocks, 256, 0, st>>>(x, n, d, tiles, reinterpret_cast<uint4 *>(act));
+        launch_pdl(rot_split_x_kernel<CQ_DTYPE_BF16, 1>, blocks, 256, 0, st, x, n, d, tiles, reinterpret_cast<uint4 *>(act));
     else
-        rot_split_x_kernel<CQ_DTYPE_F32, 3><<<blocks, 256, 0, st>>>(x, n, d, tiles, reinterpret_cast<uint4 *>(act));
+        launch_pdl(rot_split_x_kernel<CQ_DTYPE_F32, 3>, blocks, 256, 0, st, x, n, d, tiles, reinterpret_cast<uint4 *>(act));
     CQ_TRY(check_launch("rotation_split_x"));
     static bool attr = false;
     const size_t smem = (size_t)rt::STAGES * (rt::A_BYTES + rt::B_BYTES);
@@ -268,9 +271,9 @@ cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const voi
     const dim3 grid((unsigned)(d / rt::BN), (unsigned)ceil_div(n, rt::BM));
     const uint8_t *a = reinterpret_cast<const uint8_t *>(act), *b = reinterpret_cast<const uint8_t *>(prepared);
     if (dtype == CQ_DTYPE_BF16)
-        rot_gemm_kernel<1><<<grid, rt::THREADS, smem, st>>>(a, tiles, b, d, n, v);
+        launch_pdl(rot_gemm_kernel<1>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v);
     else
-        rot_gemm_kernel<3><<<grid, rt::THREADS, smem, st>>>(a, tiles, b, d, n, v);
+        launch_pdl(rot_gemm_kernel<3>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v);
     return check_launch("rotation_gemm");
 }
 

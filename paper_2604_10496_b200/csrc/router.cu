@@ -18,6 +18,7 @@ namespace cq {
 __global__ void router_logits_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
                                      const float *__restrict__ w, int64_t n, int64_t d, int64_t n_exp, int rk,
                                      float *__restrict__ logits) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     extern __shared__ float rsm[];
     const int tt_n = blockDim.x / (int)n_exp;
     float *ws = rsm;                 // [rk][E]
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__r
                                                                 const float *__restrict__ w, int64_t n, int64_t d,
                                                                 int64_t n_exp, int tt, int rk,
                                                                 float *__restrict__ logits) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     extern __shared__ __align__(16) float rds[];
     const int E = EC ? EC : (int)n_exp;
     float *xs = rds;                         // [2][tt][rk]
@@ -146,6 +148,7 @@ template <int EC, int TPT>
 __global__ void __launch_bounds__(RD_THREADS) router_multi_kernel(const float *__restrict__ xdeq,
                                                                   const float *__restrict__ w, int64_t n, int64_t d,
                                                                   int rk, float *__restrict__ logits) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     constexpr int TG = RD_THREADS / EC;  // token groups per CTA
     constexpr int TT = TG * TPT;         // tokens per CTA
     extern __shared__ __align__(16) float rds[];
@@ -237,6 +240,7 @@ __global__ void __launch_bounds__(TOPK_WARPS * 32) topk_kernel(const float *__re
                                                                int64_t n_exp, int64_t k, int32_t *__restrict__ selected,
                                                                float *__restrict__ weights, int32_t *__restrict__ counts,
                                                                int64_t local_begin, int64_t n_local) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int lane = threadIdx.x & 31;
     const int64_t t = blockIdx.x * (int64_t)TOPK_WARPS + (threadIdx.x >> 5);
     if (t >= n) return;  // warp-uniform
@@ -295,6 +299,7 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(
     const int32_t *__restrict__ selected, const int32_t *__restrict__ counts, int64_t n, int64_t k,
     int64_t local_begin, int64_t n_local, int32_t *__restrict__ offsets,
     int32_t *__restrict__ perm_token, int32_t *__restrict__ perm_slot, int32_t *__restrict__ inv) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     __shared__ int32_t s_base;
     __shared__ int32_t warp_tot[PERM_THREADS / 32];
     const int e_loc = blockIdx.x;
@@ -347,6 +352,7 @@ __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *
                                    const int32_t *__restrict__ perm_token,
                                    const int32_t *__restrict__ offsets, int64_t n_local, int64_t d,
                                    int8_t *__restrict__ dst, float *__restrict__ dscale) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t r = blockIdx.x;
     if (r >= offsets[n_local]) return;
     const int64_t t = perm_token[r];
@@ -385,11 +391,11 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         }
         const dim3 grid((unsigned)ceil_div(n, tt));
         if (n_exp == 32)
-            router_multi_kernel<32, TPT><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, rk, logits);
+            launch_pdl(router_multi_kernel<32, TPT>, grid, RD_THREADS, smem, st, xdeq, w, n, d, rk, logits);
         else if (n_exp == 64)
-            router_multi_kernel<64, TPT><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, rk, logits);
+            launch_pdl(router_multi_kernel<64, TPT>, grid, RD_THREADS, smem, st, xdeq, w, n, d, rk, logits);
         else
-            router_multi_kernel<128, TPT><<<grid, RD_THREADS, smem, st>>>(xdeq, w, n, d, rk, logits);
+            launch_pdl(router_multi_kernel<128, TPT>, grid, RD_THREADS, smem, st, xdeq, w, n, d, rk, logits);
         return check_launch("router_logits");
     }
     if (xdeq != nullptr && n_exp <= RD_THREADS && d % 16 == 0) {
@@ -419,13 +425,13 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         }
         const dim3 grid((unsigned)ceil_div(n, tt));
         switch (n_exp) {
-            case 8: router_deq_kernel<8><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
-            case 16: router_deq_kernel<16><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
-            case 64: router_deq_kernel<64><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 8: launch_pdl(router_deq_kernel<8>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 16: launch_pdl(router_deq_kernel<16>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, rk, logits); break;
+            case 64: launch_pdl(router_deq_kernel<64>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, rk, logits); break;
             case 128:
-                router_deq_kernel<128><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
+                launch_pdl(router_deq_kernel<128>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, rk, logits);
                 break;
-            default: router_deq_kernel<0><<<grid, threads, smem, st>>>(xdeq, w, n, d, n_exp, tt, rk, logits);
+            default: launch_pdl(router_deq_kernel<0>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, rk, logits);
         }
         return check_launch("router_logits");
     }
@@ -445,8 +451,8 @@ cq_status topk(const float *logits, int64_t n, int64_t n_exp, int64_t k, int32_t
         return CQ_ERR_CONFIG;
     }
     if (n == 0) return CQ_OK;
-    topk_kernel<<<(unsigned)ceil_div(n, TOPK_WARPS), TOPK_WARPS * 32, 0, st>>>(logits, n, n_exp, k, sel, wts,
-                                                                             counts, local_begin, n_local);
+    launch_pdl(topk_kernel, (unsigned)ceil_div(n, TOPK_WARPS), TOPK_WARPS * 32, 0, st, logits, n, n_exp, k, sel, wts,
+               counts, local_begin, n_local);
     return check_launch("topk");
 }
 
@@ -454,7 +460,7 @@ cq_status permute(const int32_t *sel, const int32_t *counts, int64_t n, int64_t 
                   int64_t n_local, int32_t *offsets, int32_t *perm_token, int32_t *perm_slot,
                   int32_t *inv, cudaStream_t st) {
     if (n_local == 0) return CQ_OK;
-    permute_kernel<<<(unsigned)n_local, PERM_THREADS, 0, st>>>(sel, counts, n, k, local_begin, n_local,
+    launch_pdl(permute_kernel, (unsigned)n_local, PERM_THREADS, 0, st, sel, counts, n, k, local_begin, n_local,
                                                                offsets, perm_token, perm_slot, inv);
     return check_launch("permute");
 }
@@ -463,7 +469,7 @@ cq_status gather_rows(const int8_t *src, const float *sscale, const int32_t *per
                       const int32_t *offsets, int64_t n_local, int64_t rows_bound, int64_t d,
                       int8_t *dst, float *dscale, cudaStream_t st) {
     if (rows_bound == 0) return CQ_OK;
-    gather_rows_kernel<<<(unsigned)rows_bound, 128, 0, st>>>(src, sscale, perm_token, offsets, n_local, d,
+    launch_pdl(gather_rows_kernel, (unsigned)rows_bound, 128, 0, st, src, sscale, perm_token, offsets, n_local, d,
                                                              dst, dscale);
     return check_launch("gather_rows");
 }
