@@ -83,7 +83,10 @@ struct UmGeo {
     static constexpr int PART_WORDS = 3 * NT * 128;  // int32 partial accumulators per slot (P <= 3)
 };
 using UmDecode = UmGeo<32, UM_CK>;
-using UmPrefill = UmGeo<128, 64>;
+#ifndef UM_PF_NT
+#define UM_PF_NT 128
+#endif
+using UmPrefill = UmGeo<UM_PF_NT, 64>;
 
 template <int P, bool MERGED, class GEO>
 struct UmStage {
@@ -706,7 +709,8 @@ static int64_t umma_part_off(int64_t rows, int64_t d_in) {
 static bool umma_prefill(int64_t rows, int64_t n_seg) { return rows >= 256 && rows >= 64 * n_seg; }
 // The scratch is sized for the largest geometry `rows` can select.
 static int64_t umma_part_words(int64_t rows) {
-    return rows >= 256 ? UmPrefill::PART_WORDS : UmDecode::PART_WORDS;
+    return rows >= 256 ? (UmPrefill::PART_WORDS > UmDecode::PART_WORDS ? UmPrefill::PART_WORDS : UmDecode::PART_WORDS)
+                       : UmDecode::PART_WORDS;
 }
 static int64_t umma_cnt_off(int64_t rows, int64_t d_in) {
     return umma_part_off(rows, d_in) + (int64_t)2 * umma_grid() * umma_part_words(rows) * 4;
