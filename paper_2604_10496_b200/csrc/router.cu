@@ -140,6 +140,123 @@ __global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__r
     if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
 }
 
+// Decode batches: each chain (token, expert) is d dependent fp32 adds, and with
+// one token per CTA the chain warp of router_deq_kernel issues ~5 instructions
+// per column (loads, FMUL, FADD), above the 4-cycle FADD latency.  Here warp 0
+// holds only the chains (lane c = token c / EG, expert e0 + c % EG) and adds
+// precomputed products with one LDS.128 per 4 columns.  Warps 1-3 stage raw
+// W / x chunks by cp.async (3 buffers) and write the rounded products
+// fmul(x[t][j], w[j][e]) of the next chunk into the other product buffer.
+// Summation order and rounding are those of router_deq_kernel (bit-exact).
+constexpr int RC_THREADS = 128, RC_K = 256, RC_PITCH = RC_K + 4;
+
+template <int EG>
+__global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *__restrict__ xdeq,
+                                                                  const float *__restrict__ w, int64_t n,
+                                                                  int64_t d, int64_t n_exp, int tt,
+                                                                  float *__restrict__ logits) {
+    griddep_wait();
+    extern __shared__ __align__(16) float rcs[];
+    float *pbuf = rcs;                           // [2][32][RC_PITCH] products
+    float *wraw = pbuf + 2 * 32 * RC_PITCH;      // [3][RC_K][EG]
+    float *xraw = wraw + 3 * RC_K * EG;          // [3][tt][RC_K]
+    const int tid = threadIdx.x;
+    const int64_t t0 = blockIdx.x * (int64_t)tt;
+    const int e0 = blockIdx.y * EG;
+    const int n_chunks = (int)((d + RC_K - 1) / RC_K);
+    const int ptid = tid - 32;  // producer index, warps 1-3
+    auto stage = [&](int i) {
+        if (i < n_chunks) {
+            const int64_t k0 = (int64_t)i * RC_K;
+            const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
+            float *wb = wraw + (i % 3) * RC_K * EG;
+            for (int x = ptid; x < kn * (EG / 4); x += RC_THREADS - 32) {
+                const int r = x / (EG / 4), q = x - r * (EG / 4);
+                cp_async16(wb + r * EG + 4 * q, w + (k0 + r) * n_exp + e0 + 4 * q);
+            }
+            float *xb = xraw + (i % 3) * tt * RC_K;
+            const int rowv = kn / 4;
+            for (int x = ptid; x < tt * rowv; x += RC_THREADS - 32) {
+                const int tl = x / rowv, v = x - tl * rowv;
+                const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // rows past n are never stored
+                cp_async16(xb + tl * RC_K + 4 * v, xdeq + tg * d + k0 + 4 * v);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto produce = [&](int i) {  // chunk i landed in raw buffer i % 3 (own copies waited for)
+        asm volatile("bar.sync 1, %0;" ::"n"(RC_THREADS - 32) : "memory");
+        const int64_t k0 = (int64_t)i * RC_K;
+        const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
+        const float *wb = wraw + (i % 3) * RC_K * EG;
+        const float *xb = xraw + (i % 3) * tt * RC_K;
+        float *pb = pbuf + (i & 1) * 32 * RC_PITCH;
+        for (int j = ptid; j < kn; j += RC_THREADS - 32) {
+            float wr[EG];
+#pragma unroll
+            for (int q = 0; q < EG / 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4 *>(wb + j * EG + 4 * q);
+                wr[4 * q] = v.x, wr[4 * q + 1] = v.y, wr[4 * q + 2] = v.z, wr[4 * q + 3] = v.w;
+            }
+            for (int t = 0; t < tt; ++t) {
+                const float xv = xb[t * RC_K + j];
+#pragma unroll
+                for (int e = 0; e < EG; ++e) pb[(t * EG + e) * RC_PITCH + j] = __fmul_rn(xv, wr[e]);
+            }
+        }
+    };
+    if (tid >= 32) {
+        stage(0);
+        stage(1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        produce(0);
+    }
+    __syncthreads();
+    const bool chain = tid < tt * EG;
+    float acc = 0.0f;
+    for (int i = 0; i < n_chunks; ++i) {
+        if (tid >= 32) {
+            if (i + 1 < n_chunks) {
+                stage(i + 2);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                produce(i + 1);
+            }
+        } else if (chain) {
+            const int kn = (int)((d - (int64_t)i * RC_K) < RC_K ? (d - (int64_t)i * RC_K) : RC_K);  // % 16 == 0
+            const float4 *pr = reinterpret_cast<const float4 *>(pbuf + (i & 1) * 32 * RC_PITCH + tid * RC_PITCH);
+            float4 cur[4], nxt[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cur[u] = pr[u];
+            for (int j = 16; j < kn; j += 16) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nxt[u] = pr[(j >> 2) + u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc = __fadd_rn(acc, cur[u].x);
+                    acc = __fadd_rn(acc, cur[u].y);
+                    acc = __fadd_rn(acc, cur[u].z);
+                    acc = __fadd_rn(acc, cur[u].w);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc = __fadd_rn(acc, cur[u].x);
+                acc = __fadd_rn(acc, cur[u].y);
+                acc = __fadd_rn(acc, cur[u].z);
+                acc = __fadd_rn(acc, cur[u].w);
+            }
+        }
+        __syncthreads();  // product buffer i & 1 is rewritten by iteration i + 1's producers
+    }
+    if (chain && t0 + tid / EG < n) logits[(t0 + tid / EG) * n_exp + e0 + tid % EG] = acc;
+}
+
+static size_t router_chain_smem(int eg, int tt) {
+    return sizeof(float) * ((size_t)2 * 32 * RC_PITCH + (size_t)3 * RC_K * eg + (size_t)3 * tt * RC_K);
+}
+
 // Many experts (E in {32, 64, 128}): thread = (token group, expert), TPT
 // independent token chains per thread, so a staged W element is reused TPT
 // times instead of once (with one chain per thread every CTA streams all of W
@@ -374,6 +491,39 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
     if (n_exp > 256) {
         set_error("router: at most 256 experts");
         return CQ_ERR_CONFIG;
+    }
+    static int chain_env = -1;
+    if (chain_env < 0) {
+        const char *e = getenv("CQ_ROUTER_CHAIN");
+        chain_env = e ? atoi(e) : 1;
+    }
+    if (xdeq != nullptr && d % 16 == 0 && n_exp % 8 == 0 && chain_env) {
+        // decode-sized batches: at most one wave of CTAs, each holding tt * EG <= 32 chains
+        const int eg = n_exp % 32 == 0 ? 32 : (n_exp % 16 == 0 ? 16 : 8);
+        const int64_t groups = n_exp / eg;
+        const int tt = (int)std::min<int64_t>(32 / eg, std::max<int64_t>(1, ceil_div(n * groups, 148)));
+        const int64_t ctas = ceil_div(n, tt) * groups;
+        if (ctas <= (eg <= 16 ? 2 : 1) * 148) {
+            const size_t smem = router_chain_smem(eg, tt);
+            static bool attr_c = false;
+            if (!attr_c) {
+                cudaFuncSetAttribute(router_chain_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)router_chain_smem(8, 4));
+                cudaFuncSetAttribute(router_chain_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)router_chain_smem(16, 2));
+                cudaFuncSetAttribute(router_chain_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)router_chain_smem(32, 1));
+                attr_c = true;
+            }
+            const dim3 grid((unsigned)ceil_div(n, tt), (unsigned)groups);
+            if (eg == 32)
+                launch_pdl(router_chain_kernel<32>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits);
+            else if (eg == 16)
+                launch_pdl(router_chain_kernel<16>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits);
+            else
+                launch_pdl(router_chain_kernel<8>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits);
+            return check_launch("router_logits");
+        }
     }
     if (xdeq != nullptr && d % 16 == 0 && (n_exp == 32 || n_exp == 64 || n_exp == 128) && n >= 64) {
         constexpr int TPT = 16;

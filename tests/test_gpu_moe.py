@@ -152,6 +152,26 @@ def test_router_many_experts_bit_exact(E, k):
     assert np.array_equal(tr["inv"].cpu().numpy(), inv)
 
 
+@pytest.mark.parametrize("n,d,E", [(1, 1024, 8), (64, 4096, 8), (130, 1040, 8), (296, 1024, 8), (7, 2048, 16),
+                                   (200, 1024, 16), (64, 2048, 64), (33, 1024, 128), (5, 1040, 24), (64, 1024, 32)])
+def test_router_decode_chain_bit_exact(n, d, E):
+    """Decode-sized batches take router_chain_kernel (chains alone on warp 0,
+    products from warps 1-3): logits bit-exact with _core.matmul_f32's ordered
+    chain, for 8/16/32-expert groups, several tokens per CTA and a partial
+    last chunk (d = 1040)."""
+    g = 16
+    v, w, sites, _ = moe_inputs_device(50 + n + E, n, d, 128, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=2, path="f32")
+    layer(v)
+    tr = layer.trace(n)
+    codes, scales = oracle.c_quantize(v.float().cpu().numpy())
+    logits = oracle.c_matmul(codes.astype(np.float32) * scales[:, None], w.cpu().numpy())
+    assert np.array_equal(tr["logits"].cpu().numpy().view(np.int32), logits.view(np.int32))
+    sel, _ = o.select_top_k(logits, 2)
+    assert np.array_equal(tr["selected"].cpu().numpy(), sel)
+
+
 @pytest.mark.parametrize("cfg", ["qw", "ds"])
 def test_many_expert_layers_tc_vs_oracle(cfg):
     """QW (d2048/ff768/E128/top-8) and DS (d2048/ff1408/E64+2 shared/top-6)
