@@ -8,6 +8,8 @@
 //   -> grouped down LUT GEMM                      (model.py:399)
 //   -> weighted combine, experts ascending        (model.py:389-401)
 //   [+ shared experts, weight 1 — builder-defined, SURVEY §8(a) a18]
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace cq {
@@ -125,10 +127,101 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     }
 }
 
+// Few rows (decode: a row per route): one CTA per row leaves SMs idle and
+// serialises each row's load -> max -> quantize.  Here a cluster of CL CTAs
+// shares a row, each taking ff / CL columns; the row max is combined through
+// distributed shared memory.  Same per-element math as silu_quant_vec_kernel.
+template <int V, int CL>
+__global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ a, const float *__restrict__ b,
+                                                             int64_t ff, int8_t *__restrict__ codes,
+                                                             float *__restrict__ scales,
+                                                             const int32_t *__restrict__ live) {
+    namespace cg = cooperative_groups;
+    griddep_wait();
+    const int64_t row = blockIdx.x / CL;
+    if (live != nullptr && row >= *live) return;  // uniform over the cluster (one row)
+    cg::cluster_group cluster = cg::this_cluster();
+    const int part = (int)cluster.block_rank();
+    const int64_t seg = ff / CL;
+    float4 *ar = reinterpret_cast<float4 *>(a + row * ff + part * seg);
+    const float4 *br = reinterpret_cast<const float4 *>(b + row * ff + part * seg);
+    const int nv = (int)(seg >> 2);
+    float4 h[V];
+    float mx = 0.0f;
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+        const int j = threadIdx.x + u * 256;
+        if (j < nv) {
+            const float4 x = ar[j], y = br[j];
+            h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
+                               __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
+            ar[j] = h[u];
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
+        }
+    }
+    __shared__ float red[8];
+    __shared__ float part_max, s_sh;
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float m = threadIdx.x < 8 ? red[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0) part_max = m;
+    }
+    cluster.sync();
+    if (threadIdx.x == 0) {
+        float m = 0.0f;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) m = fmaxf(m, *cluster.map_shared_rank(&part_max, r));
+        s_sh = a4_scale(m);
+        if (part == 0) scales[row] = s_sh;
+    }
+    cluster.sync();  // s_sh visible; no CTA leaves while its part_max may still be read
+    const float s = s_sh;
+    char4 *cr = reinterpret_cast<char4 *>(codes + row * ff + part * seg);
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+        const int j = threadIdx.x + u * 256;
+        if (j < nv) cr[j] = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+    }
+}
+
+template <int CL>
+static bool silu_quant_cluster(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
+                               const int32_t *live, cudaStream_t st) {
+    if (ff % (4 * CL)) return false;
+    const int64_t v = ceil_div(ff / CL / 4, 256);
+    const dim3 grid((unsigned)(rows * CL));
+    switch (v) {
+        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
+        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
+        case 3:
+        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
+        case 5: case 6: case 7:
+        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
+        default: return false;
+    }
+    return true;
+}
+
 // `live` (device, nullable): rows at or past *live are skipped (EP slot bounds).
 cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
                      const int32_t *live, cudaStream_t st) {
     if (rows == 0) return CQ_OK;
+    static int cl_env = -1;
+    if (cl_env < 0) {
+        const char *e = getenv("CQ_SILU_CLUSTER");
+        cl_env = e ? atoi(e) : 1;
+    }
+    // about two CTAs per SM over the whole grid; long rows only (a cluster CTA keeps >= 256 float4)
+    if (cl_env && ff >= 8192) {
+        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, st)) return check_launch("silu_quant");
+        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, st))
+            return check_launch("silu_quant");
+        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, st))
+            return check_launch("silu_quant");
+    }
     const int64_t v = ceil_div(ff / 4, 512);
     if (ff % 4 == 0 && v <= 8) {
         switch (v) {

@@ -172,6 +172,29 @@ def test_router_decode_chain_bit_exact(n, d, E):
     assert np.array_equal(tr["selected"].cpu().numpy(), sel)
 
 
+@pytest.mark.parametrize("n", [4, 60, 140])
+def test_silu_requant_cluster_rows(n):
+    """Long hidden rows (ff = 14336) at decode row counts take the cluster
+    silu|re-quantize kernel (8 / 4 / 2 CTAs per row, row max through DSMEM):
+    codes and scales are bit-exact with the oracle quantizer on the kernel's own
+    h, and h = silu(a)*b agrees with the ordered path."""
+    d, ff, E, k, g = 256, 14336, 4, 2, 128
+    v, w, sites, _ = moe_inputs_device(70 + n, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
+    layer.prepare_tc()
+    layer(v)
+    tr = {key: t.clone() for key, t in layer.trace(n).items()}
+    layer(v, path="ordered")
+    tro = layer.trace(n, path="ordered")
+    R = n * k
+    h = tr["hidden"][:R].cpu().numpy()
+    codes, scales = oracle.c_quantize(h)
+    assert np.array_equal(tr["hcodes"][:R].cpu().numpy(), codes)
+    assert np.array_equal(tr["hscales"][:R].cpu().numpy().view(np.int32), scales.view(np.int32))
+    assert o.relative_error(h, tro["hidden"][:R].cpu().numpy()) <= 1e-5
+
+
 @pytest.mark.parametrize("cfg", ["qw", "ds"])
 def test_many_expert_layers_tc_vs_oracle(cfg):
     """QW (d2048/ff768/E128/top-8) and DS (d2048/ff1408/E64+2 shared/top-6)
