@@ -555,8 +555,9 @@ def run_ours(args):
     # dominant kernel: the grouped gate|up LUT GEMM, timed per stage with CUDA
     # events on its stream (cq_moe_profile_experts records events between the
     # expert-stage kernels: gate|up GEMM | silu*up + re-quantize | down GEMM)
-    tr = layer.trace(n)
     with torch.cuda.stream(stream):
+        layer.route(v)  # codes_perm / scales_perm (the tensor-core forward gathers in-kernel)
+        tr = layer.trace(n)
         n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, tr["codes_perm"], tr["scales_perm"],
                                                                     tr["offsets"], n * k, max(3, args.steps))
     pk = peaks()

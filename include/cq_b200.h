@@ -142,7 +142,7 @@ enum {
     CQ_WS_LOGITS,       /* f32  [n][E]         ordered router logits         */
     CQ_WS_SELECTED,     /* i32  [n][k]                                       */
     CQ_WS_WEIGHTS,      /* f32  [n][k]                                       */
-    CQ_WS_COUNTS,       /* i32  [E]                                          */
+    CQ_WS_COUNTS,       /* i32  [E+1]          routes per expert; [E] arrival counter */
     CQ_WS_OFFSETS,      /* i32  [E+1]          local expert segments         */
     CQ_WS_PERM_TOKEN,   /* i32  [n*k]                                        */
     CQ_WS_PERM_SLOT,    /* i32  [n*k]                                        */
@@ -158,6 +158,7 @@ enum {
     CQ_WS_CODES_FRAG,   /* int8 [ceil(n*k/8)*8][d_model] codes in mma-B fragment order */
     CQ_WS_HCODES_FRAG,  /* int8 [ceil(n*k/8)*8][d_ff]    hidden codes, fragment order  */
     CQ_WS_ROT_ACT,      /* bf16 [3][ceil(n/128)*128][d_model] rotation operand planes (rotation_tc) */
+    CQ_WS_TOK_SUMS,     /* i32  [n]            per-token code sums (GEMM bias term) */
     CQ_WS_COUNT_
 };
 

@@ -25,7 +25,8 @@ CQ_TC_MMA16, CQ_TC_UMMA128, CQ_TC_UMMA128U = 0, 1, 2
 TC_LAYOUTS = {"mma16": CQ_TC_MMA16, "umma128": CQ_TC_UMMA128, "umma128u": CQ_TC_UMMA128U}
 WS_NAMES = ("codes", "scales", "logits", "selected", "weights", "counts", "offsets",
             "perm_token", "perm_slot", "inv", "codes_perm", "scales_perm", "hidden",
-            "hcodes", "hscales", "fout", "rotated", "shared", "codes_frag", "hcodes_frag", "rot_act")
+            "hcodes", "hscales", "fout", "rotated", "shared", "codes_frag", "hcodes_frag", "rot_act",
+            "tok_sums")
 
 _vp, _i64, _i32, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 

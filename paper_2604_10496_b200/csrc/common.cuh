@@ -86,6 +86,19 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Sum of v over the CTA (blockDim.x a multiple of 32), valid in thread 0.
+__device__ __forceinline__ int block_sum_int(int v) {
+    __shared__ int s_part[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int t = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w];
+    return t;
+}
+
 }  // namespace cq
 
 // ---------------------------------------------------------------------------
@@ -119,6 +132,14 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+
+// Optional inputs of the tcgen05 grouped GEMM's B-operand build (lut_umma.cu).
+struct UmmaIn {
+    const int32_t *perm = nullptr;      // gather: segment row r reads codes[perm[r]] (codes per token)
+    const int32_t *tok_sums = nullptr;  // with perm: per-token code sums, gathered into the row sums
+    float *scales_out = nullptr;        // with perm: scales[perm[r]] lands here; the GEMM reads it
+    bool sums_ready = false;            // without perm: the row sums are already in the B buffer
+};
 
 // launch_pdl with a thread-block cluster of cluster_x CTAs along x.
 template <typename... KArgs, typename... Args>

@@ -466,7 +466,7 @@ cq_status umma_prepare(const uint8_t *, const int8_t *, int64_t, int64_t, int64_
                        cudaStream_t);
 cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
                            const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
-                           cudaStream_t);
+                           cudaStream_t, const UmmaIn &in = UmmaIn{});
 bool umma_ok(int64_t d_in, int64_t d_out, int64_t g);
 int64_t umma_b_bytes(int64_t rows, int64_t d_in);
 

@@ -594,19 +594,36 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 // the canonical K-major no-swizzle UMMA B layout per k-step; rows >= n are zero.
 // Also zeroes the GEMM's split-unit counters (zero[0..n_zero)).
 template <int CK>
+// perm (nullable): gather form, segment row r < *live reads token row perm[r]
+// of src, rows past *live are zero, and the per-row scale and code sum are
+// gathered from the token arrays (gather_rows + row_sums without their launches).
 __global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
-                                 uint4 *__restrict__ dst, int32_t *__restrict__ zero, int n_zero) {
+                                 uint4 *__restrict__ dst, int32_t *__restrict__ zero, int n_zero,
+                                 const int32_t *__restrict__ perm, const int32_t *__restrict__ live,
+                                 const float *__restrict__ tscales, float *__restrict__ scales_out,
+                                 const int32_t *__restrict__ tsum, int32_t *__restrict__ sums) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     constexpr int PIECES = 16 * (CK / 32);  // 16-byte pieces per tile-chunk: k-steps x 2 khalf x 8 rows
     const int64_t total = (K / CK) * tiles * PIECES;
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nrow = perm != nullptr ? (int64_t)*live : n;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (perm != nullptr)
+        for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nrow; x += stride) {
+            const int32_t t = perm[x];
+            scales_out[x] = tscales[t];
+            if (sums != nullptr) sums[x] = tsum[t];
+        }
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += stride) {
         const int r = (int)(x & 7), kh = (int)((x >> 3) & 1), ks = (int)((x >> 4) % (CK / 32));
         const int64_t j = (x / PIECES) % tiles, c = (x / PIECES) / tiles;
         const int64_t row = j * 8 + r;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (row < n) v = *reinterpret_cast<const uint4 *>(src + row * K + c * CK + ks * 32 + kh * 16);
+        if (row < nrow) {
+            const int64_t sr = perm != nullptr ? (int64_t)perm[row] : row;
+            v = *reinterpret_cast<const uint4 *>(src + sr * K + c * CK + ks * 32 + kh * 16);
+        }
         dst[x] = v;
     }
 }
@@ -672,13 +689,15 @@ size_t umma_smem() {
 
 template <int CK>
 cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, int8_t *dst, int32_t *sums,
-                    int32_t *zero, int n_zero, cudaStream_t st) {
+                    int32_t *zero, int n_zero, const UmmaIn &in, const float *tscales, const int32_t *live,
+                    cudaStream_t st) {
     const int64_t total = (K / CK) * tiles * 16 * (CK / 32);
     if (total == 0) return CQ_OK;
     launch_pdl(to_umma_b_kernel<CK>, (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st, codes,
-               n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero);
+               n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero, in.perm, live, tscales, in.scales_out,
+               in.tok_sums, in.perm != nullptr ? sums : nullptr);
     CQ_TRY(check_launch("to_umma_b"));
-    if (sums == nullptr) return CQ_OK;
+    if (sums == nullptr || in.perm != nullptr || in.sums_ready) return CQ_OK;
     launch_pdl(row_sums_kernel, (unsigned)ceil_div(n, 8), 256, 0, st, codes, n, K, sums);
     return check_launch("row_sums");
 }
@@ -740,13 +759,15 @@ cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales,
 template <class GEO>
 cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, const int32_t *offsets, int64_t n_seg,
                        int64_t seg_first, int64_t rows, const cq_expert_site *a, float *out_a,
-                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
+                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, const UmmaIn &in,
+                       cudaStream_t st) {
     const bool merged = a->tc_layout == CQ_TC_UMMA128U;
     const int64_t tiles = umma_b_tiles(rows);
     int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in)) : nullptr;
     int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
     int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
-    CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), st));
+    CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), in, scales, offsets + n_seg, st));
+    if (in.perm != nullptr) scales = in.scales_out;  // per segment row from here on
 #define CQ_UMMA(P_, M_)                                                                                   \
     launch_umma<P_, M_, GEO>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, \
                              d_out, part, cnt, st)
@@ -767,7 +788,8 @@ cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, c
 // up -> out_b) in one launch.
 cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scales, const int32_t *offsets,
                            int64_t n_seg, int64_t seg_first, int64_t rows, const cq_expert_site *a, float *out_a,
-                           const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st) {
+                           const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st,
+                           const UmmaIn &in) {
     if (rows == 0 || n_seg == 0) return CQ_OK;
     if (!umma_ok(d_in, d_out, a->group_size) || a->tc_lut == nullptr || (b && b->tc_lut == nullptr)) {
         set_error("tcgen05 path: site not prepared or shape outside envelope");
@@ -788,9 +810,14 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
     // prefill geometry (128-token passes, merged layout only) when segments are long
     if (umma_prefill(rows, n_seg) && a->tc_layout == CQ_TC_UMMA128U && getenv("CQ_UMMA_NO_PREFILL") == nullptr)
         return lut_umma_geo<UmPrefill>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b,
-                                       d_in, d_out, st);
+                                       d_in, d_out, in, st);
     return lut_umma_geo<UmDecode>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b, d_in,
-                                  d_out, st);
+                                  d_out, in, st);
+}
+
+// Where the merged layout's int32 row sums live in a B buffer (silu_quant writes them directly).
+int32_t *umma_row_sums(int8_t *bbuf, int64_t rows, int64_t d_in) {
+    return reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in));
 }
 
 // One-time re-layout for the tcgen05 kernel from the 16-row LUT layout.

@@ -15,9 +15,12 @@
 namespace cq {
 
 // --- stage kernels defined in other units
-cq_status quantize_a4(const void *, int, int64_t, int64_t, int8_t *, float *, int *, float *, cudaStream_t);
+cq_status quantize_a4(const void *, int, int64_t, int64_t, int8_t *, float *, int *, float *, cudaStream_t,
+                      int32_t *tsum = nullptr, int32_t *zero = nullptr, int n_zero = 0);
 cq_status router_logits(const int8_t *, const float *, const float *, const float *, int64_t, int64_t, int64_t,
                         float *, cudaStream_t);
+cq_status router_fused(const float *, const float *, int64_t, int64_t, int64_t, float *, int32_t *, float *, int32_t *,
+                       int64_t, int64_t, int64_t, int32_t *, int32_t *, int32_t *, int32_t *, cudaStream_t, bool *);
 cq_status topk(const float *, int64_t, int64_t, int64_t, int32_t *, float *, int32_t *, int64_t, int64_t,
                cudaStream_t);
 cq_status permute(const int32_t *, const int32_t *, int64_t, int64_t, int64_t, int64_t, int32_t *,
@@ -34,8 +37,9 @@ cq_status lut_tc_grouped_frag(const int8_t *, uint2 *, const float *, const int3
 bool tc_path_ok(int64_t d_in, int64_t d_out, int64_t g);
 cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
                            const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
-                           cudaStream_t);
+                           cudaStream_t, const UmmaIn &in = UmmaIn{});
 int64_t umma_b_bytes(int64_t rows, int64_t d_in);
+int32_t *umma_row_sums(int8_t *bbuf, int64_t rows, int64_t d_in);
 int64_t rot_tc_act_bytes(int64_t n, int64_t d);
 cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const void *prepared, void *act, float *v,
                        cudaStream_t st);
@@ -47,7 +51,8 @@ cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const voi
 __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, const float *__restrict__ b,
                                                           int64_t ff, int8_t *__restrict__ codes,
                                                           float *__restrict__ scales,
-                                                          const int32_t *__restrict__ live) {
+                                                          const int32_t *__restrict__ live,
+                                                          int32_t *__restrict__ sums) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
@@ -74,7 +79,16 @@ __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, 
     }
     __syncthreads();
     const float s = s_sh;
-    for (int64_t j = threadIdx.x; j < ff; j += blockDim.x) codes[row * ff + j] = a4_code(ar[j], s);
+    int cs = 0;
+    for (int64_t j = threadIdx.x; j < ff; j += blockDim.x) {
+        const int8_t c = a4_code(ar[j], s);
+        codes[row * ff + j] = c;
+        cs += c;
+    }
+    if (sums != nullptr) {  // the down GEMM's unsigned-digit bias term (row_sums_kernel's value)
+        const int t = block_sum_int(cs);
+        if (threadIdx.x == 0) sums[row] = t;
+    }
 }
 
 // Same, register-resident: 512 threads x V float4 cover the row (ff % 4 == 0,
@@ -84,7 +98,8 @@ template <int V>
 __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__ a, const float *__restrict__ b,
                                                               int64_t ff, int8_t *__restrict__ codes,
                                                               float *__restrict__ scales,
-                                                              const int32_t *__restrict__ live) {
+                                                              const int32_t *__restrict__ live,
+                                                              int32_t *__restrict__ sums) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
@@ -120,10 +135,19 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     __syncthreads();
     const float s = s_sh;
     char4 *cr = reinterpret_cast<char4 *>(codes + row * ff);
+    int cs = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * (int)blockDim.x;
-        if (j < nv) cr[j] = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+        if (j < nv) {
+            const char4 c = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+            cr[j] = c;
+            cs += c.x + c.y + c.z + c.w;
+        }
+    }
+    if (sums != nullptr) {
+        const int t = block_sum_int(cs);
+        if (threadIdx.x == 0) sums[row] = t;
     }
 }
 
@@ -135,7 +159,8 @@ template <int V, int CL>
 __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ a, const float *__restrict__ b,
                                                              int64_t ff, int8_t *__restrict__ codes,
                                                              float *__restrict__ scales,
-                                                             const int32_t *__restrict__ live) {
+                                                             const int32_t *__restrict__ live,
+                                                             int32_t *__restrict__ sums) {
     namespace cg = cooperative_groups;
     griddep_wait();
     const int64_t row = blockIdx.x / CL;
@@ -161,6 +186,8 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
     }
     __shared__ float red[8];
     __shared__ float part_max, s_sh;
+    __shared__ int row_sum;  // rank 0's: the cluster's code sum
+    if (part == 0 && threadIdx.x == 0) row_sum = 0;
     mx = warp_max(mx);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
     __syncthreads();
@@ -177,37 +204,54 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
         s_sh = a4_scale(m);
         if (part == 0) scales[row] = s_sh;
     }
-    cluster.sync();  // s_sh visible; no CTA leaves while its part_max may still be read
+    // s_sh visible; no CTA leaves while its part_max may still be read (with sums:
+    // the cluster barrier below, before any CTA exits)
+    if (sums != nullptr)
+        __syncthreads();
+    else
+        cluster.sync();
     const float s = s_sh;
     char4 *cr = reinterpret_cast<char4 *>(codes + row * ff + part * seg);
+    int cs = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * 256;
-        if (j < nv) cr[j] = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+        if (j < nv) {
+            const char4 c = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+            cr[j] = c;
+            cs += c.x + c.y + c.z + c.w;
+        }
+    }
+    if (sums != nullptr) {
+        const int t = block_sum_int(cs);
+        if (threadIdx.x == 0) atomicAdd(cluster.map_shared_rank(&row_sum, 0), t);
+        cluster.sync();
+        if (part == 0 && threadIdx.x == 0) sums[row] = row_sum;
     }
 }
 
 template <int CL>
 static bool silu_quant_cluster(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                               const int32_t *live, cudaStream_t st) {
+                               const int32_t *live, int32_t *sums, cudaStream_t st) {
     if (ff % (4 * CL)) return false;
     const int64_t v = ceil_div(ff / CL / 4, 256);
     const dim3 grid((unsigned)(rows * CL));
     switch (v) {
-        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
-        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
+        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
+        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
         case 3:
-        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
+        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
         case 5: case 6: case 7:
-        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live); break;
+        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
         default: return false;
     }
     return true;
 }
 
 // `live` (device, nullable): rows at or past *live are skipped (EP slot bounds).
+// sums (nullable): per-row code sums (the merged-layout GEMM's bias term).
 cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                     const int32_t *live, cudaStream_t st) {
+                     const int32_t *live, cudaStream_t st, int32_t *sums) {
     if (rows == 0) return CQ_OK;
     static int cl_env = -1;
     if (cl_env < 0) {
@@ -216,10 +260,10 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
     }
     // about two CTAs per SM over the whole grid; long rows only (a cluster CTA keeps >= 256 float4)
     if (cl_env && ff >= 8192) {
-        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, st)) return check_launch("silu_quant");
-        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, st))
+        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, st)) return check_launch("silu_quant");
+        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, st))
             return check_launch("silu_quant");
-        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, st))
+        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, st))
             return check_launch("silu_quant");
     }
     const int64_t v = ceil_div(ff / 4, 512);
@@ -227,16 +271,16 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
         switch (v) {
             case 1: {  // short rows: one float4 per thread, CTA sized to the row
                 const int thr = (int)std::max<int64_t>(64, ceil_div(ff / 4, 32) * 32);
-                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live);
+                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums);
                 break;
             }
-            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live); break;
+            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums); break;
             case 3:
-            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live); break;
-            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live); break;
+            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums); break;
+            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums); break;
         }
     } else {
-        launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live);
+        launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live, sums);
     }
     return check_launch("silu_quant");
 }
@@ -430,6 +474,7 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_CODES_FRAG] = umma_b_bytes(Rh, d);     // >= the mma16 fragment size too
     sz[CQ_WS_HCODES_FRAG] = umma_b_bytes(Rh, ff);
     sz[CQ_WS_ROT_ACT] = dsc->rotation_tc ? rot_tc_act_bytes(n, d) : 0;
+    sz[CQ_WS_TOK_SUMS] = n * 4;
     int64_t pos = 0;
     for (int b = 0; b < CQ_WS_COUNT_; ++b) {
         if (off) off[b] = pos;
@@ -441,7 +486,7 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
 struct Ws {
     int8_t *codes;
     float *scales, *logits, *weights, *scales_perm, *hidden, *hscales, *fout, *rotated, *shared;
-    int32_t *selected, *counts, *offsets, *perm_token, *perm_slot, *inv;
+    int32_t *selected, *counts, *offsets, *perm_token, *perm_slot, *inv, *tok_sums;
     int8_t *codes_perm, *hcodes;
     uint2 *codes_frag, *hcodes_frag;
     void *rot_act;
@@ -460,6 +505,7 @@ Ws carve(void *base, const int64_t *o) {
     w.perm_token = reinterpret_cast<int32_t *>(b + o[CQ_WS_PERM_TOKEN]);
     w.perm_slot = reinterpret_cast<int32_t *>(b + o[CQ_WS_PERM_SLOT]);
     w.inv = reinterpret_cast<int32_t *>(b + o[CQ_WS_INV]);
+    w.tok_sums = reinterpret_cast<int32_t *>(b + o[CQ_WS_TOK_SUMS]);
     w.codes_perm = reinterpret_cast<int8_t *>(b + o[CQ_WS_CODES_PERM]);
     w.scales_perm = reinterpret_cast<float *>(b + o[CQ_WS_SCALES_PERM]);
     w.hidden = reinterpret_cast<float *>(b + o[CQ_WS_HIDDEN]);
@@ -520,19 +566,24 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
                       const cq_expert_site &down, int64_t n_seg, int64_t seg_first, const int8_t *codes,
                       const float *scales, const int32_t *offsets, int64_t rows, float *hidden,
                       int8_t *hcodes, float *hscales, float *fout, uint2 *frag_in, uint2 *frag_h,
-                      cudaStream_t st, cudaEvent_t *ev = nullptr) {
+                      cudaStream_t st, cudaEvent_t *ev = nullptr, const UmmaIn &in = UmmaIn{}) {
     const int64_t d = dsc->d_model, ff = dsc->d_ff;
     if (rows == 0 || n_seg == 0) return CQ_OK;
     if (path == CQ_PATH_TC && gate.tc_layout != CQ_TC_MMA16) {
         float *bbuf = hidden + rows * ff;
         if (ev) cudaEventRecord(ev[0], st);
+        // `in` may make the B build gather token rows (codes / scales per token, in.perm)
         CQ_TRY(lut_umma_grouped(codes, reinterpret_cast<int8_t *>(frag_in), scales, offsets, n_seg, seg_first, rows,
-                                &gate, hidden, &up, bbuf, d, ff, st));
+                                &gate, hidden, &up, bbuf, d, ff, st, in));
         if (ev) cudaEventRecord(ev[1], st);
-        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, offsets + n_seg, st));
+        // the re-quantizer writes the down GEMM's row sums straight into its B buffer
+        UmmaIn hin;
+        hin.sums_ready = down.tc_layout == CQ_TC_UMMA128U;
+        int32_t *hsums = hin.sums_ready ? umma_row_sums(reinterpret_cast<int8_t *>(frag_h), rows, ff) : nullptr;
+        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, offsets + n_seg, st, hsums));
         if (ev) cudaEventRecord(ev[2], st);
         CQ_TRY(lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
-                                &down, fout, nullptr, nullptr, ff, d, st));
+                                &down, fout, nullptr, nullptr, ff, d, st, hin));
         if (ev) cudaEventRecord(ev[3], st);
         return CQ_OK;
     }
@@ -591,7 +642,10 @@ __global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n)
     for (int64_t s = 0; s <= n_shared; ++s) off[s] = (int32_t)(s * n);
 }
 
-cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, const Ws &w, cudaStream_t st) {
+// gather = false: leave codes_perm / scales_perm unwritten (the tcgen05 expert
+// stage gathers token rows itself, UmmaIn::perm).
+cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, const Ws &w, cudaStream_t st,
+                bool gather = true) {
     const int64_t d = dsc->d_model;
     const void *qin = x;
     int qdt = dtype;
@@ -609,17 +663,22 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
         qin = w.rotated;
         qdt = CQ_DTYPE_F32;
     }
-    // the dequantized rows (router input) go to the fout buffer, unused until the down GEMM
-    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, w.fout, st));
-    CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
-    if (cudaMemsetAsync(w.counts, 0, (dsc->n_experts + 1) * 4, st) != cudaSuccess) {
-        set_error("moe: memset counts failed");
-        return CQ_ERR_CUDA;
+    // the dequantized rows (router input) go to the fout buffer, unused until the down GEMM;
+    // the quantizer also clears the route counts and the arrival counter (counts[E])
+    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, w.fout, st, w.tok_sums, w.counts,
+                       (int)dsc->n_experts + 1));
+    bool fused = false;  // logits + top-k + permutation in one launch (decode batches)
+    CQ_TRY(router_fused(w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, w.selected, w.weights, w.counts,
+                        dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets, w.perm_token, w.perm_slot,
+                        w.inv, st, &fused));
+    if (!fused) {
+        CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
+        CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, w.counts, dsc->expert_begin,
+                    dsc->n_local_experts, st));
+        CQ_TRY(permute(w.selected, w.counts, n, dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets,
+                       w.perm_token, w.perm_slot, w.inv, st));
     }
-    CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, w.counts, dsc->expert_begin,
-                dsc->n_local_experts, st));
-    CQ_TRY(permute(w.selected, w.counts, n, dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets,
-                   w.perm_token, w.perm_slot, w.inv, st));
+    if (!gather) return CQ_OK;
     return gather_rows(w.codes, w.scales, w.perm_token, w.offsets, dsc->n_local_experts, n * dsc->top_k, d,
                        w.codes_perm, w.scales_perm, st);
 }
@@ -727,11 +786,23 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
     cudaStream_t st = as_stream(stream);
     Ws w = carve(workspace, off);
     const int path = choose_path(desc);
-    CQ_TRY(route(desc, x, dtype, n_tokens, w, st));
+    // tcgen05 layouts: the expert stage's B build gathers the token rows itself (no codes_perm)
+    const bool umma = path == CQ_PATH_TC && desc->gate.tc_layout != CQ_TC_MMA16;
+    CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma));
     const int64_t R = n_tokens * desc->top_k;
-    CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes_perm,
-                       w.scales_perm, w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag,
-                       w.hcodes_frag, st));
+    if (umma) {
+        UmmaIn in;
+        in.perm = w.perm_token;
+        in.tok_sums = w.tok_sums;
+        in.scales_out = w.scales_perm;
+        CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes, w.scales,
+                           w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag, w.hcodes_frag, st,
+                           nullptr, in));
+    } else {
+        CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes_perm,
+                           w.scales_perm, w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag,
+                           w.hcodes_frag, st));
+    }
     CQ_TRY(cq_moe_combine(w.selected, w.weights, w.inv, w.fout, n_tokens, desc->top_k, desc->d_model, nullptr,
                           out, stream));
     // builder-defined shared experts: out = ((routed + sh_0) + sh_1) ...,

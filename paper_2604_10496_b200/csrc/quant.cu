@@ -17,9 +17,12 @@ __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict
                                                           int8_t *__restrict__ codes,
                                                           float *__restrict__ scales,
                                                           int *__restrict__ nonfinite,
-                                                          float *__restrict__ deq) {
+                                                          float *__restrict__ deq, int32_t *__restrict__ tsum,
+                                                          int32_t *__restrict__ zero, int n_zero) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
+    if (row == 0)  // counters the next kernels accumulate into (route counts)
+        for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
     const int64_t base = row * d;
     float mx = 0.0f;
     bool bad = false;
@@ -45,11 +48,25 @@ __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict
     }
     __syncthreads();
     const float s = s_sh;
+    int csum = 0;
     for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
         const int8_t c = a4_code(load_x<DT>(x, base + j), s);
         codes[base + j] = c;
+        csum += c;
         // dequantized value, rounded exactly as codes.astype(f32) * scales (model.py:379-381)
         if (deq != nullptr) deq[base + j] = __fmul_rn((float)c, s);
+    }
+    if (tsum != nullptr) {  // sum of the row's codes (exact): the unsigned-digit bias term of the GEMM
+        __shared__ int ired[8];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+        if ((threadIdx.x & 31) == 0) ired[threadIdx.x >> 5] = csum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ired[w];
+            tsum[row] = t;
+        }
     }
 }
 
@@ -67,13 +84,16 @@ __global__ void unpack_ids_kernel(const uint8_t *__restrict__ packed, int64_t ro
 }
 
 // deq (nullable): also write code * scale as f32 (the router's input).
+// tsum (nullable): per-row code sums.  zero[0..n_zero) is cleared by CTA 0.
 cq_status quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes, float *scales,
-                      int *nonfinite_dev, float *deq, cudaStream_t st) {
+                      int *nonfinite_dev, float *deq, cudaStream_t st, int32_t *tsum, int32_t *zero, int n_zero) {
     if (n == 0) return CQ_OK;
     if (dtype == CQ_DTYPE_F32)
-        launch_pdl(quantize_a4_kernel<CQ_DTYPE_F32>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq);
+        launch_pdl(quantize_a4_kernel<CQ_DTYPE_F32>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq,
+                   tsum, zero, n_zero);
     else
-        launch_pdl(quantize_a4_kernel<CQ_DTYPE_BF16>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq);
+        launch_pdl(quantize_a4_kernel<CQ_DTYPE_BF16>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq,
+                   tsum, zero, n_zero);
     return check_launch("quantize_a4");
 }
 
@@ -105,7 +125,7 @@ extern "C" cq_status cq_quantize_a4(const void *x, int dtype, int64_t n, int64_t
             return CQ_ERR_CUDA;
         }
     }
-    cq_status rc = quantize_a4(x, dtype, n, d, codes, scales, flag, nullptr, st);
+    cq_status rc = quantize_a4(x, dtype, n, d, codes, scales, flag, nullptr, st, nullptr, nullptr, 0);
     if (check_finite) {
         int host = 0;
         cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);

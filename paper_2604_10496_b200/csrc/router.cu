@@ -140,123 +140,6 @@ __global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__r
     if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
 }
 
-// Decode batches: each chain (token, expert) is d dependent fp32 adds, and with
-// one token per CTA the chain warp of router_deq_kernel issues ~5 instructions
-// per column (loads, FMUL, FADD), above the 4-cycle FADD latency.  Here warp 0
-// holds only the chains (lane c = token c / EG, expert e0 + c % EG) and adds
-// precomputed products with one LDS.128 per 4 columns.  Warps 1-3 stage raw
-// W / x chunks by cp.async (3 buffers) and write the rounded products
-// fmul(x[t][j], w[j][e]) of the next chunk into the other product buffer.
-// Summation order and rounding are those of router_deq_kernel (bit-exact).
-constexpr int RC_THREADS = 128, RC_K = 256, RC_PITCH = RC_K + 4;
-
-template <int EG>
-__global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *__restrict__ xdeq,
-                                                                  const float *__restrict__ w, int64_t n,
-                                                                  int64_t d, int64_t n_exp, int tt,
-                                                                  float *__restrict__ logits) {
-    griddep_wait();
-    extern __shared__ __align__(16) float rcs[];
-    float *pbuf = rcs;                           // [2][32][RC_PITCH] products
-    float *wraw = pbuf + 2 * 32 * RC_PITCH;      // [3][RC_K][EG]
-    float *xraw = wraw + 3 * RC_K * EG;          // [3][tt][RC_K]
-    const int tid = threadIdx.x;
-    const int64_t t0 = blockIdx.x * (int64_t)tt;
-    const int e0 = blockIdx.y * EG;
-    const int n_chunks = (int)((d + RC_K - 1) / RC_K);
-    const int ptid = tid - 32;  // producer index, warps 1-3
-    auto stage = [&](int i) {
-        if (i < n_chunks) {
-            const int64_t k0 = (int64_t)i * RC_K;
-            const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
-            float *wb = wraw + (i % 3) * RC_K * EG;
-            for (int x = ptid; x < kn * (EG / 4); x += RC_THREADS - 32) {
-                const int r = x / (EG / 4), q = x - r * (EG / 4);
-                cp_async16(wb + r * EG + 4 * q, w + (k0 + r) * n_exp + e0 + 4 * q);
-            }
-            float *xb = xraw + (i % 3) * tt * RC_K;
-            const int rowv = kn / 4;
-            for (int x = ptid; x < tt * rowv; x += RC_THREADS - 32) {
-                const int tl = x / rowv, v = x - tl * rowv;
-                const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // rows past n are never stored
-                cp_async16(xb + tl * RC_K + 4 * v, xdeq + tg * d + k0 + 4 * v);
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    auto produce = [&](int i) {  // chunk i landed in raw buffer i % 3 (own copies waited for)
-        asm volatile("bar.sync 1, %0;" ::"n"(RC_THREADS - 32) : "memory");
-        const int64_t k0 = (int64_t)i * RC_K;
-        const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
-        const float *wb = wraw + (i % 3) * RC_K * EG;
-        const float *xb = xraw + (i % 3) * tt * RC_K;
-        float *pb = pbuf + (i & 1) * 32 * RC_PITCH;
-        for (int j = ptid; j < kn; j += RC_THREADS - 32) {
-            float wr[EG];
-#pragma unroll
-            for (int q = 0; q < EG / 4; ++q) {
-                const float4 v = *reinterpret_cast<const float4 *>(wb + j * EG + 4 * q);
-                wr[4 * q] = v.x, wr[4 * q + 1] = v.y, wr[4 * q + 2] = v.z, wr[4 * q + 3] = v.w;
-            }
-            for (int t = 0; t < tt; ++t) {
-                const float xv = xb[t * RC_K + j];
-#pragma unroll
-                for (int e = 0; e < EG; ++e) pb[(t * EG + e) * RC_PITCH + j] = __fmul_rn(xv, wr[e]);
-            }
-        }
-    };
-    if (tid >= 32) {
-        stage(0);
-        stage(1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        produce(0);
-    }
-    __syncthreads();
-    const bool chain = tid < tt * EG;
-    float acc = 0.0f;
-    for (int i = 0; i < n_chunks; ++i) {
-        if (tid >= 32) {
-            if (i + 1 < n_chunks) {
-                stage(i + 2);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-                produce(i + 1);
-            }
-        } else if (chain) {
-            const int kn = (int)((d - (int64_t)i * RC_K) < RC_K ? (d - (int64_t)i * RC_K) : RC_K);  // % 16 == 0
-            const float4 *pr = reinterpret_cast<const float4 *>(pbuf + (i & 1) * 32 * RC_PITCH + tid * RC_PITCH);
-            float4 cur[4], nxt[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) cur[u] = pr[u];
-            for (int j = 16; j < kn; j += 16) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) nxt[u] = pr[(j >> 2) + u];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    acc = __fadd_rn(acc, cur[u].x);
-                    acc = __fadd_rn(acc, cur[u].y);
-                    acc = __fadd_rn(acc, cur[u].z);
-                    acc = __fadd_rn(acc, cur[u].w);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                acc = __fadd_rn(acc, cur[u].x);
-                acc = __fadd_rn(acc, cur[u].y);
-                acc = __fadd_rn(acc, cur[u].z);
-                acc = __fadd_rn(acc, cur[u].w);
-            }
-        }
-        __syncthreads();  // product buffer i & 1 is rewritten by iteration i + 1's producers
-    }
-    if (chain && t0 + tid / EG < n) logits[(t0 + tid / EG) * n_exp + e0 + tid % EG] = acc;
-}
-
-static size_t router_chain_smem(int eg, int tt) {
-    return sizeof(float) * ((size_t)2 * 32 * RC_PITCH + (size_t)3 * RC_K * eg + (size_t)3 * tt * RC_K);
-}
-
 // Many experts (E in {32, 64, 128}): thread = (token group, expert), TPT
 // independent token chains per thread, so a staged W element is reused TPT
 // times instead of once (with one chain per thread every CTA streams all of W
@@ -353,22 +236,17 @@ constexpr int MAX_TOPK = 16;
 // selected logits and counts the routes of the local expert range.
 constexpr int TOPK_WARPS = 4;
 
-__global__ void __launch_bounds__(TOPK_WARPS * 32) topk_kernel(const float *__restrict__ logits, int64_t n,
-                                                               int64_t n_exp, int64_t k, int32_t *__restrict__ selected,
-                                                               float *__restrict__ weights, int32_t *__restrict__ counts,
-                                                               int64_t local_begin, int64_t n_local) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    const int lane = threadIdx.x & 31;
-    const int64_t t = blockIdx.x * (int64_t)TOPK_WARPS + (threadIdx.x >> 5);
-    if (t >= n) return;  // warp-uniform
-    const float *row = logits + t * n_exp;
+// `row`: the token's n_exp logits, global or shared memory.
+__device__ __forceinline__ void topk_token(const float *row, int64_t t, int64_t n_exp, int64_t k, int lane,
+                                           int32_t *__restrict__ selected, float *__restrict__ weights,
+                                           int32_t *__restrict__ counts, int64_t local_begin, int64_t n_local) {
     constexpr int PER = 256 / 32;  // <= 256 experts
     float lv[PER];
     uint32_t taken = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int64_t e = lane + 32 * i;
-        lv[i] = e < n_exp ? __ldg(row + e) : 0.0f;
+        lv[i] = e < n_exp ? row[e] : 0.0f;
         if (e >= n_exp) taken |= 1u << i;
     }
     int sel[MAX_TOPK];
@@ -406,6 +284,17 @@ __global__ void __launch_bounds__(TOPK_WARPS * 32) topk_kernel(const float *__re
         const int64_t le = sel[s] - local_begin;
         if (counts != nullptr && le >= 0 && le < n_local) atomicAdd(counts + le, 1);
     }
+}
+
+__global__ void __launch_bounds__(TOPK_WARPS * 32) topk_kernel(const float *__restrict__ logits, int64_t n,
+                                                               int64_t n_exp, int64_t k, int32_t *__restrict__ selected,
+                                                               float *__restrict__ weights, int32_t *__restrict__ counts,
+                                                               int64_t local_begin, int64_t n_local) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
+    const int lane = threadIdx.x & 31;
+    const int64_t t = blockIdx.x * (int64_t)TOPK_WARPS + (threadIdx.x >> 5);
+    if (t >= n) return;  // warp-uniform
+    topk_token(logits + t * n_exp, t, n_exp, k, lane, selected, weights, counts, local_begin, n_local);
 }
 
 // CTA per local expert: a stable block scan over tokens assigns each route of
@@ -464,6 +353,232 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(
     }
 }
 
+// permute_kernel's result computed by one CTA of NT threads, for n_local <= 32
+// local experts (the decode router's last CTA): offsets, then per chunk of NT
+// tokens one ballot per expert gives each route its stable rank.  selected and
+// counts were written by other CTAs, so they are read through L2 (ld.cg).
+template <int NT>
+__device__ void permute_cta(const int32_t *selected, const int32_t *counts, int64_t n, int64_t k,
+                            int64_t local_begin, int n_local, int32_t *__restrict__ offsets,
+                            int32_t *__restrict__ perm_token, int32_t *__restrict__ perm_slot,
+                            int32_t *__restrict__ inv) {
+    __shared__ int32_t s_run[32];
+    __shared__ int32_t s_wtot[NT / 32][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        int32_t run = 0;
+        for (int e = 0; e < n_local; ++e) {
+            offsets[e] = run;
+            s_run[e] = run;
+            run += __ldcg(counts + e);
+        }
+        offsets[n_local] = run;
+    }
+    __syncthreads();
+    for (int64_t t0 = 0; t0 < n; t0 += NT) {
+        const int64_t t = t0 + tid;
+        int le[MAX_TOPK], pre[MAX_TOPK];
+        uint32_t mine = 0;
+#pragma unroll
+        for (int s = 0; s < MAX_TOPK; ++s) {
+            le[s] = -1;
+            pre[s] = 0;
+            if (s < k && t < n) {
+                const int64_t e = __ldcg(selected + t * k + s) - local_begin;
+                if (e >= 0 && e < n_local) {
+                    le[s] = (int)e;
+                    mine |= 1u << e;
+                }
+            }
+        }
+        for (int e = 0; e < n_local; ++e) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (mine >> e) & 1u);
+            if (lane == 0) s_wtot[warp][e] = __popc(b);
+#pragma unroll
+            for (int s = 0; s < MAX_TOPK; ++s)
+                if (le[s] == e) pre[s] = __popc(b & ((1u << lane) - 1u));
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < MAX_TOPK; ++s) {
+            if (le[s] < 0) continue;
+            int32_t pos = s_run[le[s]] + pre[s];
+            for (int w = 0; w < warp; ++w) pos += s_wtot[w][le[s]];
+            perm_token[pos] = (int32_t)t;
+            perm_slot[pos] = s;
+            if (inv != nullptr) inv[t * k + s] = pos;
+        }
+        __syncthreads();
+        if (tid < n_local) {
+            int32_t tot = 0;
+            for (int w = 0; w < NT / 32; ++w) tot += s_wtot[w][tid];
+            s_run[tid] += tot;
+        }
+        __syncthreads();
+    }
+}
+
+// What the decode router's fused tail writes (top-k, counts, permutation).
+struct RouteFuse {
+    int32_t *selected;
+    float *weights;
+    int32_t *counts;  // [n_local] zeroed by the quantizer, then accumulated here
+    int32_t *done;    // CTA arrival counter, zeroed by the quantizer
+    int32_t *offsets, *perm_token, *perm_slot, *inv;
+    int64_t k, local_begin, n_local;
+};
+
+// Decode batches: each chain (token, expert) is d dependent fp32 adds, and with
+// one token per CTA the chain warp of router_deq_kernel issues ~5 instructions
+// per column (loads, FMUL, FADD), above the 4-cycle FADD latency.  Here warp 0
+// holds only the chains (lane c = token c / EG, expert e0 + c % EG) and adds
+// precomputed products with one LDS.128 per 4 columns.  Warps 1-3 stage raw
+// W / x chunks by cp.async (NR buffers) and write the rounded products
+// fmul(x[t][j], w[j][e]) of the next chunk into the other product buffer.
+// Summation order and rounding are those of router_deq_kernel (bit-exact).
+constexpr int RC_THREADS = 128, RC_K = 256, RC_PITCH = RC_K + 4;
+// raw stages: W leaves L2 under the expert weight stream, so chunks come from
+// DRAM; prefetch NR - 1 chunks (~0.55 us of chain each) ahead
+template <int EG>
+struct RcStages {
+    static constexpr int NR = EG >= 32 ? 4 : 8;
+};
+
+// FUSE (one expert group, n_exp == EG): the CTA also selects its tokens'
+// top-k from the logits in shared memory, and the last CTA to finish lays out
+// the permutation (topk_kernel + permute_kernel without their launches).
+template <int EG, bool FUSE>
+__global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *__restrict__ xdeq,
+                                                                  const float *__restrict__ w, int64_t n,
+                                                                  int64_t d, int64_t n_exp, int tt,
+                                                                  float *__restrict__ logits, RouteFuse f) {
+    griddep_wait();
+    extern __shared__ __align__(16) float rcs[];
+    const int nc = tt * EG;                      // chains
+    float *pbuf = rcs;                           // [2][nc][RC_PITCH] products
+    constexpr int NR = RcStages<EG>::NR;
+    float *wraw = pbuf + 2 * nc * RC_PITCH;      // [NR][RC_K][EG]
+    float *xraw = wraw + NR * RC_K * EG;         // [NR][tt][RC_K]
+    const int tid = threadIdx.x;
+    const int64_t t0 = blockIdx.x * (int64_t)tt;
+    const int e0 = blockIdx.y * EG;
+    const int n_chunks = (int)((d + RC_K - 1) / RC_K);
+    const int ptid = tid - 32;  // producer index, warps 1-3
+    auto stage = [&](int i) {
+        if (i < n_chunks) {
+            const int64_t k0 = (int64_t)i * RC_K;
+            const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
+            float *wb = wraw + (i % NR) * RC_K * EG;
+            for (int x = ptid; x < kn * (EG / 4); x += RC_THREADS - 32) {
+                const int r = x / (EG / 4), q = x - r * (EG / 4);
+                cp_async16(wb + r * EG + 4 * q, w + (k0 + r) * n_exp + e0 + 4 * q);
+            }
+            float *xb = xraw + (i % NR) * tt * RC_K;
+            const int rowv = kn / 4;
+            for (int x = ptid; x < tt * rowv; x += RC_THREADS - 32) {
+                const int tl = x / rowv, v = x - tl * rowv;
+                const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // rows past n are never stored
+                cp_async16(xb + tl * RC_K + 4 * v, xdeq + tg * d + k0 + 4 * v);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto produce = [&](int i) {  // chunk i landed in raw buffer i % NR (own copies waited for)
+        asm volatile("bar.sync 1, %0;" ::"n"(RC_THREADS - 32) : "memory");
+        const int64_t k0 = (int64_t)i * RC_K;
+        const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
+        const float *wb = wraw + (i % NR) * RC_K * EG;
+        const float *xb = xraw + (i % NR) * tt * RC_K;
+        float *pb = pbuf + (i & 1) * nc * RC_PITCH;
+        for (int j = ptid; j < kn; j += RC_THREADS - 32) {
+            float wr[EG];
+#pragma unroll
+            for (int q = 0; q < EG / 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4 *>(wb + j * EG + 4 * q);
+                wr[4 * q] = v.x, wr[4 * q + 1] = v.y, wr[4 * q + 2] = v.z, wr[4 * q + 3] = v.w;
+            }
+            for (int t = 0; t < tt; ++t) {
+                const float xv = xb[t * RC_K + j];
+#pragma unroll
+                for (int e = 0; e < EG; ++e) pb[(t * EG + e) * RC_PITCH + j] = __fmul_rn(xv, wr[e]);
+            }
+        }
+    };
+    if (tid >= 32) {
+#pragma unroll
+        for (int i = 0; i < NR - 1; ++i) stage(i);
+        asm volatile("cp.async.wait_group %0;" ::"n"(NR - 2) : "memory");
+        produce(0);
+    }
+    __syncthreads();
+    const bool chain = tid < nc;
+    float acc = 0.0f;
+    for (int i = 0; i < n_chunks; ++i) {
+        if (tid >= 32) {
+            if (i + 1 < n_chunks) {
+                stage(i + NR - 1);  // into the buffer produce(i - 1) read
+                asm volatile("cp.async.wait_group %0;" ::"n"(NR - 2) : "memory");
+                produce(i + 1);
+            }
+        } else if (chain) {
+            const int kn = (int)((d - (int64_t)i * RC_K) < RC_K ? (d - (int64_t)i * RC_K) : RC_K);  // % 16 == 0
+            const float4 *pr = reinterpret_cast<const float4 *>(pbuf + (i & 1) * nc * RC_PITCH + tid * RC_PITCH);
+            float4 cur[4], nxt[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cur[u] = pr[u];
+            for (int j = 16; j < kn; j += 16) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nxt[u] = pr[(j >> 2) + u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc = __fadd_rn(acc, cur[u].x);
+                    acc = __fadd_rn(acc, cur[u].y);
+                    acc = __fadd_rn(acc, cur[u].z);
+                    acc = __fadd_rn(acc, cur[u].w);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc = __fadd_rn(acc, cur[u].x);
+                acc = __fadd_rn(acc, cur[u].y);
+                acc = __fadd_rn(acc, cur[u].z);
+                acc = __fadd_rn(acc, cur[u].w);
+            }
+        }
+        __syncthreads();  // product buffer i & 1 is rewritten by iteration i + 1's producers
+    }
+    if (chain && t0 + tid / EG < n) logits[(t0 + tid / EG) * n_exp + e0 + tid % EG] = acc;
+    if constexpr (FUSE) {
+        __shared__ float lg[32];  // [tt][EG]
+        __shared__ int s_last;
+        if (chain) lg[tid] = acc;
+        __syncthreads();
+        const int warp = tid >> 5;
+        if (warp < tt && t0 + warp < n) {
+            topk_token(lg + warp * EG, t0 + warp, EG, f.k, tid & 31, f.selected, f.weights, f.counts, f.local_begin,
+                       f.n_local);
+            __threadfence();  // this token's selection and counts before the arrival below
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int last = atomicAdd(f.done, 1) == (int)(gridDim.x * gridDim.y) - 1;
+            if (last) __threadfence();
+            s_last = last;
+        }
+        __syncthreads();
+        if (s_last)
+            permute_cta<RC_THREADS>(f.selected, f.counts, n, f.k, f.local_begin, (int)f.n_local, f.offsets,
+                                    f.perm_token, f.perm_slot, f.inv);
+    }
+}
+
+static size_t router_chain_smem(int eg, int tt) {
+    const size_t nr = eg >= 32 ? RcStages<32>::NR : RcStages<8>::NR;
+    return sizeof(float) * ((size_t)2 * tt * eg * RC_PITCH + nr * RC_K * eg + nr * tt * RC_K);
+}
+
 // rows_out[r, :] = rows_in[perm_token[r], :], r < offsets[n_local]; also scales.
 __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *__restrict__ sscale,
                                    const int32_t *__restrict__ perm_token,
@@ -484,6 +599,76 @@ __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *
     }
 }
 
+template <bool FUSE>
+static void launch_chain(int eg, dim3 grid, size_t smem, cudaStream_t st, const float *xdeq, const float *w,
+                         int64_t n, int64_t d, int64_t n_exp, int tt, float *logits, const RouteFuse &f) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(router_chain_kernel<8, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)router_chain_smem(8, 4));
+        cudaFuncSetAttribute(router_chain_kernel<16, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)router_chain_smem(16, 2));
+        cudaFuncSetAttribute(router_chain_kernel<32, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)router_chain_smem(32, 1));
+        attr = true;
+    }
+    if (eg == 32)
+        launch_pdl(router_chain_kernel<32, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+    else if (eg == 16)
+        launch_pdl(router_chain_kernel<16, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+    else
+        launch_pdl(router_chain_kernel<8, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+}
+
+static int chain_mode() {  // CQ_ROUTER_CHAIN: 0 off, 1 chain kernel, 2 chain kernel without the fused tail
+    static int mode = -1;
+    if (mode < 0) {
+        const char *e = getenv("CQ_ROUTER_CHAIN");
+        mode = e ? atoi(e) : 1;
+    }
+    return mode;
+}
+
+// Decode-sized batches (at most one wave of CTAs, each holding tt * EG <= 32
+// chains) take router_chain_kernel.  With `fuse` given and a single expert
+// group, the same launch also does top-k and the permutation; *fused says so
+// (the counts and the arrival counter must have been zeroed).
+static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d, int64_t n_exp, float *logits,
+                         const RouteFuse *fuse, cudaStream_t st, bool *fused) {
+    if (fused) *fused = false;
+    if (xdeq == nullptr || d % 16 || n_exp % 8 || chain_mode() == 0) return false;
+    const int eg = n_exp % 32 == 0 ? 32 : (n_exp % 16 == 0 ? 16 : 8);
+    const int64_t groups = n_exp / eg;
+    const int tt = (int)std::min<int64_t>(32 / eg, std::max<int64_t>(1, ceil_div(n * groups, 148)));
+    const int64_t ctas = ceil_div(n, tt) * groups;
+    const size_t smem = router_chain_smem(eg, tt);
+    const int64_t per_sm = std::max<int64_t>(1, (int64_t)(227 * 1024) / (int64_t)(smem + 1024));
+    if (ctas > per_sm * 148) return false;
+    const dim3 grid((unsigned)ceil_div(n, tt), (unsigned)groups);
+    if (fuse != nullptr && groups == 1 && chain_mode() == 1 && fuse->n_local <= 32) {
+        launch_chain<true>(eg, grid, smem, st, xdeq, w, n, d, n_exp, tt, logits, *fuse);
+        *fused = true;
+    } else {
+        launch_chain<false>(eg, grid, smem, st, xdeq, w, n, d, n_exp, tt, logits, RouteFuse{});
+    }
+    return true;
+}
+
+// Router logits + top-k + permutation in one launch where router_chain can
+// fuse them; otherwise only the logits (and *fused = false).  counts[n_exp]
+// is the arrival counter; counts[0..n_exp] must be zero on entry.
+cq_status router_fused(const float *xdeq, const float *w, int64_t n, int64_t d, int64_t n_exp, float *logits,
+                       int32_t *selected, float *weights, int32_t *counts, int64_t k, int64_t local_begin,
+                       int64_t n_local, int32_t *offsets, int32_t *perm_token, int32_t *perm_slot, int32_t *inv,
+                       cudaStream_t st, bool *fused) {
+    *fused = false;
+    if (n * n_exp == 0 || k < 1 || k > MAX_TOPK || k > n_exp || n_local < 1) return CQ_OK;
+    RouteFuse f{selected, weights, counts, counts + n_exp, offsets, perm_token, perm_slot, inv, k, local_begin,
+                n_local};
+    if (!router_chain(xdeq, w, n, d, n_exp, logits, &f, st, fused)) return CQ_OK;
+    return check_launch("router_fused");
+}
+
 // xdeq (nullable): the dequantized rows code * scale from the quantizer.
 cq_status router_logits(const int8_t *codes, const float *scales, const float *xdeq, const float *w, int64_t n,
                         int64_t d, int64_t n_exp, float *logits, cudaStream_t st) {
@@ -492,39 +677,7 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         set_error("router: at most 256 experts");
         return CQ_ERR_CONFIG;
     }
-    static int chain_env = -1;
-    if (chain_env < 0) {
-        const char *e = getenv("CQ_ROUTER_CHAIN");
-        chain_env = e ? atoi(e) : 1;
-    }
-    if (xdeq != nullptr && d % 16 == 0 && n_exp % 8 == 0 && chain_env) {
-        // decode-sized batches: at most one wave of CTAs, each holding tt * EG <= 32 chains
-        const int eg = n_exp % 32 == 0 ? 32 : (n_exp % 16 == 0 ? 16 : 8);
-        const int64_t groups = n_exp / eg;
-        const int tt = (int)std::min<int64_t>(32 / eg, std::max<int64_t>(1, ceil_div(n * groups, 148)));
-        const int64_t ctas = ceil_div(n, tt) * groups;
-        if (ctas <= (eg <= 16 ? 2 : 1) * 148) {
-            const size_t smem = router_chain_smem(eg, tt);
-            static bool attr_c = false;
-            if (!attr_c) {
-                cudaFuncSetAttribute(router_chain_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)router_chain_smem(8, 4));
-                cudaFuncSetAttribute(router_chain_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)router_chain_smem(16, 2));
-                cudaFuncSetAttribute(router_chain_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)router_chain_smem(32, 1));
-                attr_c = true;
-            }
-            const dim3 grid((unsigned)ceil_div(n, tt), (unsigned)groups);
-            if (eg == 32)
-                launch_pdl(router_chain_kernel<32>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits);
-            else if (eg == 16)
-                launch_pdl(router_chain_kernel<16>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits);
-            else
-                launch_pdl(router_chain_kernel<8>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits);
-            return check_launch("router_logits");
-        }
-    }
+    if (router_chain(xdeq, w, n, d, n_exp, logits, nullptr, st, nullptr)) return check_launch("router_logits");
     if (xdeq != nullptr && d % 16 == 0 && (n_exp == 32 || n_exp == 64 || n_exp == 128) && n >= 64) {
         constexpr int TPT = 16;
         const int tt = (RD_THREADS / (int)n_exp) * TPT;

@@ -215,6 +215,18 @@ class MoELayer:
 
     __call__ = forward
 
+    def route(self, x, path: str | None = None) -> None:
+        """The routing stage alone (`cq_moe_route`) into the workspace: codes,
+        logits, top-k, the segment permutation and the gathered codes_perm /
+        scales_perm.  (The tensor-core forward gathers inside its GEMM's B build
+        and leaves codes_perm unwritten.)"""
+        x = x.to("cuda").contiguous()
+        n = x.shape[0]
+        buf, _ = self.workspace(n, path)
+        d = self.desc(path)
+        _lib.check(_lib.lib().cq_moe_route(ctypes.byref(d), x.data_ptr(), _lib.dtype_code(x), n, buf.data_ptr(),
+                                           buf.numel(), _lib.stream()))
+
     def trace(self, n: int, path: str | None = None) -> dict:
         """Views of the workspace buffers of the last forward over n tokens."""
         buf, offs = self.workspace(n, path)
@@ -226,7 +238,7 @@ class MoELayer:
                 "inv": (torch.int32, (n, k)), "codes_perm": (torch.int8, (R, d)),
                 "scales_perm": (torch.float32, (R,)), "hidden": (torch.float32, (R, ff)),
                 "hcodes": (torch.int8, (R, ff)), "hscales": (torch.float32, (R,)),
-                "fout": (torch.float32, (R, d))}
+                "fout": (torch.float32, (R, d)), "tok_sums": (torch.int32, (n,))}
         res = {}
         for name, (dt, shape) in spec.items():
             o = offs[_lib.WS_NAMES.index(name)]

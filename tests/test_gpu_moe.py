@@ -168,8 +168,20 @@ def test_router_decode_chain_bit_exact(n, d, E):
     codes, scales = oracle.c_quantize(v.float().cpu().numpy())
     logits = oracle.c_matmul(codes.astype(np.float32) * scales[:, None], w.cpu().numpy())
     assert np.array_equal(tr["logits"].cpu().numpy().view(np.int32), logits.view(np.int32))
-    sel, _ = o.select_top_k(logits, 2)
+    sel, wts = o.select_top_k(logits, 2)
     assert np.array_equal(tr["selected"].cpu().numpy(), sel)
+    # E <= 32: the same launch did top-k and the permutation (last CTA); E > 32: separate kernels
+    ulp = np.abs(tr["weights"].cpu().numpy().view(np.int32) - wts.astype(np.float32).view(np.int32))
+    assert ulp.max() <= 8
+    tok, slot, off, inv = o.route_permutation(sel, E)
+    R = int(off[-1])
+    assert np.array_equal(tr["offsets"].cpu().numpy(), off)
+    assert np.array_equal(tr["perm_token"].cpu().numpy()[:R], tok)
+    assert np.array_equal(tr["perm_slot"].cpu().numpy()[:R], slot)
+    assert np.array_equal(tr["inv"].cpu().numpy(), inv)
+    # a second call starts from cleared counts (the quantizer zeroes them)
+    layer(v)
+    assert np.array_equal(layer.trace(n)["offsets"].cpu().numpy(), off)
 
 
 @pytest.mark.parametrize("n", [4, 60, 140])

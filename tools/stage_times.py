@@ -16,6 +16,7 @@ out = torch.empty((n, d), device="cuda")
 layer(v, out=out)
 buf, _ = layer.workspace(n)
 dsc = layer.desc()
+layer.route(v)  # codes_perm (the tensor-core forward gathers in-kernel)
 tr = layer.trace(n)
 L = _lib.lib()
 fexp = torch.empty((n * k, d), device="cuda")
