@@ -133,12 +133,23 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Route mode of the B build: the segment permutation is derived from the
+// top-k in every CTA (route_perm.cuh); CTA 0 publishes it.
+struct RoutePerm {
+    const int32_t *selected = nullptr;  // [n_tok][k] global expert ids; nullptr = off
+    int64_t n_tok = 0, local_begin = 0;
+    int k = 0, n_local = 0;
+    int32_t *offsets = nullptr, *counts = nullptr, *perm_token = nullptr, *perm_slot = nullptr, *inv = nullptr;
+};
+
 // Optional inputs of the tcgen05 grouped GEMM's B-operand build (lut_umma.cu).
 struct UmmaIn {
     const int32_t *perm = nullptr;      // gather: segment row r reads codes[perm[r]] (codes per token)
-    const int32_t *tok_sums = nullptr;  // with perm: per-token code sums, gathered into the row sums
-    float *scales_out = nullptr;        // with perm: scales[perm[r]] lands here; the GEMM reads it
-    bool sums_ready = false;            // without perm: the row sums are already in the B buffer
+    const int32_t *tok_sums = nullptr;  // gather / route: per-token code sums, gathered into the row sums
+    float *scales_out = nullptr;        // gather / route: scales[perm[r]] lands here; the GEMM reads it
+    bool sums_ready = false;            // otherwise: the row sums are already in the B buffer
+    RoutePerm route;                    // route mode (implies the gather)
+    bool gathers() const { return perm != nullptr || route.selected != nullptr; }
 };
 
 // launch_pdl with a thread-block cluster of cluster_x CTAs along x.

@@ -40,6 +40,7 @@
 // Epilogue: expanders tcgen05.ld the accumulators, combine the digits, scale
 // by the row scale and the token scale, store fp32.
 #include "common.cuh"
+#include "route_perm.cuh"
 #include "tc_ptx.cuh"
 
 #include <cstdlib>
@@ -593,21 +594,44 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 // codes (rows, K) row-major -> [chunk CK][tile8][kstep KS][khalf2][8 rows][16 B],
 // the canonical K-major no-swizzle UMMA B layout per k-step; rows >= n are zero.
 // Also zeroes the GEMM's split-unit counters (zero[0..n_zero)).
-template <int CK>
 // perm (nullable): gather form, segment row r < *live reads token row perm[r]
 // of src, rows past *live are zero, and the per-row scale and code sum are
 // gathered from the token arrays (gather_rows + row_sums without their launches).
-__global__ void to_umma_b_kernel(const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles,
-                                 uint4 *__restrict__ dst, int32_t *__restrict__ zero, int n_zero,
-                                 const int32_t *__restrict__ perm, const int32_t *__restrict__ live,
-                                 const float *__restrict__ tscales, float *__restrict__ scales_out,
-                                 const int32_t *__restrict__ tsum, int32_t *__restrict__ sums) {
+// rp.selected (route mode): the permutation is derived here from the top-k
+// (route_perm.cuh, every CTA in shared memory); CTA 0 publishes offsets,
+// counts, perm_token, perm_slot and inv.  blockDim.x == TB_THREADS.
+constexpr int TB_THREADS = 256;
+
+template <int CK>
+__global__ void __launch_bounds__(TB_THREADS) to_umma_b_kernel(
+    const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles, uint4 *__restrict__ dst,
+    int32_t *__restrict__ zero, int n_zero, const int32_t *__restrict__ perm, const int32_t *__restrict__ live,
+    const float *__restrict__ tscales, float *__restrict__ scales_out, const int32_t *__restrict__ tsum,
+    int32_t *__restrict__ sums, RoutePerm rp) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     constexpr int PIECES = 16 * (CK / 32);  // 16-byte pieces per tile-chunk: k-steps x 2 khalf x 8 rows
     const int64_t total = (K / CK) * tiles * PIECES;
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
-    const int64_t nrow = perm != nullptr ? (int64_t)*live : n;
+    int64_t nrow;
+    if (rp.selected != nullptr) {
+        extern __shared__ int32_t tb_sm[];  // [RP_MAX_LOCAL + 1] offsets | [n_tok * k] permutation
+        int32_t *s_off = tb_sm, *s_perm = tb_sm + RP_MAX_LOCAL + 1;
+        const bool pub = blockIdx.x == 0;
+        route_permute<TB_THREADS>(rp.selected, rp.n_tok, rp.k, rp.local_begin, rp.n_local, s_off, s_perm,
+                                  pub ? rp.perm_slot : nullptr, pub ? rp.inv : nullptr);
+        nrow = s_off[rp.n_local];
+        perm = s_perm;
+        if (pub) {
+            for (int64_t x = threadIdx.x; x < nrow; x += blockDim.x) rp.perm_token[x] = s_perm[x];
+            for (int e = threadIdx.x; e <= rp.n_local; e += blockDim.x) {
+                rp.offsets[e] = s_off[e];
+                if (e < rp.n_local) rp.counts[e] = s_off[e + 1] - s_off[e];
+            }
+        }
+    } else {
+        nrow = perm != nullptr ? (int64_t)*live : n;
+    }
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (perm != nullptr)
         for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nrow; x += stride) {
@@ -693,11 +717,13 @@ cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, in
                     cudaStream_t st) {
     const int64_t total = (K / CK) * tiles * 16 * (CK / 32);
     if (total == 0) return CQ_OK;
-    launch_pdl(to_umma_b_kernel<CK>, (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16), 256, 0, st, codes,
-               n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero, in.perm, live, tscales, in.scales_out,
-               in.tok_sums, in.perm != nullptr ? sums : nullptr);
+    const size_t smem =
+        in.route.selected != nullptr ? sizeof(int32_t) * (RP_MAX_LOCAL + 1 + in.route.n_tok * in.route.k) : 0;
+    launch_pdl(to_umma_b_kernel<CK>, (unsigned)std::min<int64_t>(ceil_div(total, TB_THREADS), 148 * 16), TB_THREADS,
+               smem, st, codes, n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero, in.perm, live, tscales,
+               in.scales_out, in.tok_sums, in.gathers() ? sums : nullptr, in.route);
     CQ_TRY(check_launch("to_umma_b"));
-    if (sums == nullptr || in.perm != nullptr || in.sums_ready) return CQ_OK;
+    if (sums == nullptr || in.gathers() || in.sums_ready) return CQ_OK;
     launch_pdl(row_sums_kernel, (unsigned)ceil_div(n, 8), 256, 0, st, codes, n, K, sums);
     return check_launch("row_sums");
 }
@@ -767,7 +793,7 @@ cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, c
     int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
     int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
     CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), in, scales, offsets + n_seg, st));
-    if (in.perm != nullptr) scales = in.scales_out;  // per segment row from here on
+    if (in.gathers()) scales = in.scales_out;  // per segment row from here on
 #define CQ_UMMA(P_, M_)                                                                                   \
     launch_umma<P_, M_, GEO>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, \
                              d_out, part, cnt, st)

@@ -11,6 +11,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "route_perm.cuh"
 
 namespace cq {
 
@@ -19,8 +20,8 @@ cq_status quantize_a4(const void *, int, int64_t, int64_t, int8_t *, float *, in
                       int32_t *tsum = nullptr, int32_t *zero = nullptr, int n_zero = 0);
 cq_status router_logits(const int8_t *, const float *, const float *, const float *, int64_t, int64_t, int64_t,
                         float *, cudaStream_t);
-cq_status router_fused(const float *, const float *, int64_t, int64_t, int64_t, float *, int32_t *, float *, int32_t *,
-                       int64_t, int64_t, int64_t, int32_t *, int32_t *, int32_t *, int32_t *, cudaStream_t, bool *);
+cq_status router_fused(const float *, const float *, int64_t, int64_t, int64_t, float *, int32_t *, float *, int64_t,
+                       cudaStream_t, bool *);
 cq_status topk(const float *, int64_t, int64_t, int64_t, int32_t *, float *, int32_t *, int64_t, int64_t,
                cudaStream_t);
 cq_status permute(const int32_t *, const int32_t *, int64_t, int64_t, int64_t, int64_t, int32_t *,
@@ -643,9 +644,11 @@ __global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n)
 }
 
 // gather = false: leave codes_perm / scales_perm unwritten (the tcgen05 expert
-// stage gathers token rows itself, UmmaIn::perm).
+// stage gathers token rows itself, UmmaIn::perm).  topk_only (nullable): where
+// the router can also do top-k in its launch, stop there and set *topk_only;
+// the permutation is then the consumer's (UmmaIn::route).
 cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, const Ws &w, cudaStream_t st,
-                bool gather = true) {
+                bool gather = true, bool *topk_only = nullptr) {
     const int64_t d = dsc->d_model;
     const void *qin = x;
     int qdt = dtype;
@@ -667,17 +670,20 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
     // the quantizer also clears the route counts and the arrival counter (counts[E])
     CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, w.fout, st, w.tok_sums, w.counts,
                        (int)dsc->n_experts + 1));
-    bool fused = false;  // logits + top-k + permutation in one launch (decode batches)
-    CQ_TRY(router_fused(w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, w.selected, w.weights, w.counts,
-                        dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets, w.perm_token, w.perm_slot,
-                        w.inv, st, &fused));
-    if (!fused) {
-        CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
-        CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, w.counts, dsc->expert_begin,
-                    dsc->n_local_experts, st));
-        CQ_TRY(permute(w.selected, w.counts, n, dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets,
-                       w.perm_token, w.perm_slot, w.inv, st));
+    if (topk_only != nullptr) {
+        *topk_only = false;
+        if (n * dsc->top_k <= RP_MAX_ROUTES && dsc->n_local_experts <= RP_MAX_LOCAL) {
+            // logits + top-k in one launch (decode batches)
+            CQ_TRY(router_fused(w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, w.selected, w.weights,
+                                dsc->top_k, st, topk_only));
+            if (*topk_only) return CQ_OK;
+        }
     }
+    CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
+    CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, w.counts, dsc->expert_begin,
+                dsc->n_local_experts, st));
+    CQ_TRY(permute(w.selected, w.counts, n, dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets,
+                   w.perm_token, w.perm_slot, w.inv, st));
     if (!gather) return CQ_OK;
     return gather_rows(w.codes, w.scales, w.perm_token, w.offsets, dsc->n_local_experts, n * dsc->top_k, d,
                        w.codes_perm, w.scales_perm, st);
@@ -788,13 +794,27 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
     const int path = choose_path(desc);
     // tcgen05 layouts: the expert stage's B build gathers the token rows itself (no codes_perm)
     const bool umma = path == CQ_PATH_TC && desc->gate.tc_layout != CQ_TC_MMA16;
-    CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma));
+    bool topk_only = false;
+    CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma, umma ? &topk_only : nullptr));
     const int64_t R = n_tokens * desc->top_k;
     if (umma) {
         UmmaIn in;
-        in.perm = w.perm_token;
         in.tok_sums = w.tok_sums;
         in.scales_out = w.scales_perm;
+        if (topk_only) {  // the B build derives the permutation from the top-k and publishes it
+            in.route.selected = w.selected;
+            in.route.n_tok = n_tokens;
+            in.route.k = (int)desc->top_k;
+            in.route.local_begin = desc->expert_begin;
+            in.route.n_local = (int)desc->n_local_experts;
+            in.route.offsets = w.offsets;
+            in.route.counts = w.counts;
+            in.route.perm_token = w.perm_token;
+            in.route.perm_slot = w.perm_slot;
+            in.route.inv = w.inv;
+        } else {
+            in.perm = w.perm_token;
+        }
         CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes, w.scales,
                            w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag, w.hcodes_frag, st,
                            nullptr, in));

@@ -6,6 +6,7 @@
 // (quant.py:8-13); top-k ids, their order, counts, offsets and the permutation
 // are therefore bit-exact.  Route weights use CUDA expf (ulp-bounded vs numpy).
 #include "common.cuh"
+#include "route_perm.cuh"
 
 #include <cstdlib>
 
@@ -227,8 +228,6 @@ __device__ __forceinline__ float np_sum(const float *v, int n) {
     return res;
 }
 
-constexpr int MAX_TOPK = 16;
-
 // One warp per token: the lanes hold the token's logits (expert e in lane e % 32),
 // and each of the k rounds is a warp argmax (larger logit first, ties -> lower
 // expert id, +0 and -0 equal like numpy's sort): the stable descending
@@ -353,79 +352,11 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(
     }
 }
 
-// permute_kernel's result computed by one CTA of NT threads, for n_local <= 32
-// local experts (the decode router's last CTA): offsets, then per chunk of NT
-// tokens one ballot per expert gives each route its stable rank.  selected and
-// counts were written by other CTAs, so they are read through L2 (ld.cg).
-template <int NT>
-__device__ void permute_cta(const int32_t *selected, const int32_t *counts, int64_t n, int64_t k,
-                            int64_t local_begin, int n_local, int32_t *__restrict__ offsets,
-                            int32_t *__restrict__ perm_token, int32_t *__restrict__ perm_slot,
-                            int32_t *__restrict__ inv) {
-    __shared__ int32_t s_run[32];
-    __shared__ int32_t s_wtot[NT / 32][32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        int32_t run = 0;
-        for (int e = 0; e < n_local; ++e) {
-            offsets[e] = run;
-            s_run[e] = run;
-            run += __ldcg(counts + e);
-        }
-        offsets[n_local] = run;
-    }
-    __syncthreads();
-    for (int64_t t0 = 0; t0 < n; t0 += NT) {
-        const int64_t t = t0 + tid;
-        int le[MAX_TOPK], pre[MAX_TOPK];
-        uint32_t mine = 0;
-#pragma unroll
-        for (int s = 0; s < MAX_TOPK; ++s) {
-            le[s] = -1;
-            pre[s] = 0;
-            if (s < k && t < n) {
-                const int64_t e = __ldcg(selected + t * k + s) - local_begin;
-                if (e >= 0 && e < n_local) {
-                    le[s] = (int)e;
-                    mine |= 1u << e;
-                }
-            }
-        }
-        for (int e = 0; e < n_local; ++e) {
-            const uint32_t b = __ballot_sync(0xffffffffu, (mine >> e) & 1u);
-            if (lane == 0) s_wtot[warp][e] = __popc(b);
-#pragma unroll
-            for (int s = 0; s < MAX_TOPK; ++s)
-                if (le[s] == e) pre[s] = __popc(b & ((1u << lane) - 1u));
-        }
-        __syncthreads();
-#pragma unroll
-        for (int s = 0; s < MAX_TOPK; ++s) {
-            if (le[s] < 0) continue;
-            int32_t pos = s_run[le[s]] + pre[s];
-            for (int w = 0; w < warp; ++w) pos += s_wtot[w][le[s]];
-            perm_token[pos] = (int32_t)t;
-            perm_slot[pos] = s;
-            if (inv != nullptr) inv[t * k + s] = pos;
-        }
-        __syncthreads();
-        if (tid < n_local) {
-            int32_t tot = 0;
-            for (int w = 0; w < NT / 32; ++w) tot += s_wtot[w][tid];
-            s_run[tid] += tot;
-        }
-        __syncthreads();
-    }
-}
-
-// What the decode router's fused tail writes (top-k, counts, permutation).
+// What the decode router's fused tail writes: the top-k of its tokens.
 struct RouteFuse {
     int32_t *selected;
     float *weights;
-    int32_t *counts;  // [n_local] zeroed by the quantizer, then accumulated here
-    int32_t *done;    // CTA arrival counter, zeroed by the quantizer
-    int32_t *offsets, *perm_token, *perm_slot, *inv;
-    int64_t k, local_begin, n_local;
+    int64_t k;
 };
 
 // Decode batches: each chain (token, expert) is d dependent fp32 adds, and with
@@ -436,7 +367,10 @@ struct RouteFuse {
 // W / x chunks by cp.async (NR buffers) and write the rounded products
 // fmul(x[t][j], w[j][e]) of the next chunk into the other product buffer.
 // Summation order and rounding are those of router_deq_kernel (bit-exact).
-constexpr int RC_THREADS = 128, RC_K = 256, RC_PITCH = RC_K + 4;
+#ifndef RC_KCOLS
+#define RC_KCOLS 256
+#endif
+constexpr int RC_THREADS = 128, RC_K = RC_KCOLS, RC_PITCH = RC_K + 4;
 // raw stages: W leaves L2 under the expert weight stream, so chunks come from
 // DRAM; prefetch NR - 1 chunks (~0.55 us of chain each) ahead
 template <int EG>
@@ -444,15 +378,53 @@ struct RcStages {
     static constexpr int NR = EG >= 32 ? 4 : 8;
 };
 
+// acc + p[0] + p[1] + ... + p[kn-1] in order (kn % 16 == 0), 16 columns loaded
+// ahead of the adds; KC > 0 fixes kn = KC at compile time.
+template <int KC>
+__device__ __forceinline__ float chain_add(float acc, const float4 *__restrict__ pr, int kn) {
+    if (KC > 0) kn = KC;
+    float4 cur[4], nxt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cur[u] = pr[u];
+#pragma unroll 3
+    for (int j = 16; j < kn; j += 16) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) nxt[u] = pr[(j >> 2) + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            acc = __fadd_rn(acc, cur[u].x);
+            acc = __fadd_rn(acc, cur[u].y);
+            acc = __fadd_rn(acc, cur[u].z);
+            acc = __fadd_rn(acc, cur[u].w);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        acc = __fadd_rn(acc, cur[u].x);
+        acc = __fadd_rn(acc, cur[u].y);
+        acc = __fadd_rn(acc, cur[u].z);
+        acc = __fadd_rn(acc, cur[u].w);
+    }
+    return acc;
+}
+
 // FUSE (one expert group, n_exp == EG): the CTA also selects its tokens'
-// top-k from the logits in shared memory, and the last CTA to finish lays out
-// the permutation (topk_kernel + permute_kernel without their launches).
+// top-k from the logits in shared memory (topk_kernel without its launch; the
+// permutation is derived by the consumer, route_perm.cuh).
 template <int EG, bool FUSE>
 __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *__restrict__ xdeq,
                                                                   const float *__restrict__ w, int64_t n,
                                                                   int64_t d, int64_t n_exp, int tt,
                                                                   float *__restrict__ logits, RouteFuse f) {
+#ifdef RC_EXP_TIMING
+    const long long ph_launch = clock64();
+#endif
     griddep_wait();
+#ifdef RC_EXP_TIMING
+    const long long ph0 = clock64();
+#endif
     extern __shared__ __align__(16) float rcs[];
     const int nc = tt * EG;                      // chains
     float *pbuf = rcs;                           // [2][nc][RC_PITCH] products
@@ -490,6 +462,9 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
         const float *wb = wraw + (i % NR) * RC_K * EG;
         const float *xb = xraw + (i % NR) * tt * RC_K;
         float *pb = pbuf + (i & 1) * nc * RC_PITCH;
+#ifdef RC_EXP_NO_PRODUCE
+        return;
+#endif
         for (int j = ptid; j < kn; j += RC_THREADS - 32) {
             float wr[EG];
 #pragma unroll
@@ -511,8 +486,14 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
         produce(0);
     }
     __syncthreads();
+#ifdef RC_EXP_TIMING
+    const long long ph1 = clock64();
+#endif
     const bool chain = tid < nc;
     float acc = 0.0f;
+#ifdef RC_EXP_CHUNKS
+    __shared__ long long chunk_t[64];
+#endif
     for (int i = 0; i < n_chunks; ++i) {
         if (tid >= 32) {
             if (i + 1 < n_chunks) {
@@ -523,54 +504,40 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
         } else if (chain) {
             const int kn = (int)((d - (int64_t)i * RC_K) < RC_K ? (d - (int64_t)i * RC_K) : RC_K);  // % 16 == 0
             const float4 *pr = reinterpret_cast<const float4 *>(pbuf + (i & 1) * nc * RC_PITCH + tid * RC_PITCH);
-            float4 cur[4], nxt[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) cur[u] = pr[u];
-            for (int j = 16; j < kn; j += 16) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) nxt[u] = pr[(j >> 2) + u];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    acc = __fadd_rn(acc, cur[u].x);
-                    acc = __fadd_rn(acc, cur[u].y);
-                    acc = __fadd_rn(acc, cur[u].z);
-                    acc = __fadd_rn(acc, cur[u].w);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                acc = __fadd_rn(acc, cur[u].x);
-                acc = __fadd_rn(acc, cur[u].y);
-                acc = __fadd_rn(acc, cur[u].z);
-                acc = __fadd_rn(acc, cur[u].w);
-            }
+            if (kn == RC_K)
+                acc = chain_add<RC_K>(acc, pr, RC_K);  // full chunk: compile-time trip count
+            else
+                acc = chain_add<0>(acc, pr, kn);
         }
+#ifndef RC_EXP_NO_SYNC
         __syncthreads();  // product buffer i & 1 is rewritten by iteration i + 1's producers
+#endif
+#ifdef RC_EXP_CHUNKS
+        if (tid == 0 && i < 64) {
+            asm volatile("" : "+f"(acc));
+            chunk_t[i] = clock64();
+        }
+#endif
     }
+#ifdef RC_EXP_CHUNKS
+    if (tid == 0 && blockIdx.x == 0) {
+        printf("chunks:");
+        for (int i = 1; i < n_chunks && i < 64; ++i) printf(" %lld", chunk_t[i] - chunk_t[i - 1]);
+        printf("\n");
+    }
+#endif
+#ifdef RC_EXP_TIMING
+    asm volatile("" : "+f"(acc));
+    const long long ph2 = clock64();
+#endif
     if (chain && t0 + tid / EG < n) logits[(t0 + tid / EG) * n_exp + e0 + tid % EG] = acc;
     if constexpr (FUSE) {
         __shared__ float lg[32];  // [tt][EG]
-        __shared__ int s_last;
         if (chain) lg[tid] = acc;
         __syncthreads();
         const int warp = tid >> 5;
-        if (warp < tt && t0 + warp < n) {
-            topk_token(lg + warp * EG, t0 + warp, EG, f.k, tid & 31, f.selected, f.weights, f.counts, f.local_begin,
-                       f.n_local);
-            __threadfence();  // this token's selection and counts before the arrival below
-        }
-        __syncthreads();
-        if (tid == 0) {
-            const int last = atomicAdd(f.done, 1) == (int)(gridDim.x * gridDim.y) - 1;
-            if (last) __threadfence();
-            s_last = last;
-        }
-        __syncthreads();
-        if (s_last)
-            permute_cta<RC_THREADS>(f.selected, f.counts, n, f.k, f.local_begin, (int)f.n_local, f.offsets,
-                                    f.perm_token, f.perm_slot, f.inv);
+        if (warp < tt && t0 + warp < n)
+            topk_token(lg + warp * EG, t0 + warp, EG, f.k, tid & 31, f.selected, f.weights, nullptr, 0, 0);
     }
 }
 
@@ -644,8 +611,10 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
     const size_t smem = router_chain_smem(eg, tt);
     const int64_t per_sm = std::max<int64_t>(1, (int64_t)(227 * 1024) / (int64_t)(smem + 1024));
     if (ctas > per_sm * 148) return false;
+    const bool can_fuse = groups == 1 && chain_mode() == 1 && fuse != nullptr;
+    if (fuse != nullptr && !can_fuse) return false;  // the caller runs the separate kernels
     const dim3 grid((unsigned)ceil_div(n, tt), (unsigned)groups);
-    if (fuse != nullptr && groups == 1 && chain_mode() == 1 && fuse->n_local <= 32) {
+    if (can_fuse) {
         launch_chain<true>(eg, grid, smem, st, xdeq, w, n, d, n_exp, tt, logits, *fuse);
         *fused = true;
     } else {
@@ -654,17 +623,13 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
     return true;
 }
 
-// Router logits + top-k + permutation in one launch where router_chain can
-// fuse them; otherwise only the logits (and *fused = false).  counts[n_exp]
-// is the arrival counter; counts[0..n_exp] must be zero on entry.
+// Router logits + top-k in one launch where router_chain can fuse them
+// (*fused); otherwise nothing is launched.
 cq_status router_fused(const float *xdeq, const float *w, int64_t n, int64_t d, int64_t n_exp, float *logits,
-                       int32_t *selected, float *weights, int32_t *counts, int64_t k, int64_t local_begin,
-                       int64_t n_local, int32_t *offsets, int32_t *perm_token, int32_t *perm_slot, int32_t *inv,
-                       cudaStream_t st, bool *fused) {
+                       int32_t *selected, float *weights, int64_t k, cudaStream_t st, bool *fused) {
     *fused = false;
-    if (n * n_exp == 0 || k < 1 || k > MAX_TOPK || k > n_exp || n_local < 1) return CQ_OK;
-    RouteFuse f{selected, weights, counts, counts + n_exp, offsets, perm_token, perm_slot, inv, k, local_begin,
-                n_local};
+    if (n * n_exp == 0 || k < 1 || k > MAX_TOPK || k > n_exp) return CQ_OK;
+    RouteFuse f{selected, weights, k};
     if (!router_chain(xdeq, w, n, d, n_exp, logits, &f, st, fused)) return CQ_OK;
     return check_launch("router_fused");
 }

@@ -233,7 +233,8 @@ class MoELayer:
         k, d, ff, E, R = self.top_k, self.d_model, self.d_ff, self.n_experts, n * self.top_k
         spec = {"codes": (torch.int8, (n, d)), "scales": (torch.float32, (n,)),
                 "logits": (torch.float32, (n, E)), "selected": (torch.int32, (n, k)),
-                "weights": (torch.float32, (n, k)), "offsets": (torch.int32, (self.n_local + 1,)),
+                "weights": (torch.float32, (n, k)), "counts": (torch.int32, (E + 1,)),
+                "offsets": (torch.int32, (self.n_local + 1,)),
                 "perm_token": (torch.int32, (R,)), "perm_slot": (torch.int32, (R,)),
                 "inv": (torch.int32, (n, k)), "codes_perm": (torch.int8, (R, d)),
                 "scales_perm": (torch.float32, (R,)), "hidden": (torch.float32, (R, ff)),

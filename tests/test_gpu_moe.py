@@ -184,6 +184,40 @@ def test_router_decode_chain_bit_exact(n, d, E):
     assert np.array_equal(layer.trace(n)["offsets"].cpu().numpy(), off)
 
 
+@pytest.mark.parametrize("n,E,k", [(1, 8, 2), (64, 8, 2), (33, 16, 4), (100, 32, 8), (296, 8, 2), (7, 24, 3)])
+def test_tc_decode_route_mode(n, E, k):
+    """Tensor-core forward at decode sizes: the router launch also does top-k,
+    and the GEMM's B build derives the segment permutation in every CTA
+    (route_perm.cuh) and publishes it.  Routing arrays bit-exact with the
+    oracle, the layer output within the layer tolerance of the ordered path,
+    and identical across two calls."""
+    d, ff, g = 256, 256, 128
+    v, w, sites, _ = moe_inputs_device(90 + n + E, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
+    layer.prepare_tc()
+    out = layer(v).clone()
+    tr = layer.trace(n)
+    codes, scales = oracle.c_quantize(v.float().cpu().numpy())
+    logits = oracle.c_matmul(codes.astype(np.float32) * scales[:, None], w.cpu().numpy())
+    sel, wts = o.select_top_k(logits, k)
+    assert np.array_equal(tr["logits"].cpu().numpy().view(np.int32), logits.view(np.int32))
+    assert np.array_equal(tr["selected"].cpu().numpy(), sel)
+    ulp = np.abs(tr["weights"].cpu().numpy().view(np.int32) - wts.astype(np.float32).view(np.int32))
+    assert ulp.max() <= 8
+    tok, slot, off, inv = o.route_permutation(sel, E)
+    R = int(off[-1])
+    assert np.array_equal(tr["offsets"].cpu().numpy(), off)
+    assert np.array_equal(tr["counts"].cpu().numpy()[:E], np.diff(off))
+    assert np.array_equal(tr["perm_token"].cpu().numpy()[:R], tok)
+    assert np.array_equal(tr["perm_slot"].cpu().numpy()[:R], slot)
+    assert np.array_equal(tr["inv"].cpu().numpy(), inv)
+    assert np.array_equal(tr["scales_perm"].cpu().numpy()[:R].view(np.int32), scales[tok].view(np.int32))
+    ordered = layer(v, path="ordered")
+    assert o.relative_error(out.cpu().numpy(), ordered.cpu().numpy()) <= LAYER_TOL
+    assert torch.equal(layer(v), out)
+
+
 @pytest.mark.parametrize("n", [4, 60, 140])
 def test_silu_requant_cluster_rows(n):
     """Long hidden rows (ff = 14336) at decode row counts take the cluster

@@ -2,7 +2,7 @@
 logits, top-k, permutation, gather) replayed as a CUDA graph, over d_model, so
 the slope gives the router chain's cost per column.
 
-    python tools/route_bench.py [n] [E]
+    python tools/route_bench.py [n] [E] [d ...]
 """
 import ctypes
 import sys
@@ -18,7 +18,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 E = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 L = _lib.lib()
 s = torch.cuda.Stream()
-for d in (1024, 2048, 4096, 8192):
+for d in ([int(a) for a in sys.argv[3:]] or (1024, 2048, 4096, 8192)):
     v, w, sites, _ = moe_inputs_device(0, n, d, 128, E, 128)
     stacks = [ExpertStack(sites[x][0], sites[x][1], sites[x][2], sites[x][3], 128) for x in ("gate", "up", "down")]
     layer = MoELayer.from_stacks(w, *stacks, top_k=2, path="f32")
