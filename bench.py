@@ -40,6 +40,8 @@ CONFIGS = {
     "mx": dict(name="mixtral-8x7b-moe-layer-decode", d_model=4096, d_ff=14336, n_experts=8, top_k=2, batch=64),
     "mx1": dict(name="mixtral-8x7b-moe-layer-decode-b1", d_model=4096, d_ff=14336, n_experts=8, top_k=2, batch=1),
     "mx8": dict(name="mixtral-8x7b-moe-layer-decode-b8", d_model=4096, d_ff=14336, n_experts=8, top_k=2, batch=8),
+    "mxe": dict(name="mixtral-8x7b-moe-layer-decode-embedding-wise", d_model=4096, d_ff=14336, n_experts=8,
+                top_k=2, batch=64, group_size=0),
     "c1": dict(name="c1-moe-layer-cpu-parity", d_model=1024, d_ff=2816, n_experts=8, top_k=2, batch=64),
     "ph": dict(name="phi-3.5-moe-layer-prefill-rotation", d_model=4096, d_ff=6400, n_experts=16, top_k=2,
                batch=4096, rotation=True),
@@ -75,8 +77,8 @@ def layer_bytes(n_active: int, R: int) -> dict:
     weights of the active experts + activations, per layer and for the gate|up
     kernel."""
     d, ff, g = CFG["d_model"], CFG["d_ff"], CFG["group_size"]
-    w_gu = 2 * (ff * d // 2 + ff * (d // g) * 16 * 4)        # gate + up ids + centroids
-    w_dn = d * ff // 2 + d * (ff // g) * 16 * 4
+    w_gu = 2 * (ff * d // 2 + ff * (d // (g or d)) * 16 * 4)  # gate + up ids + centroids (g = 0: g = d_in)
+    w_dn = d * ff // 2 + d * (ff // (g or ff)) * 16 * 4
     gu = n_active * w_gu + R * d + R * 4 + R * ff * 4         # + codes, scales in; hidden out
     dn = n_active * w_dn + R * ff + R * 4 + R * d * 4
     return dict(gate_up=gu, down=dn, layer=gu + dn + d * CFG["n_experts"] * 4)
@@ -159,8 +161,9 @@ def host_layer(seed: int, n: int):
     for _ in range(E):
         mats = []
         for di, do in ((d, ff), (d, ff), (ff, d)):
-            mats.append(((rng.standard_normal((do, di // g, 16), dtype=np.float32) / math.sqrt(di)),
-                         rng.integers(0, 256, (do, di // 2), dtype=np.uint8), g))
+            gs = g or di
+            mats.append(((rng.standard_normal((do, di // gs, 16), dtype=np.float32) / math.sqrt(di)),
+                         rng.integers(0, 256, (do, di // 2), dtype=np.uint8), gs))
         experts.append(mats)
     return v, w, experts
 
@@ -230,7 +233,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": CFG["name"], "d_model": CFG["d_model"], "d_ff": CFG["d_ff"],
-                   "n_experts": E, "top_k": k, "group_size": CFG["group_size"], "batch": n},
+                   "n_experts": E, "top_k": k, "group_size": CFG["group_size"] or "d_in", "batch": n},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -438,7 +441,7 @@ def run_ep(args, rank, world, local):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32",
             "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
             "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
-                       "group_size": g, "batch_per_rank": n, "parallelism": f"ep{world}",
+                       "group_size": g or "d_in", "batch_per_rank": n, "parallelism": f"ep{world}",
                        "experts_per_rank": per, "path": args.path, "layout": args.layout,
                        "l2": "weights > L2, no flush needed", "cuda_graph": graph is not None,
                        "capacity_per_peer": step.cap, **({"capture_error": capture_err} if capture_err else {})},
@@ -578,7 +581,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32",
             "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
             "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
-                       "group_size": g, "batch": n,
+                       "group_size": g or "d_in", "batch": n,
                        "parallelism": (f"replicas{world}" + (f" (ep failed: {args.ep_error})"
                                                              if getattr(args, "ep_error", None) else ""))
                        if world > 1 else "single",
@@ -632,7 +635,7 @@ def main():
     os.dup2(2, 1)
     args = parse()
     CFG.clear()
-    CFG.update(CONFIGS[args.config], group_size=128)
+    CFG.update(dict(CONFIGS[args.config]), group_size=CONFIGS[args.config].get("group_size", 128))
     if args.batch is None:
         args.batch = CFG["batch"]
     if args.config != "mx":

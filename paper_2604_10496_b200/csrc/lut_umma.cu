@@ -53,6 +53,9 @@ namespace cq {
 #ifndef UM_GS4  // chunk streams when >= 4 A stages fit (measured: 4 beats 2 double-buffered)
 #define UM_GS4 4
 #endif
+#ifndef UM_SPLIT_AFREE  // data (full) and A-stage-free (afree) as separate barriers: 0 never, 1 always,
+#define UM_SPLIT_AFREE 2  // 2: prefill geometry, 3 planes only (decode and the 2-plane down GEMM measured slower)
+#endif
 #ifndef UM_LAG  // chunks of data issued ahead of arming (smem ring = A stages + UM_LAG)
 #define UM_LAG 4
 #endif
@@ -125,6 +128,7 @@ struct UmStage {
     static constexpr int LAG = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? UM_LAG : 0;
     static constexpr int NS = NA + LAG;
     static_assert(NS % GS == 0 && NA % GS == 0 && NS * BYTES <= 200 * 1024, "smem ring");
+    static constexpr bool SPLIT_AFREE = UM_SPLIT_AFREE == 1 || (UM_SPLIT_AFREE == 2 && GEO::NT == 128 && P == 3);
 };
 
 // ---------------------------------------------------------------------------
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     constexpr int NT = GEO::NT, CK = GEO::CK, NCB = GEO::NCB;
     constexpr int TPP = NT / 8;       // token tiles per pass
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA];
+    __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA], afree_bar[NA];
     __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
     __shared__ uint32_t tmem_base_sh;
     __shared__ int32_t unit_pre[um::MAX_SEG + 1], seg_off[um::MAX_SEG + 1];
@@ -283,10 +287,13 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
-            u_bar_init(u_smem(&full_bar[s]), LAG > 0 ? 2 : 1);
+            u_bar_init(u_smem(&full_bar[s]), (LAG > 0 && !S::SPLIT_AFREE) ? 2 : 1);
             u_bar_init(u_smem(&empty_bar[s]), 1);
         }
-        for (int s = 0; s < NA; ++s) u_bar_init(u_smem(&afull_bar[s]), 4 * WPS);  // the warps of one stream
+        for (int s = 0; s < NA; ++s) {
+            u_bar_init(u_smem(&afull_bar[s]), 4 * WPS);  // the warps of one stream
+            u_bar_init(u_smem(&afree_bar[s]), 1);         // SPLIT_AFREE: MMAs of the stage's last chunk done
+        }
         // (splitting afull per chunk half, so the MMAs start earlier, measured slower: the extra
         //  tcgen05.wait::st mid-chunk costs more than the overlap gains)
         u_bar_init(u_smem(&accfull_bar), 1);
@@ -308,6 +315,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     // (volatile moves: ptxas would otherwise re-derive them from SR_CgaCtaId in every loop iteration)
     const uint32_t full_a = u_pin(u_smem(&full_bar[0])), empty_a = u_pin(u_smem(&empty_bar[0]));
     const uint32_t afull_a = u_pin(u_smem(&afull_bar[0])), stage_a = u_pin(u_smem(smem));
+    const uint32_t afree_a = u_pin(u_smem(&afree_bar[0]));
 
     if (warp == um::PROD_WARP) {
         // ------------------------------------------------------------ producer (converged warp, elected lane)
@@ -329,7 +337,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 const uint32_t bar = full_a + 8 * s;
                 const uint32_t dst = stage_a + s * S::BYTES;
                 u_bar_expect_elect(bar, GEO::IDS + (new_group ? S::LUT : 0) + ntc16 * GEO::BTILE);
-                if (LAG > 0 && (int)k < NA) u_bar_arrive_elect(bar);  // no chunk k - NA: A stage already free
+                if (LAG > 0 && !S::SPLIT_AFREE && (int)k < NA) u_bar_arrive_elect(bar);  // no chunk k - NA yet
                 u_bulk_elect(dst, ids + ((size_t)x.tile * n_chunks + c) * GEO::IDS, GEO::IDS, bar);
                 if (new_group)
                     u_bulk_elect(dst + GEO::IDS, lut + ((size_t)x.tile * n_groups + grp) * S::LUT, S::LUT, bar);
@@ -373,7 +381,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     }
                 }
                 tc_commit_elect(empty_a + 8 * s);  // frees the smem stage (and with LAG == 0 the A stage)
-                if (LAG > 0) tc_commit_elect(full_a + 8 * ((k + NA) % NS));  // A stage free for chunk k + NA
+                if (S::SPLIT_AFREE)
+                    tc_commit_elect(afree_a + 8 * sa);  // A stage free for chunk k + NA
+                else if (LAG > 0)
+                    tc_commit_elect(full_a + 8 * ((k + NA) % NS));  // A stage free for chunk k + NA
                 if (c == c1 - 1) tc_commit_elect(u_smem(&accfull_bar));
             }
         }
@@ -439,7 +450,20 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                         xsel[2 * q + 1] = hi16(xx);
                     }
                     const uint32_t abase = abase0 + (uint32_t)(ks * S::ACOLS);
-                    if (MERGED) {
+                    if (S::SPLIT_AFREE && MERGED && ks == ks0) {
+                        // the first k-step expands into registers before the A stage is known free: the
+                        // MMAs of this stage's previous chunk (k - NA) overlap its PRMT work
+                        uint32_t v[P][8];
+#pragma unroll
+                        for (int p = 0; p < P; ++p)
+#pragma unroll
+                            for (int cc = 0; cc < 8; ++cc)
+                                v[p][cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
+                        u_bar_wait(afree_a + 8 * sa, ((k / NA) & 1) ^ 1);  // first use of a stage passes at once
+                        tc_fence_after();
+#pragma unroll
+                        for (int p = 0; p < P; ++p) tc_st8(abase + p * 8, v[p]);
+                    } else if (MERGED) {
                         // one 8-column store per plane as soon as it is expanded (keeps the register peak low)
 #pragma unroll
                         for (int p = 0; p < P; ++p) {
@@ -450,6 +474,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                             tc_st8(abase + p * 8, v);
                         }
                     } else {
+                        if (S::SPLIT_AFREE && ks == ks0) {
+                            u_bar_wait(afree_a + 8 * sa, ((k / NA) & 1) ^ 1);
+                            tc_fence_after();
+                        }
 #pragma unroll
                         for (int p = 0; p < P; ++p) {
                             uint32_t v[16];

@@ -41,7 +41,21 @@ __device__ __forceinline__ void u_bar_arrive(uint32_t bar) {
 __device__ __forceinline__ void u_bar_expect(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// UM_WAIT_NS > 0: try_wait with a suspend-time hint, so a waiting warp sleeps
+// until the phase completes (up to the hint) instead of re-issuing the probe.
+#ifndef UM_WAIT_NS
+#define UM_WAIT_NS 0
+#endif
 __device__ __forceinline__ void u_bar_wait(uint32_t bar, uint32_t phase) {
+#if UM_WAIT_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "UW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra UW_%=;\n}" ::"r"(bar),
+        "r"(phase), "n"(UM_WAIT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "UW_%=:\n\t"
@@ -49,6 +63,7 @@ __device__ __forceinline__ void u_bar_wait(uint32_t bar, uint32_t phase) {
         "@!p bra UW_%=;\n}" ::"r"(bar),
         "r"(phase)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void u_bulk(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),

@@ -40,8 +40,12 @@ class ExpertStack:
     centroids: torch.Tensor  # (E, d_out, d_in/g, 16) float32
     d_in: int
     d_out: int
-    group_size: int
+    group_size: int          # 0: embedding-wise (one group per row, g = d_in)
     tc: dict | None = None
+
+    def __post_init__(self):
+        if self.group_size == 0:
+            self.group_size = self.d_in
 
     @classmethod
     def from_packed(cls, pws) -> "ExpertStack":

@@ -46,21 +46,38 @@ def pack_ids_np(ids: np.ndarray) -> np.ndarray:
     return (ids[:, 0::2] | (ids[:, 1::2] << np.uint8(4))).astype(np.uint8)
 
 
-def moe_inputs_host(seed: int, n: int, d: int, ff: int, n_exp: int, g: int, n_shared: int = 0):
+def plant_outliers(v: np.ndarray, channel_scale: float = 8.0, row_scale: float = 50.0) -> np.ndarray:
+    """The planted-outlier activation variant (after
+    generate_calibration, model.py:191-221): max(1, d/16) evenly spaced channels
+    scaled by channel_scale (the pipeline default 8, pipeline.py:59) and max(1,
+    n/50) evenly spaced rows by row_scale; bf16-exact again afterwards."""
+    v = np.array(v, dtype=np.float32, copy=True)
+    n, d = v.shape
+    v[:, np.linspace(0, d - 1, max(1, d // 16)).astype(int)] *= channel_scale
+    v[np.linspace(0, n - 1, max(1, n // 50)).astype(int)] *= row_scale
+    return round_bf16(v)
+
+
+def moe_inputs_host(seed: int, n: int, d: int, ff: int, n_exp: int, g: int, n_shared: int = 0,
+                    outliers: bool = False):
     """Host arrays: v (n,d) f32 (bf16-exact), w_router (d,E) f32, experts =
     [(gate, up, down)] with each site (centroids (d_out, d_in/g, 16) f32,
-    ids_packed (d_out, d_in/2) u8, g)."""
+    ids_packed (d_out, d_in/2) u8, g).  g = 0: embedding-wise groups (g = the
+    site's d_in)."""
     rng = RngState(seed)
     v = round_bf16(rng.stream("moe.v").standard_normal((n, d)).astype(np.float32))
+    if outliers:
+        v = plant_outliers(v)
     w_router = (rng.stream("moe.router").standard_normal((d, n_exp)) / np.sqrt(d)).astype(np.float32)
 
     def expert(tag):
         mats = []
         for site, (di, do) in (("gate", (d, ff)), ("up", (d, ff)), ("down", (ff, d))):
-            cents = (rng.stream(f"{tag}.{site}.c").standard_normal((do, di // g, 16))
+            gs = g or di
+            cents = (rng.stream(f"{tag}.{site}.c").standard_normal((do, di // gs, 16))
                      / np.sqrt(di)).astype(np.float32)
             ids = rng.stream(f"{tag}.{site}.i").integers(0, 16, (do, di)).astype(np.uint8)
-            mats.append((cents, pack_ids_np(ids), g))
+            mats.append((cents, pack_ids_np(ids), gs))
         return mats
 
     experts = [expert(f"moe.e{e}") for e in range(n_exp)]
@@ -88,18 +105,23 @@ def to_device_experts(experts):
     return out
 
 
-def moe_inputs_device(seed: int, n: int, d: int, ff: int, n_exp: int, g: int, n_shared: int = 0):
+def moe_inputs_device(seed: int, n: int, d: int, ff: int, n_exp: int, g: int, n_shared: int = 0,
+                      outliers: bool = False):
     """Same distributions drawn on cuda:0 (torch Philox).  Returns v (n,d) bf16,
-    w_router (d,E) f32 and stacked sites as dicts of device tensors."""
+    w_router (d,E) f32 and stacked sites as dicts of device tensors.  g = 0:
+    embedding-wise groups (ExpertStack takes group_size 0 the same way)."""
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
-    v = torch.randn((n, d), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((n, d), generator=gen, device="cuda")
+    if outliers:
+        v = torch.from_numpy(plant_outliers(v.cpu().numpy())).cuda()
+    v = v.to(torch.bfloat16)
     w_router = torch.randn((d, n_exp), generator=gen, device="cuda") / float(np.sqrt(d))
 
     def stack(ne):
         sites = {}
         for site, (di, do) in (("gate", (d, ff)), ("up", (d, ff)), ("down", (ff, d))):
-            cents = torch.randn((ne, do, di // g, 16), generator=gen, device="cuda") / float(np.sqrt(di))
+            cents = torch.randn((ne, do, di // (g or di), 16), generator=gen, device="cuda") / float(np.sqrt(di))
             ids = torch.randint(0, 256, (ne, do, di // 2), generator=gen, device="cuda",
                                 dtype=torch.int32).to(torch.uint8)
             sites[site] = (ids, cents, di, do)

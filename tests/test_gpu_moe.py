@@ -218,6 +218,25 @@ def test_tc_decode_route_mode(n, E, k):
     assert torch.equal(layer(v), out)
 
 
+@pytest.mark.parametrize("g", [0, 128])
+@pytest.mark.parametrize("outliers", [False, True])
+def test_tc_layer_embedding_wise_and_outliers_vs_oracle(g, outliers):
+    """SURVEY §8(d)'s second group-size row (g = d_in, one centroid set per
+    output row) and the planted-outlier activations (8x channels, 50x rows):
+    the tensor-core layer against the composed CPU oracle."""
+    n, d, ff, E, k = 48, 256, 384, 8, 2
+    v, w, experts, _ = moe_inputs_host(13, n, d, ff, E, g, outliers=outliers)
+    if g == 0:
+        assert [m[2] for m in experts[0]] == [d, d, ff]
+    layer = MoELayer(w, to_device_experts(experts), k, path="tc")
+    layer.prepare_tc()
+    out = layer(torch.from_numpy(v).cuda()).cpu().numpy()
+    want = oracle.moe_layer_fast(v, w, experts, k)
+    assert o.relative_error(out, want) <= LAYER_TOL
+    ordered = layer(torch.from_numpy(v).cuda(), path="ordered").cpu().numpy()
+    assert o.relative_error(ordered, want) <= 1e-5
+
+
 @pytest.mark.parametrize("n", [4, 60, 140])
 def test_silu_requant_cluster_rows(n):
     """Long hidden rows (ff = 14336) at decode row counts take the cluster
