@@ -42,6 +42,10 @@ CONFIGS = {
     "mx8": dict(name="mixtral-8x7b-moe-layer-decode-b8", d_model=4096, d_ff=14336, n_experts=8, top_k=2, batch=8),
     "mxe": dict(name="mixtral-8x7b-moe-layer-decode-embedding-wise", d_model=4096, d_ff=14336, n_experts=8,
                 top_k=2, batch=64, group_size=0),
+    "mx3": dict(name="mixtral-8x7b-moe-layer-decode-w3", d_model=4096, d_ff=14336, n_experts=8, top_k=2,
+                batch=64, kc=8),
+    "mx2": dict(name="mixtral-8x7b-moe-layer-decode-w2", d_model=4096, d_ff=14336, n_experts=8, top_k=2,
+                batch=64, kc=4),
     "c1": dict(name="c1-moe-layer-cpu-parity", d_model=1024, d_ff=2816, n_experts=8, top_k=2, batch=64),
     "ph": dict(name="phi-3.5-moe-layer-prefill-rotation", d_model=4096, d_ff=6400, n_experts=16, top_k=2,
                batch=4096, rotation=True),
@@ -357,7 +361,7 @@ def run_ep(args, rank, world, local):
     from paper_2604_10496_b200.synthetic import moe_inputs_device
 
     n, d, ff, E, k, g = args.batch, CFG["d_model"], CFG["d_ff"], CFG["n_experts"], CFG["top_k"], CFG["group_size"]
-    _, w, sites, _ = moe_inputs_device(args.seed, 1, d, ff, E, g)
+    _, w, sites, _ = moe_inputs_device(args.seed, 1, d, ff, E, g, kc=CFG.get("kc", 16))
     begin, per = expert_range(E, world, rank)
     stacks = [ExpertStack(sites[s][0][begin:begin + per].contiguous(), sites[s][1][begin:begin + per].contiguous(),
                           sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
@@ -485,7 +489,8 @@ def run_ours(args):
 
     n, d, ff, E, k, g = args.batch, CFG["d_model"], CFG["d_ff"], CFG["n_experts"], CFG["top_k"], CFG["group_size"]
     n_sh = CFG.get("n_shared", 0)
-    v, w, sites, sh_sites = moe_inputs_device(args.seed + 17 * rank, n, d, ff, E, g, n_shared=n_sh)
+    v, w, sites, sh_sites = moe_inputs_device(args.seed + 17 * rank, n, d, ff, E, g, n_shared=n_sh,
+                                              kc=CFG.get("kc", 16))
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
     shared = (tuple(ExpertStack(sh_sites[s][0], sh_sites[s][1], sh_sites[s][2], sh_sites[s][3], g)
                     for s in ("gate", "up", "down")) if n_sh else None)
@@ -581,7 +586,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32",
             "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
             "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
-                       "group_size": g or "d_in", "batch": n,
+                       "group_size": g or "d_in", "codebook_k": CFG.get("kc", 16), "batch": n,
                        "parallelism": (f"replicas{world}" + (f" (ep failed: {args.ep_error})"
                                                              if getattr(args, "ep_error", None) else ""))
                        if world > 1 else "single",

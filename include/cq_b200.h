@@ -117,7 +117,10 @@ typedef struct {
                                   kernel; signed P/Q digit slices / unsigned OR-merged digits) */
 } cq_expert_site;
 
-enum { CQ_TC_MMA16 = 0, CQ_TC_UMMA128 = 1, CQ_TC_UMMA128U = 2 };
+/* CQ_TC_UMMA128U8: the data of CQ_TC_UMMA128U, declared to have every id < 8
+   (codebooks with K <= 8, W3/W2): one PRMT per 4 operand bytes instead of three
+   instructions.  The caller guarantees the ids; the preparation is identical. */
+enum { CQ_TC_MMA16 = 0, CQ_TC_UMMA128 = 1, CQ_TC_UMMA128U = 2, CQ_TC_UMMA128U8 = 3 };
 
 typedef struct {
     int64_t d_model, d_ff, n_experts, top_k;

@@ -21,8 +21,9 @@ LIB_PATH = os.environ.get("CQ_B200_LIB") or os.path.join(_HERE, "libcq_b200.so")
 CQ_OK, CQ_ERR_SHAPE, CQ_ERR_CONFIG, CQ_ERR_DIVERGENCE, CQ_ERR_CUDA, CQ_ERR_UNSUPPORTED = range(6)
 CQ_DTYPE_F32, CQ_DTYPE_BF16 = 0, 1
 CQ_PATH_AUTO, CQ_PATH_F32, CQ_PATH_TC, CQ_PATH_ORDERED = 0, 1, 2, 3
-CQ_TC_MMA16, CQ_TC_UMMA128, CQ_TC_UMMA128U = 0, 1, 2
-TC_LAYOUTS = {"mma16": CQ_TC_MMA16, "umma128": CQ_TC_UMMA128, "umma128u": CQ_TC_UMMA128U}
+CQ_TC_MMA16, CQ_TC_UMMA128, CQ_TC_UMMA128U, CQ_TC_UMMA128U8 = 0, 1, 2, 3
+TC_LAYOUTS = {"mma16": CQ_TC_MMA16, "umma128": CQ_TC_UMMA128, "umma128u": CQ_TC_UMMA128U,
+              "umma128u8": CQ_TC_UMMA128U8}
 WS_NAMES = ("codes", "scales", "logits", "selected", "weights", "counts", "offsets",
             "perm_token", "perm_slot", "inv", "codes_perm", "scales_perm", "hidden",
             "hcodes", "hscales", "fout", "rotated", "shared", "codes_frag", "hcodes_frag", "rot_act",

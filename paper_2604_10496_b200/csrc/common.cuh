@@ -142,6 +142,10 @@ struct RoutePerm {
     int32_t *offsets = nullptr, *counts = nullptr, *perm_token = nullptr, *perm_slot = nullptr, *inv = nullptr;
 };
 
+// Tensor-core layouts: UMMA128U8 is UMMA128U's data with every id < 8.
+inline bool umma_merged(int64_t layout) { return layout == CQ_TC_UMMA128U || layout == CQ_TC_UMMA128U8; }
+inline int64_t umma_family(int64_t layout) { return layout == CQ_TC_UMMA128U8 ? CQ_TC_UMMA128U : layout; }
+
 // Optional inputs of the tcgen05 grouped GEMM's B-operand build (lut_umma.cu).
 struct UmmaIn {
     const int32_t *perm = nullptr;      // gather: segment row r reads codes[perm[r]] (codes per token)

@@ -476,7 +476,7 @@ cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int6
         set_error("lut8_prepare: planes must be 2 or 3");
         return CQ_ERR_CONFIG;
     }
-    if (layout < CQ_TC_MMA16 || layout > CQ_TC_UMMA128U) {
+    if (layout < CQ_TC_MMA16 || layout > CQ_TC_UMMA128U8) {
         set_error("lut8_prepare: unknown layout");
         return CQ_ERR_CONFIG;
     }
@@ -486,13 +486,13 @@ cq_status lut8_prepare(const uint8_t *ids, const float *cent, int64_t rows, int6
     }
     if (rows == 0) return CQ_OK;
     const int64_t n_groups = d_in / g;
-    const bool um = layout == CQ_TC_UMMA128U;  // unsigned base-128 digits (lut7_kernel)
+    const bool um = umma_merged(layout);  // unsigned base-128 digits (lut7_kernel)
     const int64_t mb = um ? (1LL << (7 * planes - 1)) - 1 : (planes == 3 ? TC_M3 : TC_M2);
     rowscale_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(cent, rows, n_groups * 16,
                                                                  (double)mb, rowscale);
     CQ_TRY(check_launch("rowscale"));
     int8_t *lut16 = tc_lut;
-    const bool relayout = layout == CQ_TC_UMMA128 || layout == CQ_TC_UMMA128U;
+    const bool relayout = layout == CQ_TC_UMMA128 || umma_merged(layout);
     if (relayout) {
         if (cudaMallocAsync(&lut16, rows * n_groups * planes * 16, st) != cudaSuccess) {
             set_error("lut8_prepare: scratch alloc failed");
@@ -552,7 +552,7 @@ extern "C" cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, co
     site.tc_planes = planes;
     site.tc_layout = layout;
     void *scratch = nullptr;
-    const bool um = layout == CQ_TC_UMMA128 || layout == CQ_TC_UMMA128U;
+    const bool um = layout == CQ_TC_UMMA128 || umma_merged(layout);
     const int64_t frag_bytes = um ? umma_b_bytes(n, d_in) : ceil_div(n, 8) * 8 * d_in;
     if (cudaMallocAsync(&scratch, frag_bytes + 256, st) != cudaSuccess) {
         set_error("lut_gemm_tc: scratch alloc failed");

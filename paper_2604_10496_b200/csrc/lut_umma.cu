@@ -211,7 +211,10 @@ __device__ __forceinline__ UmUnit um_unit(const UmWork &w, int64_t seg_first, in
 }
 
 // grid: (#SMs); n_mat = 2 computes gate (ids0 ... out0) and up (ids1 ... out1).
-template <int P, bool MERGED, class GEO>
+// NARROW (merged layout, every id < 8: codebooks with K <= 8): the 8 table
+// bytes of entries 0..7 sit in L.x, L.y, so one PRMT yields 4 A bytes (no
+// second PRMT over entries 8..15, no merge).
+template <int P, bool MERGED, class GEO, bool NARROW = false>
 __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
     const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int n_seg, int64_t seg_first,
@@ -458,7 +461,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                         for (int p = 0; p < P; ++p)
 #pragma unroll
                             for (int cc = 0; cc < 8; ++cc)
-                                v[p][cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
+                                v[p][cc] = NARROW ? u_prmt(L[p].x, L[p].y, sel[cc])
+                                                  : u_merge(u_prmt(L[p].x, L[p].y, sel[cc]),
+                                                            u_prmt(L[p].z, L[p].w, xsel[cc]));
                         u_bar_wait(afree_a + 8 * sa, ((k / NA) & 1) ^ 1);  // first use of a stage passes at once
                         tc_fence_after();
 #pragma unroll
@@ -470,7 +475,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                             uint32_t v[8];
 #pragma unroll
                             for (int cc = 0; cc < 8; ++cc)
-                                v[cc] = u_merge(u_prmt(L[p].x, L[p].y, sel[cc]), u_prmt(L[p].z, L[p].w, xsel[cc]));
+                                v[cc] = NARROW ? u_prmt(L[p].x, L[p].y, sel[cc])
+                                               : u_merge(u_prmt(L[p].x, L[p].y, sel[cc]),
+                                                         u_prmt(L[p].z, L[p].w, xsel[cc]));
                             tc_st8(abase + p * 8, v);
                         }
                     } else {
@@ -792,7 +799,7 @@ int64_t umma_b_bytes(int64_t rows, int64_t d_in) {
     return umma_cnt_off(rows, d_in) + ceil_div((int64_t)umma_grid() * 4, 256) * 256;
 }
 
-template <int P, bool MERGED, class GEO>
+template <int P, bool MERGED, class GEO, bool NARROW = false>
 cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *sums,
                       const int32_t *offsets, int64_t n_seg, int64_t seg_first, const cq_expert_site *a, float *out_a,
                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, int32_t *part,
@@ -800,10 +807,11 @@ cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales,
     static bool attr = false;
     const size_t smem = umma_smem<P, MERGED, GEO>();
     if (!attr) {
-        cudaFuncSetAttribute(lut_umma_kernel<P, MERGED, GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lut_umma_kernel<P, MERGED, GEO, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         attr = true;
     }
-    launch_pdl(lut_umma_kernel<P, MERGED, GEO>, umma_grid(), um::THREADS, smem, st, 
+    launch_pdl(lut_umma_kernel<P, MERGED, GEO, NARROW>, umma_grid(), um::THREADS, smem, st,
         bfrag, n_tiles, scales, sums, offsets, (int)n_seg, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
         b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, b ? 2 : 1, (int)d_in,
         (int)d_out, (int)a->group_size, part, cnt);
@@ -815,22 +823,27 @@ cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, c
                        int64_t seg_first, int64_t rows, const cq_expert_site *a, float *out_a,
                        const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, const UmmaIn &in,
                        cudaStream_t st) {
-    const bool merged = a->tc_layout == CQ_TC_UMMA128U;
+    const bool merged = umma_merged(a->tc_layout);
+    // narrow lookup only when every matrix of the launch has ids < 8 (the data is that of UMMA128U)
+    const bool narrow = a->tc_layout == CQ_TC_UMMA128U8 && (b == nullptr || b->tc_layout == CQ_TC_UMMA128U8);
     const int64_t tiles = umma_b_tiles(rows);
     int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in)) : nullptr;
     int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
     int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
     CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), in, scales, offsets + n_seg, st));
     if (in.gathers()) scales = in.scales_out;  // per segment row from here on
-#define CQ_UMMA(P_, M_)                                                                                   \
-    launch_umma<P_, M_, GEO>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, \
-                             d_out, part, cnt, st)
-    if (merged) {
-        if (a->tc_planes == 3) return CQ_UMMA(3, true);
-        if (a->tc_planes == 2) return CQ_UMMA(2, true);
+#define CQ_UMMA(P_, M_, N_)                                                                                   \
+    launch_umma<P_, M_, GEO, N_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, \
+                                 d_out, part, cnt, st)
+    if (merged && narrow) {
+        if (a->tc_planes == 3) return CQ_UMMA(3, true, true);
+        if (a->tc_planes == 2) return CQ_UMMA(2, true, true);
+    } else if (merged) {
+        if (a->tc_planes == 3) return CQ_UMMA(3, true, false);
+        if (a->tc_planes == 2) return CQ_UMMA(2, true, false);
     } else if constexpr (GEO::NT == 32) {  // the signed layouts exist in the decode geometry only
-        if (a->tc_planes == 3) return CQ_UMMA(3, false);
-        if (a->tc_planes == 2) return CQ_UMMA(2, false);
+        if (a->tc_planes == 3) return CQ_UMMA(3, false, false);
+        if (a->tc_planes == 2) return CQ_UMMA(2, false, false);
     }
 #undef CQ_UMMA
     set_error("tcgen05 path: planes must be 2 or 3");
@@ -853,7 +866,7 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         set_error("tcgen05 path: paired matrices must share planes and group size");
         return CQ_ERR_CONFIG;
     }
-    if (b && b->tc_layout != a->tc_layout) {
+    if (b && umma_family(b->tc_layout) != umma_family(a->tc_layout)) {
         set_error("tcgen05 path: paired matrices must share the layout");
         return CQ_ERR_CONFIG;
     }
@@ -862,7 +875,7 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         return CQ_ERR_UNSUPPORTED;
     }
     // prefill geometry (128-token passes, merged layout only) when segments are long
-    if (umma_prefill(rows, n_seg) && a->tc_layout == CQ_TC_UMMA128U && getenv("CQ_UMMA_NO_PREFILL") == nullptr)
+    if (umma_prefill(rows, n_seg) && umma_merged(a->tc_layout) && getenv("CQ_UMMA_NO_PREFILL") == nullptr)
         return lut_umma_geo<UmPrefill>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b,
                                        d_in, d_out, in, st);
     return lut_umma_geo<UmDecode>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b, d_in,

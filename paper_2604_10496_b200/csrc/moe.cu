@@ -552,8 +552,9 @@ cq_status validate_desc(const cq_moe_desc *d) {
 
 int choose_path(const cq_moe_desc *d) {
     if (d->path != CQ_PATH_AUTO) return d->path;
-    const bool tc = d->gate.tc_lut && d->up.tc_lut && d->down.tc_lut && d->gate.tc_layout == d->up.tc_layout &&
-                    d->up.tc_layout == d->down.tc_layout &&
+    const bool tc = d->gate.tc_lut && d->up.tc_lut && d->down.tc_lut &&
+                    umma_family(d->gate.tc_layout) == umma_family(d->up.tc_layout) &&
+                    umma_family(d->up.tc_layout) == umma_family(d->down.tc_layout) &&
                     tc_path_ok(d->d_model, d->d_ff, d->gate.group_size) &&
                     tc_path_ok(d->d_ff, d->d_model, d->down.group_size);
     if (tc) return CQ_PATH_TC;
@@ -579,7 +580,7 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
         if (ev) cudaEventRecord(ev[1], st);
         // the re-quantizer writes the down GEMM's row sums straight into its B buffer
         UmmaIn hin;
-        hin.sums_ready = down.tc_layout == CQ_TC_UMMA128U;
+        hin.sums_ready = umma_merged(down.tc_layout);
         int32_t *hsums = hin.sums_ready ? umma_row_sums(reinterpret_cast<int8_t *>(frag_h), rows, ff) : nullptr;
         CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, offsets + n_seg, st, hsums));
         if (ev) cudaEventRecord(ev[2], st);

@@ -82,7 +82,7 @@ class ExpertStack:
             s.tc_lut = self.tc["lut"].data_ptr()
             s.tc_rowscale = self.tc["rowscale"].data_ptr()
             s.tc_planes = self.tc["planes"]
-            s.tc_layout = _lib.TC_LAYOUTS[self.tc["layout"]]
+            s.tc_layout = _lib.TC_LAYOUTS[self.tc["kernel_layout"]]
         return s
 
 

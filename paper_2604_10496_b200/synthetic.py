@@ -106,10 +106,12 @@ def to_device_experts(experts):
 
 
 def moe_inputs_device(seed: int, n: int, d: int, ff: int, n_exp: int, g: int, n_shared: int = 0,
-                      outliers: bool = False):
+                      outliers: bool = False, kc: int = 16):
     """Same distributions drawn on cuda:0 (torch Philox).  Returns v (n,d) bf16,
     w_router (d,E) f32 and stacked sites as dicts of device tensors.  g = 0:
-    embedding-wise groups (ExpertStack takes group_size 0 the same way)."""
+    embedding-wise groups (ExpertStack takes group_size 0 the same way).  kc:
+    centroids per group (K; ids < K, centroids zero-padded to 16 as
+    pack_weights does, lutgemm.py:109-110)."""
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
     v = torch.randn((n, d), generator=gen, device="cuda")
@@ -122,8 +124,14 @@ def moe_inputs_device(seed: int, n: int, d: int, ff: int, n_exp: int, g: int, n_
         sites = {}
         for site, (di, do) in (("gate", (d, ff)), ("up", (d, ff)), ("down", (ff, d))):
             cents = torch.randn((ne, do, di // (g or di), 16), generator=gen, device="cuda") / float(np.sqrt(di))
-            ids = torch.randint(0, 256, (ne, do, di // 2), generator=gen, device="cuda",
-                                dtype=torch.int32).to(torch.uint8)
+            if kc < 16:
+                cents[..., kc:] = 0.0
+                lo = torch.randint(0, kc, (ne, do, di // 2), generator=gen, device="cuda", dtype=torch.int32)
+                hi = torch.randint(0, kc, (ne, do, di // 2), generator=gen, device="cuda", dtype=torch.int32)
+                ids = (lo | (hi << 4)).to(torch.uint8)
+            else:
+                ids = torch.randint(0, 256, (ne, do, di // 2), generator=gen, device="cuda",
+                                    dtype=torch.int32).to(torch.uint8)
             sites[site] = (ids, cents, di, do)
         return sites
 

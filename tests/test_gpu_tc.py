@@ -192,3 +192,71 @@ def test_a8_codes_tensor_core_vs_reference_gemm(layout, n, d_in, d_out, g):
     qa = QuantizedActivations(torch.from_numpy(codes).cuda(), torch.from_numpy(scales).cuda(), 8)
     got = lut_gemm_tc(qa, pw, 3, layout).cpu().numpy()
     assert o.relative_error(got, want) <= 2e-6
+
+
+def _pw_k(rng, d_out, d_in, g, kc):
+    """A K = kc codebook in the reference's packed format (centroids zero-padded to 16)."""
+    cent = (rng.standard_normal((d_out, d_in // g, 16)) * 0.05).astype(np.float32)
+    cent[:, :, kc:] = 0.0
+    ids = rng.integers(0, kc, (d_out, d_in)).astype(np.uint8)
+    packed = (ids[:, 0::2] | (ids[:, 1::2] << 4)).astype(np.uint8)
+    return cent, packed, PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(packed), d_in, g)
+
+
+@pytest.mark.parametrize("kc", [4, 8])
+@pytest.mark.parametrize("n,d_in,d_out,planes", [(9, 1024, 512, 3), (300, 2048, 768, 3), (40, 1024, 256, 2)])
+def test_narrow_codebooks_single_prmt_bitwise_equals_wide(monkeypatch, kc, n, d_in, d_out, planes):
+    """K <= 8 codebooks (W3 / W2): prepare_tc selects the
+    single-PRMT lookup (umma128u8) from the data; on the same prepared tables it
+    is bitwise equal to the 16-entry lookup, and within the plane tolerance of
+    the ordered reference GEMM."""
+    rng = np.random.default_rng(kc * 100 + n)
+    cent, packed, pw = _pw_k(rng, d_out, d_in, 128, kc)
+    codes = rng.integers(-8, 8, (n, d_in)).astype(np.int8)
+    scales = (rng.random(n) + 0.5).astype(np.float32)
+    qa = QuantizedActivations(torch.from_numpy(codes).cuda(), torch.from_numpy(scales).cuda(), 4)
+    pw.prepare_tc(planes, "umma128u")
+    assert pw.tc["kernel_layout"] == "umma128u8"
+    narrow = lut_gemm_tc(qa, pw, planes, "umma128u")
+    monkeypatch.setenv("CQ_NARROW", "0")
+    _, _, wide_pw = _pw_k(np.random.default_rng(kc * 100 + n), d_out, d_in, 128, kc)
+    wide_pw.prepare_tc(planes, "umma128u")
+    assert wide_pw.tc["kernel_layout"] == "umma128u"
+    wide = lut_gemm_tc(qa, wide_pw, planes, "umma128u")
+    assert torch.equal(narrow, wide)
+    want = oracle.c_lut_gemm(codes, scales, packed, cent, 128)
+    assert o.relative_error(narrow.cpu().numpy(), want) <= (2e-6 if planes == 3 else 2e-4)
+
+
+def test_narrow_ids_detection_rejects_wide_codebooks():
+    rng = np.random.default_rng(3)
+    _, _, pw = _pw_k(rng, 128, 256, 128, 8)
+    ids = pw.ids_packed.clone()
+    ids[5, 7] |= 0x80  # one id 8 or more
+    pw2 = PackedClusteredWeights(pw.centroids, ids, 256, 128)
+    pw2.prepare_tc(3, "umma128u")
+    assert pw2.tc["kernel_layout"] == "umma128u"
+
+
+@pytest.mark.parametrize("kc", [4, 8])
+def test_w3_w2_moe_layer_tc_vs_oracle_and_wide(monkeypatch, kc):
+    """A MoE layer whose codebooks all have K = kc: the narrow kernels for
+    gate|up and down, against the composed CPU oracle and bitwise against the
+    16-entry lookup."""
+    n, d, ff, E, k, g = 40, 512, 384, 8, 2, 128
+    v, w, sites, _ = moe_inputs_device(kc + 5, n, d, ff, E, g, kc=kc)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
+    layer.prepare_tc()
+    assert all(s.tc["kernel_layout"] == "umma128u8" for s in stacks)
+    out = layer(v).clone()
+    monkeypatch.setenv("CQ_NARROW", "0")
+    stacks_w = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    wide = MoELayer.from_stacks(w, *stacks_w, top_k=k, path="tc")
+    wide.prepare_tc()
+    assert all(s.tc["kernel_layout"] == "umma128u" for s in stacks_w)
+    assert torch.equal(wide(v), out)
+    host = [[(sites[s][1][e].cpu().numpy(), sites[s][0][e].cpu().numpy(), g) for s in ("gate", "up", "down")]
+            for e in range(E)]
+    want = oracle.moe_layer_fast(v.float().cpu().numpy(), w.cpu().numpy(), host, k)
+    assert o.relative_error(out.cpu().numpy(), want) <= 1e-2
