@@ -464,6 +464,12 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                                 v[p][cc] = NARROW ? u_prmt(L[p].x, L[p].y, sel[cc])
                                                   : u_merge(u_prmt(L[p].x, L[p].y, sel[cc]),
                                                             u_prmt(L[p].z, L[p].w, xsel[cc]));
+                        // pin the values: the PRMTs must run before the wait (register-only code may
+                        // otherwise sink past the volatile barrier probe)
+#pragma unroll
+                        for (int p = 0; p < P; ++p)
+#pragma unroll
+                            for (int cc = 0; cc < 8; ++cc) asm volatile("" : "+r"(v[p][cc]));
                         u_bar_wait(afree_a + 8 * sa, ((k / NA) & 1) ^ 1);  // first use of a stage passes at once
                         tc_fence_after();
 #pragma unroll
@@ -560,11 +566,20 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 for (int c2 = 0; c2 < 8; ++c2) {
                     const int64_t tok = x.j0 * 8 + cbi + c2;
                     if (tok < x.rb || tok >= x.re) continue;
-                    const double base = MERGED ? 128.0 : 255.0;
-                    double sum = (double)acc[P - 1][c2];
+                    double sum;
+                    if (MERGED) {
+                        // exact integer digit sum (|.| < 2^39) in int64, one conversion: the same double
+                        // as summing converted planes, at a third of the fp64-pipe work
+                        int64_t s64 = (int64_t)acc[P - 1][c2];
 #pragma unroll
-                    for (int p = P - 2; p >= 0; --p) sum = sum * base + (double)acc[p][c2];
-                    if (MERGED) sum -= (double)(1LL << (7 * P - 1)) * (double)tqsum[c2];
+                        for (int p = P - 2; p >= 0; --p) s64 = s64 * 128 + (int64_t)acc[p][c2];
+                        s64 -= (int64_t)tqsum[c2] << (7 * P - 1);
+                        sum = (double)s64;
+                    } else {
+                        sum = (double)acc[P - 1][c2];
+#pragma unroll
+                        for (int p = P - 2; p >= 0; --p) sum = sum * 255.0 + (double)acc[p][c2];
+                    }
                     const float v2 = (float)(sum * (double)rscale);
                     out[tok * d_out + (int64_t)x.rt * 128 + row] = __fmul_rn(v2, tscale[c2]);
                 }
@@ -785,11 +800,20 @@ static int64_t umma_sums_off(int64_t rows, int64_t d_in) { return umma_b_tiles(r
 static int64_t umma_part_off(int64_t rows, int64_t d_in) {
     return umma_sums_off(rows, d_in) + ceil_div(rows * 4, 256) * 256;
 }
-// Prefill geometry when the segments average >= 64 rows (and there are >= 256 rows).
-static bool umma_prefill(int64_t rows, int64_t n_seg) { return rows >= 256 && rows >= 64 * n_seg; }
+// Prefill geometry when the segments average >= 64 rows (tools/geometry_sweep.py).
+static int64_t umma_prefill_min() {  // CQ_UMMA_PREFILL_MIN overrides (experiments)
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *e = getenv("CQ_UMMA_PREFILL_MIN");
+        v = e ? atoll(e) : 64;  // one 4096x28672 expert: 64 rows 72 vs 83 us, 128 rows 93 vs 140 us
+    }
+    return v;
+}
+static bool umma_prefill(int64_t rows, int64_t n_seg) { return rows >= umma_prefill_min() && rows >= 64 * n_seg; }
 // The scratch is sized for the largest geometry `rows` can select.
 static int64_t umma_part_words(int64_t rows) {
-    return rows >= 256 ? (UmPrefill::PART_WORDS > UmDecode::PART_WORDS ? UmPrefill::PART_WORDS : UmDecode::PART_WORDS)
+    return rows >= umma_prefill_min() ? (UmPrefill::PART_WORDS > UmDecode::PART_WORDS ? UmPrefill::PART_WORDS
+                                                                                      : UmDecode::PART_WORDS)
                        : UmDecode::PART_WORDS;
 }
 static int64_t umma_cnt_off(int64_t rows, int64_t d_in) {

@@ -143,7 +143,9 @@ def test_mixtral_decode_tc_vs_ordered(layout):
 
 
 @pytest.mark.parametrize("n,d_in,d_out,g,planes", [(256, 1024, 512, 128, 3), (300, 2048, 768, 128, 2),
-                                                   (777, 1024, 1408, 256, 3), (1024, 4096, 256, 128, 3)])
+                                                   (777, 1024, 1408, 256, 3), (1024, 4096, 256, 128, 3),
+                                                   (64, 1024, 512, 128, 3), (96, 2048, 384, 128, 2),
+                                                   (128, 4096, 1024, 128, 3)])
 def test_prefill_geometry_bitwise_equals_decode(monkeypatch, n, d_in, d_out, g, planes):
     """Long segments take the prefill geometry (128-token passes, 64-column
     chunks).  Both geometries accumulate exact int32 digit products, so the
