@@ -800,20 +800,26 @@ static int64_t umma_sums_off(int64_t rows, int64_t d_in) { return umma_b_tiles(r
 static int64_t umma_part_off(int64_t rows, int64_t d_in) {
     return umma_sums_off(rows, d_in) + ceil_div(rows * 4, 256) * 256;
 }
-// Prefill geometry when the segments average >= 64 rows (tools/geometry_sweep.py).
 static int64_t umma_prefill_min() {  // CQ_UMMA_PREFILL_MIN overrides (experiments)
     static int64_t v = -1;
     if (v < 0) {
         const char *e = getenv("CQ_UMMA_PREFILL_MIN");
-        v = e ? atoll(e) : 64;  // one 4096x28672 expert: 64 rows 72 vs 83 us, 128 rows 93 vs 140 us
+        v = e ? atoll(e) : 96;
     }
     return v;
 }
-static bool umma_prefill(int64_t rows, int64_t n_seg) { return rows >= umma_prefill_min() && rows >= 64 * n_seg; }
+// 128-token passes pay when segments are long and the decode geometry would have many
+// chunk iterations per CTA (tools/geometry_sweep.py: one 4096x28672 expert at 128 rows 93 vs
+// 140 us, at 32 rows 62 vs 55 us; a 2048x1536 expert at 96 rows 34 vs 23 us).  `rows` is a
+// bound (expert parallelism passes its slot capacity, ~2x the routed rows), hence 96 per segment.
+static bool umma_prefill(int64_t rows, int64_t n_seg, int64_t d_in, int64_t d_out, int mats) {
+    if (rows < umma_prefill_min() * n_seg) return false;
+    const int64_t decode_iters = ceil_div(rows / n_seg, 32) * n_seg * (d_out / 128) * mats * (d_in / 128);
+    return decode_iters >= 32LL * umma_grid();
+}
 // The scratch is sized for the largest geometry `rows` can select.
 static int64_t umma_part_words(int64_t rows) {
-    return rows >= umma_prefill_min() ? (UmPrefill::PART_WORDS > UmDecode::PART_WORDS ? UmPrefill::PART_WORDS
-                                                                                      : UmDecode::PART_WORDS)
+    return rows >= 64 ? (UmPrefill::PART_WORDS > UmDecode::PART_WORDS ? UmPrefill::PART_WORDS : UmDecode::PART_WORDS)
                        : UmDecode::PART_WORDS;
 }
 static int64_t umma_cnt_off(int64_t rows, int64_t d_in) {
@@ -899,7 +905,11 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         return CQ_ERR_UNSUPPORTED;
     }
     // prefill geometry (128-token passes, merged layout only) when segments are long
-    if (umma_prefill(rows, n_seg) && umma_merged(a->tc_layout) && getenv("CQ_UMMA_NO_PREFILL") == nullptr)
+    // CQ_UMMA_GEOMETRY=prefill|decode forces one (tests; prefill needs rows >= 64 for its scratch)
+    const char *geo = getenv("CQ_UMMA_GEOMETRY");
+    const bool force_pf = geo != nullptr && geo[0] == 'p' && rows >= 64;
+    const bool force_dc = (geo != nullptr && geo[0] == 'd') || getenv("CQ_UMMA_NO_PREFILL") != nullptr;
+    if (umma_merged(a->tc_layout) && !force_dc && (force_pf || umma_prefill(rows, n_seg, d_in, d_out, b ? 2 : 1)))
         return lut_umma_geo<UmPrefill>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b,
                                        d_in, d_out, in, st);
     return lut_umma_geo<UmDecode>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b, d_in,

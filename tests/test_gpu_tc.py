@@ -156,8 +156,9 @@ def test_prefill_geometry_bitwise_equals_decode(monkeypatch, n, d_in, d_out, g, 
     codes = rng.integers(-8, 8, (n, d_in)).astype(np.int8)
     scales = (0.5 + rng.random(n)).astype(np.float32)
     qa = QuantizedActivations(torch.from_numpy(codes).cuda(), torch.from_numpy(scales).cuda(), 4)
+    monkeypatch.setenv("CQ_UMMA_GEOMETRY", "prefill")
     pre = lut_gemm_tc(qa, pw, planes, "umma128u").clone()
-    monkeypatch.setenv("CQ_UMMA_NO_PREFILL", "1")
+    monkeypatch.setenv("CQ_UMMA_GEOMETRY", "decode")
     dec = lut_gemm_tc(qa, pw, planes, "umma128u").clone()
     torch.cuda.synchronize()
     assert torch.equal(pre, dec)
@@ -173,8 +174,9 @@ def test_prefill_moe_layer_bitwise_equals_decode(monkeypatch):
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
     layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
     layer.prepare_tc()
+    monkeypatch.setenv("CQ_UMMA_GEOMETRY", "prefill")
     pre = layer(v).clone()
-    monkeypatch.setenv("CQ_UMMA_NO_PREFILL", "1")
+    monkeypatch.setenv("CQ_UMMA_GEOMETRY", "decode")
     dec = layer(v).clone()
     torch.cuda.synchronize()
     assert torch.equal(pre, dec)

@@ -1,7 +1,7 @@
 """Decode (32-token passes) vs prefill (128-token passes) geometry of the
 tcgen05 LUT GEMM on one expert's gate|up shape, over the routed row count
-(expert parallelism grows rows per expert with the GPU count).  CQ_UMMA_NO_PREFILL
-forces the decode geometry; run once with and once without it.
+(expert parallelism grows rows per expert with the GPU count).  CQ_UMMA_GEOMETRY=decode|prefill
+forces one geometry; run once with each and once without.
 
     python tools/geometry_sweep.py [d_in d_out]
 """
