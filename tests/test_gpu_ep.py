@@ -141,6 +141,26 @@ def test_ep_step_slots_match_single_gpu_layer(world, n_tok, E, k, path):
     assert torch.equal(got, want)
 
 
+@pytest.mark.parametrize("geometry", ["prefill", "decode"])
+@pytest.mark.parametrize("world,n_tok", [(4, 48), (8, 32)])
+def test_ep_step_rank_gemm_geometries(monkeypatch, geometry, world, n_tok):
+    """The per-rank expert GEMMs with the slot capacity as the row bound and the
+    routed row count on the device, in either geometry (4 and 8 GPUs take the
+    prefill geometry at Mixtral size): bitwise equal to the single-GPU layer."""
+    E, k, d, ff, g = 8, 2, 1024, 1536, 128
+    v, w, sites, _ = moe_inputs_device(29 + world, n_tok * world, d, ff, E, g)
+    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
+    ref.prepare_tc()
+    want = ref(v).clone()
+    monkeypatch.setenv("CQ_UMMA_GEOMETRY", geometry)
+    layers = _sharded_layers(w, full, E, k, world)
+    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
+    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
 def test_ep_step_skewed_routing_fills_one_rank():
     """All tokens routed to the experts of rank 0 (router columns of the other
     ranks pushed to -inf-like values): rank 0's slots fill to capacity, the
