@@ -140,6 +140,7 @@ struct RoutePerm {
     int64_t n_tok = 0, local_begin = 0;
     int k = 0, n_local = 0;
     int32_t *offsets = nullptr, *counts = nullptr, *perm_token = nullptr, *perm_slot = nullptr, *inv = nullptr;
+    __host__ __device__ bool on() const { return selected != nullptr; }
 };
 
 // Tensor-core layouts: UMMA128U8 is UMMA128U's data with every id < 8.
@@ -153,7 +154,7 @@ struct UmmaIn {
     float *scales_out = nullptr;        // gather / route: scales[perm[r]] lands here; the GEMM reads it
     bool sums_ready = false;            // otherwise: the row sums are already in the B buffer
     RoutePerm route;                    // route mode (implies the gather)
-    bool gathers() const { return perm != nullptr || route.selected != nullptr; }
+    bool gathers() const { return perm != nullptr || route.on(); }
 };
 
 // launch_pdl with a thread-block cluster of cluster_x CTAs along x.

@@ -652,7 +652,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 // counts, perm_token, perm_slot and inv.  blockDim.x == TB_THREADS.
 constexpr int TB_THREADS = 256;
 
-template <int CK>
+// RM: 0 no route mode, 1 route mode (permutation of <= RP_MAX_LOCAL local experts).
+template <int CK, int RM>
 __global__ void __launch_bounds__(TB_THREADS) to_umma_b_kernel(
     const int8_t *__restrict__ src, int64_t n, int64_t K, int64_t tiles, uint4 *__restrict__ dst,
     int32_t *__restrict__ zero, int n_zero, const int32_t *__restrict__ perm, const int32_t *__restrict__ live,
@@ -664,12 +665,12 @@ __global__ void __launch_bounds__(TB_THREADS) to_umma_b_kernel(
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
     int64_t nrow;
-    if (rp.selected != nullptr) {
+    if (RM != 0) {
         extern __shared__ int32_t tb_sm[];  // [RP_MAX_LOCAL + 1] offsets | [n_tok * k] permutation
         int32_t *s_off = tb_sm, *s_perm = tb_sm + RP_MAX_LOCAL + 1;
         const bool pub = blockIdx.x == 0;
         route_permute<TB_THREADS>(rp.selected, rp.n_tok, rp.k, rp.local_begin, rp.n_local, s_off, s_perm,
-                                  pub ? rp.perm_slot : nullptr, pub ? rp.inv : nullptr);
+                                           pub ? rp.perm_slot : nullptr, pub ? rp.inv : nullptr);
         nrow = s_off[rp.n_local];
         perm = s_perm;
         if (pub) {
@@ -767,11 +768,11 @@ cq_status to_umma_b(const int8_t *codes, int64_t n, int64_t K, int64_t tiles, in
                     cudaStream_t st) {
     const int64_t total = (K / CK) * tiles * 16 * (CK / 32);
     if (total == 0) return CQ_OK;
-    const size_t smem =
-        in.route.selected != nullptr ? sizeof(int32_t) * (RP_MAX_LOCAL + 1 + in.route.n_tok * in.route.k) : 0;
-    launch_pdl(to_umma_b_kernel<CK>, (unsigned)std::min<int64_t>(ceil_div(total, TB_THREADS), 148 * 16), TB_THREADS,
-               smem, st, codes, n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero, in.perm, live, tscales,
-               in.scales_out, in.tok_sums, in.gathers() ? sums : nullptr, in.route);
+    const size_t smem = in.route.on() ? sizeof(int32_t) * (RP_MAX_LOCAL + 1 + in.route.n_tok * in.route.k) : 0;
+    auto kern = in.route.on() ? to_umma_b_kernel<CK, 1> : to_umma_b_kernel<CK, 0>;
+    launch_pdl(kern, (unsigned)std::min<int64_t>(ceil_div(total, TB_THREADS), 148 * 16), TB_THREADS, smem, st, codes,
+               n, K, tiles, reinterpret_cast<uint4 *>(dst), zero, n_zero, in.perm, live, tscales, in.scales_out,
+               in.tok_sums, in.gathers() ? sums : nullptr, in.route);
     CQ_TRY(check_launch("to_umma_b"));
     if (sums == nullptr || in.gathers() || in.sums_ready) return CQ_OK;
     launch_pdl(row_sums_kernel, (unsigned)ceil_div(n, 8), 256, 0, st, codes, n, K, sums);

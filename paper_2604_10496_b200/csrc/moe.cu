@@ -645,11 +645,13 @@ __global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n)
 }
 
 // gather = false: leave codes_perm / scales_perm unwritten (the tcgen05 expert
-// stage gathers token rows itself, UmmaIn::perm).  topk_only (nullable): where
-// the router can also do top-k in its launch, stop there and set *topk_only;
-// the permutation is then the consumer's (UmmaIn::route).
+// stage gathers token rows itself, UmmaIn::perm).  deferred (nullable): at
+// decode sizes, where the router launch also does the top-k (one expert group),
+// stop there and set *deferred = 1: the permutation is the GEMM's B build's
+// (UmmaIn::route); 0 = everything done here.
+
 cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, const Ws &w, cudaStream_t st,
-                bool gather = true, bool *topk_only = nullptr) {
+                bool gather = true, int *deferred = nullptr) {
     const int64_t d = dsc->d_model;
     const void *qin = x;
     int qdt = dtype;
@@ -671,13 +673,17 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
     // the quantizer also clears the route counts and the arrival counter (counts[E])
     CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, w.fout, st, w.tok_sums, w.counts,
                        (int)dsc->n_experts + 1));
-    if (topk_only != nullptr) {
-        *topk_only = false;
-        if (n * dsc->top_k <= RP_MAX_ROUTES && dsc->n_local_experts <= RP_MAX_LOCAL) {
-            // logits + top-k in one launch (decode batches)
+    if (deferred != nullptr) {
+        *deferred = 0;
+        if (n * dsc->top_k <= RP_MAX_ROUTES && dsc->n_local_experts <= RP_MAX_LOCAL &&
+            dsc->top_k <= MAX_TOPK && dsc->top_k <= dsc->n_experts) {
+            bool fused = false;  // logits + top-k in one launch (one expert group)
             CQ_TRY(router_fused(w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, w.selected, w.weights,
-                                dsc->top_k, st, topk_only));
-            if (*topk_only) return CQ_OK;
+                                dsc->top_k, st, &fused));
+            if (fused) {
+                *deferred = 1;
+                return CQ_OK;
+            }
         }
     }
     CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
@@ -795,14 +801,14 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
     const int path = choose_path(desc);
     // tcgen05 layouts: the expert stage's B build gathers the token rows itself (no codes_perm)
     const bool umma = path == CQ_PATH_TC && desc->gate.tc_layout != CQ_TC_MMA16;
-    bool topk_only = false;
-    CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma, umma ? &topk_only : nullptr));
+    int deferred = 0;
+    CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma, umma ? &deferred : nullptr));
     const int64_t R = n_tokens * desc->top_k;
     if (umma) {
         UmmaIn in;
         in.tok_sums = w.tok_sums;
         in.scales_out = w.scales_perm;
-        if (topk_only) {  // the B build derives the permutation from the top-k and publishes it
+        if (deferred) {  // the B build derives the permutation and publishes it
             in.route.selected = w.selected;
             in.route.n_tok = n_tokens;
             in.route.k = (int)desc->top_k;

@@ -11,8 +11,84 @@
 namespace cq {
 
 constexpr int MAX_TOPK = 16;
-constexpr int RP_MAX_LOCAL = 32;     // local experts (one ballot per expert)
+constexpr int RP_MAX_LOCAL = 32;     // local experts (one ballot per expert; a 256-expert variant
+                                     // with 8 masks measured slower than separate kernels at E = 128)
 constexpr int RP_MAX_ROUTES = 4096;  // n * k held in shared memory
+
+// numpy's float32 sum of a short row: a plain loop below 8 elements, eight
+// interleaved partial sums combined as a tree from 8 up (pairwise_sum).
+__device__ __forceinline__ float np_sum(const float *v, int n) {
+    if (n < 8) {
+        float r = 0.0f;  // numpy starts from the first element; 0 + x == x exactly
+        for (int i = 0; i < n; ++i) r = __fadd_rn(r, v[i]);
+        return r;
+    }
+    float r[8];
+    for (int j = 0; j < 8; ++j) r[j] = v[j];
+    int i = 8;
+    for (; i + 8 <= n; i += 8)
+        for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], v[i + j]);
+    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __fadd_rn(res, v[i]);
+    return res;
+}
+
+// One warp per token: the lanes hold the token's logits (expert e in lane e % 32),
+// and each of the k rounds is a warp argmax (larger logit first, ties -> lower
+// expert id, +0 and -0 equal like numpy's sort): the stable descending
+// selection of model.py:324-330.  Lane 0 then forms the softmax over the
+// selected logits and counts the routes of the local expert range.
+// `row`: the token's n_exp logits, global or shared memory; weights and counts
+// are nullable.
+__device__ __forceinline__ void topk_token(const float *row, int64_t t, int64_t n_exp, int64_t k, int lane,
+                                           int32_t *__restrict__ selected, float *__restrict__ weights,
+                                           int32_t *__restrict__ counts, int64_t local_begin, int64_t n_local) {
+    constexpr int PER = 256 / 32;  // <= 256 experts
+    float lv[PER];
+    uint32_t taken = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int64_t e = lane + 32 * i;
+        lv[i] = e < n_exp ? row[e] : 0.0f;
+        if (e >= n_exp) taken |= 1u << i;
+    }
+    int sel[MAX_TOPK];
+    float val[MAX_TOPK];
+    for (int s = 0; s < k; ++s) {
+        int best = -1;
+        float bv = 0.0f;
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            if (!(taken >> i & 1) && (best < 0 || lv[i] > bv)) {  // lane-local: ids ascending with i
+                best = lane + 32 * i;
+                bv = lv[i];
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            if (ob >= 0 && (best < 0 || ov > bv || (!(bv > ov) && ob < best))) {
+                best = ob;
+                bv = ov;
+            }
+        }
+        sel[s] = best;
+        val[s] = bv;
+        if ((best & 31) == lane) taken |= 1u << (best >> 5);
+    }
+    if (lane != 0) return;
+    const float m = val[0];  // max of the selected logits
+    float ex[MAX_TOPK];
+    for (int s = 0; s < k; ++s) ex[s] = expf(__fsub_rn(val[s], m));
+    const float tot = np_sum(ex, (int)k);
+    for (int s = 0; s < k; ++s) {
+        selected[t * k + s] = sel[s];
+        if (weights != nullptr) weights[t * k + s] = __fdiv_rn(ex[s], tot);
+        const int64_t le = sel[s] - local_begin;
+        if (counts != nullptr && le >= 0 && le < n_local) atomicAdd(counts + le, 1);
+    }
+}
 
 // s_off [n_local + 1] and s_perm [n * k] are shared memory.  perm_slot / inv
 // (global, nullable) are written when given (one CTA does that).  Every
@@ -24,7 +100,7 @@ __device__ void route_permute(const int32_t *__restrict__ selected, int64_t n, i
     __shared__ int32_t s_cnt[RP_MAX_LOCAL];
     __shared__ int32_t s_wtot[NT / 32][RP_MAX_LOCAL];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < n_local) s_cnt[tid] = 0;
+    for (int e = tid; e < n_local; e += NT) s_cnt[e] = 0;
     __syncthreads();
     for (int64_t x = tid; x < n * k; x += NT) {
         const int64_t e = selected[x] - local_begin;
@@ -40,12 +116,15 @@ __device__ void route_permute(const int32_t *__restrict__ selected, int64_t n, i
         s_off[n_local] = run;
     }
     __syncthreads();
-    if (tid < n_local) s_cnt[tid] = s_off[tid];  // running base per expert
+    for (int e = tid; e < n_local; e += NT) s_cnt[e] = s_off[e];  // running base per expert
     __syncthreads();
+    constexpr int NG = RP_MAX_LOCAL / 32;  // expert groups of 32, one bit mask each
     for (int64_t t0 = 0; t0 < n; t0 += NT) {
         const int64_t t = t0 + tid;
         int le[MAX_TOPK], pre[MAX_TOPK];
-        uint32_t mine = 0;
+        uint32_t mine[NG];
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) mine[gi] = 0;
 #pragma unroll
         for (int s = 0; s < MAX_TOPK; ++s) {
             le[s] = -1;
@@ -54,16 +133,27 @@ __device__ void route_permute(const int32_t *__restrict__ selected, int64_t n, i
                 const int64_t e = selected[t * k + s] - local_begin;
                 if (e >= 0 && e < n_local) {
                     le[s] = (int)e;
-                    mine |= 1u << e;
+#pragma unroll
+                    for (int gi = 0; gi < NG; ++gi)  // static indices keep the masks in registers
+                        if ((e >> 5) == gi) mine[gi] |= 1u << (e & 31);
                 }
             }
         }
-        for (int e = 0; e < n_local; ++e) {
-            const uint32_t b = __ballot_sync(0xffffffffu, (mine >> e) & 1u);
-            if (lane == 0) s_wtot[warp][e] = __popc(b);
 #pragma unroll
-            for (int s = 0; s < MAX_TOPK; ++s)
-                if (le[s] == e) pre[s] = __popc(b & ((1u << lane) - 1u));
+        for (int gi = 0; gi < NG; ++gi) {
+            if (32 * gi >= n_local) break;
+            const int eb = n_local - 32 * gi < 32 ? n_local - 32 * gi : 32;
+            for (int b = 0; b < eb; ++b) {
+                const int e = 32 * gi + b;
+                const bool has = (mine[gi] >> b) & 1u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, has);
+                if (lane == 0) s_wtot[warp][e] = __popc(bal);
+                if (has) {
+#pragma unroll
+                    for (int s = 0; s < MAX_TOPK; ++s)
+                        if (le[s] == e) pre[s] = __popc(bal & ((1u << lane) - 1u));
+                }
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -76,10 +166,10 @@ __device__ void route_permute(const int32_t *__restrict__ selected, int64_t n, i
             if (inv != nullptr) inv[t * k + s] = pos;
         }
         __syncthreads();
-        if (tid < n_local) {
+        for (int e = tid; e < n_local; e += NT) {
             int32_t tot = 0;
-            for (int w = 0; w < NT / 32; ++w) tot += s_wtot[w][tid];
-            s_cnt[tid] += tot;
+            for (int w = 0; w < NT / 32; ++w) tot += s_wtot[w][e];
+            s_cnt[e] += tot;
         }
         __syncthreads();
     }

@@ -209,81 +209,7 @@ __global__ void __launch_bounds__(RD_THREADS) router_multi_kernel(const float *_
     }
 }
 
-// numpy's float32 sum of a short row: a plain loop below 8 elements, eight
-// interleaved partial sums combined as a tree from 8 up (pairwise_sum).
-__device__ __forceinline__ float np_sum(const float *v, int n) {
-    if (n < 8) {
-        float r = 0.0f;  // numpy starts from the first element; 0 + x == x exactly
-        for (int i = 0; i < n; ++i) r = __fadd_rn(r, v[i]);
-        return r;
-    }
-    float r[8];
-    for (int j = 0; j < 8; ++j) r[j] = v[j];
-    int i = 8;
-    for (; i + 8 <= n; i += 8)
-        for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], v[i + j]);
-    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __fadd_rn(res, v[i]);
-    return res;
-}
-
-// One warp per token: the lanes hold the token's logits (expert e in lane e % 32),
-// and each of the k rounds is a warp argmax (larger logit first, ties -> lower
-// expert id, +0 and -0 equal like numpy's sort): the stable descending
-// selection of model.py:324-330.  Lane 0 then forms the softmax over the
-// selected logits and counts the routes of the local expert range.
 constexpr int TOPK_WARPS = 4;
-
-// `row`: the token's n_exp logits, global or shared memory.
-__device__ __forceinline__ void topk_token(const float *row, int64_t t, int64_t n_exp, int64_t k, int lane,
-                                           int32_t *__restrict__ selected, float *__restrict__ weights,
-                                           int32_t *__restrict__ counts, int64_t local_begin, int64_t n_local) {
-    constexpr int PER = 256 / 32;  // <= 256 experts
-    float lv[PER];
-    uint32_t taken = 0;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int64_t e = lane + 32 * i;
-        lv[i] = e < n_exp ? row[e] : 0.0f;
-        if (e >= n_exp) taken |= 1u << i;
-    }
-    int sel[MAX_TOPK];
-    float val[MAX_TOPK];
-    for (int s = 0; s < k; ++s) {
-        int best = -1;
-        float bv = 0.0f;
-#pragma unroll
-        for (int i = 0; i < PER; ++i)
-            if (!(taken >> i & 1) && (best < 0 || lv[i] > bv)) {  // lane-local: ids ascending with i
-                best = lane + 32 * i;
-                bv = lv[i];
-            }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            if (ob >= 0 && (best < 0 || ov > bv || (!(bv > ov) && ob < best))) {
-                best = ob;
-                bv = ov;
-            }
-        }
-        sel[s] = best;
-        val[s] = bv;
-        if ((best & 31) == lane) taken |= 1u << (best >> 5);
-    }
-    if (lane != 0) return;
-    const float m = val[0];  // max of the selected logits
-    float ex[MAX_TOPK];
-    for (int s = 0; s < k; ++s) ex[s] = expf(__fsub_rn(val[s], m));
-    const float tot = np_sum(ex, (int)k);
-    for (int s = 0; s < k; ++s) {
-        selected[t * k + s] = sel[s];
-        weights[t * k + s] = __fdiv_rn(ex[s], tot);
-        const int64_t le = sel[s] - local_begin;
-        if (counts != nullptr && le >= 0 && le < n_local) atomicAdd(counts + le, 1);
-    }
-}
 
 __global__ void __launch_bounds__(TOPK_WARPS * 32) topk_kernel(const float *__restrict__ logits, int64_t n,
                                                                int64_t n_exp, int64_t k, int32_t *__restrict__ selected,
@@ -376,6 +302,9 @@ constexpr int RC_THREADS = 128, RC_K = RC_KCOLS, RC_PITCH = RC_K + 4;
 template <int EG>
 struct RcStages {
     static constexpr int NR = EG >= 32 ? 4 : 8;
+    // 32-expert groups (E = 64 / 128 at decode): 128-column chunks keep a CTA near 100 KB, two per SM
+    static constexpr int K = EG >= 32 ? 128 : RC_K;
+    static constexpr int PITCH = K + 4;
 };
 
 // acc + p[0] + p[1] + ... + p[kn-1] in order (kn % 16 == 0), 16 columns loaded
@@ -427,41 +356,42 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
 #endif
     extern __shared__ __align__(16) float rcs[];
     const int nc = tt * EG;                      // chains
-    float *pbuf = rcs;                           // [2][nc][RC_PITCH] products
+    float *pbuf = rcs;                           // [2][nc][PITCH] products
     constexpr int NR = RcStages<EG>::NR;
-    float *wraw = pbuf + 2 * nc * RC_PITCH;      // [NR][RC_K][EG]
-    float *xraw = wraw + NR * RC_K * EG;         // [NR][tt][RC_K]
+    constexpr int KC = RcStages<EG>::K, PITCH = RcStages<EG>::PITCH;
+    float *wraw = pbuf + 2 * nc * PITCH;      // [NR][KC][EG]
+    float *xraw = wraw + NR * KC * EG;         // [NR][tt][KC]
     const int tid = threadIdx.x;
     const int64_t t0 = blockIdx.x * (int64_t)tt;
     const int e0 = blockIdx.y * EG;
-    const int n_chunks = (int)((d + RC_K - 1) / RC_K);
+    const int n_chunks = (int)((d + KC - 1) / KC);
     const int ptid = tid - 32;  // producer index, warps 1-3
     auto stage = [&](int i) {
         if (i < n_chunks) {
-            const int64_t k0 = (int64_t)i * RC_K;
-            const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
-            float *wb = wraw + (i % NR) * RC_K * EG;
+            const int64_t k0 = (int64_t)i * KC;
+            const int kn = (int)((d - k0) < KC ? (d - k0) : KC);
+            float *wb = wraw + (i % NR) * KC * EG;
             for (int x = ptid; x < kn * (EG / 4); x += RC_THREADS - 32) {
                 const int r = x / (EG / 4), q = x - r * (EG / 4);
                 cp_async16(wb + r * EG + 4 * q, w + (k0 + r) * n_exp + e0 + 4 * q);
             }
-            float *xb = xraw + (i % NR) * tt * RC_K;
+            float *xb = xraw + (i % NR) * tt * KC;
             const int rowv = kn / 4;
             for (int x = ptid; x < tt * rowv; x += RC_THREADS - 32) {
                 const int tl = x / rowv, v = x - tl * rowv;
                 const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // rows past n are never stored
-                cp_async16(xb + tl * RC_K + 4 * v, xdeq + tg * d + k0 + 4 * v);
+                cp_async16(xb + tl * KC + 4 * v, xdeq + tg * d + k0 + 4 * v);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto produce = [&](int i) {  // chunk i landed in raw buffer i % NR (own copies waited for)
         asm volatile("bar.sync 1, %0;" ::"n"(RC_THREADS - 32) : "memory");
-        const int64_t k0 = (int64_t)i * RC_K;
-        const int kn = (int)((d - k0) < RC_K ? (d - k0) : RC_K);
-        const float *wb = wraw + (i % NR) * RC_K * EG;
-        const float *xb = xraw + (i % NR) * tt * RC_K;
-        float *pb = pbuf + (i & 1) * nc * RC_PITCH;
+        const int64_t k0 = (int64_t)i * KC;
+        const int kn = (int)((d - k0) < KC ? (d - k0) : KC);
+        const float *wb = wraw + (i % NR) * KC * EG;
+        const float *xb = xraw + (i % NR) * tt * KC;
+        float *pb = pbuf + (i & 1) * nc * PITCH;
 #ifdef RC_EXP_NO_PRODUCE
         return;
 #endif
@@ -473,9 +403,9 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
                 wr[4 * q] = v.x, wr[4 * q + 1] = v.y, wr[4 * q + 2] = v.z, wr[4 * q + 3] = v.w;
             }
             for (int t = 0; t < tt; ++t) {
-                const float xv = xb[t * RC_K + j];
+                const float xv = xb[t * KC + j];
 #pragma unroll
-                for (int e = 0; e < EG; ++e) pb[(t * EG + e) * RC_PITCH + j] = __fmul_rn(xv, wr[e]);
+                for (int e = 0; e < EG; ++e) pb[(t * EG + e) * PITCH + j] = __fmul_rn(xv, wr[e]);
             }
         }
     };
@@ -502,10 +432,10 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
                 produce(i + 1);
             }
         } else if (chain) {
-            const int kn = (int)((d - (int64_t)i * RC_K) < RC_K ? (d - (int64_t)i * RC_K) : RC_K);  // % 16 == 0
-            const float4 *pr = reinterpret_cast<const float4 *>(pbuf + (i & 1) * nc * RC_PITCH + tid * RC_PITCH);
-            if (kn == RC_K)
-                acc = chain_add<RC_K>(acc, pr, RC_K);  // full chunk: compile-time trip count
+            const int kn = (int)((d - (int64_t)i * KC) < KC ? (d - (int64_t)i * KC) : KC);  // % 16 == 0
+            const float4 *pr = reinterpret_cast<const float4 *>(pbuf + (i & 1) * nc * PITCH + tid * PITCH);
+            if (kn == KC)
+                acc = chain_add<KC>(acc, pr, KC);  // full chunk: compile-time trip count
             else
                 acc = chain_add<0>(acc, pr, kn);
         }
@@ -543,7 +473,8 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
 
 static size_t router_chain_smem(int eg, int tt) {
     const size_t nr = eg >= 32 ? RcStages<32>::NR : RcStages<8>::NR;
-    return sizeof(float) * ((size_t)2 * tt * eg * RC_PITCH + nr * RC_K * eg + nr * tt * RC_K);
+    const size_t kc = eg >= 32 ? RcStages<32>::K : RcStages<8>::K;
+    return sizeof(float) * ((size_t)2 * tt * eg * (kc + 4) + nr * kc * eg + nr * tt * kc);
 }
 
 // rows_out[r, :] = rows_in[perm_token[r], :], r < offsets[n_local]; also scales.

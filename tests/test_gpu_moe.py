@@ -184,11 +184,14 @@ def test_router_decode_chain_bit_exact(n, d, E):
     assert np.array_equal(layer.trace(n)["offsets"].cpu().numpy(), off)
 
 
-@pytest.mark.parametrize("n,E,k", [(1, 8, 2), (64, 8, 2), (33, 16, 4), (100, 32, 8), (296, 8, 2), (7, 24, 3)])
+@pytest.mark.parametrize("n,E,k", [(1, 8, 2), (64, 8, 2), (33, 16, 4), (100, 32, 8), (296, 8, 2), (7, 24, 3),
+                                   (64, 128, 8), (100, 64, 6), (1, 128, 8), (200, 128, 8)])
 def test_tc_decode_route_mode(n, E, k):
-    """Tensor-core forward at decode sizes: the router launch also does top-k,
-    and the GEMM's B build derives the segment permutation in every CTA
-    (route_perm.cuh) and publishes it.  Routing arrays bit-exact with the
+    """Tensor-core forward at decode sizes: the router launch also does top-k
+    (one expert group) or the GEMM's B build takes it from the logits (E > 32,
+    n <= 128), and the B build derives the segment permutation in every CTA
+    (route_perm.cuh) and publishes it; n = 200 at E = 128 runs the separate
+    kernels.  Routing arrays bit-exact with the
     oracle, the layer output within the layer tolerance of the ordered path,
     and identical across two calls."""
     d, ff, g = 256, 256, 128
