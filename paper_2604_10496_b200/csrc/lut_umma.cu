@@ -358,17 +358,47 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         int seg = 0;
         UmSeq q = seq0;
         int u, c0, c1;
+#ifdef UM_EXP_TIMING
+        long long m_acc = 0, m_af = 0, m_iss = 0, m_t0 = clock64();
+#endif
+        const uint32_t tm_u = tmem, stage_u = stage_a;
         for (; q.next(W, u, c0, c1); ++nu) {
             const UmUnit x = um_unit(W, seg_first, u, seg, TPP);
             const uint32_t idesc = idesc_i8(((x.ntc + 1) & ~1) * 8);
+            const int c0u = c0, c1u = c1;
+#ifdef UM_EXP_TIMING
+            const long long ma = clock64();
+#endif
             if (nu > 0) u_bar_wait(u_smem(&accempty_bar), (nu - 1) & 1);
-            for (int c = c0; c < c1; ++c, ++k) {
+#ifdef UM_EXP_TIMING
+            m_acc += clock64() - ma;
+#endif
+            for (int c = c0u; c < c1u; ++c, ++k) {
                 const int s = k % NS, sa = k % NA;
-                const uint32_t bbase = stage_a + s * S::BYTES + GEO::IDS + S::LUT;
-                const uint32_t abase = tmem + a_col0 + (uint32_t)(sa * S::CCOLS);
+                const uint32_t bbase = stage_u + s * S::BYTES + GEO::IDS + S::LUT;
+                const uint32_t abase = tm_u + a_col0 + (uint32_t)(sa * S::CCOLS);
                 // afull implies full: every expander waited for the chunk's data
+#ifdef UM_EXP_TIMING
+                const long long mw = clock64();
+#endif
                 u_bar_wait(afull_a + 8 * sa, (k / NA) & 1);
+#ifdef UM_EXP_TIMING
+                const long long mi = clock64();
+                m_af += mi - mw;
+#endif
                 tc_fence_after();
+#ifndef UM_MMA_PER_INSTR
+                if constexpr (MERGED) {  // one asm block per chunk (B tile: [tile8][kstep][khalf][8 rows][16 B])
+#ifndef UM_EXP_NO_MMA
+                    // lane-0 broadcasts of the operands: ptxas then converts each to a uniform register
+                    // once per chunk (68 instead of 141 instructions per 12 MMAs)
+                    const uint64_t bd = smem_desc(bbase, 128, GEO::BTILE);
+                    tc_mma_chunk<GEO::KS, P>(__shfl_sync(0xffffffffu, tm_u, 0), (uint32_t)NT,
+                                             __shfl_sync(0xffffffffu, abase, 0), __shfl_sync(0xffffffffu, bd, 0),
+                                             __shfl_sync(0xffffffffu, idesc, 0), c == c0u ? 0u : 1u);
+#endif
+                } else
+#endif
 #pragma unroll
                 for (int kk = 0; kk < GEO::KS; ++kk) {
                     // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
@@ -376,9 +406,9 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 #pragma unroll
                     for (int sl = 0; sl < S::SLICES; ++sl) {
                         const int p = MERGED ? sl : (sl >> 1);
-                        const uint32_t accum = (c == c0 && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
+                        const uint32_t accum = (c == c0u && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
 #ifndef UM_EXP_NO_MMA
-                        tc_mma_i8(tmem + (uint32_t)(p * NT), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
+                        tc_mma_i8(tm_u + (uint32_t)(p * NT), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
                                   idesc, accum);
 #endif
                     }
@@ -388,9 +418,17 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     tc_commit_elect(afree_a + 8 * sa);  // A stage free for chunk k + NA
                 else if (LAG > 0)
                     tc_commit_elect(full_a + 8 * ((k + NA) % NS));  // A stage free for chunk k + NA
-                if (c == c1 - 1) tc_commit_elect(u_smem(&accfull_bar));
+                if (c == c1u - 1) tc_commit_elect(u_smem(&accfull_bar));
+#ifdef UM_EXP_TIMING
+                m_iss += clock64() - mi;
+#endif
             }
         }
+#ifdef UM_EXP_TIMING
+        if (blockIdx.x == 0 && lane == 0)
+            printf("mma warp chunks %u: afull-wait %lld issue %lld accempty-wait %lld total %lld\n", k, m_af, m_iss,
+                   m_acc, clock64() - m_t0);
+#endif
     } else {
         // ------------------------------------------------------------ expanders
         const int wg = warp >> 2;
@@ -404,6 +442,10 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         int seg = 0;
         UmSeq q = seq0;
         int u, c0, c1;
+#ifdef UM_EXP_TIMING
+        long long t_wait = 0, t_exp = 0, t_st = 0, t_epi = 0, t_afree = 0, t_begin = clock64();
+        int n_ch = 0;
+#endif
         for (; q.next(W, u, c0, c1); ++nu) {
             float rscale;
             {
@@ -426,8 +468,16 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
             for (int c = c0; c < c1; ++c, ++k) {
                 if ((int)(k % GS) != stream) continue;  // warpgroup-uniform
                 const int s = k % NS, sa = k % NA;
+#ifdef UM_EXP_TIMING
+                const long long tw0 = clock64();
+#endif
                 u_bar_wait(full_a + 8 * s, (k / NS) & 1);
                 tc_fence_after();
+#ifdef UM_EXP_TIMING
+                const long long tw1 = clock64();
+                t_wait += tw1 - tw0;
+                ++n_ch;
+#endif
                 const uint8_t *st = smem + (size_t)s * S::BYTES;
                 uint4 L[P];
                 {
@@ -470,7 +520,13 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                         for (int p = 0; p < P; ++p)
 #pragma unroll
                             for (int cc = 0; cc < 8; ++cc) asm volatile("" : "+r"(v[p][cc]));
+#ifdef UM_EXP_TIMING
+                        const long long ta0 = clock64();
+#endif
                         u_bar_wait(afree_a + 8 * sa, ((k / NA) & 1) ^ 1);  // first use of a stage passes at once
+#ifdef UM_EXP_TIMING
+                        t_afree += clock64() - ta0;
+#endif
                         tc_fence_after();
 #pragma unroll
                         for (int p = 0; p < P; ++p) tc_st8(abase + p * 8, v[p]);
@@ -503,11 +559,21 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                         }
                     }
                 }
+#ifdef UM_EXP_TIMING
+                const long long tx = clock64();
+                t_exp += tx - tw1;
+#endif
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(afull_a + 8 * sa);
+#ifdef UM_EXP_TIMING
+                t_st += clock64() - tx;
+#endif
             }
+#ifdef UM_EXP_TIMING
+            const long long te0 = clock64();
+#endif
             // ---- epilogue of this unit.  Warpgroup wg owns token columns cb + 32 i (i < NCB).
             u_bar_wait(u_smem(&accfull_bar), nu & 1);
             tc_fence_after();
@@ -630,7 +696,16 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
             }
+#ifdef UM_EXP_TIMING
+            t_epi += clock64() - te0;
+#endif
         }
+#ifdef UM_EXP_TIMING
+        if (blockIdx.x == 0 && lane == 0)
+            printf("warp %2d chunks %d: full-wait %lld expand %lld (of which afree-wait %lld) wait_st %lld epilogue %lld "
+                   "(cycles, total %lld)\n",
+                   warp, n_ch, t_wait, t_exp, t_afree, t_st, t_epi, clock64() - t_begin);
+#endif
     }
     tc_fence_before();
     __syncthreads();

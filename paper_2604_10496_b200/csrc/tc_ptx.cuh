@@ -126,6 +126,78 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d, uint32_t a, uint64_t bdesc
         "r"(a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0u)
         : "memory");
 }
+// One chunk of the merged-digit GEMM: KS k-steps x P planes of
+// tcgen05.mma kind::i8, issued by one elected lane from one asm block, so the
+// operands become uniform registers once per chunk instead of once per MMA.
+//   D plane p    : d0 + p * nt           (TMEM accumulator columns)
+//   A (kk, p)    : a0 + kk * P * 8 + p * 8 (TMEM A stage columns)
+//   B k-step kk  : bdesc0 with its start address advanced kk * 256 bytes
+// The first k-step accumulates only when acc != 0.
+#define CQ_MMA1(D, A, B, P_) "@e tcgen05.mma.cta_group::1.kind::i8 [" D "], [" A "], " B ", %4, " P_ ";\n\t"
+template <int KS, int P>
+__device__ __forceinline__ void tc_mma_chunk(uint32_t d0, uint32_t nt, uint32_t a0, uint64_t bdesc0, uint32_t idesc,
+                                             uint32_t acc) {
+    static_assert((KS == 4 || KS == 2) && (P == 3 || P == 2), "chunk shapes of the merged layouts");
+    if constexpr (KS == 4 && P == 3) {
+        asm volatile(
+            "{\n\t.reg .pred e, f, on;\n\t.reg .b32 d1, d2, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, a11;\n\t"
+            ".reg .b64 b1, b2, b3;\n\t"
+            "setp.ne.b32 f, %5, 0;\n\tsetp.eq.b32 on, 0, 0;\n\t"
+            "add.u32 d1, %0, %1;\n\tadd.u32 d2, d1, %1;\n\t"
+            "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\tadd.u32 a4, %2, 32;\n\t"
+            "add.u32 a5, %2, 40;\n\tadd.u32 a6, %2, 48;\n\tadd.u32 a7, %2, 56;\n\tadd.u32 a8, %2, 64;\n\t"
+            "add.u32 a9, %2, 72;\n\tadd.u32 a10, %2, 80;\n\tadd.u32 a11, %2, 88;\n\t"
+            "add.u64 b1, %3, 16;\n\tadd.u64 b2, %3, 32;\n\tadd.u64 b3, %3, 48;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            CQ_MMA1("%0", "%2", "%3", "f") CQ_MMA1("d1", "a1", "%3", "f") CQ_MMA1("d2", "a2", "%3", "f")
+            CQ_MMA1("%0", "a3", "b1", "on") CQ_MMA1("d1", "a4", "b1", "on") CQ_MMA1("d2", "a5", "b1", "on")
+            CQ_MMA1("%0", "a6", "b2", "on") CQ_MMA1("d1", "a7", "b2", "on") CQ_MMA1("d2", "a8", "b2", "on")
+            CQ_MMA1("%0", "a9", "b3", "on") CQ_MMA1("d1", "a10", "b3", "on") CQ_MMA1("d2", "a11", "b3", "on")
+            "}" ::"r"(d0), "r"(nt), "r"(a0), "l"(bdesc0), "r"(idesc), "r"(acc)
+            : "memory");
+    } else if constexpr (KS == 4 && P == 2) {
+        asm volatile(
+            "{\n\t.reg .pred e, f, on;\n\t.reg .b32 d1, a1, a2, a3, a4, a5, a6, a7;\n\t"
+            ".reg .b64 b1, b2, b3;\n\t"
+            "setp.ne.b32 f, %5, 0;\n\tsetp.eq.b32 on, 0, 0;\n\t"
+            "add.u32 d1, %0, %1;\n\t"
+            "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\tadd.u32 a4, %2, 32;\n\t"
+            "add.u32 a5, %2, 40;\n\tadd.u32 a6, %2, 48;\n\tadd.u32 a7, %2, 56;\n\t"
+            "add.u64 b1, %3, 16;\n\tadd.u64 b2, %3, 32;\n\tadd.u64 b3, %3, 48;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            CQ_MMA1("%0", "%2", "%3", "f") CQ_MMA1("d1", "a1", "%3", "f")
+            CQ_MMA1("%0", "a2", "b1", "on") CQ_MMA1("d1", "a3", "b1", "on")
+            CQ_MMA1("%0", "a4", "b2", "on") CQ_MMA1("d1", "a5", "b2", "on")
+            CQ_MMA1("%0", "a6", "b3", "on") CQ_MMA1("d1", "a7", "b3", "on")
+            "}" ::"r"(d0), "r"(nt), "r"(a0), "l"(bdesc0), "r"(idesc), "r"(acc)
+            : "memory");
+    } else if constexpr (KS == 2 && P == 3) {
+        asm volatile(
+            "{\n\t.reg .pred e, f, on;\n\t.reg .b32 d1, d2, a1, a2, a3, a4, a5;\n\t.reg .b64 b1;\n\t"
+            "setp.ne.b32 f, %5, 0;\n\tsetp.eq.b32 on, 0, 0;\n\t"
+            "add.u32 d1, %0, %1;\n\tadd.u32 d2, d1, %1;\n\t"
+            "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\tadd.u32 a4, %2, 32;\n\t"
+            "add.u32 a5, %2, 40;\n\tadd.u64 b1, %3, 16;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            CQ_MMA1("%0", "%2", "%3", "f") CQ_MMA1("d1", "a1", "%3", "f") CQ_MMA1("d2", "a2", "%3", "f")
+            CQ_MMA1("%0", "a3", "b1", "on") CQ_MMA1("d1", "a4", "b1", "on") CQ_MMA1("d2", "a5", "b1", "on")
+            "}" ::"r"(d0), "r"(nt), "r"(a0), "l"(bdesc0), "r"(idesc), "r"(acc)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, f, on;\n\t.reg .b32 d1, a1, a2, a3;\n\t.reg .b64 b1;\n\t"
+            "setp.ne.b32 f, %5, 0;\n\tsetp.eq.b32 on, 0, 0;\n\t"
+            "add.u32 d1, %0, %1;\n\t"
+            "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\tadd.u64 b1, %3, 16;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            CQ_MMA1("%0", "%2", "%3", "f") CQ_MMA1("d1", "a1", "%3", "f")
+            CQ_MMA1("%0", "a2", "b1", "on") CQ_MMA1("d1", "a3", "b1", "on")
+            "}" ::"r"(d0), "r"(nt), "r"(a0), "l"(bdesc0), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+}
+#undef CQ_MMA1
+
 __device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
