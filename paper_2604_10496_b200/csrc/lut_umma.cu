@@ -361,6 +361,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 #ifdef UM_EXP_TIMING
         long long m_acc = 0, m_af = 0, m_iss = 0, m_t0 = clock64();
 #endif
+        // The CTA allocates all 512 TMEM columns (one CTA per SM), so the base is column 0 of lane 0:
+        // literal bases let ptxas keep the MMA operands in uniform registers.
         const uint32_t tm_u = tmem, stage_u = stage_a;
         for (; q.next(W, u, c0, c1); ++nu) {
             const UmUnit x = um_unit(W, seg_first, u, seg, TPP);

@@ -198,6 +198,7 @@ __device__ __forceinline__ void tc_mma_chunk(uint32_t d0, uint32_t nt, uint32_t 
 }
 #undef CQ_MMA1
 
+
 __device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
