@@ -68,10 +68,24 @@ namespace cq {
 namespace um {
 constexpr int STAGES = 8;        // most A stages used
 constexpr int WG = 4;            // expander warpgroups; warpgroup w expands k-step w of every chunk
-constexpr int EXP_WARPS = 4 * WG, PROD_WARP = EXP_WARPS, MMA_WARP = EXP_WARPS + 1, WARPS = EXP_WARPS + 2;
-constexpr int THREADS = WARPS * 32;
+constexpr int EXP_WARPS = 4 * WG, PROD_WARP = EXP_WARPS, MMA_WARP = EXP_WARPS + 1;
 constexpr uint32_t TMEM_COLS = 512;
 }  // namespace um
+
+#ifndef UM_MMA_PER_PLANE  // merged layouts: one MMA warp per digit plane (own accumulator, own SMSP)
+#define UM_MMA_PER_PLANE 1
+#endif
+// Warps of a CTA: the expanders, the producer, and NMMA MMA-issuing warps.  The
+// MMA warp's issue rate (~55 cycles per tcgen05.mma, sharing an SMSP with 4
+// expander warps) bounded the decode GEMM; with one warp per plane each issues
+// a third (P = 3) of the MMAs from a different SMSP.  Planes accumulate into
+// disjoint TMEM columns, so the warps never touch one accumulator concurrently.
+template <int P, bool MERGED>
+struct UmWarps {
+    static constexpr int NMMA = (MERGED && UM_MMA_PER_PLANE) ? P : 1;
+    static constexpr int WARPS = um::EXP_WARPS + 1 + NMMA;
+    static constexpr int THREADS = WARPS * 32;
+};
 
 // Pass geometry: NT tokens per pass (MMA N), CK input columns per chunk.  Decode
 // uses NT 32 / CK 128 (4 A stages of 4 k-steps); prefill NT 128 / CK 64 (the
@@ -215,7 +229,7 @@ __device__ __forceinline__ UmUnit um_unit(const UmWork &w, int64_t seg_first, in
 // bytes of entries 0..7 sit in L.x, L.y, so one PRMT yields 4 A bytes (no
 // second PRMT over entries 8..15, no merge).
 template <int P, bool MERGED, class GEO, bool NARROW = false>
-__global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
+__global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
     const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int n_seg, int64_t seg_first,
     const uint8_t *__restrict__ ids0, const int8_t *__restrict__ lut0, const float *__restrict__ rs0,
@@ -224,6 +238,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
     int32_t *__restrict__ part, int32_t *__restrict__ cnt) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     using S = UmStage<P, MERGED, GEO>;
+    constexpr int NMMA = UmWarps<P, MERGED>::NMMA;
     constexpr int NA = S::NA, NS = S::NS, GS = S::GS, LAG = S::LAG;
     constexpr int WPS = um::WG / GS;  // warpgroups per stream
     constexpr int NT = GEO::NT, CK = GEO::CK, NCB = GEO::NCB;
@@ -290,16 +305,16 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
-            u_bar_init(u_smem(&full_bar[s]), (LAG > 0 && !S::SPLIT_AFREE) ? 2 : 1);
-            u_bar_init(u_smem(&empty_bar[s]), 1);
+            u_bar_init(u_smem(&full_bar[s]), (LAG > 0 && !S::SPLIT_AFREE) ? 1 + NMMA : 1);
+            u_bar_init(u_smem(&empty_bar[s]), NMMA);
         }
         for (int s = 0; s < NA; ++s) {
             u_bar_init(u_smem(&afull_bar[s]), 4 * WPS);  // the warps of one stream
-            u_bar_init(u_smem(&afree_bar[s]), 1);         // SPLIT_AFREE: MMAs of the stage's last chunk done
+            u_bar_init(u_smem(&afree_bar[s]), NMMA);      // SPLIT_AFREE: MMAs of the stage's last chunk done
         }
         // (splitting afull per chunk half, so the MMAs start earlier, measured slower: the extra
         //  tcgen05.wait::st mid-chunk costs more than the overlap gains)
-        u_bar_init(u_smem(&accfull_bar), 1);
+        u_bar_init(u_smem(&accfull_bar), NMMA);
         u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -340,7 +355,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 const uint32_t bar = full_a + 8 * s;
                 const uint32_t dst = stage_a + s * S::BYTES;
                 u_bar_expect_elect(bar, GEO::IDS + (new_group ? S::LUT : 0) + ntc16 * GEO::BTILE);
-                if (LAG > 0 && !S::SPLIT_AFREE && (int)k < NA) u_bar_arrive_elect(bar);  // no chunk k - NA yet
+                if (LAG > 0 && !S::SPLIT_AFREE && (int)k < NA)
+                    u_bar_arrive_cnt_elect(bar, NMMA);  // no chunk k - NA yet: stands in for its MMA commits
                 u_bulk_elect(dst, ids + ((size_t)x.tile * n_chunks + c) * GEO::IDS, GEO::IDS, bar);
                 if (new_group)
                     u_bulk_elect(dst + GEO::IDS, lut + ((size_t)x.tile * n_groups + grp) * S::LUT, S::LUT, bar);
@@ -352,7 +368,7 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                 }
             }
         }
-    } else if (warp == um::MMA_WARP) {
+    } else if (warp >= um::MMA_WARP && warp < um::MMA_WARP + NMMA) {
         // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
         uint32_t k = 0, nu = 0;
         int seg = 0;
@@ -395,9 +411,17 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
                     // lane-0 broadcasts of the operands: ptxas then converts each to a uniform register
                     // once per chunk (68 instead of 141 instructions per 12 MMAs)
                     const uint64_t bd = smem_desc(bbase, 128, GEO::BTILE);
-                    tc_mma_chunk<GEO::KS, P>(__shfl_sync(0xffffffffu, tm_u, 0), (uint32_t)NT,
-                                             __shfl_sync(0xffffffffu, abase, 0), __shfl_sync(0xffffffffu, bd, 0),
-                                             __shfl_sync(0xffffffffu, idesc, 0), c == c0u ? 0u : 1u);
+                    if constexpr (NMMA > 1) {  // this warp's plane: accumulator columns p * NT, A columns p * 8
+                        const uint32_t pl = (uint32_t)(warp - um::MMA_WARP);
+                        tc_mma_plane<GEO::KS>(__shfl_sync(0xffffffffu, tm_u + pl * NT, 0),
+                                              __shfl_sync(0xffffffffu, abase + pl * 8, 0), (uint32_t)S::ACOLS,
+                                              __shfl_sync(0xffffffffu, bd, 0), __shfl_sync(0xffffffffu, idesc, 0),
+                                              c == c0u ? 0u : 1u);
+                    } else {
+                        tc_mma_chunk<GEO::KS, P>(__shfl_sync(0xffffffffu, tm_u, 0), (uint32_t)NT,
+                                                 __shfl_sync(0xffffffffu, abase, 0), __shfl_sync(0xffffffffu, bd, 0),
+                                                 __shfl_sync(0xffffffffu, idesc, 0), c == c0u ? 0u : 1u);
+                    }
 #endif
                 } else
 #endif
@@ -428,8 +452,8 @@ __global__ void __launch_bounds__(um::THREADS, 1) lut_umma_kernel(
         }
 #ifdef UM_EXP_TIMING
         if (blockIdx.x == 0 && lane == 0)
-            printf("mma warp chunks %u: afull-wait %lld issue %lld accempty-wait %lld total %lld\n", k, m_af, m_iss,
-                   m_acc, clock64() - m_t0);
+            printf("mma warp %d chunks %u: afull-wait %lld issue %lld accempty-wait %lld total %lld\n", warp, k, m_af,
+                   m_iss, m_acc, clock64() - m_t0);
 #endif
     } else {
         // ------------------------------------------------------------ expanders
@@ -919,7 +943,7 @@ cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales,
                              (int)smem);
         attr = true;
     }
-    launch_pdl(lut_umma_kernel<P, MERGED, GEO, NARROW>, umma_grid(), um::THREADS, smem, st,
+    launch_pdl(lut_umma_kernel<P, MERGED, GEO, NARROW>, umma_grid(), UmWarps<P, MERGED>::THREADS, smem, st,
         bfrag, n_tiles, scales, sums, offsets, (int)n_seg, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
         b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, b ? 2 : 1, (int)d_in,
         (int)d_out, (int)a->group_size, part, cnt);

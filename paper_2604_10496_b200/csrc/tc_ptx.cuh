@@ -199,6 +199,47 @@ __device__ __forceinline__ void tc_mma_chunk(uint32_t d0, uint32_t nt, uint32_t 
 #undef CQ_MMA1
 
 
+// One digit plane of a merged-layout chunk: KS MMAs into the plane's accumulator d, A k-step kk at
+// a0 + kk * astride, B k-step kk at bdesc0 advanced kk * 256 bytes (per-plane MMA warps).
+template <int KS>
+__device__ __forceinline__ void tc_mma_plane(uint32_t d, uint32_t a0, uint32_t astride, uint64_t bdesc0, uint32_t idesc,
+                                             uint32_t acc) {
+    static_assert(KS == 4 || KS == 2, "chunk shapes of the merged layouts");
+    if constexpr (KS == 4) {
+        asm volatile(
+            "{\n\t.reg .pred e, f, on;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+            "setp.ne.b32 f, %5, 0;\n\tsetp.eq.b32 on, 0, 0;\n\t"
+            "add.u32 a1, %1, %2;\n\tadd.u32 a2, a1, %2;\n\tadd.u32 a3, a2, %2;\n\t"
+            "add.u64 b1, %3, 16;\n\tadd.u64 b2, %3, 32;\n\tadd.u64 b3, %3, 48;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %3, %4, f;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, on;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a2], b2, %4, on;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a3], b3, %4, on;\n\t}" ::"r"(d),
+            "r"(a0), "r"(astride), "l"(bdesc0), "r"(idesc), "r"(acc)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, f, on;\n\t.reg .b32 a1;\n\t.reg .b64 b1;\n\t"
+            "setp.ne.b32 f, %5, 0;\n\tsetp.eq.b32 on, 0, 0;\n\t"
+            "add.u32 a1, %1, %2;\n\tadd.u64 b1, %3, 16;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %3, %4, f;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, on;\n\t}" ::"r"(d),
+            "r"(a0), "r"(astride), "l"(bdesc0), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+}
+
+// Arrive `count` times on an mbarrier from one elected lane of a converged warp.
+__device__ __forceinline__ void u_bar_arrive_cnt_elect(uint32_t bar, uint32_t count) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
+        "r"(count)
+        : "memory");
+}
+
 __device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
