@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
         int u, c0, c1;
 #ifdef UM_EXP_TIMING
         long long t_wait = 0, t_exp = 0, t_st = 0, t_epi = 0, t_afree = 0, t_begin = clock64();
+        long long t_eacc = 0, t_esplit = 0, t_eld = 0, t_est = 0;
         int n_ch = 0;
 #endif
         for (; q.next(W, u, c0, c1); ++nu) {
@@ -602,6 +603,9 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
 #endif
             // ---- epilogue of this unit.  Warpgroup wg owns token columns cb + 32 i (i < NCB).
             u_bar_wait(u_smem(&accfull_bar), nu & 1);
+#ifdef UM_EXP_TIMING
+            t_eacc += clock64() - te0;
+#endif
             tc_fence_after();
             const UmUnit x = um_unit(W, seg_first, u, seg, TPP);  // re-decoded (smem) rather than kept live
             const int n = ((x.ntc + 1) & ~1) * 8;
@@ -652,12 +656,17 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
             auto store = [&](int i, const int32_t (&acc)[P][8]) {
                 const int cbi = cb + 32 * i;
                 float *out = x.mat ? out1 : out0;
-                const float *tscale = reinterpret_cast<const float *>(tok_sh[warp][i]);
-                const int32_t *tqsum = reinterpret_cast<const int32_t *>(tok_sh[warp][i]) + 8;
+                // the block's 8 token scales and code sums (smem, two vector loads each); entries of
+                // tokens outside [rb, re) are stale and their results are never stored
+                const float4 sa = *reinterpret_cast<const float4 *>(&tok_sh[warp][i][0]);
+                const float4 sb = *reinterpret_cast<const float4 *>(&tok_sh[warp][i][4]);
+                const int4 qa = *reinterpret_cast<const int4 *>(&tok_sh[warp][i][8]);
+                const int4 qb = *reinterpret_cast<const int4 *>(&tok_sh[warp][i][12]);
+                const float tscale[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+                const int32_t tqsum[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+                float v[8];
 #pragma unroll
-                for (int c2 = 0; c2 < 8; ++c2) {
-                    const int64_t tok = x.j0 * 8 + cbi + c2;
-                    if (tok < x.rb || tok >= x.re) continue;
+                for (int c2 = 0; c2 < 8; ++c2) {  // branch-free, so the 8 conversion chains overlap
                     double sum;
                     if (MERGED) {
                         // exact integer digit sum (|.| < 2^39) in int64, one conversion: the same double
@@ -672,8 +681,17 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
 #pragma unroll
                         for (int p = P - 2; p >= 0; --p) sum = sum * 255.0 + (double)acc[p][c2];
                     }
-                    const float v2 = (float)(sum * (double)rscale);
-                    out[tok * d_out + (int64_t)x.rt * 128 + row] = __fmul_rn(v2, tscale[c2]);
+                    v[c2] = __fmul_rn((float)(sum * (double)rscale), tscale[c2]);
+                }
+                const int64_t tok0 = x.j0 * 8 + cbi;
+                float *o = out + tok0 * d_out + (int64_t)x.rt * 128 + row;
+                if (tok0 >= x.rb && tok0 + 8 <= x.re) {
+#pragma unroll
+                    for (int c2 = 0; c2 < 8; ++c2) o[(int64_t)c2 * d_out] = v[c2];
+                } else {
+#pragma unroll
+                    for (int c2 = 0; c2 < 8; ++c2)
+                        if (tok0 + c2 >= x.rb && tok0 + c2 < x.re) o[(int64_t)c2 * d_out] = v[c2];
                 }
             };
             if constexpr (NCB == 1) {
@@ -695,6 +713,9 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                 if (finish && cb < n) store(0, acc);
             } else {
                 // several blocks: read TMEM block by block, release it after the last
+#ifdef UM_EXP_TIMING
+                const long long e0 = clock64();
+#endif
                 bool finish = true;
                 if (split) {
 #pragma unroll 1
@@ -708,16 +729,31 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                 }
                 asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
+#ifdef UM_EXP_TIMING
+                const long long e1 = clock64();
+                t_esplit += e1 - e0;
+                long long tl = 0;
+#endif
                 if (finish) {
 #pragma unroll 1
                     for (int i = 0; i < NCB; ++i) {
                         if (cb + 32 * i >= n) break;
                         int32_t acc[P][8];
+#ifdef UM_EXP_TIMING
+                        const long long l0 = clock64();
+#endif
                         load_acc(cb + 32 * i, acc);
+#ifdef UM_EXP_TIMING
+                        tl += clock64() - l0;
+#endif
                         if (split) add_partials(cb + 32 * i, acc);
                         store(i, acc);
                     }
                 }
+#ifdef UM_EXP_TIMING
+                t_eld += tl;
+                t_est += clock64() - e1 - tl;
+#endif
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
@@ -729,8 +765,9 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
 #ifdef UM_EXP_TIMING
         if (blockIdx.x == 0 && lane == 0)
             printf("warp %2d chunks %d: full-wait %lld expand %lld (of which afree-wait %lld) wait_st %lld epilogue %lld "
-                   "(cycles, total %lld)\n",
-                   warp, n_ch, t_wait, t_exp, t_afree, t_st, t_epi, clock64() - t_begin);
+                   "[acc-wait %lld split %lld tmem-ld %lld store %lld] (cycles, total %lld)\n",
+                   warp, n_ch, t_wait, t_exp, t_afree, t_st, t_epi, t_eacc, t_esplit, t_eld, t_est,
+                   clock64() - t_begin);
 #endif
     }
     tc_fence_before();
