@@ -293,10 +293,7 @@ struct RouteFuse {
 // W / x chunks by cp.async (NR buffers) and write the rounded products
 // fmul(x[t][j], w[j][e]) of the next chunk into the other product buffer.
 // Summation order and rounding are those of router_deq_kernel (bit-exact).
-#ifndef RC_KCOLS
-#define RC_KCOLS 256
-#endif
-constexpr int RC_THREADS = 128, RC_K = RC_KCOLS, RC_PITCH = RC_K + 4;
+constexpr int RC_THREADS = 128, RC_K = 256, RC_PITCH = RC_K + 4;
 // raw stages: W leaves L2 under the expert weight stream, so chunks come from
 // DRAM; prefetch NR - 1 chunks (~0.55 us of chain each) ahead
 template <int EG>
@@ -347,13 +344,7 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
                                                                   const float *__restrict__ w, int64_t n,
                                                                   int64_t d, int64_t n_exp, int tt,
                                                                   float *__restrict__ logits, RouteFuse f) {
-#ifdef RC_EXP_TIMING
-    const long long ph_launch = clock64();
-#endif
     griddep_wait();
-#ifdef RC_EXP_TIMING
-    const long long ph0 = clock64();
-#endif
     extern __shared__ __align__(16) float rcs[];
     const int nc = tt * EG;                      // chains
     float *pbuf = rcs;                           // [2][nc][PITCH] products
@@ -392,9 +383,6 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
         const float *wb = wraw + (i % NR) * KC * EG;
         const float *xb = xraw + (i % NR) * tt * KC;
         float *pb = pbuf + (i & 1) * nc * PITCH;
-#ifdef RC_EXP_NO_PRODUCE
-        return;
-#endif
         for (int j = ptid; j < kn; j += RC_THREADS - 32) {
             float wr[EG];
 #pragma unroll
@@ -416,14 +404,8 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
         produce(0);
     }
     __syncthreads();
-#ifdef RC_EXP_TIMING
-    const long long ph1 = clock64();
-#endif
     const bool chain = tid < nc;
     float acc = 0.0f;
-#ifdef RC_EXP_CHUNKS
-    __shared__ long long chunk_t[64];
-#endif
     for (int i = 0; i < n_chunks; ++i) {
         if (tid >= 32) {
             if (i + 1 < n_chunks) {
@@ -439,27 +421,8 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
             else
                 acc = chain_add<0>(acc, pr, kn);
         }
-#ifndef RC_EXP_NO_SYNC
         __syncthreads();  // product buffer i & 1 is rewritten by iteration i + 1's producers
-#endif
-#ifdef RC_EXP_CHUNKS
-        if (tid == 0 && i < 64) {
-            asm volatile("" : "+f"(acc));
-            chunk_t[i] = clock64();
-        }
-#endif
     }
-#ifdef RC_EXP_CHUNKS
-    if (tid == 0 && blockIdx.x == 0) {
-        printf("chunks:");
-        for (int i = 1; i < n_chunks && i < 64; ++i) printf(" %lld", chunk_t[i] - chunk_t[i - 1]);
-        printf("\n");
-    }
-#endif
-#ifdef RC_EXP_TIMING
-    asm volatile("" : "+f"(acc));
-    const long long ph2 = clock64();
-#endif
     if (chain && t0 + tid / EG < n) logits[(t0 + tid / EG) * n_exp + e0 + tid % EG] = acc;
     if constexpr (FUSE) {
         __shared__ float lg[32];  // [tt][EG]
