@@ -202,8 +202,9 @@ CQ_API cq_status cq_moe_combine(const int32_t *selected, const float *weights, c
  * experts, scatter, exchange, combine) can be captured in one CUDA graph.
  *
  * Every rank sends each peer `capacity` slots of cq_ep_row_bytes(d_model)
- * bytes ([codes][f32 scale][i32 local expert id][pad]; id -1 = empty), so both
- * exchanges are equal-split all_to_alls.  capacity >= n_tokens *
+ * bytes ([codes][f32 scale][i32 local expert id][pad]; id -1 = empty; codes
+ * as packed nibbles when d_model % 32 == 0, else int8), so both exchanges are
+ * equal-split all_to_alls.  capacity >= n_tokens *
  * min(top_k, experts_per_rank).  Experts [r*per, (r+1)*per) live on rank r. */
 CQ_API int64_t cq_ep_row_bytes(int64_t d_model);
 /* Scratch bytes for cq_ep_dispatch / cq_ep_group with these sizes. */

@@ -4,8 +4,10 @@
 //
 // Slots.  Every rank sends every peer a fixed block of `capacity` rows, so the
 // exchanges are equal-split all_to_alls (or peer-memory copies).  A row is
-// [d_model code bytes][f32 scale][i32 local expert id][8 pad bytes]; unused
-// slots carry expert id -1.  capacity >= n_tokens * min(top_k,
+// [codes][f32 scale][i32 local expert id][8 pad bytes]; unused slots carry
+// expert id -1.  The codes are A4 values in [-8, 7], sent as packed nibbles
+// (d_model / 2 bytes, low nibble first, the reference's int4 format) when
+// d_model % 32 == 0, else one byte each.  capacity >= n_tokens * min(top_k,
 // experts_per_rank) is enough for any routing (a token's top-k experts are
 // distinct, so it sends at most min(k, per) routes to one rank).
 //
@@ -98,26 +100,55 @@ cq_status bucket_rank(const KeySrc &ks, int64_t n, int nb, int32_t *rank, int32_
 
 // Send rows: slot s = (dst, p).  Filled slots copy the token's codes, scale
 // and local expert id; empty slots get expert id -1.  Also inv[route] = slot.
+__host__ __device__ inline bool ep_packed(int64_t d) { return d % 32 == 0; }
+__host__ __device__ inline int64_t ep_code_bytes(int64_t d) { return ep_packed(d) ? d / 2 : d; }
+
+// 8 int8 codes (two words) -> 8 nibbles, low first
+__device__ __forceinline__ uint32_t nib_pack8(uint32_t a, uint32_t b) {
+    uint32_t x = a & 0x0F0F0F0Fu, y = b & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    y = (y | (y >> 4)) & 0x00FF00FFu;
+    x = (x | (x >> 8)) & 0x0000FFFFu;
+    y = (y | (y >> 8)) & 0x0000FFFFu;
+    return x | (y << 16);
+}
+// 4 nibbles (low 16 bits) -> 4 sign-extended int8 codes
+__device__ __forceinline__ uint32_t nib_unpack4(uint32_t h) {
+    uint32_t y = h & 0xFFFFu;
+    y = (y | (y << 8)) & 0x00FF00FFu;
+    y = (y | (y << 4)) & 0x0F0F0F0Fu;
+    return __vsub4(y ^ 0x08080808u, 0x08080808u);  // per byte: (n ^ 8) - 8, no borrow across bytes
+}
+
 __global__ void ep_pack_kernel(const int8_t *__restrict__ codes, const float *__restrict__ scales,
                                const int32_t *__restrict__ selected, const int32_t *__restrict__ rank, int64_t R,
                                int64_t k, int64_t d, int32_t per, const int32_t *__restrict__ counts,
                                const int32_t *__restrict__ slot_route, int64_t cap, int64_t slots,
                                uint8_t *__restrict__ send, int32_t *__restrict__ inv) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    const int64_t pieces = d / 16 + 1, total = slots * pieces;
+    const int64_t cb = ep_code_bytes(d), cp = cb / 16;  // code pieces of 16 bytes
+    const int64_t pieces = cp + 1, total = slots * pieces;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += stride) {
         const int64_t s = x / pieces, pc = x - s * pieces;
         const int64_t dst = s / cap, p = s - dst * cap;
-        uint4 *out = reinterpret_cast<uint4 *>(send + s * (d + 16)) + pc;
+        uint4 *out = reinterpret_cast<uint4 *>(send + s * (cb + 16)) + pc;
         if (p < counts[dst]) {
             const int32_t r = slot_route[s];
             const int64_t t = r / k;
-            if (pc < d / 16)
-                *out = reinterpret_cast<const uint4 *>(codes + t * d)[pc];
-            else
+            if (pc < cp) {
+                if (ep_packed(d)) {  // 32 codes -> 16 bytes
+                    const uint4 *src = reinterpret_cast<const uint4 *>(codes + t * d) + 2 * pc;
+                    const uint4 u = src[0], v = src[1];
+                    *out = make_uint4(nib_pack8(u.x, u.y), nib_pack8(u.z, u.w), nib_pack8(v.x, v.y),
+                                      nib_pack8(v.z, v.w));
+                } else {
+                    *out = reinterpret_cast<const uint4 *>(codes + t * d)[pc];
+                }
+            } else {
                 *out = make_uint4(__float_as_uint(scales[t]), (uint32_t)(selected[r] % per), 0u, 0u);
-        } else if (pc == d / 16) {
+            }
+        } else if (pc == cp) {
             *out = make_uint4(0u, 0xffffffffu, 0u, 0u);
         }
     }
@@ -131,16 +162,23 @@ __global__ void ep_group_kernel(const uint8_t *__restrict__ recv, int64_t slots,
                                 int8_t *__restrict__ codes_perm, float *__restrict__ scales_perm,
                                 int32_t *__restrict__ slot_of_row) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    const int64_t pieces = d / 16, total = slots * pieces;
+    const int64_t cb = ep_code_bytes(d), pieces = cb / 16, total = slots * pieces;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = x / pieces, pc = x - s * pieces;
-        const uint8_t *row = recv + s * (d + 16);
-        const int32_t e = *reinterpret_cast<const int32_t *>(row + d + 4);
+        const uint8_t *row = recv + s * (cb + 16);
+        const int32_t e = *reinterpret_cast<const int32_t *>(row + cb + 4);
         if (e < 0) continue;
         const int64_t pos = offsets[e] + rank[s];
-        reinterpret_cast<uint4 *>(codes_perm + pos * d)[pc] = reinterpret_cast<const uint4 *>(row)[pc];
+        const uint4 w = reinterpret_cast<const uint4 *>(row)[pc];
+        if (ep_packed(d)) {  // 16 bytes -> 32 codes
+            uint4 *dst = reinterpret_cast<uint4 *>(codes_perm + pos * d) + 2 * pc;
+            dst[0] = make_uint4(nib_unpack4(w.x), nib_unpack4(w.x >> 16), nib_unpack4(w.y), nib_unpack4(w.y >> 16));
+            dst[1] = make_uint4(nib_unpack4(w.z), nib_unpack4(w.z >> 16), nib_unpack4(w.w), nib_unpack4(w.w >> 16));
+        } else {
+            reinterpret_cast<uint4 *>(codes_perm + pos * d)[pc] = w;
+        }
         if (pc == 0) {
-            scales_perm[pos] = *reinterpret_cast<const float *>(row + d);
+            scales_perm[pos] = *reinterpret_cast<const float *>(row + cb);
             slot_of_row[pos] = (int32_t)s;
         }
     }
@@ -171,7 +209,7 @@ EpScratch ep_carve(void *scratch, int64_t items, int64_t buckets) {
 
 using namespace cq;
 
-extern "C" int64_t cq_ep_row_bytes(int64_t d_model) { return d_model + 16; }
+extern "C" int64_t cq_ep_row_bytes(int64_t d_model) { return ep_code_bytes(d_model) + 16; }
 
 extern "C" int64_t cq_ep_scratch_bytes(int64_t n_tokens, int64_t top_k, int32_t world, int64_t capacity,
                                        int64_t n_local) {
@@ -218,7 +256,8 @@ extern "C" cq_status cq_ep_group(const uint8_t *recv, int64_t slots, int64_t d_m
     }
     cudaStream_t st = as_stream(stream);
     EpScratch s = ep_carve(scratch, std::max<int64_t>(slots, 1), n_local);
-    const KeySrc ks{reinterpret_cast<const int32_t *>(recv + d_model + 4), (d_model + 16) / 4, 1};
+    const int64_t cb = ep_code_bytes(d_model);  // expert id after the codes and the scale
+    const KeySrc ks{reinterpret_cast<const int32_t *>(recv + cb + 4), (cb + 16) / 4, 1};
     CQ_TRY(bucket_rank(ks, slots, (int)n_local, s.rank, s.counts, offsets, nullptr, 0, st));
     const int64_t total = slots * (d_model / 16);
     if (total == 0) return CQ_OK;

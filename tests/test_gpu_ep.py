@@ -141,6 +141,22 @@ def test_ep_step_slots_match_single_gpu_layer(world, n_tok, E, k, path):
     assert torch.equal(got, want)
 
 
+def test_ep_step_unpacked_slots_for_odd_width():
+    """d_model % 32 != 0 (1040) sends int8 codes instead of packed nibbles; the
+    step is still bitwise equal to the single-GPU layer (fp32 path, g = 16)."""
+    world, n_tok, E, k, d, ff, g = 2, 20, 8, 2, 1040, 256, 16
+    v, w, sites, _ = moe_inputs_device(37, n_tok * world, d, ff, E, g)
+    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    ref = MoELayer.from_stacks(w, *full, top_k=k, path="f32")
+    want = ref(v).clone()
+    layers = _sharded_layers(w, full, E, k, world, "f32")
+    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
+    assert steps[0].send.shape[-1] == d + 16  # int8 codes
+    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
 @pytest.mark.parametrize("geometry", ["prefill", "decode"])
 @pytest.mark.parametrize("world,n_tok", [(4, 48), (8, 32)])
 def test_ep_step_rank_gemm_geometries(monkeypatch, geometry, world, n_tok):
@@ -156,6 +172,7 @@ def test_ep_step_rank_gemm_geometries(monkeypatch, geometry, world, n_tok):
     monkeypatch.setenv("CQ_UMMA_GEOMETRY", geometry)
     layers = _sharded_layers(w, full, E, k, world)
     steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
+    assert steps[0].send.shape[-1] == d // 2 + 16  # codes as packed nibbles
     got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
     torch.cuda.synchronize()
     assert torch.equal(got, want)
