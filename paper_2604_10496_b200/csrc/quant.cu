@@ -70,6 +70,82 @@ __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict
     }
 }
 
+// Same quantizer with the row held in registers (d % 4 == 0, d <= 8192): 256
+// threads x V groups of 4 values, loaded once with 16-byte (fp32) / 8-byte
+// (bf16) loads; codes, dequantized values and code sums as before.
+template <int DT, int V>
+__global__ void __launch_bounds__(256) quantize_a4_vec_kernel(const void *__restrict__ x, int64_t d,
+                                                              int8_t *__restrict__ codes,
+                                                              float *__restrict__ scales,
+                                                              int *__restrict__ nonfinite,
+                                                              float *__restrict__ deq, int32_t *__restrict__ tsum,
+                                                              int32_t *__restrict__ zero, int n_zero) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
+    const int64_t row = blockIdx.x;
+    if (row == 0)
+        for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
+    const int nv = (int)(d >> 2);
+    float h[V][4];
+    float mx = 0.0f;
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+        const int j = threadIdx.x + u * 256;
+        if (j < nv) {
+            if (DT == CQ_DTYPE_F32) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(x) + row * nv + j);
+                h[u][0] = v.x, h[u][1] = v.y, h[u][2] = v.z, h[u][3] = v.w;
+            } else {
+                const uint2 v = __ldg(reinterpret_cast<const uint2 *>(x) + row * nv + j);
+                h[u][0] = __uint_as_float(v.x << 16), h[u][1] = __uint_as_float(v.x & 0xFFFF0000u);
+                h[u][2] = __uint_as_float(v.y << 16), h[u][3] = __uint_as_float(v.y & 0xFFFF0000u);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bad |= !isfinite(h[u][q]);
+                mx = fmaxf(mx, fabsf(h[u][q]));
+            }
+        }
+    }
+    __shared__ float red[8];
+    __shared__ float s_sh;
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float m = threadIdx.x < 8 ? red[threadIdx.x] : 0.0f;
+        m = warp_max(m);
+        if (threadIdx.x == 0) {
+            const float sc = a4_scale(m);
+            s_sh = sc;
+            scales[row] = sc;
+        }
+    }
+    __syncthreads();
+    const float sc = s_sh;
+    int csum = 0;
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+        const int j = threadIdx.x + u * 256;
+        if (j < nv) {
+            const char4 c = make_char4(a4_code(h[u][0], sc), a4_code(h[u][1], sc), a4_code(h[u][2], sc),
+                                       a4_code(h[u][3], sc));
+            reinterpret_cast<char4 *>(codes + row * d)[j] = c;
+            csum += c.x + c.y + c.z + c.w;
+            // dequantized value, rounded exactly as codes.astype(f32) * scales (model.py:379-381)
+            if (deq != nullptr)
+                reinterpret_cast<float4 *>(deq + row * d)[j] =
+                    make_float4(__fmul_rn((float)c.x, sc), __fmul_rn((float)c.y, sc), __fmul_rn((float)c.z, sc),
+                                __fmul_rn((float)c.w, sc));
+        }
+    }
+    if (tsum != nullptr) {
+        const int t = block_sum_int(csum);
+        if (threadIdx.x == 0) tsum[row] = t;
+    }
+}
+
 __global__ void unpack_ids_kernel(const uint8_t *__restrict__ packed, int64_t rows, int64_t d_in,
                                   uint8_t *__restrict__ ids) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
@@ -88,6 +164,21 @@ __global__ void unpack_ids_kernel(const uint8_t *__restrict__ packed, int64_t ro
 cq_status quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes, float *scales,
                       int *nonfinite_dev, float *deq, cudaStream_t st, int32_t *tsum, int32_t *zero, int n_zero) {
     if (n == 0) return CQ_OK;
+    if (d % 4 == 0 && d <= 8 * 1024) {  // row in registers
+        const int64_t v = ceil_div(d / 4, 256);
+#define CQ_QVEC(DT_, V_)                                                                                          \
+    launch_pdl(quantize_a4_vec_kernel<DT_, V_>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq, \
+               tsum, zero, n_zero)
+        if (dtype == CQ_DTYPE_F32) {
+            if (v == 1) CQ_QVEC(CQ_DTYPE_F32, 1); else if (v == 2) CQ_QVEC(CQ_DTYPE_F32, 2);
+            else if (v <= 4) CQ_QVEC(CQ_DTYPE_F32, 4); else CQ_QVEC(CQ_DTYPE_F32, 8);
+        } else {
+            if (v == 1) CQ_QVEC(CQ_DTYPE_BF16, 1); else if (v == 2) CQ_QVEC(CQ_DTYPE_BF16, 2);
+            else if (v <= 4) CQ_QVEC(CQ_DTYPE_BF16, 4); else CQ_QVEC(CQ_DTYPE_BF16, 8);
+        }
+#undef CQ_QVEC
+        return check_launch("quantize_a4");
+    }
     if (dtype == CQ_DTYPE_F32)
         launch_pdl(quantize_a4_kernel<CQ_DTYPE_F32>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq,
                    tsum, zero, n_zero);
