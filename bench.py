@@ -431,6 +431,32 @@ def run_ep(args, rank, world, local):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
 
+    # phase breakdown (eager, CUDA events on the step's stream, max over ranks): how much of a step
+    # the two exchanges take; both are exposed in this design (SURVEY 8(e) scaling report)
+    names = ("route_dispatch", "exchange_out", "experts", "exchange_back", "combine")
+    ph = torch.zeros(len(names), device="cuda")
+    n_ph = max(3, min(args.steps, 20))
+    with torch.cuda.stream(stream):
+        for _ in range(n_ph):
+            barrier()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+            ev[0].record(stream)
+            step.route_and_pack(v)
+            ev[1].record(stream)
+            step.a2a(step.recv, step.send)
+            ev[2].record(stream)
+            step.run_experts()
+            ev[3].record(stream)
+            step.a2a(step.ret, step.back)
+            ev[4].record(stream)
+            step.combine()
+            ev[5].record(stream)
+            ev[5].synchronize()
+            ph += torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(len(names))], device="cuda")
+    ph /= n_ph
+    if world > 1:
+        dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+    ep_phases = {nm: round(float(x), 4) for nm, x in zip(names, ph.tolist())}
     with torch.cuda.stream(stream):
         step(v)
         n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, step.codes_perm, step.scales_perm,
@@ -461,6 +487,11 @@ def run_ep(args, rank, world, local):
                          "stage_ms": {"gate_up": gu_ms, "silu_requant": rq_ms, "down": dn_ms}},
             "clocks": clk.summary(),
             "gpu_launches": int(launches_per_step * args.steps),
+            "ep": {"phases_ms": ep_phases, "comm_exposed_ms": round(ep_phases["exchange_out"]
+                                                                   + ep_phases["exchange_back"], 4),
+                   "exchange_bytes_per_rank": {"out": int(step.send.numel()), "back": int(step.back.numel() * 4)},
+                   "note": "phases timed eagerly with CUDA events, max over ranks; equal-split NCCL "
+                           "all_to_all over fixed-capacity slots, both exchanges exposed"},
         }
         emit(res)
     dist.destroy_process_group()
