@@ -698,10 +698,17 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                 // one block: keep it in registers and release TMEM at once, so the MMAs of the next
                 // unit overlap this epilogue
                 int32_t acc[P][8];
+#ifdef UM_EXP_TIMING
+                const long long f0 = clock64();
+#endif
                 if (cb < n) load_acc(cb, acc);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
+#ifdef UM_EXP_TIMING
+                const long long f1 = clock64();
+                t_eld += f1 - f0;
+#endif
                 bool finish = true;
                 if (split) {
                     if (cb < n) publish(cb, acc);
@@ -710,7 +717,14 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                 }
                 asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
+#ifdef UM_EXP_TIMING
+                const long long f2 = clock64();
+                t_esplit += f2 - f1;
+#endif
                 if (finish && cb < n) store(0, acc);
+#ifdef UM_EXP_TIMING
+                t_est += clock64() - f2;
+#endif
             } else {
                 // several blocks: read TMEM block by block, release it after the last
 #ifdef UM_EXP_TIMING
