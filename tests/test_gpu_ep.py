@@ -223,3 +223,26 @@ def test_ep_step_world1_nccl_graph_capture(nccl_world1):
     torch.cuda.synchronize()
     assert torch.equal(eager, want)
     assert torch.equal(step.out, want)
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_ep_step_random_shapes(i):
+    """Random world size, expert count, top-k, batch and width: the sharded EP
+    step (in-process ranks) bitwise equal to the single-GPU layer."""
+    rng = np.random.default_rng(700 + i)
+    world = int(rng.choice([2, 4, 8]))
+    E = world * int(rng.choice([1, 2, 4]))
+    k = int(rng.integers(1, min(4, E) + 1))
+    n_tok = int(rng.choice([1, 7, 32, 50]))
+    d = int(rng.choice([512, 1024]))
+    ff, g = 512, 128
+    v, w, sites, _ = moe_inputs_device(800 + i, n_tok * world, d, ff, E, g)
+    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
+    ref.prepare_tc()
+    want = ref(v).clone()
+    layers = _sharded_layers(w, full, E, k, world)
+    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
+    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
