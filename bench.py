@@ -142,6 +142,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
+SPEC_HBM_GBS, SPEC_BF16_TFLOPS = 8000.0, 2250.0  # B200 data-sheet HBM3e bandwidth, dense bf16
+
+
 def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -482,6 +485,7 @@ def run_ep(args, rank, world, local):
             "roofline": {"bound": "hbm", "kernel": "rank 0's grouped gate|up LUT GEMM (lut_umma_kernel)",
                          "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"] if achieved else None, "peak_src": pk["src"],
+                         "peak_spec": SPEC_HBM_GBS, "frac_spec": achieved / SPEC_HBM_GBS if achieved else None,
                          "traffic": None, "algorithmic_bytes": byt["gate_up"], "kernel_ms": gu_ms,
                          "rows_received": R, "active_local_experts": n_active,
                          "stage_ms": {"gate_up": gu_ms, "silu_requant": rq_ms, "down": dn_ms}},
@@ -632,6 +636,8 @@ def run_ours(args):
                          "kernel": "grouped gate|up LUT GEMM (lut_umma_kernel<3>, tcgen05 kind::i8, A from TMEM)",
                          "achieved": achieved, "peak": peak_v, "unit": unit,
                          "frac": achieved / peak_v, "peak_src": pk["src"],
+                         "peak_spec": SPEC_BF16_TFLOPS if tensor_bound else SPEC_HBM_GBS,
+                         "frac_spec": achieved / (SPEC_BF16_TFLOPS if tensor_bound else SPEC_HBM_GBS),
                          "traffic": traffic, "algorithmic_bytes": byt["gate_up"], "kernel_ms": gu_ms,
                          "bytes_def": "SURVEY 8(d): ids d_out*d_in/2 + fp32 centroids d_out*(d_in/g)*64 per active "
                                       "expert and matrix, + codes/scales in + fp32 outputs",
