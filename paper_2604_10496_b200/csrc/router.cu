@@ -141,21 +141,30 @@ __global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__r
     if (live) logits[(t0 + t_loc) * n_exp + e] = acc;
 }
 
-// Many experts (E in {32, 64, 128}): thread = (token group, expert), TPT
-// independent token chains per thread, so a staged W element is reused TPT
-// times instead of once (with one chain per thread every CTA streams all of W
-// for a single token).  Each chain is still one ordered fp32 add per column.
-template <int EC, int TPT>
-__global__ void __launch_bounds__(RD_THREADS) router_multi_kernel(const float *__restrict__ xdeq,
-                                                                  const float *__restrict__ w, int64_t n, int64_t d,
-                                                                  int rk, float *__restrict__ logits) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    constexpr int TG = RD_THREADS / EC;  // token groups per CTA
-    constexpr int TT = TG * TPT;         // tokens per CTA
-    extern __shared__ __align__(16) float rds[];
-    float *xs = rds;                          // [2][TT][rk]
-    float *ws = rds + (size_t)2 * TT * rk;    // [2][rk][EC]
-    const int tid = threadIdx.x, e = tid % EC, tg = tid / EC;
+// Many experts (E in {32, 64, 128}) at prefill sizes: each thread runs TI x 4
+// ordered chains, TI consecutive tokens x 4 consecutive experts, so a step of
+// 4 columns costs TI x-row and 4 w-row 128-bit loads (4 x 4: 8 loads for 128
+// fp32 operations; one expert x 16 tokens per thread needed 20).  Each chain
+// adds its products in column order (one ordered fp32 add per column), so the
+// logits are bit-identical to _core.matmul_f32.
+// CTA: blockDim (<= 256) threads = EC / 4 expert quads x token groups.  Every
+// CTA streams all of w through shared memory, so the host sizes the token tile
+// to one CTA per SM (QW: 124 us with 16-token tiles on 2 CTAs per SM, 115 us
+// with 32 on 128 SMs, 28 on 147 SMs below; profiles/README.md).
+template <int EC, int TI>
+__global__ void __launch_bounds__(256) router_tile_kernel(const float *__restrict__ xdeq,
+                                                                 const float *__restrict__ w, int64_t n, int64_t d,
+                                                                 int rk, float *__restrict__ logits) {
+    griddep_wait();
+    constexpr int EQ = EC / 4;                 // expert quads
+    const int NT = blockDim.x;
+    const int TQ = NT / EQ;                    // token groups of TI
+    const int TT = TI * TQ;                    // tokens per CTA
+    extern __shared__ __align__(16) float rts[];
+    const int xp = rk + 4;                     // x row pitch: token quads' rows on different banks
+    float *xs = rts;                           // [2][TT][xp]
+    float *ws = rts + (size_t)2 * TT * xp;     // [2][rk][EC]
+    const int tid = threadIdx.x, eq = tid % EQ, tq = tid / EQ;
     const int64_t t0 = blockIdx.x * (int64_t)TT;
     const int n_chunks = (int)((d + rk - 1) / rk);
     auto stage = [&](int i) {
@@ -163,20 +172,22 @@ __global__ void __launch_bounds__(RD_THREADS) router_multi_kernel(const float *_
         const int64_t k0 = (int64_t)i * rk;
         const int kn = (int)((d - k0) < rk ? (d - k0) : rk);
         float *wsb = ws + (size_t)b * rk * EC;
-        for (int x = tid; x < kn * EC / 4; x += RD_THREADS) cp_async16(wsb + 4 * x, w + k0 * EC + 4 * x);
+        for (int x = tid; x < kn * EC / 4; x += NT) cp_async16(wsb + 4 * x, w + k0 * EC + 4 * x);
         const int rowv = kn / 4;
-        float *xsb = xs + (size_t)b * TT * rk;
-        for (int x = tid; x < TT * rowv; x += RD_THREADS) {
+        float *xsb = xs + (size_t)b * TT * xp;
+        for (int x = tid; x < TT * rowv; x += NT) {
             const int tl = x / rowv, v = x - tl * rowv;
-            const int64_t tg2 = t0 + tl < n ? t0 + tl : n - 1;  // clamp: rows past n are never stored
-            cp_async16(xsb + tl * rk + 4 * v, xdeq + tg2 * d + k0 + 4 * v);
+            const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // clamp: rows past n are never stored
+            cp_async16(xsb + tl * xp + 4 * v, xdeq + tg * d + k0 + 4 * v);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     stage(0);
-    float acc[TPT];
+    float acc[TI][4];
 #pragma unroll
-    for (int i = 0; i < TPT; ++i) acc[i] = 0.0f;
+    for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[i][m] = 0.0f;
     for (int c = 0; c < n_chunks; ++c) {
         const int b = c & 1;
         if (c + 1 < n_chunks) {
@@ -187,25 +198,34 @@ __global__ void __launch_bounds__(RD_THREADS) router_multi_kernel(const float *_
         }
         __syncthreads();
         const int kn = (int)((d - (int64_t)c * rk) < rk ? (d - (int64_t)c * rk) : rk);  // multiple of 16
-        const float *wr = ws + (size_t)b * rk * EC + e;
-        const float *xr = xs + (size_t)b * TT * rk + (size_t)tg * TPT * rk;
+        const float *wr = ws + (size_t)b * rk * EC + 4 * eq;
+        const float *xr = xs + (size_t)b * TT * xp + (size_t)(TI * tq) * xp;
         for (int j = 0; j < kn; j += 4) {
-            const float w0 = wr[(j + 0) * EC], w1 = wr[(j + 1) * EC], w2 = wr[(j + 2) * EC], w3 = wr[(j + 3) * EC];
+            float4 wv[4], xv[TI];
 #pragma unroll
-            for (int i = 0; i < TPT; ++i) {
-                const float4 xv = *reinterpret_cast<const float4 *>(xr + i * rk + j);
-                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.x, w0));
-                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.y, w1));
-                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.z, w2));
-                acc[i] = __fadd_rn(acc[i], __fmul_rn(xv.w, w3));
+            for (int q = 0; q < 4; ++q) wv[q] = *reinterpret_cast<const float4 *>(wr + (j + q) * EC);
+#pragma unroll
+            for (int i = 0; i < TI; ++i) xv[i] = *reinterpret_cast<const float4 *>(xr + i * xp + j);
+#pragma unroll
+            for (int i = 0; i < TI; ++i) {
+                const float xq[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[i][0] = __fadd_rn(acc[i][0], __fmul_rn(xq[q], wv[q].x));
+                    acc[i][1] = __fadd_rn(acc[i][1], __fmul_rn(xq[q], wv[q].y));
+                    acc[i][2] = __fadd_rn(acc[i][2], __fmul_rn(xq[q], wv[q].z));
+                    acc[i][3] = __fadd_rn(acc[i][3], __fmul_rn(xq[q], wv[q].w));
+                }
             }
         }
         __syncthreads();  // buffer b is refilled by the next iteration's prefetch
     }
 #pragma unroll
-    for (int i = 0; i < TPT; ++i) {
-        const int64_t t = t0 + tg * TPT + i;
-        if (t < n) logits[t * EC + e] = acc[i];
+    for (int i = 0; i < TI; ++i) {
+        const int64_t t = t0 + TI * tq + i;
+        if (t < n)
+            *reinterpret_cast<float4 *>(logits + t * EC + 4 * eq) =
+                make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
     }
 }
 
@@ -528,6 +548,35 @@ cq_status router_fused(const float *xdeq, const float *w, int64_t n, int64_t d, 
     return check_launch("router_fused");
 }
 
+// Token tile: TI x tq tokens, tq groups per expert quad chosen so the grid is about one CTA per SM.
+template <int TI>
+static cq_status router_tile_launch(const float *xdeq, const float *w, int64_t n, int64_t d, int64_t n_exp,
+                                    float *logits, cudaStream_t st) {
+    const int eq = (int)n_exp / 4;
+    const int tq = (int)std::min<int64_t>(256 / eq, std::max<int64_t>(128 / eq, ceil_div(n, 148 * TI)));
+    const int nt = tq * eq, tt = TI * tq;
+    const int64_t ctas = ceil_div(n, tt);
+    const int smem_max = ctas <= 148 ? 200 * 1024 : 96 * 1024;  // one CTA per SM, else two
+    int rk = (int)std::min<int64_t>(512, (smem_max / 8 - 4 * tt) / (tt + n_exp)) & ~15;
+    if (rk < 16) rk = 16;
+    const size_t smem = (size_t)8 * ((size_t)tt * (rk + 4) + (size_t)rk * n_exp);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(router_tile_kernel<32, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<64, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<128, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    const dim3 grid((unsigned)ctas);
+    if (n_exp == 32)
+        launch_pdl(router_tile_kernel<32, TI>, grid, nt, smem, st, xdeq, w, n, d, rk, logits);
+    else if (n_exp == 64)
+        launch_pdl(router_tile_kernel<64, TI>, grid, nt, smem, st, xdeq, w, n, d, rk, logits);
+    else
+        launch_pdl(router_tile_kernel<128, TI>, grid, nt, smem, st, xdeq, w, n, d, rk, logits);
+    return check_launch("router_logits");
+}
+
 // xdeq (nullable): the dequantized rows code * scale from the quantizer.
 cq_status router_logits(const int8_t *codes, const float *scales, const float *xdeq, const float *w, int64_t n,
                         int64_t d, int64_t n_exp, float *logits, cudaStream_t st) {
@@ -538,27 +587,7 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
     }
     if (router_chain(xdeq, w, n, d, n_exp, logits, nullptr, st, nullptr)) return check_launch("router_logits");
     if (xdeq != nullptr && d % 16 == 0 && (n_exp == 32 || n_exp == 64 || n_exp == 128) && n >= 64) {
-        constexpr int TPT = 16;
-        const int tt = (RD_THREADS / (int)n_exp) * TPT;
-        int rk = (int)std::min<int64_t>(512, ((96 * 1024) / (8 * (tt + n_exp))) & ~15LL);
-        if (rk < 16) rk = 16;
-        const size_t smem = (size_t)8 * rk * (tt + n_exp);
-        static bool attr_m = false;
-        if (!attr_m) {
-            cudaFuncSetAttribute(router_multi_kernel<32, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            cudaFuncSetAttribute(router_multi_kernel<64, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            cudaFuncSetAttribute(router_multi_kernel<128, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 96 * 1024);
-            attr_m = true;
-        }
-        const dim3 grid((unsigned)ceil_div(n, tt));
-        if (n_exp == 32)
-            launch_pdl(router_multi_kernel<32, TPT>, grid, RD_THREADS, smem, st, xdeq, w, n, d, rk, logits);
-        else if (n_exp == 64)
-            launch_pdl(router_multi_kernel<64, TPT>, grid, RD_THREADS, smem, st, xdeq, w, n, d, rk, logits);
-        else
-            launch_pdl(router_multi_kernel<128, TPT>, grid, RD_THREADS, smem, st, xdeq, w, n, d, rk, logits);
-        return check_launch("router_logits");
+        return router_tile_launch<4>(xdeq, w, n, d, n_exp, logits, st);
     }
     if (xdeq != nullptr && n_exp <= RD_THREADS && d % 16 == 0) {
         // tokens per CTA: fewer, smaller CTAs stage less per chunk (CQ_ROUTER_TT overrides, experiments)

@@ -128,12 +128,15 @@ def _host_experts(sites, n_exp, g):
     return out
 
 
-@pytest.mark.parametrize("E,k", [(32, 6), (64, 6), (128, 8), (16, 2)])
-def test_router_many_experts_bit_exact(E, k):
-    """Routing at the QW / DS / PH expert counts (the multi-chain router kernel
-    for E in {32, 64, 128}): logits and the selected experts bit-exact with the
-    ordered chain of _core.matmul_f32 + select_top_k; weights ulp-bounded."""
-    n, d, ff, g = 300, 1024, 128, 128
+@pytest.mark.parametrize("E,k,n", [(32, 6, 300), (64, 6, 300), (128, 8, 300), (16, 2, 300), (128, 8, 4100),
+                                   (64, 6, 8200)])
+def test_router_many_experts_bit_exact(E, k, n):
+    """Routing at the QW / DS / PH expert counts (the register-tiled router
+    kernel for E in {32, 64, 128}; 16-token tiles at n = 300, 4096 / E-token
+    tiles with a ragged last one at n * E >= 128 * 4096): logits and the selected
+    experts bit-exact with the ordered chain of _core.matmul_f32 +
+    select_top_k; weights ulp-bounded."""
+    d, ff, g = 1024, 128, 128
     v, w, sites, _ = moe_inputs_device(23 + E, n, d, ff, E, g)
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
     layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="f32")
