@@ -586,9 +586,8 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         return CQ_ERR_CONFIG;
     }
     if (router_chain(xdeq, w, n, d, n_exp, logits, nullptr, st, nullptr)) return check_launch("router_logits");
-    if (xdeq != nullptr && d % 16 == 0 && (n_exp == 32 || n_exp == 64 || n_exp == 128) && n >= 64) {
+    if (xdeq != nullptr && d % 16 == 0 && (n_exp == 32 || n_exp == 64 || n_exp == 128) && n >= 64)
         return router_tile_launch<4>(xdeq, w, n, d, n_exp, logits, st);
-    }
     if (xdeq != nullptr && n_exp <= RD_THREADS && d % 16 == 0) {
         // tokens per CTA: fewer, smaller CTAs stage less per chunk (CQ_ROUTER_TT overrides, experiments)
         static int tt_env = -1;

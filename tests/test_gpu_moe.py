@@ -129,7 +129,7 @@ def _host_experts(sites, n_exp, g):
 
 
 @pytest.mark.parametrize("E,k,n", [(32, 6, 300), (64, 6, 300), (128, 8, 300), (16, 2, 300), (128, 8, 4100),
-                                   (64, 6, 8200)])
+                                   (64, 6, 8200), (16, 2, 4100)])
 def test_router_many_experts_bit_exact(E, k, n):
     """Routing at the QW / DS / PH expert counts (the register-tiled router
     kernel for E in {32, 64, 128}; 16-token tiles at n = 300, 4096 / E-token
