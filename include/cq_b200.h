@@ -134,7 +134,14 @@ typedef struct {
     int32_t path;              /* CQ_PATH_* */
     const void *rotation_tc;   /* optional: R prepared by cq_rotation_prepare (tensor-core rotation);
                                   NULL -> fp32 CUDA-core rotation of `rotation` */
+    int64_t flags;             /* CQ_FLAG_* */
 } cq_moe_desc;
+
+/* CQ_FLAG_KEEP_HIDDEN: the tensor-core path also stores h = silu(a) * b in
+   CQ_WS_HIDDEN (fp32, for tracing / parity checks).  Without it the expert stage
+   writes only the re-quantized h (codes, scales), and CQ_WS_HIDDEN holds the
+   gate output; the f32 and ordered paths always store h. */
+enum { CQ_FLAG_KEEP_HIDDEN = 1 };
 
 enum { CQ_PATH_AUTO = 0, CQ_PATH_F32 = 1, CQ_PATH_TC = 2, CQ_PATH_ORDERED = 3 };
 
@@ -152,7 +159,7 @@ enum {
     CQ_WS_INV,          /* i32  [n][k]         route -> segment row          */
     CQ_WS_CODES_PERM,   /* int8 [n*k][d_model] codes gathered per segment    */
     CQ_WS_SCALES_PERM,  /* f32  [n*k]                                        */
-    CQ_WS_HIDDEN,       /* f32  [n*k][d_ff]    silu(a)*b                     */
+    CQ_WS_HIDDEN,       /* f32  [n*k][d_ff]    silu(a)*b (tc path: CQ_FLAG_KEEP_HIDDEN) */
     CQ_WS_HCODES,       /* int8 [n*k][d_ff]    re-quantized hidden           */
     CQ_WS_HSCALES,      /* f32  [n*k]                                        */
     CQ_WS_FOUT,         /* f32  [n*k][d_model] per-route down output         */

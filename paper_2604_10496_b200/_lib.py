@@ -45,7 +45,10 @@ class MoEDesc(ctypes.Structure):
                 ("gate", ExpertSite), ("up", ExpertSite), ("down", ExpertSite),
                 ("n_shared", _i64),
                 ("sh_gate", ExpertSite), ("sh_up", ExpertSite), ("sh_down", ExpertSite),
-                ("path", _i32), ("rotation_tc", _vp)]
+                ("path", _i32), ("rotation_tc", _vp), ("flags", _i64)]
+
+
+FLAG_KEEP_HIDDEN = 1  # CQ_FLAG_KEEP_HIDDEN
 
 
 _SIGS = {

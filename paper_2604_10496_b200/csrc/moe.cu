@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
                                                               int64_t ff, int8_t *__restrict__ codes,
                                                               float *__restrict__ scales,
                                                               const int32_t *__restrict__ live,
-                                                              int32_t *__restrict__ sums) {
+                                                              int32_t *__restrict__ sums, int keep) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
             const float4 x = ar[j], y = br[j];
             h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
                                __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
-            ar[j] = h[u];
+            if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
             mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
         }
     }
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
                                                              int64_t ff, int8_t *__restrict__ codes,
                                                              float *__restrict__ scales,
                                                              const int32_t *__restrict__ live,
-                                                             int32_t *__restrict__ sums) {
+                                                             int32_t *__restrict__ sums, int keep) {
     namespace cg = cooperative_groups;
     griddep_wait();
     const int64_t row = blockIdx.x / CL;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
             const float4 x = ar[j], y = br[j];
             h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
                                __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
-            ar[j] = h[u];
+            if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
             mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
         }
     }
@@ -233,17 +233,17 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
 
 template <int CL>
 static bool silu_quant_cluster(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                               const int32_t *live, int32_t *sums, cudaStream_t st) {
+                               const int32_t *live, int32_t *sums, int keep, cudaStream_t st) {
     if (ff % (4 * CL)) return false;
     const int64_t v = ceil_div(ff / CL / 4, 256);
     const dim3 grid((unsigned)(rows * CL));
     switch (v) {
-        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
-        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
+        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
+        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
         case 3:
-        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
+        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
         case 5: case 6: case 7:
-        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums); break;
+        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
         default: return false;
     }
     return true;
@@ -251,8 +251,10 @@ static bool silu_quant_cluster(float *a, const float *b, int64_t rows, int64_t f
 
 // `live` (device, nullable): rows at or past *live are skipped (EP slot bounds).
 // sums (nullable): per-row code sums (the merged-layout GEMM's bias term).
+// keep: also store h = silu(a) * b over a (fp32, read only by tracing); else a
+// keeps the gate output and only the codes, scales and sums are written.
 cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                     const int32_t *live, cudaStream_t st, int32_t *sums) {
+                     const int32_t *live, cudaStream_t st, int32_t *sums, int keep) {
     if (rows == 0) return CQ_OK;
     static int cl_env = -1;
     if (cl_env < 0) {
@@ -261,10 +263,10 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
     }
     // about two CTAs per SM over the whole grid; long rows only (a cluster CTA keeps >= 256 float4)
     if (cl_env && ff >= 8192) {
-        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, st)) return check_launch("silu_quant");
-        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, st))
+        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, keep, st)) return check_launch("silu_quant");
+        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, keep, st))
             return check_launch("silu_quant");
-        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, st))
+        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, keep, st))
             return check_launch("silu_quant");
     }
     const int64_t v = ceil_div(ff / 4, 512);
@@ -272,13 +274,13 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
         switch (v) {
             case 1: {  // short rows: one float4 per thread, CTA sized to the row
                 const int thr = (int)std::max<int64_t>(64, ceil_div(ff / 4, 32) * 32);
-                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums);
+                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums, keep);
                 break;
             }
-            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums); break;
+            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums, keep); break;
             case 3:
-            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums); break;
-            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums); break;
+            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums, keep); break;
+            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums, keep); break;
         }
     } else {
         launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live, sums);
@@ -582,7 +584,8 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
         UmmaIn hin;
         hin.sums_ready = umma_merged(down.tc_layout);
         int32_t *hsums = hin.sums_ready ? umma_row_sums(reinterpret_cast<int8_t *>(frag_h), rows, ff) : nullptr;
-        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, offsets + n_seg, st, hsums));
+        const int keep = (dsc->flags & CQ_FLAG_KEEP_HIDDEN) != 0;
+        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, offsets + n_seg, st, hsums, keep));
         if (ev) cudaEventRecord(ev[2], st);
         CQ_TRY(lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
                                 &down, fout, nullptr, nullptr, ff, d, st, hin));

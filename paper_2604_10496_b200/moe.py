@@ -148,6 +148,9 @@ class MoELayer:
         if path not in _PATHS:
             raise ConfigError(f"unknown path {path!r}; one of {sorted(_PATHS)}")
         self.path = path
+        # store h = silu(a) * b in the workspace on the tensor-core path too (trace(); costs an
+        # fp32 write of every routed hidden row)
+        self.keep_hidden = False
         self._ws = {}
         self._rot_tc = None  # R as three bf16 planes for the tensor-core rotation (prepare_tc)
 
@@ -184,6 +187,7 @@ class MoELayer:
             d.n_shared = self.shared[0].n
             d.sh_gate, d.sh_up, d.sh_down = (s.site() for s in self.shared)
         d.path = _PATHS[path or self.path]
+        d.flags = _lib.FLAG_KEEP_HIDDEN if self.keep_hidden else 0
         # the tensor-core rotation goes with the tensor-core path; f32 / ordered keep the fp32 rotation
         if self._rot_tc is not None and (path or self.path) in ("tc", "auto"):
             d.rotation_tc = self._rot_tc.data_ptr()
@@ -232,7 +236,9 @@ class MoELayer:
                                            buf.numel(), _lib.stream()))
 
     def trace(self, n: int, path: str | None = None) -> dict:
-        """Views of the workspace buffers of the last forward over n tokens."""
+        """Views of the workspace buffers of the last forward over n tokens.
+        "hidden" is h = silu(a) * b on the tensor-core path only with
+        `keep_hidden` set before that forward (else the gate output)."""
         buf, offs = self.workspace(n, path)
         k, d, ff, E, R = self.top_k, self.d_model, self.d_ff, self.n_experts, n * self.top_k
         spec = {"codes": (torch.int8, (n, d)), "scales": (torch.float32, (n,)),

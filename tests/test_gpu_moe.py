@@ -243,18 +243,23 @@ def test_tc_layer_embedding_wise_and_outliers_vs_oracle(g, outliers):
     assert o.relative_error(ordered, want) <= 1e-5
 
 
-@pytest.mark.parametrize("n", [4, 60, 140])
-def test_silu_requant_cluster_rows(n):
-    """Long hidden rows (ff = 14336) at decode row counts take the cluster
-    silu|re-quantize kernel (8 / 4 / 2 CTAs per row, row max through DSMEM):
-    codes and scales are bit-exact with the oracle quantizer on the kernel's own
-    h, and h = silu(a)*b agrees with the ordered path."""
-    d, ff, E, k, g = 256, 14336, 4, 2, 128
+@pytest.mark.parametrize("n,ff", [(4, 14336), (60, 14336), (140, 14336), (300, 768), (130, 1408), (50, 256),
+                                  (40, 6400)])
+def test_silu_requant_rows(n, ff):
+    """The silu|re-quantize kernels: long rows (ff = 14336) at decode row counts
+    take the cluster kernel (8 / 4 / 2 CTAs per row, row max through DSMEM),
+    others a CTA per row (one float4 per thread for short rows).  Codes and
+    scales are bit-exact with the oracle quantizer on the kernel's own h,
+    h = silu(a)*b agrees with the ordered path, and the layer output does not
+    depend on keeping h (CQ_FLAG_KEEP_HIDDEN)."""
+    d, E, k, g = 256, 4, 2, 128
     v, w, sites, _ = moe_inputs_device(70 + n, n, d, ff, E, g)
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
     layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
     layer.prepare_tc()
-    layer(v)
+    plain = layer(v).clone()
+    layer.keep_hidden = True  # trace h on the tensor-core path
+    assert torch.equal(layer(v), plain)
     tr = {key: t.clone() for key, t in layer.trace(n).items()}
     layer(v, path="ordered")
     tro = layer.trace(n, path="ordered")

@@ -129,6 +129,7 @@ def test_mixtral_decode_tc_vs_ordered(layout):
     v, w, sites, _ = moe_inputs_device(11, n, d, ff, E, g)
     stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
     layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc").prepare_tc(layout=layout)
+    layer.keep_hidden = True  # trace h on the tensor-core path
     out = layer(v).float()
     tr = {key: t.clone() for key, t in layer.trace(n).items()}
     ordered = layer(v, path="ordered").float()
