@@ -164,7 +164,7 @@ enum {
     CQ_WS_HSCALES,      /* f32  [n*k]                                        */
     CQ_WS_FOUT,         /* f32  [n*k][d_model] per-route down output         */
     CQ_WS_ROTATED,      /* f32  [n][d_model]   x @ R (online rotation only)  */
-    CQ_WS_SHARED,       /* f32  [n][d_model]   shared-expert sum             */
+    CQ_WS_SHARED,       /* f32  [n_shared][n][d_model] per shared expert    */
     CQ_WS_CODES_FRAG,   /* int8 [ceil(n*k/8)*8][d_model] codes in mma-B fragment order */
     CQ_WS_HCODES_FRAG,  /* int8 [ceil(n*k/8)*8][d_ff]    hidden codes, fragment order  */
     CQ_WS_ROT_ACT,      /* bf16 [3][ceil(n/128)*128][d_model] rotation operand planes (rotation_tc) */

@@ -350,7 +350,8 @@ __global__ void silu_mul_kernel(float *__restrict__ a, const float *__restrict__
 // then + add[t, :] (shared experts) when given.  grid (n, column blocks).
 __global__ void combine_kernel(const int32_t *__restrict__ selected, const float *__restrict__ weights,
                                const int32_t *__restrict__ inv, const float *__restrict__ fout, int64_t k,
-                               int64_t d, const float *__restrict__ add, float *__restrict__ out) {
+                               int64_t d, const float *__restrict__ add, int n_add, int64_t add_stride,
+                               float *__restrict__ out) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t t = blockIdx.x;
     __shared__ int32_t pos_sh[16];
@@ -389,8 +390,8 @@ __global__ void combine_kernel(const int32_t *__restrict__ selected, const float
                 acc.z = __fadd_rn(acc.z, __fmul_rn(ws, f.z));
                 acc.w = __fadd_rn(acc.w, __fmul_rn(ws, f.w));
             }
-            if (add != nullptr) {
-                const float4 a4 = reinterpret_cast<const float4 *>(add)[t * d4 + j];
+            for (int u = 0; u < n_add; ++u) {  // ((routed + add_0) + add_1) ...
+                const float4 a4 = reinterpret_cast<const float4 *>(add + u * add_stride)[t * d4 + j];
                 acc.x = __fadd_rn(acc.x, a4.x);
                 acc.y = __fadd_rn(acc.y, a4.y);
                 acc.z = __fadd_rn(acc.z, a4.z);
@@ -403,7 +404,7 @@ __global__ void combine_kernel(const int32_t *__restrict__ selected, const float
     for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < d; j += (int64_t)gridDim.y * blockDim.x) {
         float acc = 0.0f;
         for (int s = 0; s < kk; ++s) acc = __fadd_rn(acc, __fmul_rn(w_sh[s], __ldg(fout + (int64_t)pos_sh[s] * d + j)));
-        if (add != nullptr) acc = __fadd_rn(acc, add[t * d + j]);
+        for (int u = 0; u < n_add; ++u) acc = __fadd_rn(acc, add[u * add_stride + t * d + j]);
         out[t * d + j] = acc;
     }
 }
@@ -473,7 +474,7 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_HSCALES] = Rh * 4;
     sz[CQ_WS_FOUT] = Rh * d * 4;
     sz[CQ_WS_ROTATED] = (dsc->rotation || dsc->rotation_tc) ? n * d * 4 : 0;
-    sz[CQ_WS_SHARED] = dsc->n_shared > 0 ? n * d * 4 : 0;
+    sz[CQ_WS_SHARED] = dsc->n_shared * n * d * 4;  // one output per shared expert
     sz[CQ_WS_CODES_FRAG] = umma_b_bytes(Rh, d);     // >= the mma16 fragment size too
     sz[CQ_WS_HCODES_FRAG] = umma_b_bytes(Rh, ff);
     sz[CQ_WS_ROT_ACT] = dsc->rotation_tc ? rot_tc_act_bytes(n, d) : 0;
@@ -636,12 +637,6 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
                            down.group_size, fout, st);
 }
 
-__global__ void add_inplace_kernel(float *__restrict__ a, const float *__restrict__ b, int64_t count) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count; x += (int64_t)gridDim.x * blockDim.x)
-        a[x] = __fadd_rn(a[x], b[x]);
-}
-
 __global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     for (int64_t s = 0; s <= n_shared; ++s) off[s] = (int32_t)(s * n);
@@ -771,9 +766,11 @@ extern "C" cq_status cq_moe_profile_experts(const cq_moe_desc *desc, const int8_
     return rc;
 }
 
-extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
-                                    const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
-                                    const float *add, float *out, void *stream) {
+// add (nullable): n_add buffers of [n_tokens][d_model], n_tokens * d_model apart, added to the
+// routed sum in order.
+static cq_status combine_n(const int32_t *selected, const float *weights, const int32_t *inv, const float *fout,
+                           int64_t n_tokens, int64_t top_k, int64_t d_model, const float *add, int n_add, float *out,
+                           void *stream) {
     if (n_tokens == 0) return CQ_OK;
     if (top_k < 1 || top_k > 16) {
         set_error("combine: top_k out of range");
@@ -782,8 +779,15 @@ extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weight
     const int64_t cols = (d_model & 3) == 0 ? d_model / 4 : d_model;  // work items per token
     const int threads = (int)std::min<int64_t>(256, ceil_div(cols, 32) * 32);
     dim3 grid((unsigned)n_tokens, (unsigned)std::max<int64_t>(1, std::min<int64_t>(16, ceil_div(cols, threads))));
-    launch_pdl(combine_kernel, grid, threads, 0, as_stream(stream), selected, weights, inv, fout, top_k, d_model, add, out);
+    launch_pdl(combine_kernel, grid, threads, 0, as_stream(stream), selected, weights, inv, fout, top_k, d_model, add,
+               add ? n_add : 0, n_tokens * d_model, out);
     return check_launch("combine");
+}
+
+extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
+                                    const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
+                                    const float *add, float *out, void *stream) {
+    return combine_n(selected, weights, inv, fout, n_tokens, top_k, d_model, add, 1, out, stream);
 }
 
 extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int dtype, int64_t n_tokens, float *out,
@@ -833,20 +837,20 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
                            w.scales_perm, w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag,
                            w.hcodes_frag, st));
     }
-    CQ_TRY(cq_moe_combine(w.selected, w.weights, w.inv, w.fout, n_tokens, desc->top_k, desc->d_model, nullptr,
-                          out, stream));
     // builder-defined shared experts: out = ((routed + sh_0) + sh_1) ...,
-    // each shared expert run as one segment over all n tokens (un-permuted codes).
-    for (int64_t s = 0; s < desc->n_shared; ++s) {
+    // each shared expert run as one segment over all n tokens (un-permuted codes) into its own
+    // slice of w.shared; the combine adds them in order (one pass over out)
+    if (desc->n_shared > 0) {
         int32_t *soff = w.counts;  // counts were consumed by permute; E+1 >= 2 ints
         shared_offsets_kernel<<<1, 1, 0, st>>>(soff, 1, n_tokens);
         CQ_TRY(check_launch("shared_offsets"));
-        const int sp = (path == CQ_PATH_TC && desc->sh_gate.tc_lut == nullptr) ? CQ_PATH_F32 : path;
-        CQ_TRY(run_experts(desc, sp, desc->sh_gate, desc->sh_up, desc->sh_down, 1, s, w.codes, w.scales, soff,
-                           n_tokens, w.hidden, w.hcodes, w.hscales, w.shared, w.codes_frag, w.hcodes_frag, st));
-        add_inplace_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_tokens * desc->d_model, 256), 148 * 16), 256, 0,
-                             st>>>(out, w.shared, n_tokens * desc->d_model);
-        CQ_TRY(check_launch("add_shared"));
     }
-    return CQ_OK;
+    for (int64_t s = 0; s < desc->n_shared; ++s) {
+        const int sp = (path == CQ_PATH_TC && desc->sh_gate.tc_lut == nullptr) ? CQ_PATH_F32 : path;
+        CQ_TRY(run_experts(desc, sp, desc->sh_gate, desc->sh_up, desc->sh_down, 1, s, w.codes, w.scales, w.counts,
+                           n_tokens, w.hidden, w.hcodes, w.hscales, w.shared + s * n_tokens * desc->d_model,
+                           w.codes_frag, w.hcodes_frag, st));
+    }
+    return combine_n(w.selected, w.weights, w.inv, w.fout, n_tokens, desc->top_k, desc->d_model,
+                     desc->n_shared > 0 ? w.shared : nullptr, (int)desc->n_shared, out, stream);
 }
