@@ -249,6 +249,10 @@ static bool silu_quant_cluster(float *a, const float *b, int64_t rows, int64_t f
     return true;
 }
 
+static int vec_threads(int64_t ff, int v) {
+    return (int)std::min<int64_t>(512, ceil_div(ceil_div(ff / 4, v), 32) * 32);
+}
+
 // `live` (device, nullable): rows at or past *live are skipped (EP slot bounds).
 // sums (nullable): per-row code sums (the merged-layout GEMM's bias term).
 // keep: also store h = silu(a) * b over a (fp32, read only by tracing); else a
@@ -277,10 +281,11 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
                 launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums, keep);
                 break;
             }
-            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums, keep); break;
+            // CTA sized to the row at V float4 per thread (PH ff = 6400: 416 threads instead of 512)
+            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, vec_threads(ff, 2), 0, st, a, b, ff, codes, scales, live, sums, keep); break;
             case 3:
-            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums, keep); break;
-            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, 512, 0, st, a, b, ff, codes, scales, live, sums, keep); break;
+            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, vec_threads(ff, 4), 0, st, a, b, ff, codes, scales, live, sums, keep); break;
+            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, vec_threads(ff, 8), 0, st, a, b, ff, codes, scales, live, sums, keep); break;
         }
     } else {
         launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live, sums);
