@@ -66,7 +66,7 @@ def parse():
     p.add_argument("--batch", type=int, default=None, help="tokens per step (per rank); default: the config's")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--path", default="auto", choices=["auto", "tc", "f32", "ordered"])
-    p.add_argument("--layout", default="umma128u", choices=["umma128", "umma128u", "mma16"],
+    p.add_argument("--layout", default="umma128u", choices=["umma128u"],
                    help="tensor-core weight layout / kernel")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--replicas", action="store_true",

@@ -20,6 +20,13 @@
  *                                                  has no such entry point.
  *   cq_lut8_prepare         (new) one-time device re-layout of PackedClusteredWeights for the
  *                           tensor-core path; consumes lutgemm.py:53-87 tensors unchanged.
+ *   cq_lut_gemm_tc          (new) the tcgen05 LUT GEMM on prepared weights (lutgemm.py:133-144's
+ *                           contract within the digit-plane representation error).
+ *
+ * Host synchronisation: no entry point synchronises the stream.  Errors the
+ * reference raises from data (non-finite activations -> DivergenceError,
+ * quant.py:93-94, model.py:307-309) are reported through caller-owned device
+ * flags that the caller reads at its next sync.
  */
 #ifndef CQ_B200_H
 #define CQ_B200_H
@@ -57,10 +64,10 @@ CQ_API int64_t cq_launch_count(void);
 /* Per-token symmetric 4-bit quantization, bit-exact with quant.py:89-100 for
  * float32 input (bf16 input is quantized as its exact float32 upcast).
  * x: (n, d) row-major, dtype CQ_DTYPE_*.  codes: (n, d) int8, scales: (n,) f32.
- * Non-finite input -> CQ_ERR_DIVERGENCE (checked on the host after a sync;
- * pass check_finite=0 on the hot path to skip the sync). */
+ * nonfinite (device int32, nullable): set to 1 when a row holds inf / NaN (the
+ * reference's DivergenceError, quant.py:93-94); never cleared here. */
 CQ_API cq_status cq_quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes,
-                         float *scales, int check_finite, void *stream);
+                         float *scales, int32_t *nonfinite, void *stream);
 
 /* Low-nibble-first unpack, bit-exact: ids[r, 2m] = b & 15, ids[r, 2m+1] = b >> 4.
  * packed: (rows, ceil(d_in/2)) u8 -> ids: (rows, d_in) u8. */
@@ -77,10 +84,10 @@ CQ_API cq_status cq_reference_gemm_f32(const int8_t *codes, const float *scales,
                                 int64_t d_in, int64_t d_out, int64_t g, float *out,
                                 void *stream);
 
-/* LUT GEMM, fp32 CUDA-core path: same contract as cq_reference_gemm_f32 but
- * accumulated in parallel (FMA, warp-split K), so equal within ~1e-6 relative
- * rather than bitwise.  Falls through to the ordered kernel for shapes
- * outside its envelope (g % 8 != 0 or d_in % 8 != 0). */
+/* lut_gemm_f32 (_core.pyx:41-151): the reference's table entry T[id][q+8] =
+ * C_id * float(q) is the same single fp32 product as reference_gemm's, and the
+ * chains run in the same order, so this is the same BIT-EXACT computation as
+ * cq_reference_gemm_f32 (acceptance #8, tests/test_acceptance.py:358-387). */
 CQ_API cq_status cq_lut_gemm_f32(const int8_t *codes, const float *scales, const uint8_t *ids_packed,
                           const float *centroids, int64_t n, int64_t d_in, int64_t d_out,
                           int64_t g, float *out, void *stream);
@@ -112,15 +119,16 @@ typedef struct {
     const uint8_t *tc_ids;     /* [E*d_out/16][d_in/128][1024] fragment-ordered nibbles (same bytes as ids) */
     const int8_t *tc_lut;      /* [E*d_out/16][d_in/g][16 rows][planes][16] int8 digit-plane LUTs */
     const float *tc_rowscale;  /* [E*d_out] */
-    int64_t tc_planes;         /* 2 or 3 base-255 digit planes (3 where the output is re-quantized) */
-    int64_t tc_layout;         /* CQ_TC_MMA16 (mma.sync kernel), CQ_TC_UMMA128 / _UMMA128U (tcgen05
-                                  kernel; signed P/Q digit slices / unsigned OR-merged digits) */
+    int64_t tc_planes;         /* 2 or 3 unsigned base-128 digit planes (3 where the output is re-quantized) */
+    int64_t tc_layout;         /* CQ_TC_UMMA128U / CQ_TC_UMMA128U8 */
 } cq_expert_site;
 
-/* CQ_TC_UMMA128U8: the data of CQ_TC_UMMA128U, declared to have every id < 8
-   (codebooks with K <= 8, W3/W2): one PRMT per 4 operand bytes instead of three
-   instructions.  The caller guarantees the ids; the preparation is identical. */
-enum { CQ_TC_MMA16 = 0, CQ_TC_UMMA128 = 1, CQ_TC_UMMA128U = 2, CQ_TC_UMMA128U8 = 3 };
+/* Tensor-core layouts (tcgen05 kernel, cq_lut8_prepare).  CQ_TC_UMMA128U8: the
+   data of CQ_TC_UMMA128U, declared to have every id < 8 (codebooks with K <= 8,
+   W3/W2): one PRMT per 4 operand bytes instead of three instructions.  The
+   caller guarantees the ids; the preparation is identical.  (Values 0 and 1
+   were the retired mma.sync and signed-digit layouts.) */
+enum { CQ_TC_UMMA128U = 2, CQ_TC_UMMA128U8 = 3 };
 
 typedef struct {
     int64_t d_model, d_ff, n_experts, top_k;
@@ -169,6 +177,10 @@ enum {
     CQ_WS_HCODES_FRAG,  /* int8 [ceil(n*k/8)*8][d_ff]    hidden codes, fragment order  */
     CQ_WS_ROT_ACT,      /* bf16 [3][ceil(n/128)*128][d_model] rotation operand planes (rotation_tc) */
     CQ_WS_TOK_SUMS,     /* i32  [n]            per-token code sums (GEMM bias term) */
+    CQ_WS_STATUS,       /* i32  [4]            sticky non-finite flags: [0] layer input (router / gate /
+                                               up sites), [1] hidden (down input).  Zero it once when
+                                               the workspace is created; the layer only sets it. */
+    CQ_WS_SH_OFFSETS,   /* i32  [2]            shared-expert segment (0, n)                  */
     CQ_WS_COUNT_
 };
 
@@ -176,7 +188,8 @@ enum {
 CQ_API int64_t cq_moe_workspace(const cq_moe_desc *desc, int64_t n_tokens, int64_t *offsets_out);
 
 /* Full layer: x (n, d_model) dtype CQ_DTYPE_* -> out (n, d_model) f32 = moe_sum.
- * No host synchronisation; deterministic for a given path. */
+ * No host synchronisation; deterministic for a given path.  Non-finite values
+ * set CQ_WS_STATUS (read it after a sync; the reference raises DivergenceError). */
 CQ_API cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int dtype, int64_t n_tokens,
                          float *out, void *workspace, int64_t workspace_bytes, void *stream);
 
@@ -197,10 +210,18 @@ CQ_API cq_status cq_moe_profile_experts(const cq_moe_desc *desc, const int8_t *c
                                  const float *scales_perm, const int32_t *offsets, int64_t rows,
                                  float *fout, void *workspace, int64_t workspace_bytes,
                                  int32_t iters, float *stage_ms_host, void *stream);
-/* Weighted combine in ascending expert order (model.py:389-401). */
+/* Weighted combine in ascending expert order (model.py:389-401), then
+ * out = ((routed + add_0) + add_1) ... over n_add buffers of [n_tokens][d_model]
+ * laid end to end (shared-expert outputs; add may be NULL when n_add == 0). */
 CQ_API cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
                          const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
-                         const float *add, float *out, void *stream);
+                         const float *add, int64_t n_add, float *out, void *stream);
+/* The builder-defined shared experts (weight 1) of desc over the
+ * n_tokens layer-input codes cq_moe_route left in the workspace:
+ * shared_out [n_shared][n_tokens][d_model] f32.  Expert parallelism runs them on
+ * every rank for its own tokens (they are replicated, no exchange). */
+CQ_API cq_status cq_moe_shared_experts(const cq_moe_desc *desc, int64_t n_tokens, float *shared_out,
+                                void *workspace, int64_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Expert parallelism, device-side planning (the reference has
@@ -245,23 +266,26 @@ CQ_API int64_t cq_rotation_prepared_bytes(int64_t d_model);
 CQ_API cq_status cq_rotation_prepare(const float *rotation, int64_t d_model, void *prepared, void *stream);
 
 /* One-time re-layout of one stacked site (rows = E*d_out) for the tensor-core path:
- * every row's centroids become `planes` int8 base-255 digit planes at one
- * per-row scale (m = rint(c / rowscale), |m| < 255^planes / 2), stored as
- * 16-entry byte LUTs pre-compensated for the PRMT sign-replicate lookup; ids
- * are permuted (2-byte units) into mma.m16n8k32 A-fragment order.
- * Requires rows % 16 == 0 (layout CQ_TC_MMA16) or rows % 128 == 0 (CQ_TC_UMMA128),
- * d_in % 128 == 0, g % 128 == 0, planes in {2, 3}. */
+ * every row's centroids become integers m = rint(c / rowscale), |m| < 2^(7P-1),
+ * at one per-row scale, stored as P unsigned base-128 digit planes of 16-entry
+ * byte LUTs (m + 2^(7P-1)); ids are re-tiled into 128-row k-step blocks (same
+ * bytes).  tc_ids: d_in/2 bytes per row; tc_lut: rows * (d_in/g) * planes * 16;
+ * tc_rowscale: rows floats.  Requires rows % 128 == 0, d_in % 128 == 0,
+ * g % 128 == 0, planes in {2, 3}, layout CQ_TC_UMMA128U / _UMMA128U8. */
 CQ_API cq_status cq_lut8_prepare(const uint8_t *ids, const float *centroids, int64_t rows,
                           int64_t d_in, int64_t g, int64_t planes, int64_t layout,
                           uint8_t *tc_ids, int8_t *tc_lut, float *tc_rowscale, void *stream);
 
 /* Tensor-core LUT GEMM on prepared weights (one matrix): codes (n, d_in) int8
- * row-major, out (n, d_out) f32.  Same contract as cq_lut_gemm_f32 within the
- * digit-plane representation error (<= 2^-23 of the row max per weight). */
+ * row-major (4- or 8-bit values), out (n, d_out) f32.  Same contract as
+ * cq_lut_gemm_f32 within the digit-plane representation error (<= 2^-(7P-1) of
+ * the row max per weight).  workspace: device scratch of at least
+ * cq_lut_gemm_tc_workspace(n, d_in) bytes (no allocation inside). */
+CQ_API int64_t cq_lut_gemm_tc_workspace(int64_t n, int64_t d_in);
 CQ_API cq_status cq_lut_gemm_tc(const int8_t *codes, const float *scales, const uint8_t *tc_ids,
                          const int8_t *tc_lut, const float *tc_rowscale, int64_t planes,
                          int64_t layout, int64_t n, int64_t d_in, int64_t d_out, int64_t g,
-                         float *out, void *stream);
+                         float *out, void *workspace, int64_t workspace_bytes, void *stream);
 
 #ifdef __cplusplus
 }

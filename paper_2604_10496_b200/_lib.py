@@ -21,13 +21,12 @@ LIB_PATH = os.environ.get("CQ_B200_LIB") or os.path.join(_HERE, "libcq_b200.so")
 CQ_OK, CQ_ERR_SHAPE, CQ_ERR_CONFIG, CQ_ERR_DIVERGENCE, CQ_ERR_CUDA, CQ_ERR_UNSUPPORTED = range(6)
 CQ_DTYPE_F32, CQ_DTYPE_BF16 = 0, 1
 CQ_PATH_AUTO, CQ_PATH_F32, CQ_PATH_TC, CQ_PATH_ORDERED = 0, 1, 2, 3
-CQ_TC_MMA16, CQ_TC_UMMA128, CQ_TC_UMMA128U, CQ_TC_UMMA128U8 = 0, 1, 2, 3
-TC_LAYOUTS = {"mma16": CQ_TC_MMA16, "umma128": CQ_TC_UMMA128, "umma128u": CQ_TC_UMMA128U,
-              "umma128u8": CQ_TC_UMMA128U8}
+CQ_TC_UMMA128U, CQ_TC_UMMA128U8 = 2, 3
+TC_LAYOUTS = {"umma128u": CQ_TC_UMMA128U, "umma128u8": CQ_TC_UMMA128U8}
 WS_NAMES = ("codes", "scales", "logits", "selected", "weights", "counts", "offsets",
             "perm_token", "perm_slot", "inv", "codes_perm", "scales_perm", "hidden",
             "hcodes", "hscales", "fout", "rotated", "shared", "codes_frag", "hcodes_frag", "rot_act",
-            "tok_sums")
+            "tok_sums", "status", "sh_offsets")
 
 _vp, _i64, _i32, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 
@@ -52,7 +51,7 @@ FLAG_KEEP_HIDDEN = 1  # CQ_FLAG_KEEP_HIDDEN
 
 
 _SIGS = {
-    "cq_quantize_a4": [_vp, _int, _i64, _i64, _vp, _vp, _int, _vp],
+    "cq_quantize_a4": [_vp, _int, _i64, _i64, _vp, _vp, _vp, _vp],
     "cq_unpack_ids": [_vp, _i64, _i64, _vp, _vp],
     "cq_reference_gemm_f32": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp],
     "cq_lut_gemm_f32": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp],
@@ -61,10 +60,11 @@ _SIGS = {
     "cq_moe_forward": [ctypes.POINTER(MoEDesc), _vp, _int, _i64, _vp, _vp, _i64, _vp],
     "cq_moe_route": [ctypes.POINTER(MoEDesc), _vp, _int, _i64, _vp, _i64, _vp],
     "cq_moe_experts": [ctypes.POINTER(MoEDesc), _vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp],
-    "cq_moe_combine": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp],
+    "cq_moe_combine": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp],
+    "cq_moe_shared_experts": [ctypes.POINTER(MoEDesc), _i64, _vp, _vp, _i64, _vp],
     "cq_moe_profile_experts": [ctypes.POINTER(MoEDesc), _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp],
     "cq_lut8_prepare": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
-    "cq_lut_gemm_tc": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
+    "cq_lut_gemm_tc": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
     "cq_ep_dispatch": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _vp, _vp],
     "cq_ep_group": [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
     "cq_ep_scatter": [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp],
@@ -72,7 +72,8 @@ _SIGS = {
 }
 
 EXPORTS = tuple(_SIGS) + ("cq_last_error", "cq_abi_version", "cq_launch_count", "cq_moe_workspace",
-                          "cq_ep_row_bytes", "cq_ep_scratch_bytes", "cq_rotation_prepared_bytes")
+                          "cq_ep_row_bytes", "cq_ep_scratch_bytes", "cq_rotation_prepared_bytes",
+                          "cq_lut_gemm_tc_workspace")
 
 _LIB = None
 
@@ -100,6 +101,8 @@ def load_library() -> ctypes.CDLL:
         lib.cq_ep_scratch_bytes.restype = _i64
         lib.cq_rotation_prepared_bytes.argtypes = [_i64]
         lib.cq_rotation_prepared_bytes.restype = _i64
+        lib.cq_lut_gemm_tc_workspace.argtypes = [_i64, _i64]
+        lib.cq_lut_gemm_tc_workspace.restype = _i64
         _LIB = lib
     return _LIB
 
@@ -131,6 +134,20 @@ def ptr(t) -> int | None:
 
 def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
+
+
+_SCRATCH = {}
+
+
+def scratch(nbytes: int, tag: str = "tc") -> torch.Tensor:
+    """A cached device scratch buffer of at least nbytes per (tag, device):
+    C entry points take caller-owned workspaces instead of allocating."""
+    key = (tag, torch.cuda.current_device())
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
+        _SCRATCH[key] = buf
+    return buf
 
 
 def launch_count() -> int:

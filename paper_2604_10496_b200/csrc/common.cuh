@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cfloat>
 #include <cstdio>
 #include <string>
 #include <utility>

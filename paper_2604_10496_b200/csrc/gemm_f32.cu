@@ -1,4 +1,4 @@
-// fp32 CUDA-core LUT GEMM / GEMV (the decode path for few tokens per expert).
+// fp32 CUDA-core LUT GEMM / GEMV: the MoE layer's path="f32" expert stage.
 //
 // Same contract as _core.lut_gemm_f32 (kernels/_core.pyx:41-151): the product
 // of centroid c = C[i, j/g, id[i,j]] and code q is exact-ish fp32 (FMA) and the
@@ -101,39 +101,4 @@ cq_status lut_f32_grouped(const int8_t *codes, const float *scales, const int32_
     return check_launch("lut_f32_grouped");
 }
 
-cq_status reference_gemm(const int8_t *, const float *, const uint8_t *, const float *, int64_t,
-                         int64_t, int64_t, int64_t, float *, cudaStream_t);
-cq_status validate_gemm(int64_t, int64_t, int64_t, int64_t);
-
-__global__ void single_segment_kernel(int32_t *off, int64_t n) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    off[0] = 0;
-    off[1] = (int32_t)n;
-}
-
 }  // namespace cq
-
-using namespace cq;
-
-extern "C" cq_status cq_lut_gemm_f32(const int8_t *codes, const float *scales,
-                                     const uint8_t *ids_packed, const float *centroids, int64_t n,
-                                     int64_t d_in, int64_t d_out, int64_t g, float *out,
-                                     void *stream) {
-    CQ_TRY(validate_gemm(n, d_in, d_out, g));
-    cudaStream_t st = as_stream(stream);
-    if (n == 0 || d_out == 0) return CQ_OK;
-    if (!f32_path_ok(d_in, g) || n > INT32_MAX)
-        return reference_gemm(codes, scales, ids_packed, centroids, n, d_in, d_out, g, out, st);
-    int32_t *off = nullptr;
-    if (cudaMallocAsync(&off, 2 * sizeof(int32_t), st) != cudaSuccess) {
-        set_error("lut_gemm: offsets alloc failed");
-        return CQ_ERR_CUDA;
-    }
-    single_segment_kernel<<<1, 1, 0, st>>>(off, n);
-    cq_status rc = check_launch("single_segment");
-    if (rc == CQ_OK)
-        rc = lut_f32_grouped(codes, scales, off, 1, 0, ids_packed, centroids, nullptr, nullptr, d_in,
-                             d_out, g, out, st);
-    cudaFreeAsync(off, st);
-    return rc;
-}

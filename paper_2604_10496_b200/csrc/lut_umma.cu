@@ -13,15 +13,12 @@
 // (two ids per byte, low nibble first, lutgemm.py:111-116); ids 8..15 set the
 // selector's sign-replicate bit, so prmt(entries 0..7, sel) and prmt(entries
 // 8..15, sel ^ 0x8888) each give the right bytes for their half and a
-// replicated sign byte for the other.  Two digit formats (layouts):
-//   CQ_TC_UMMA128  (default) signed base-255 digits in [-128, 126], the sign
-//      garbage pre-compensated per (a, a+8) pair (lut8_kernel): both PRMT
-//      halves go through the MMA as separate K-slices whose sum is the lookup.
-//      2 ALU ops per 4 weights per plane; 2P MMAs per k-step.
-//   CQ_TC_UMMA128U unsigned base-128 digits, biased by 2^(7P-1) (lut7_kernel):
-//      sign bits clear, so the halves merge with one OR (3 ALU ops per 4
-//      weights per plane, P MMAs per k-step), and the bias returns in the
-//      epilogue as 2^(7P-1) * sum_j q[t,j].
+// replicated sign byte for the other.  Digits are unsigned base 128, biased
+// by 2^(7P-1) (CQ_TC_UMMA128U, lut7_kernel in prepare.cu): their sign bits are
+// clear, so the replicated byte is 0 and the halves merge with one integer
+// add (2 PRMT + 1 IMAD per 4 weights per plane, P MMAs per k-step); the bias
+// returns in the epilogue as 2^(7P-1) * sum_j q[t,j].  CQ_TC_UMMA128U8 (every
+// id < 8, codebooks with K <= 8) needs the first PRMT only.
 //
 // CTA = one 128-row weight tile of one expert matrix x token passes of <= 32
 // tokens (MMA N = 16 or 32), warp-specialised, one CTA per SM (it owns all
@@ -80,9 +77,9 @@ constexpr uint32_t TMEM_COLS = 512;
 // expander warps) bounded the decode GEMM; with one warp per plane each issues
 // a third (P = 3) of the MMAs from a different SMSP.  Planes accumulate into
 // disjoint TMEM columns, so the warps never touch one accumulator concurrently.
-template <int P, bool MERGED>
+template <int P>
 struct UmWarps {
-    static constexpr int NMMA = (MERGED && UM_MMA_PER_PLANE) ? P : 1;
+    static constexpr int NMMA = UM_MMA_PER_PLANE ? P : 1;
     static constexpr int WARPS = um::EXP_WARPS + 1 + NMMA;
     static constexpr int THREADS = WARPS * 32;
 };
@@ -106,12 +103,12 @@ using UmDecode = UmGeo<32, UM_CK>;
 #endif
 using UmPrefill = UmGeo<UM_PF_NT, 64>;
 
-template <int P, bool MERGED, class GEO>
+template <int P, class GEO>
 struct UmStage {
     static constexpr int LUT = 128 * P * 16;
     static constexpr int B = (GEO::NT / 8) * GEO::BTILE;
     static constexpr int BYTES = GEO::IDS + LUT + B;
-    static constexpr int SLICES = MERGED ? P : 2 * P;            // MMA K-slices per k-step
+    static constexpr int SLICES = P;                             // MMA K-slices per k-step
     static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per k-step
     static constexpr int CCOLS = GEO::KS * ACOLS;                // TMEM columns per A stage (one chunk)
     static constexpr int ACC = P * GEO::NT;                      // accumulator columns
@@ -228,8 +225,8 @@ __device__ __forceinline__ UmUnit um_unit(const UmWork &w, int64_t seg_first, in
 // NARROW (merged layout, every id < 8: codebooks with K <= 8): the 8 table
 // bytes of entries 0..7 sit in L.x, L.y, so one PRMT yields 4 A bytes (no
 // second PRMT over entries 8..15, no merge).
-template <int P, bool MERGED, class GEO, bool NARROW = false>
-__global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kernel(
+template <int P, class GEO, bool NARROW = false>
+__global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
     const int8_t *__restrict__ bfrag, int64_t n_tiles, const float *__restrict__ scales,
     const int32_t *__restrict__ qsums, const int32_t *__restrict__ offsets, int n_seg, int64_t seg_first,
     const uint8_t *__restrict__ ids0, const int8_t *__restrict__ lut0, const float *__restrict__ rs0,
@@ -237,8 +234,8 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
     const float *__restrict__ rs1, float *__restrict__ out1, int n_mat, int d_in, int d_out, int g,
     int32_t *__restrict__ part, int32_t *__restrict__ cnt) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    using S = UmStage<P, MERGED, GEO>;
-    constexpr int NMMA = UmWarps<P, MERGED>::NMMA;
+    using S = UmStage<P, GEO>;
+    constexpr int NMMA = UmWarps<P>::NMMA;
     constexpr int NA = S::NA, NS = S::NS, GS = S::GS, LAG = S::LAG;
     constexpr int WPS = um::WG / GS;  // warpgroups per stream
     constexpr int NT = GEO::NT, CK = GEO::CK, NCB = GEO::NCB;
@@ -405,9 +402,9 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                 m_af += mi - mw;
 #endif
                 tc_fence_after();
-#ifndef UM_MMA_PER_INSTR
-                if constexpr (MERGED) {  // one asm block per chunk (B tile: [tile8][kstep][khalf][8 rows][16 B])
+                // one asm block per chunk (B tile: [tile8][kstep][khalf][8 rows][16 B])
 #ifndef UM_EXP_NO_MMA
+                {
                     // lane-0 broadcasts of the operands: ptxas then converts each to a uniform register
                     // once per chunk (68 instead of 141 instructions per 12 MMAs)
                     const uint64_t bd = smem_desc(bbase, 128, GEO::BTILE);
@@ -422,23 +419,8 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                                                  __shfl_sync(0xffffffffu, abase, 0), __shfl_sync(0xffffffffu, bd, 0),
                                                  __shfl_sync(0xffffffffu, idesc, 0), c == c0u ? 0u : 1u);
                     }
-#endif
-                } else
-#endif
-#pragma unroll
-                for (int kk = 0; kk < GEO::KS; ++kk) {
-                    // B tile in smem: [tile8][kstep][khalf][8 rows][16 B]
-                    const uint64_t bdesc = smem_desc(bbase + kk * 256, 128, GEO::BTILE);
-#pragma unroll
-                    for (int sl = 0; sl < S::SLICES; ++sl) {
-                        const int p = MERGED ? sl : (sl >> 1);
-                        const uint32_t accum = (c == c0u && kk == 0 && (MERGED || !(sl & 1))) ? 0u : 1u;
-#ifndef UM_EXP_NO_MMA
-                        tc_mma_i8(tm_u + (uint32_t)(p * NT), abase + (uint32_t)(kk * S::ACOLS + sl * 8), bdesc,
-                                  idesc, accum);
-#endif
-                    }
                 }
+#endif
                 tc_commit_elect(empty_a + 8 * s);  // frees the smem stage (and with LAG == 0 the A stage)
                 if (S::SPLIT_AFREE)
                     tc_commit_elect(afree_a + 8 * sa);  // A stage free for chunk k + NA
@@ -484,7 +466,7 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                 for (int i = 0; i < NCB; ++i)
                     if (lane < 16 && cb + 32 * i < ((x.ntc + 1) & ~1) * 8) {
                         const int64_t tok = x.j0 * 8 + cb + 32 * i + (lane & 7);
-                        if (tok >= x.rb && tok < x.re && (lane < 8 || MERGED))
+                        if (tok >= x.rb && tok < x.re)
                             cp_async4(&tok_sh[warp][i][lane],
                                       lane < 8 ? (const void *)(scales + tok) : (const void *)(qsums + tok));
                     }
@@ -530,7 +512,7 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                         xsel[2 * q + 1] = hi16(xx);
                     }
                     const uint32_t abase = abase0 + (uint32_t)(ks * S::ACOLS);
-                    if (S::SPLIT_AFREE && MERGED && ks == ks0) {
+                    if (S::SPLIT_AFREE && ks == ks0) {
                         // the first k-step expands into registers before the A stage is known free: the
                         // MMAs of this stage's previous chunk (k - NA) overlap its PRMT work
                         uint32_t v[P][8];
@@ -557,7 +539,7 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                         tc_fence_after();
 #pragma unroll
                         for (int p = 0; p < P; ++p) tc_st8(abase + p * 8, v[p]);
-                    } else if (MERGED) {
+                    } else {
                         // one 8-column store per plane as soon as it is expanded (keeps the register peak low)
 #pragma unroll
                         for (int p = 0; p < P; ++p) {
@@ -568,21 +550,6 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                                                : u_merge(u_prmt(L[p].x, L[p].y, sel[cc]),
                                                          u_prmt(L[p].z, L[p].w, xsel[cc]));
                             tc_st8(abase + p * 8, v);
-                        }
-                    } else {
-                        if (S::SPLIT_AFREE && ks == ks0) {
-                            u_bar_wait(afree_a + 8 * sa, ((k / NA) & 1) ^ 1);
-                            tc_fence_after();
-                        }
-#pragma unroll
-                        for (int p = 0; p < P; ++p) {
-                            uint32_t v[16];
-#pragma unroll
-                            for (int cc = 0; cc < 8; ++cc) {
-                                v[cc] = u_prmt(L[p].x, L[p].y, sel[cc]);       // ids 0..7 (+ compensated sign byte)
-                                v[8 + cc] = u_prmt(L[p].z, L[p].w, xsel[cc]);  // ids 8..15
-                            }
-                            tc_st16(abase + p * 16, v);
                         }
                     }
                 }
@@ -667,20 +634,13 @@ __global__ void __launch_bounds__(UmWarps<P, MERGED>::THREADS, 1) lut_umma_kerne
                 float v[8];
 #pragma unroll
                 for (int c2 = 0; c2 < 8; ++c2) {  // branch-free, so the 8 conversion chains overlap
-                    double sum;
-                    if (MERGED) {
-                        // exact integer digit sum (|.| < 2^39) in int64, one conversion: the same double
-                        // as summing converted planes, at a third of the fp64-pipe work
-                        int64_t s64 = (int64_t)acc[P - 1][c2];
+                    // exact integer digit sum (|.| < 2^39) in int64, one conversion: the same double
+                    // as summing converted planes, at a third of the fp64-pipe work
+                    int64_t s64 = (int64_t)acc[P - 1][c2];
 #pragma unroll
-                        for (int p = P - 2; p >= 0; --p) s64 = s64 * 128 + (int64_t)acc[p][c2];
-                        s64 -= (int64_t)tqsum[c2] << (7 * P - 1);
-                        sum = (double)s64;
-                    } else {
-                        sum = (double)acc[P - 1][c2];
-#pragma unroll
-                        for (int p = P - 2; p >= 0; --p) sum = sum * 255.0 + (double)acc[p][c2];
-                    }
+                    for (int p = P - 2; p >= 0; --p) s64 = s64 * 128 + (int64_t)acc[p][c2];
+                    s64 -= (int64_t)tqsum[c2] << (7 * P - 1);
+                    const double sum = (double)s64;
                     v[c2] = __fmul_rn((float)(sum * (double)rscale), tscale[c2]);
                 }
                 const int64_t tok0 = x.j0 * 8 + cbi;
@@ -877,41 +837,14 @@ __global__ void row_sums_kernel(const int8_t *__restrict__ codes, int64_t n, int
     if ((threadIdx.x & 31) == 0) sums[row] = acc;
 }
 
-// ids (rows, d_in/2) -> [tile128][chunk][kstep][row][16 B] (the 16 packed bytes of
-// a row's 32 columns are already 8 PRMT selectors, low nibble first).
-__global__ void ids_umma_kernel(const uint8_t *__restrict__ ids, int64_t rows, int64_t d_in, uint4 *__restrict__ out) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    const int64_t n_chunks = d_in / 128;
-    const int64_t total = (rows / 128) * n_chunks * 4 * 128;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = x & 127, ks = (x >> 7) & 3, c = (x >> 9) % n_chunks, t = (x >> 9) / n_chunks;
-        out[x] = *reinterpret_cast<const uint4 *>(ids + (t * 128 + r) * (d_in / 2) + c * 64 + ks * 16);
-    }
-}
-
-// lut16 [rows/16][G][16][P][16] (lut7_kernel layout) -> [rows/128][G][128][P][16].
-__global__ void lut_relayout_kernel(const int8_t *__restrict__ lut16, int64_t rows, int64_t n_groups, int planes,
-                                    int8_t *__restrict__ out) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    const int64_t per = (int64_t)planes * 16;
-    const int64_t total = rows * n_groups;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = x % rows, grp = x / rows;
-        const int8_t *src = lut16 + (((row / 16) * n_groups + grp) * 16 + row % 16) * per;
-        int8_t *d = out + (((row / 128) * n_groups + grp) * 128 + row % 128) * per;
-        for (int64_t b = 0; b < per; b += 16)
-            *reinterpret_cast<uint4 *>(d + b) = *reinterpret_cast<const uint4 *>(src + b);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // host side
 
 bool umma_ok(int64_t d_in, int64_t d_out, int64_t g) { return d_in % 128 == 0 && g % 128 == 0 && d_out % 128 == 0; }
 
-template <int P, bool MERGED, class GEO>
+template <int P, class GEO>
 size_t umma_smem() {
-    return (size_t)UmStage<P, MERGED, GEO>::NS * UmStage<P, MERGED, GEO>::BYTES;
+    return (size_t)UmStage<P, GEO>::NS * UmStage<P, GEO>::BYTES;
 }
 
 template <int CK>
@@ -982,19 +915,15 @@ int64_t umma_b_bytes(int64_t rows, int64_t d_in) {
     return umma_cnt_off(rows, d_in) + ceil_div((int64_t)umma_grid() * 4, 256) * 256;
 }
 
-template <int P, bool MERGED, class GEO, bool NARROW = false>
+template <int P, class GEO, bool NARROW = false>
 cq_status launch_umma(const int8_t *bfrag, int64_t n_tiles, const float *scales, const int32_t *sums,
                       const int32_t *offsets, int64_t n_seg, int64_t seg_first, const cq_expert_site *a, float *out_a,
                       const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, int32_t *part,
                       int32_t *cnt, cudaStream_t st) {
-    static bool attr = false;
-    const size_t smem = umma_smem<P, MERGED, GEO>();
-    if (!attr) {
-        cudaFuncSetAttribute(lut_umma_kernel<P, MERGED, GEO, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr = true;
-    }
-    launch_pdl(lut_umma_kernel<P, MERGED, GEO, NARROW>, umma_grid(), UmWarps<P, MERGED>::THREADS, smem, st,
+    // the dynamic-smem opt-in is per device: set it on every launch (cheap next to the kernel)
+    const size_t smem = umma_smem<P, GEO>();
+    cudaFuncSetAttribute(lut_umma_kernel<P, GEO, NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(lut_umma_kernel<P, GEO, NARROW>, umma_grid(), UmWarps<P>::THREADS, smem, st,
         bfrag, n_tiles, scales, sums, offsets, (int)n_seg, seg_first, a->tc_ids, a->tc_lut, a->tc_rowscale, out_a,
         b ? b->tc_ids : nullptr, b ? b->tc_lut : nullptr, b ? b->tc_rowscale : nullptr, out_b, b ? 2 : 1, (int)d_in,
         (int)d_out, (int)a->group_size, part, cnt);
@@ -1006,27 +935,23 @@ cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, c
                        int64_t seg_first, int64_t rows, const cq_expert_site *a, float *out_a,
                        const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, const UmmaIn &in,
                        cudaStream_t st) {
-    const bool merged = umma_merged(a->tc_layout);
     // narrow lookup only when every matrix of the launch has ids < 8 (the data is that of UMMA128U)
     const bool narrow = a->tc_layout == CQ_TC_UMMA128U8 && (b == nullptr || b->tc_layout == CQ_TC_UMMA128U8);
     const int64_t tiles = umma_b_tiles(rows);
-    int32_t *sums = merged ? reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in)) : nullptr;
+    int32_t *sums = reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in));
     int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
     int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
     CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), in, scales, offsets + n_seg, st));
     if (in.gathers()) scales = in.scales_out;  // per segment row from here on
-#define CQ_UMMA(P_, M_, N_)                                                                                   \
-    launch_umma<P_, M_, GEO, N_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, \
-                                 d_out, part, cnt, st)
-    if (merged && narrow) {
-        if (a->tc_planes == 3) return CQ_UMMA(3, true, true);
-        if (a->tc_planes == 2) return CQ_UMMA(2, true, true);
-    } else if (merged) {
-        if (a->tc_planes == 3) return CQ_UMMA(3, true, false);
-        if (a->tc_planes == 2) return CQ_UMMA(2, true, false);
-    } else if constexpr (GEO::NT == 32) {  // the signed layouts exist in the decode geometry only
-        if (a->tc_planes == 3) return CQ_UMMA(3, false, false);
-        if (a->tc_planes == 2) return CQ_UMMA(2, false, false);
+#define CQ_UMMA(P_, N_)                                                                                        \
+    launch_umma<P_, GEO, N_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, \
+                             part, cnt, st)
+    if (narrow) {
+        if (a->tc_planes == 3) return CQ_UMMA(3, true);
+        if (a->tc_planes == 2) return CQ_UMMA(2, true);
+    } else {
+        if (a->tc_planes == 3) return CQ_UMMA(3, false);
+        if (a->tc_planes == 2) return CQ_UMMA(2, false);
     }
 #undef CQ_UMMA
     set_error("tcgen05 path: planes must be 2 or 3");
@@ -1041,7 +966,8 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
                            const cq_expert_site *b, float *out_b, int64_t d_in, int64_t d_out, cudaStream_t st,
                            const UmmaIn &in) {
     if (rows == 0 || n_seg == 0) return CQ_OK;
-    if (!umma_ok(d_in, d_out, a->group_size) || a->tc_lut == nullptr || (b && b->tc_lut == nullptr)) {
+    if (!umma_ok(d_in, d_out, a->group_size) || a->tc_lut == nullptr || (b && b->tc_lut == nullptr) ||
+        !umma_merged(a->tc_layout)) {
         set_error("tcgen05 path: site not prepared or shape outside envelope");
         return CQ_ERR_UNSUPPORTED;
     }
@@ -1062,7 +988,7 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
     const char *geo = getenv("CQ_UMMA_GEOMETRY");
     const bool force_pf = geo != nullptr && geo[0] == 'p' && rows >= 64;
     const bool force_dc = (geo != nullptr && geo[0] == 'd') || getenv("CQ_UMMA_NO_PREFILL") != nullptr;
-    if (umma_merged(a->tc_layout) && !force_dc && (force_pf || umma_prefill(rows, n_seg, d_in, d_out, b ? 2 : 1)))
+    if (!force_dc && (force_pf || umma_prefill(rows, n_seg, d_in, d_out, b ? 2 : 1)))
         return lut_umma_geo<UmPrefill>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b,
                                        d_in, d_out, in, st);
     return lut_umma_geo<UmDecode>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b, d_in,
@@ -1072,19 +998,6 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
 // Where the merged layout's int32 row sums live in a B buffer (silu_quant writes them directly).
 int32_t *umma_row_sums(int8_t *bbuf, int64_t rows, int64_t d_in) {
     return reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in));
-}
-
-// One-time re-layout for the tcgen05 kernel from the 16-row LUT layout.
-cq_status umma_prepare(const uint8_t *ids, const int8_t *lut16, int64_t rows, int64_t d_in, int64_t g, int64_t planes,
-                       uint8_t *tc_ids, int8_t *tc_lut, cudaStream_t st) {
-    const int64_t total_ids = (rows / 128) * (d_in / 128) * 4 * 128;
-    ids_umma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total_ids, 256), 148 * 32), 256, 0, st>>>(
-        ids, rows, d_in, reinterpret_cast<uint4 *>(tc_ids));
-    CQ_TRY(check_launch("ids_umma"));
-    const int64_t total_lut = rows * (d_in / g);
-    lut_relayout_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total_lut, 256), 148 * 32), 256, 0, st>>>(
-        lut16, rows, d_in / g, (int)planes, tc_lut);
-    return check_launch("lut_umma_relayout");
 }
 
 }  // namespace cq

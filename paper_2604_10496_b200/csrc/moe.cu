@@ -32,10 +32,10 @@ cq_status lut_f32_grouped(const int8_t *, const float *, const int32_t *, int64_
                           const uint8_t *, const float *, const uint8_t *, const float *, int64_t,
                           int64_t, int64_t, float *, cudaStream_t);
 bool f32_path_ok(int64_t d_in, int64_t g);
-cq_status lut_tc_grouped_frag(const int8_t *, uint2 *, const float *, const int32_t *, int64_t, int64_t, int64_t,
-                              const cq_expert_site *, const cq_expert_site *, int64_t, int64_t, float *,
-                              cudaStream_t);
-bool tc_path_ok(int64_t d_in, int64_t d_out, int64_t g);
+cq_status ordered_lut(const int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t, const uint8_t *,
+                      const float *, int64_t, int64_t, int64_t, float *, cudaStream_t);
+cq_status ordered_matmul(const void *, int, const float *, int64_t, int64_t, int64_t, float *, cudaStream_t);
+bool umma_ok(int64_t d_in, int64_t d_out, int64_t g);
 cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_t *, int64_t, int64_t, int64_t,
                            const cq_expert_site *, float *, const cq_expert_site *, float *, int64_t, int64_t,
                            cudaStream_t, const UmmaIn &in = UmmaIn{});
@@ -53,18 +53,21 @@ __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, 
                                                           int64_t ff, int8_t *__restrict__ codes,
                                                           float *__restrict__ scales,
                                                           const int32_t *__restrict__ live,
-                                                          int32_t *__restrict__ sums) {
+                                                          int32_t *__restrict__ sums, int *__restrict__ nonfinite) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
     float *ar = a + row * ff;
     const float *br = b + row * ff;
     float mx = 0.0f;
+    bool bad = false;
     for (int64_t j = threadIdx.x; j < ff; j += blockDim.x) {
         const float h = __fmul_rn(silu_f32(ar[j]), br[j]);
         ar[j] = h;
         mx = fmaxf(mx, fabsf(h));
+        bad |= !(fabsf(h) <= FLT_MAX);
     }
+    if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
     __shared__ float red[8];
     __shared__ float s_sh;
     mx = warp_max(mx);
@@ -100,7 +103,8 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
                                                               int64_t ff, int8_t *__restrict__ codes,
                                                               float *__restrict__ scales,
                                                               const int32_t *__restrict__ live,
-                                                              int32_t *__restrict__ sums, int keep) {
+                                                              int32_t *__restrict__ sums, int keep,
+                                                              int *__restrict__ nonfinite) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
@@ -109,6 +113,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     const int nv = (int)(ff >> 2);
     float4 h[V];
     float mx = 0.0f;
+    bool bad = false;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * (int)blockDim.x;
@@ -117,9 +122,14 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
             h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
                                __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
             if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
-            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
+            const float m4 = fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w)));
+            mx = fmaxf(mx, m4);
+            // fmaxf drops NaN: test the four values themselves
+            bad |= !(fabsf(h[u].x) <= FLT_MAX && fabsf(h[u].y) <= FLT_MAX && fabsf(h[u].z) <= FLT_MAX &&
+                     fabsf(h[u].w) <= FLT_MAX);
         }
     }
+    if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
     __shared__ float red[16];
     __shared__ float s_sh;
     mx = warp_max(mx);
@@ -161,7 +171,8 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
                                                              int64_t ff, int8_t *__restrict__ codes,
                                                              float *__restrict__ scales,
                                                              const int32_t *__restrict__ live,
-                                                             int32_t *__restrict__ sums, int keep) {
+                                                             int32_t *__restrict__ sums, int keep,
+                                                             int *__restrict__ nonfinite) {
     namespace cg = cooperative_groups;
     griddep_wait();
     const int64_t row = blockIdx.x / CL;
@@ -174,6 +185,7 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
     const int nv = (int)(seg >> 2);
     float4 h[V];
     float mx = 0.0f;
+    bool bad = false;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * 256;
@@ -183,8 +195,11 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
                                __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
             if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
             mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
+            bad |= !(fabsf(h[u].x) <= FLT_MAX && fabsf(h[u].y) <= FLT_MAX && fabsf(h[u].z) <= FLT_MAX &&
+                     fabsf(h[u].w) <= FLT_MAX);
         }
     }
+    if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
     __shared__ float red[8];
     __shared__ float part_max, s_sh;
     __shared__ int row_sum;  // rank 0's: the cluster's code sum
@@ -233,17 +248,17 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
 
 template <int CL>
 static bool silu_quant_cluster(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                               const int32_t *live, int32_t *sums, int keep, cudaStream_t st) {
+                               const int32_t *live, int32_t *sums, int keep, int *nonfinite, cudaStream_t st) {
     if (ff % (4 * CL)) return false;
     const int64_t v = ceil_div(ff / CL / 4, 256);
     const dim3 grid((unsigned)(rows * CL));
     switch (v) {
-        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
-        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
+        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
+        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
         case 3:
-        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
+        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
         case 5: case 6: case 7:
-        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep); break;
+        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
         default: return false;
     }
     return true;
@@ -257,8 +272,9 @@ static int vec_threads(int64_t ff, int v) {
 // sums (nullable): per-row code sums (the merged-layout GEMM's bias term).
 // keep: also store h = silu(a) * b over a (fp32, read only by tracing); else a
 // keeps the gate output and only the codes, scales and sums are written.
+// nonfinite (nullable): set to 1 when some h is inf / NaN (the down site's DivergenceError).
 cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                     const int32_t *live, cudaStream_t st, int32_t *sums, int keep) {
+                     const int32_t *live, cudaStream_t st, int32_t *sums, int keep, int *nonfinite) {
     if (rows == 0) return CQ_OK;
     static int cl_env = -1;
     if (cl_env < 0) {
@@ -267,10 +283,10 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
     }
     // about two CTAs per SM over the whole grid; long rows only (a cluster CTA keeps >= 256 float4)
     if (cl_env && ff >= 8192) {
-        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, keep, st)) return check_launch("silu_quant");
-        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, keep, st))
+        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, st)) return check_launch("silu_quant");
+        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, st))
             return check_launch("silu_quant");
-        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, keep, st))
+        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, st))
             return check_launch("silu_quant");
     }
     const int64_t v = ceil_div(ff / 4, 512);
@@ -278,70 +294,19 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
         switch (v) {
             case 1: {  // short rows: one float4 per thread, CTA sized to the row
                 const int thr = (int)std::max<int64_t>(64, ceil_div(ff / 4, 32) * 32);
-                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums, keep);
+                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite);
                 break;
             }
             // CTA sized to the row at V float4 per thread (PH ff = 6400: 416 threads instead of 512)
-            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, vec_threads(ff, 2), 0, st, a, b, ff, codes, scales, live, sums, keep); break;
+            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, vec_threads(ff, 2), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
             case 3:
-            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, vec_threads(ff, 4), 0, st, a, b, ff, codes, scales, live, sums, keep); break;
-            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, vec_threads(ff, 8), 0, st, a, b, ff, codes, scales, live, sums, keep); break;
+            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, vec_threads(ff, 4), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
+            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, vec_threads(ff, 8), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
         }
     } else {
-        launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live, sums);
+        launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live, sums, nonfinite);
     }
     return check_launch("silu_quant");
-}
-
-// --- ordered grouped GEMM (GPU oracle path): bit-exact chains per segment.
-constexpr int OG_ROWS = 8, OG_TOK = 32, OG_J = 64;
-
-__global__ void __launch_bounds__(256) ordered_grouped_kernel(
-    const int8_t *__restrict__ codes, const float *__restrict__ scales, const int32_t *__restrict__ offsets,
-    int64_t seg_first, const uint8_t *__restrict__ ids, const float *__restrict__ cent, int64_t d_in,
-    int64_t d_out, int64_t g, float *__restrict__ out) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    __shared__ int8_t tile[OG_J][OG_TOK];
-    const int lane = threadIdx.x, wy = threadIdx.y;
-    const int64_t seg = blockIdx.z;
-    const int64_t rb = offsets[seg], re = offsets[seg + 1];
-    const int64_t t_blk = rb + blockIdx.x * (int64_t)OG_TOK;
-    if (t_blk >= re) return;
-    const int64_t t = t_blk + lane;
-    const int64_t i = blockIdx.y * (int64_t)OG_ROWS + wy;
-    const int64_t e = seg + seg_first;
-    const int64_t row_bytes = (d_in + 1) >> 1, n_groups = d_in / g;
-    const int64_t ii = i < d_out ? i : 0;
-    const uint8_t *idrow = ids + (e * d_out + ii) * row_bytes;
-    const float *crow = cent + (e * d_out + ii) * n_groups * 16;
-    float acc = 0.0f;
-    for (int64_t j0 = 0; j0 < d_in; j0 += OG_J) {
-        __syncthreads();
-        for (int x = wy * 32 + lane; x < OG_J * OG_TOK; x += 256) {
-            const int tt = x / OG_J, jj = x % OG_J;
-            const int64_t gt = t_blk + tt, gj = j0 + jj;
-            tile[jj][tt] = (gt < re && gj < d_in) ? codes[gt * d_in + gj] : (int8_t)0;
-        }
-        __syncthreads();
-        const int jn = (int)((d_in - j0) < OG_J ? (d_in - j0) : OG_J);
-        for (int jj = 0; jj < jn; ++jj) {
-            const int64_t j = j0 + jj;
-            const uint8_t b = __ldg(idrow + (j >> 1));
-            const int id = (j & 1) ? (b >> 4) : (b & 15);
-            acc = __fadd_rn(acc, __fmul_rn(__ldg(crow + (j / g) * 16 + id), (float)tile[jj][lane]));
-        }
-    }
-    if (t < re && i < d_out) out[t * d_out + i] = __fmul_rn(__ldg(scales + t), acc);
-}
-
-cq_status ordered_grouped(const int8_t *codes, const float *scales, const int32_t *offsets, int64_t n_seg,
-                          int64_t seg_first, int64_t rows_bound, const uint8_t *ids, const float *cent,
-                          int64_t d_in, int64_t d_out, int64_t g, float *out, cudaStream_t st) {
-    if (n_seg == 0 || rows_bound == 0 || d_out == 0) return CQ_OK;
-    dim3 grid((unsigned)ceil_div(rows_bound, OG_TOK), (unsigned)ceil_div(d_out, OG_ROWS), (unsigned)n_seg);
-    ordered_grouped_kernel<<<grid, dim3(32, OG_ROWS), 0, st>>>(codes, scales, offsets, seg_first, ids, cent,
-                                                               d_in, d_out, g, out);
-    return check_launch("ordered_grouped");
 }
 
 // h = silu(a) * b elementwise (model.py:396), in place into a.
@@ -414,45 +379,6 @@ __global__ void combine_kernel(const int32_t *__restrict__ selected, const float
     }
 }
 
-// Online rotation v = x @ R in fp32 (CUDA cores, 64x64 tiles).
-template <int DT>
-__global__ void __launch_bounds__(256) rotate_kernel(const void *__restrict__ x, const float *__restrict__ r,
-                                                     int64_t n, int64_t d, float *__restrict__ v) {
-    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
-    __shared__ float xs[16][64 + 1];
-    __shared__ float rs[16][64 + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
-    float acc[4][4] = {};
-    for (int64_t k0 = 0; k0 < d; k0 += 16) {
-        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
-            const int kk = e & 15, rr = e >> 4;
-            const int64_t gr = row0 + rr, gk = k0 + kk;
-            float xv = 0.0f;
-            if (gr < n && gk < d)
-                xv = DT == CQ_DTYPE_F32 ? reinterpret_cast<const float *>(x)[gr * d + gk]
-                                        : bf16_bits_to_f32(reinterpret_cast<const uint16_t *>(x)[gr * d + gk]);
-            xs[kk][rr] = xv;
-            const int cc = e & 63, k2 = e >> 6;
-            const int64_t gc = col0 + cc, gk2 = k0 + k2;
-            rs[k2][cc] = (gc < d && gk2 < d) ? r[gk2 * d + gc] : 0.0f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk)
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xs[kk][ty * 4 + a], rs[kk][tx * 4 + b], acc[a][b]);
-        __syncthreads();
-    }
-    for (int a = 0; a < 4; ++a)
-        for (int b = 0; b < 4; ++b) {
-            const int64_t gr = row0 + ty * 4 + a, gc = col0 + tx * 4 + b;
-            if (gr < n && gc < d) v[gr * d + gc] = acc[a][b];
-        }
-}
-
 // ---------------------------------------------------------------------------
 // workspace
 
@@ -484,6 +410,8 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_HCODES_FRAG] = umma_b_bytes(Rh, ff);
     sz[CQ_WS_ROT_ACT] = dsc->rotation_tc ? rot_tc_act_bytes(n, d) : 0;
     sz[CQ_WS_TOK_SUMS] = n * 4;
+    sz[CQ_WS_STATUS] = 4 * 4;
+    sz[CQ_WS_SH_OFFSETS] = 2 * 4;
     int64_t pos = 0;
     for (int b = 0; b < CQ_WS_COUNT_; ++b) {
         if (off) off[b] = pos;
@@ -496,8 +424,10 @@ struct Ws {
     int8_t *codes;
     float *scales, *logits, *weights, *scales_perm, *hidden, *hscales, *fout, *rotated, *shared;
     int32_t *selected, *counts, *offsets, *perm_token, *perm_slot, *inv, *tok_sums;
+    int *status;  // CQ_WS_STATUS: [0] layer input non-finite, [1] hidden (down input) non-finite
+    int32_t *sh_offsets;
     int8_t *codes_perm, *hcodes;
-    uint2 *codes_frag, *hcodes_frag;
+    int8_t *codes_frag, *hcodes_frag;  // tcgen05 B-operand buffers
     void *rot_act;
 };
 
@@ -515,6 +445,8 @@ Ws carve(void *base, const int64_t *o) {
     w.perm_slot = reinterpret_cast<int32_t *>(b + o[CQ_WS_PERM_SLOT]);
     w.inv = reinterpret_cast<int32_t *>(b + o[CQ_WS_INV]);
     w.tok_sums = reinterpret_cast<int32_t *>(b + o[CQ_WS_TOK_SUMS]);
+    w.status = reinterpret_cast<int *>(b + o[CQ_WS_STATUS]);
+    w.sh_offsets = reinterpret_cast<int32_t *>(b + o[CQ_WS_SH_OFFSETS]);
     w.codes_perm = reinterpret_cast<int8_t *>(b + o[CQ_WS_CODES_PERM]);
     w.scales_perm = reinterpret_cast<float *>(b + o[CQ_WS_SCALES_PERM]);
     w.hidden = reinterpret_cast<float *>(b + o[CQ_WS_HIDDEN]);
@@ -524,8 +456,8 @@ Ws carve(void *base, const int64_t *o) {
     w.rotated = reinterpret_cast<float *>(b + o[CQ_WS_ROTATED]);
     w.rot_act = b + o[CQ_WS_ROT_ACT];
     w.shared = reinterpret_cast<float *>(b + o[CQ_WS_SHARED]);
-    w.codes_frag = reinterpret_cast<uint2 *>(b + o[CQ_WS_CODES_FRAG]);
-    w.hcodes_frag = reinterpret_cast<uint2 *>(b + o[CQ_WS_HCODES_FRAG]);
+    w.codes_frag = reinterpret_cast<int8_t *>(b + o[CQ_WS_CODES_FRAG]);
+    w.hcodes_frag = reinterpret_cast<int8_t *>(b + o[CQ_WS_HCODES_FRAG]);
     return w;
 }
 
@@ -563,8 +495,8 @@ int choose_path(const cq_moe_desc *d) {
     const bool tc = d->gate.tc_lut && d->up.tc_lut && d->down.tc_lut &&
                     umma_family(d->gate.tc_layout) == umma_family(d->up.tc_layout) &&
                     umma_family(d->up.tc_layout) == umma_family(d->down.tc_layout) &&
-                    tc_path_ok(d->d_model, d->d_ff, d->gate.group_size) &&
-                    tc_path_ok(d->d_ff, d->d_model, d->down.group_size);
+                    umma_ok(d->d_model, d->d_ff, d->gate.group_size) &&
+                    umma_ok(d->d_ff, d->d_model, d->down.group_size);
     if (tc) return CQ_PATH_TC;
     if (f32_path_ok(d->d_model, d->gate.group_size) && f32_path_ok(d->d_ff, d->down.group_size))
         return CQ_PATH_F32;
@@ -575,76 +507,74 @@ int choose_path(const cq_moe_desc *d) {
 cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &gate, const cq_expert_site &up,
                       const cq_expert_site &down, int64_t n_seg, int64_t seg_first, const int8_t *codes,
                       const float *scales, const int32_t *offsets, int64_t rows, float *hidden,
-                      int8_t *hcodes, float *hscales, float *fout, uint2 *frag_in, uint2 *frag_h,
-                      cudaStream_t st, cudaEvent_t *ev = nullptr, const UmmaIn &in = UmmaIn{}) {
+                      int8_t *hcodes, float *hscales, float *fout, int8_t *bbuf_in, int8_t *bbuf_h,
+                      int *nonfinite, cudaStream_t st, cudaEvent_t *ev = nullptr, const UmmaIn &in = UmmaIn{}) {
     const int64_t d = dsc->d_model, ff = dsc->d_ff;
     if (rows == 0 || n_seg == 0) return CQ_OK;
-    if (path == CQ_PATH_TC && gate.tc_layout != CQ_TC_MMA16) {
-        float *bbuf = hidden + rows * ff;
-        if (ev) cudaEventRecord(ev[0], st);
+    float *bout = hidden + rows * ff;  // up output (gate output / h in `hidden`)
+    if (ev) cudaEventRecord(ev[0], st);
+    if (path == CQ_PATH_TC) {
         // `in` may make the B build gather token rows (codes / scales per token, in.perm)
-        CQ_TRY(lut_umma_grouped(codes, reinterpret_cast<int8_t *>(frag_in), scales, offsets, n_seg, seg_first, rows,
-                                &gate, hidden, &up, bbuf, d, ff, st, in));
+        CQ_TRY(lut_umma_grouped(codes, bbuf_in, scales, offsets, n_seg, seg_first, rows, &gate, hidden, &up, bout, d,
+                                ff, st, in));
         if (ev) cudaEventRecord(ev[1], st);
         // the re-quantizer writes the down GEMM's row sums straight into its B buffer
         UmmaIn hin;
-        hin.sums_ready = umma_merged(down.tc_layout);
-        int32_t *hsums = hin.sums_ready ? umma_row_sums(reinterpret_cast<int8_t *>(frag_h), rows, ff) : nullptr;
+        hin.sums_ready = true;
+        int32_t *hsums = umma_row_sums(bbuf_h, rows, ff);
         const int keep = (dsc->flags & CQ_FLAG_KEEP_HIDDEN) != 0;
-        CQ_TRY(silu_quant(hidden, bbuf, rows, ff, hcodes, hscales, offsets + n_seg, st, hsums, keep));
+        CQ_TRY(silu_quant(hidden, bout, rows, ff, hcodes, hscales, offsets + n_seg, st, hsums, keep, nonfinite));
         if (ev) cudaEventRecord(ev[2], st);
-        CQ_TRY(lut_umma_grouped(hcodes, reinterpret_cast<int8_t *>(frag_h), hscales, offsets, n_seg, seg_first, rows,
-                                &down, fout, nullptr, nullptr, ff, d, st, hin));
+        CQ_TRY(lut_umma_grouped(hcodes, bbuf_h, hscales, offsets, n_seg, seg_first, rows, &down, fout, nullptr,
+                                nullptr, ff, d, st, hin));
         if (ev) cudaEventRecord(ev[3], st);
         return CQ_OK;
     }
-    if (ev) cudaEventRecord(ev[0], st);
-    if (path == CQ_PATH_TC) {
-        CQ_TRY(lut_tc_grouped_frag(codes, frag_in, scales, offsets, n_seg, seg_first, rows, &gate, &up, d, ff,
-                                   hidden, st));
-    } else if (path == CQ_PATH_F32) {
+    if (path == CQ_PATH_F32) {
         CQ_TRY(lut_f32_grouped(codes, scales, offsets, n_seg, seg_first, gate.ids, gate.centroids, up.ids,
                                up.centroids, d, ff, gate.group_size, hidden, st));
-    } else {
-        float *bbuf = hidden + rows * ff;
-        CQ_TRY(ordered_grouped(codes, scales, offsets, n_seg, seg_first, rows, gate.ids, gate.centroids, d, ff,
-                               gate.group_size, hidden, st));
-        CQ_TRY(ordered_grouped(codes, scales, offsets, n_seg, seg_first, rows, up.ids, up.centroids, d, ff,
-                               up.group_size, bbuf, st));
-        silu_mul_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * ff, 256), 148 * 16), 256, 0, st>>>(
-            hidden, bbuf, rows * ff);
+    } else {  // ordered: the reference's chains bit for bit (ordered.cu)
+        CQ_TRY(ordered_lut(codes, scales, offsets, n_seg, seg_first, rows, gate.ids, gate.centroids, d, ff,
+                           gate.group_size, hidden, st));
+        CQ_TRY(ordered_lut(codes, scales, offsets, n_seg, seg_first, rows, up.ids, up.centroids, d, ff,
+                           up.group_size, bout, st));
+        launch_pdl(silu_mul_kernel, (unsigned)std::min<int64_t>(ceil_div(rows * ff, 256), 148 * 16), 256, 0, st,
+                   hidden, (const float *)bout, rows * ff);
         CQ_TRY(check_launch("silu_mul"));
     }
     if (ev) cudaEventRecord(ev[1], st);
-    CQ_TRY(quantize_a4(hidden, CQ_DTYPE_F32, rows, ff, hcodes, hscales, nullptr, nullptr, st));
+    CQ_TRY(quantize_a4(hidden, CQ_DTYPE_F32, rows, ff, hcodes, hscales, nonfinite, nullptr, st));
     if (ev) cudaEventRecord(ev[2], st);
-    if (ev) {
-        cq_status rc;
-        if (path == CQ_PATH_TC)
-            rc = lut_tc_grouped_frag(hcodes, frag_h, hscales, offsets, n_seg, seg_first, rows, &down, nullptr, ff, d,
-                                     fout, st);
-        else if (path == CQ_PATH_F32)
-            rc = lut_f32_grouped(hcodes, hscales, offsets, n_seg, seg_first, down.ids, down.centroids, nullptr,
-                                 nullptr, ff, d, down.group_size, fout, st);
-        else
-            rc = ordered_grouped(hcodes, hscales, offsets, n_seg, seg_first, rows, down.ids, down.centroids, ff, d,
-                                 down.group_size, fout, st);
-        cudaEventRecord(ev[3], st);
-        return rc;
-    }
-    if (path == CQ_PATH_TC)
-        return lut_tc_grouped_frag(hcodes, frag_h, hscales, offsets, n_seg, seg_first, rows, &down, nullptr, ff, d,
-                                   fout, st);
+    cq_status rc;
     if (path == CQ_PATH_F32)
-        return lut_f32_grouped(hcodes, hscales, offsets, n_seg, seg_first, down.ids, down.centroids, nullptr,
-                               nullptr, ff, d, down.group_size, fout, st);
-    return ordered_grouped(hcodes, hscales, offsets, n_seg, seg_first, rows, down.ids, down.centroids, ff, d,
-                           down.group_size, fout, st);
+        rc = lut_f32_grouped(hcodes, hscales, offsets, n_seg, seg_first, down.ids, down.centroids, nullptr, nullptr,
+                             ff, d, down.group_size, fout, st);
+    else
+        rc = ordered_lut(hcodes, hscales, offsets, n_seg, seg_first, rows, down.ids, down.centroids, ff, d,
+                         down.group_size, fout, st);
+    if (ev) cudaEventRecord(ev[3], st);
+    return rc;
 }
 
 __global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     for (int64_t s = 0; s <= n_shared; ++s) off[s] = (int32_t)(s * n);
+}
+
+// Builder-defined shared experts (not in the reference,
+// SPEC.md:173): always-on experts of weight 1 over all n tokens of this rank,
+// each run as one segment on the un-permuted layer-input codes into its own
+// [n][d_model] slice of `out` (n_shared slices).
+cq_status shared_experts(const cq_moe_desc *desc, int path, int64_t n, const Ws &w, float *out, cudaStream_t st) {
+    if (desc->n_shared <= 0 || n == 0) return CQ_OK;
+    launch_pdl(shared_offsets_kernel, 1, 1, 0, st, w.sh_offsets, (int64_t)1, n);
+    CQ_TRY(check_launch("shared_offsets"));
+    const int sp = (path == CQ_PATH_TC && desc->sh_gate.tc_lut == nullptr) ? CQ_PATH_F32 : path;
+    for (int64_t s = 0; s < desc->n_shared; ++s)
+        CQ_TRY(run_experts(desc, sp, desc->sh_gate, desc->sh_up, desc->sh_down, 1, s, w.codes, w.scales,
+                           w.sh_offsets, n, w.hidden, w.hcodes, w.hscales, out + s * n * desc->d_model, w.codes_frag,
+                           w.hcodes_frag, w.status + 1, st));
+    return CQ_OK;
 }
 
 // gather = false: leave codes_perm / scales_perm unwritten (the tcgen05 expert
@@ -662,19 +592,14 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
         CQ_TRY(rot_tc_apply(x, dtype, n, d, dsc->rotation_tc, w.rot_act, w.rotated, st));
         qin = w.rotated;
         qdt = CQ_DTYPE_F32;
-    } else if (dsc->rotation != nullptr) {
-        dim3 grid((unsigned)ceil_div(d, 64), (unsigned)ceil_div(n, 64));
-        if (dtype == CQ_DTYPE_F32)
-            rotate_kernel<CQ_DTYPE_F32><<<grid, 256, 0, st>>>(x, dsc->rotation, n, d, w.rotated);
-        else
-            rotate_kernel<CQ_DTYPE_BF16><<<grid, 256, 0, st>>>(x, dsc->rotation, n, d, w.rotated);
-        CQ_TRY(check_launch("rotate"));
+    } else if (dsc->rotation != nullptr) {  // the reference's ordered chain (pipeline.py:516 -> _core.pyx:27-38)
+        CQ_TRY(ordered_matmul(x, dtype, dsc->rotation, n, d, d, w.rotated, st));
         qin = w.rotated;
         qdt = CQ_DTYPE_F32;
     }
     // the dequantized rows (router input) go to the fout buffer, unused until the down GEMM;
     // the quantizer also clears the route counts and the arrival counter (counts[E])
-    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, nullptr, w.fout, st, w.tok_sums, w.counts,
+    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, w.status, w.fout, st, w.tok_sums, w.counts,
                        (int)dsc->n_experts + 1));
     if (deferred != nullptr) {
         *deferred = 0;
@@ -734,7 +659,7 @@ extern "C" cq_status cq_moe_experts(const cq_moe_desc *desc, const int8_t *codes
     Ws w = carve(workspace, off);
     return run_experts(desc, choose_path(desc), desc->gate, desc->up, desc->down, desc->n_local_experts, 0,
                        codes_perm, scales_perm, offsets, rows, w.hidden, w.hcodes, w.hscales, fout, w.codes_frag,
-                       w.hcodes_frag, as_stream(stream));
+                       w.hcodes_frag, w.status + 1, as_stream(stream));
 }
 
 extern "C" cq_status cq_moe_profile_experts(const cq_moe_desc *desc, const int8_t *codes_perm,
@@ -758,7 +683,7 @@ extern "C" cq_status cq_moe_profile_experts(const cq_moe_desc *desc, const int8_
     for (int i = 0; i < iters && rc == CQ_OK; ++i) {
         rc = run_experts(desc, choose_path(desc), desc->gate, desc->up, desc->down, desc->n_local_experts, 0,
                          codes_perm, scales_perm, offsets, rows, w.hidden, w.hcodes, w.hscales, fout, w.codes_frag,
-                         w.hcodes_frag, st, ev);
+                         w.hcodes_frag, nullptr, st, ev);
         cudaEventSynchronize(ev[3]);
         for (int k = 0; k < 3; ++k) {
             float ms = 0.0f;
@@ -791,8 +716,27 @@ static cq_status combine_n(const int32_t *selected, const float *weights, const 
 
 extern "C" cq_status cq_moe_combine(const int32_t *selected, const float *weights, const int32_t *inv,
                                     const float *fout, int64_t n_tokens, int64_t top_k, int64_t d_model,
-                                    const float *add, float *out, void *stream) {
-    return combine_n(selected, weights, inv, fout, n_tokens, top_k, d_model, add, 1, out, stream);
+                                    const float *add, int64_t n_add, float *out, void *stream) {
+    if (n_add < 0 || (n_add > 0 && add == nullptr)) {
+        set_error("combine: n_add buffers need a non-null add");
+        return CQ_ERR_SHAPE;
+    }
+    return combine_n(selected, weights, inv, fout, n_tokens, top_k, d_model, add, (int)n_add, out, stream);
+}
+
+extern "C" cq_status cq_moe_shared_experts(const cq_moe_desc *desc, int64_t n_tokens, float *shared_out,
+                                           void *workspace, int64_t workspace_bytes, void *stream) {
+    CQ_TRY(validate_desc(desc));
+    int64_t off[CQ_WS_COUNT_];
+    if (workspace_layout(desc, n_tokens, off) > workspace_bytes) {
+        set_error("moe: workspace too small");
+        return CQ_ERR_SHAPE;
+    }
+    if (desc->n_shared > 0 && shared_out == nullptr) {
+        set_error("moe: shared experts need an output buffer");
+        return CQ_ERR_SHAPE;
+    }
+    return shared_experts(desc, choose_path(desc), n_tokens, carve(workspace, off), shared_out, as_stream(stream));
 }
 
 extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int dtype, int64_t n_tokens, float *out,
@@ -812,9 +756,12 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
     Ws w = carve(workspace, off);
     const int path = choose_path(desc);
     // tcgen05 layouts: the expert stage's B build gathers the token rows itself (no codes_perm)
-    const bool umma = path == CQ_PATH_TC && desc->gate.tc_layout != CQ_TC_MMA16;
+    const bool umma = path == CQ_PATH_TC;
     int deferred = 0;
     CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma, umma ? &deferred : nullptr));
+    // builder-defined shared experts first: they read only the layer-input codes,
+    // and the routed pass after them leaves its own counts / hidden buffers for tracing
+    CQ_TRY(shared_experts(desc, path, n_tokens, w, w.shared, st));
     const int64_t R = n_tokens * desc->top_k;
     if (umma) {
         UmmaIn in;
@@ -835,27 +782,14 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
             in.perm = w.perm_token;
         }
         CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes, w.scales,
-                           w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag, w.hcodes_frag, st,
-                           nullptr, in));
+                           w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag, w.hcodes_frag,
+                           w.status + 1, st, nullptr, in));
     } else {
         CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts, 0, w.codes_perm,
                            w.scales_perm, w.offsets, R, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag,
-                           w.hcodes_frag, st));
+                           w.hcodes_frag, w.status + 1, st));
     }
-    // builder-defined shared experts: out = ((routed + sh_0) + sh_1) ...,
-    // each shared expert run as one segment over all n tokens (un-permuted codes) into its own
-    // slice of w.shared; the combine adds them in order (one pass over out)
-    if (desc->n_shared > 0) {
-        int32_t *soff = w.counts;  // counts were consumed by permute; E+1 >= 2 ints
-        shared_offsets_kernel<<<1, 1, 0, st>>>(soff, 1, n_tokens);
-        CQ_TRY(check_launch("shared_offsets"));
-    }
-    for (int64_t s = 0; s < desc->n_shared; ++s) {
-        const int sp = (path == CQ_PATH_TC && desc->sh_gate.tc_lut == nullptr) ? CQ_PATH_F32 : path;
-        CQ_TRY(run_experts(desc, sp, desc->sh_gate, desc->sh_up, desc->sh_down, 1, s, w.codes, w.scales, w.counts,
-                           n_tokens, w.hidden, w.hcodes, w.hscales, w.shared + s * n_tokens * desc->d_model,
-                           w.codes_frag, w.hcodes_frag, st));
-    }
+    // out = ((routed + sh_0) + sh_1) ..., the shared outputs added in order inside the combine pass
     return combine_n(w.selected, w.weights, w.inv, w.fout, n_tokens, desc->top_k, desc->d_model,
                      desc->n_shared > 0 ? w.shared : nullptr, (int)desc->n_shared, out, stream);
 }

@@ -193,7 +193,7 @@ cq_status quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *co
 using namespace cq;
 
 extern "C" cq_status cq_quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *codes,
-                                    float *scales, int check_finite, void *stream) {
+                                    float *scales, int32_t *nonfinite, void *stream) {
     if (n < 0 || d < 0) {
         set_error("quantize: negative shape");
         return CQ_ERR_SHAPE;
@@ -207,30 +207,9 @@ extern "C" cq_status cq_quantize_a4(const void *x, int dtype, int64_t n, int64_t
         set_error("quantize: zero-width rows");
         return CQ_ERR_SHAPE;
     }
-    cudaStream_t st = as_stream(stream);
-    int *flag = nullptr;
-    if (check_finite) {
-        if (cudaMallocAsync(&flag, sizeof(int), st) != cudaSuccess ||
-            cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess) {
-            set_error("quantize: flag alloc failed");
-            return CQ_ERR_CUDA;
-        }
-    }
-    cq_status rc = quantize_a4(x, dtype, n, d, codes, scales, flag, nullptr, st, nullptr, nullptr, 0);
-    if (check_finite) {
-        int host = 0;
-        cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
-        cudaFreeAsync(flag, st);
-        if (cudaStreamSynchronize(st) != cudaSuccess) {
-            set_error("quantize: sync failed");
-            return CQ_ERR_CUDA;
-        }
-        if (rc == CQ_OK && host) {
-            set_error("non-finite activation input to quantizer");
-            return CQ_ERR_DIVERGENCE;
-        }
-    }
-    return rc;
+    // no host sync: a non-finite row sets *nonfinite (sticky), read by the caller at its next sync
+    return quantize_a4(x, dtype, n, d, codes, scales, reinterpret_cast<int *>(nonfinite), nullptr, as_stream(stream),
+                       nullptr, nullptr, 0);
 }
 
 extern "C" cq_status cq_unpack_ids(const uint8_t *packed, int64_t rows, int64_t d_in, uint8_t *ids,

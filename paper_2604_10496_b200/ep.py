@@ -183,7 +183,7 @@ class EPStep:
         out = self.out if out is None else out
         _lib.check(_lib.lib().cq_moe_combine(tr["selected"].data_ptr(), tr["weights"].data_ptr(),
                                              self.inv.data_ptr(), self.ret.data_ptr(), self.n, self.k, self.d,
-                                             None, out.data_ptr(), _lib.stream()))
+                                             None, 0, out.data_ptr(), _lib.stream()))
         return out
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -244,6 +244,6 @@ class CudaBackend:
         inv = torch.arange(n * k, dtype=torch.int32, device="cuda").view(n, k)
         out = torch.empty((n, d), dtype=torch.float32, device="cuda")
         _lib.check(_lib.lib().cq_moe_combine(selected.data_ptr(), weights.data_ptr(), inv.data_ptr(),
-                                             f_routes.contiguous().data_ptr(), n, k, d, None, out.data_ptr(),
+                                             f_routes.contiguous().data_ptr(), n, k, d, None, 0, out.data_ptr(),
                                              _lib.stream()))
         return out

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ConfigError, ShapeError
+from .errors import ConfigError, DivergenceError, ShapeError
 from .lutgemm import PackedClusteredWeights, prepare_tc_site
 
 _PATHS = {"auto": _lib.CQ_PATH_AUTO, "f32": _lib.CQ_PATH_F32, "tc": _lib.CQ_PATH_TC,
@@ -66,7 +66,7 @@ class ExpertStack:
     def n(self) -> int:
         return self.ids.shape[0]
 
-    def prepare_tc(self, planes: int, layout: str = "umma128") -> None:
+    def prepare_tc(self, planes: int, layout: str = "umma128u") -> None:
         if self.tc is None or (self.tc["planes"], self.tc["layout"]) != (planes, layout):
             rows = self.n * self.d_out
             self.tc = prepare_tc_site(self.ids.view(rows, -1), self.centroids.view(rows, -1, 16),
@@ -151,16 +151,22 @@ class MoELayer:
         # store h = silu(a) * b in the workspace on the tensor-core path too (trace(); costs an
         # fp32 write of every routed hidden row)
         self.keep_hidden = False
+        # tensor-core path with the ordered (bit-exact) rotation instead of the tcgen05 one:
+        # routing then matches the reference bit for bit, at CUDA-core speed
+        self.exact_rotation = False
         self._ws = {}
         self._rot_tc = None  # R as three bf16 planes for the tensor-core rotation (prepare_tc)
 
     # ------------------------------------------------------------------
+    def tc_shapes_ok(self) -> bool:
+        """The tcgen05 path's envelope: 128 | d_model, d_ff, and every group size."""
+        sites = [self.gate, self.up, self.down] + (list(self.shared) if self.shared is not None else [])
+        return all(s.d_in % 128 == 0 and s.d_out % 128 == 0 and s.group_size % 128 == 0 for s in sites)
+
     def prepare_tc(self, planes_gate_up: int = 3, planes_down: int = 2,
                    layout: str = "umma128u") -> "MoELayer":
-        """Tensor-core layouts: 3 digit planes where the output is re-quantized
-        (gate, up), 2 for down.  layout "umma128u" (tcgen05,
-        unsigned merged digits), "umma128" (tcgen05, signed P/Q digit slices)
-        or "mma16" (mma.sync kernel)."""
+        """tcgen05 layouts (unsigned base-128 digit planes): 3 planes where the
+        output is re-quantized (gate, up), 2 for down."""
         sites = [(self.gate, planes_gate_up), (self.up, planes_gate_up), (self.down, planes_down)]
         if self.shared is not None:
             sites += [(self.shared[0], planes_gate_up), (self.shared[1], planes_gate_up),
@@ -189,7 +195,7 @@ class MoELayer:
         d.path = _PATHS[path or self.path]
         d.flags = _lib.FLAG_KEEP_HIDDEN if self.keep_hidden else 0
         # the tensor-core rotation goes with the tensor-core path; f32 / ordered keep the fp32 rotation
-        if self._rot_tc is not None and (path or self.path) in ("tc", "auto"):
+        if self._rot_tc is not None and (path or self.path) in ("tc", "auto") and not self.exact_rotation:
             d.rotation_tc = self._rot_tc.data_ptr()
         return d
 
@@ -200,11 +206,31 @@ class MoELayer:
             offs = (ctypes.c_int64 * len(_lib.WS_NAMES))()
             size = _lib.load_library().cq_moe_workspace(ctypes.byref(d), n, offs)
             buf = torch.empty(max(size, 256), dtype=torch.uint8, device="cuda")
+            o = offs[_lib.WS_NAMES.index("status")]
+            buf[o:o + 16].zero_()  # sticky non-finite flags: cleared here, only ever set by the layer
             self._ws[key] = (buf, list(offs))
         return self._ws[key]
 
-    def forward(self, x, out: torch.Tensor | None = None, path: str | None = None) -> torch.Tensor:
-        """x: (N, d_model) float32/bfloat16 CUDA tensor -> moe_sum (N, d_model) float32."""
+    def check_finite(self, n: int, path: str | None = None) -> None:
+        """Read (one host sync) and clear the non-finite flags the last forwards
+        over n tokens set; raise DivergenceError naming the site like the
+        reference (model.py:307-309, quant.py:93-94)."""
+        buf, offs = self.workspace(n, path)
+        o = offs[_lib.WS_NAMES.index("status")]
+        st = buf[o:o + 16].view(torch.int32)
+        flags = st.tolist()
+        if flags[0] or flags[1]:
+            st.zero_()
+            site = "router/gate/up input" if flags[0] else "down input (silu(gate) * up)"
+            raise DivergenceError(f"non-finite values at MoE site {site!r}")
+
+    def forward(self, x, out: torch.Tensor | None = None, path: str | None = None,
+                check_finite: bool = False) -> torch.Tensor:
+        """x: (N, d_model) float32/bfloat16 CUDA tensor -> moe_sum (N, d_model) float32.
+
+        No host synchronisation unless `check_finite` (then DivergenceError on
+        non-finite input or hidden, like the reference); otherwise the flags
+        stay set for a later `check_finite(n)`."""
         if not isinstance(x, torch.Tensor):
             x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
         x = x.to("cuda").contiguous()
@@ -219,6 +245,8 @@ class MoELayer:
         d = self.desc(path)
         _lib.check(_lib.lib().cq_moe_forward(ctypes.byref(d), x.data_ptr(), _lib.dtype_code(x), n,
                                              out.data_ptr(), buf.data_ptr(), buf.numel(), _lib.stream()))
+        if check_finite:
+            self.check_finite(n, path)
         return out
 
     __call__ = forward
@@ -249,7 +277,8 @@ class MoELayer:
                 "inv": (torch.int32, (n, k)), "codes_perm": (torch.int8, (R, d)),
                 "scales_perm": (torch.float32, (R,)), "hidden": (torch.float32, (R, ff)),
                 "hcodes": (torch.int8, (R, ff)), "hscales": (torch.float32, (R,)),
-                "fout": (torch.float32, (R, d)), "tok_sums": (torch.int32, (n,))}
+                "fout": (torch.float32, (R, d)), "tok_sums": (torch.int32, (n,)),
+                "status": (torch.int32, (4,))}
         res = {}
         for name, (dt, shape) in spec.items():
             o = offs[_lib.WS_NAMES.index(name)]
@@ -259,5 +288,10 @@ class MoELayer:
 
 
 def moe_layer(v, w_router, experts, top_k: int, rotation=None, shared=(), path: str = "auto"):
-    """One-shot functional form: build the layer and run it on v."""
-    return MoELayer(w_router, experts, top_k, rotation=rotation, shared=shared, path=path).forward(v)
+    """One-shot functional form: build the layer (tcgen05 layouts prepared when
+    the shapes allow and the path is "auto" / "tc") and run it on v, raising
+    DivergenceError on non-finite values like the reference's forward."""
+    layer = MoELayer(w_router, experts, top_k, rotation=rotation, shared=shared, path=path)
+    if path in ("auto", "tc") and layer.tc_shapes_ok():
+        layer.prepare_tc()
+    return layer.forward(v, check_finite=True)

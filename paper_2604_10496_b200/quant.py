@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ConfigError, ShapeError
+from .errors import ConfigError, DivergenceError, ShapeError
 
 _ALLOWED_BITS = (2, 3, 4, 8)
 
@@ -65,8 +65,9 @@ def quantize_activations(x, spec: QuantSpec = QuantSpec(4), check_finite: bool =
     """Per-token symmetric quantization with snapped scales (quant.py:89-100).
 
     x: (N, d) float32 or bfloat16 (CUDA tensor or host array, copied to the
-    device).  Raises DivergenceError on non-finite input like the reference;
-    `check_finite=False` skips that check (and its host sync) on the hot path.
+    device).  Raises DivergenceError on non-finite input like the reference
+    (the kernel sets a device flag; reading it is one host sync);
+    `check_finite=False` skips that read on the hot path.
     """
     if spec.bits != 4:
         raise ConfigError(f"device quantizer takes 4-bit codes, got {spec.bits}-bit")
@@ -79,9 +80,12 @@ def quantize_activations(x, spec: QuantSpec = QuantSpec(4), check_finite: bool =
     codes = torch.empty((n, d), dtype=torch.int8, device=x.device)
     scales = torch.empty((n,), dtype=torch.float32, device=x.device)
     if n:
+        flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
         _lib.check(_lib.lib().cq_quantize_a4(x.data_ptr(), _lib.dtype_code(x), n, d,
-                                             codes.data_ptr(), scales.data_ptr(),
-                                             int(bool(check_finite)), _lib.stream()))
+                                             codes.data_ptr(), scales.data_ptr(), _lib.ptr(flag),
+                                             _lib.stream()))
+        if check_finite and int(flag.item()):
+            raise DivergenceError("non-finite activation input to quantizer")
     return QuantizedActivations(codes, scales, spec.bits)
 
 

@@ -42,12 +42,12 @@ def test_struct_layout_matches_header(tmp_path, py, c):
 
 def test_enums_match_header(tmp_path):
     ws = ["CQ_WS_" + n.upper() for n in _lib.WS_NAMES]
-    layouts = ["CQ_TC_MMA16", "CQ_TC_UMMA128", "CQ_TC_UMMA128U", "CQ_TC_UMMA128U8"]
+    layouts = ["CQ_TC_UMMA128U", "CQ_TC_UMMA128U8"]
     paths = ["CQ_PATH_AUTO", "CQ_PATH_F32", "CQ_PATH_TC", "CQ_PATH_ORDERED"]
     got = _c_values(tmp_path, ["CQ_WS_COUNT_"] + ws + layouts + paths + ["CQ_FLAG_KEEP_HIDDEN"])
     assert got[0] == len(_lib.WS_NAMES)
     assert got[1:1 + len(ws)] == list(range(len(ws)))
     i = 1 + len(ws)
-    assert got[i:i + 4] == [_lib.TC_LAYOUTS[k] for k in ("mma16", "umma128", "umma128u", "umma128u8")]
-    assert got[i + 4:i + 8] == [_lib.CQ_PATH_AUTO, _lib.CQ_PATH_F32, _lib.CQ_PATH_TC, _lib.CQ_PATH_ORDERED]
-    assert got[i + 8] == _lib.FLAG_KEEP_HIDDEN
+    assert got[i:i + 2] == [_lib.TC_LAYOUTS[k] for k in ("umma128u", "umma128u8")]
+    assert got[i + 2:i + 6] == [_lib.CQ_PATH_AUTO, _lib.CQ_PATH_F32, _lib.CQ_PATH_TC, _lib.CQ_PATH_ORDERED]
+    assert got[i + 6] == _lib.FLAG_KEEP_HIDDEN

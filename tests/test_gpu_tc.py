@@ -1,8 +1,8 @@
 """Tensor-core path: prepared layout invariants and parity.
 
-The digit-plane LUTs are checked by decoding them on the host exactly the way
-the kernel's PRMT pair does (entry + sign-replicated partner entry), the ids
-permutation by inverting it, and the GEMM against the CPU oracle."""
+The digit-plane LUTs are checked by decoding them on the host (unsigned
+base-128 digits, biased), the ids re-tiling by inverting it, and the GEMM
+against the CPU oracle."""
 
 import numpy as np
 import pytest
@@ -24,66 +24,45 @@ def _rand_pw(rng, d_out, d_in, g, scale=1.0):
     return cent, ids, PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), d_in, g)
 
 
-LAYOUTS = ["umma128", "umma128u", "mma16"]
+LAYOUTS = ["umma128u"]
 
 
-@pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("planes", [2, 3])
-def test_digit_plane_luts_decode_to_centroids(planes, layout):
+def test_digit_plane_luts_decode_to_centroids(planes):
     rng = np.random.default_rng(0)
-    rows, tr = 256, (16 if layout == "mma16" else 128)
+    rows, tr = 256, 128
     cent, ids, pw = _rand_pw(rng, rows, 512, 128, 0.03)
     cent[3] = 0.0  # an all-zero row gets scale 1 and zero digits
     pw = PackedClusteredWeights(torch.from_numpy(cent), torch.from_numpy(ids), 512, 128)
-    pw.prepare_tc(planes, layout)
+    pw.prepare_tc(planes, "umma128u")
     lut = pw.tc["lut"].cpu().numpy().astype(np.int64)          # tile-ordered [tile][G][tr][P][16]
     rs = pw.tc["rowscale"].cpu().numpy().astype(np.float64)
     G = 512 // 128
     lut = lut.reshape(rows // tr, G, tr, planes, 16).transpose(0, 2, 1, 3, 4).reshape(rows, G, planes, 16)
     m = np.zeros(lut.shape[:2] + (16,), np.int64)
-    if layout in ("mma16", "umma128"):
-        # signed base-255 digits, sign garbage pre-compensated: PRMT(P) + PRMT(Q)
-        partner = lut[..., np.arange(16) ^ 8]
-        digits = lut + np.where(partner < 0, -1, 0)
-        assert digits.min() >= -128 and digits.max() <= 126
-        for p in reversed(range(planes)):
-            m = m * 255 + digits[:, :, p, :]
-    else:
-        # unsigned base-128 digits (sign bits clear, so PRMT(P) | PRMT(Q) is exact), biased
-        assert lut.min() >= 0 and lut.max() <= 127
-        for p in reversed(range(planes)):
-            m = m * 128 + lut[:, :, p, :]
-        m -= 1 << (7 * planes - 1)
+    # unsigned base-128 digits (sign bits clear, so PRMT(P) | PRMT(Q) is exact), biased
+    assert lut.min() >= 0 and lut.max() <= 127
+    for p in reversed(range(planes)):
+        m = m * 128 + lut[:, :, p, :]
+    m -= 1 << (7 * planes - 1)
     rec = m * rs[:, None, None]
     err = np.abs(rec - cent.astype(np.float64)).max(axis=(1, 2))
     assert np.all(err <= rs * 0.5 + 1e-30)
     assert rs[3] == 1.0 and not m[3].any()
 
 
-def test_fragment_ids_are_a_permutation_of_packed_ids():
+def test_retired_layouts_are_rejected():
+    from paper_2604_10496_b200 import ConfigError
     rng = np.random.default_rng(1)
-    cent, ids, pw = _rand_pw(rng, 48, 384, 128)
-    pw.prepare_tc(3, "mma16")
-    frag = pw.tc["ids"].cpu().numpy().reshape(-1).view(np.uint32).reshape(48 // 16, 384 // 128, 2, 32, 4)
-    for tile in range(3):
-        for chunk in range(3):
-            for h in range(2):
-                for lane in range(32):
-                    g, t = lane >> 2, lane & 3
-                    for j in range(2):
-                        sub = 2 * h + j
-                        k_lo = chunk * 128 + 32 * sub + 4 * t
-                        w0, w1 = frag[tile, chunk, h, lane, 2 * j], frag[tile, chunk, h, lane, 2 * j + 1]
-                        r0, r1 = ids[tile * 16 + g], ids[tile * 16 + g + 8]
-                        sel = lambda r, k: int(r[k // 2]) | (int(r[k // 2 + 1]) << 8)  # noqa: E731
-                        assert w0 == sel(r0, k_lo) | (sel(r1, k_lo) << 16)
-                        assert w1 == sel(r0, k_lo + 16) | (sel(r1, k_lo + 16) << 16)
+    _, _, pw = _rand_pw(rng, 128, 256, 128)
+    with pytest.raises(ConfigError):
+        pw.prepare_tc(3, "mma16")
 
 
 def test_umma_ids_are_row_blocks_of_packed_ids():
     rng = np.random.default_rng(2)
     cent, ids, pw = _rand_pw(rng, 256, 384, 128)
-    pw.prepare_tc(3, "umma128")
+    pw.prepare_tc(3, "umma128u")
     got = pw.tc["ids"].cpu().numpy().reshape(2, 3, 4, 128, 16)     # [tile][chunk][kstep][row][16 B]
     want = ids.reshape(2, 128, 3, 4, 16).transpose(0, 2, 3, 1, 4)
     assert np.array_equal(got, want)
@@ -183,7 +162,7 @@ def test_prefill_moe_layer_bitwise_equals_decode(monkeypatch):
     assert torch.equal(pre, dec)
 
 
-@pytest.mark.parametrize("layout", ["umma128u", "umma128"])
+@pytest.mark.parametrize("layout", ["umma128u"])
 @pytest.mark.parametrize("n,d_in,d_out,g", [(5, 1024, 512, 128), (300, 2048, 768, 128)])
 def test_a8_codes_tensor_core_vs_reference_gemm(layout, n, d_in, d_out, g):
     """A8 (8-bit activation codes): the tensor-core kernel with

@@ -19,7 +19,7 @@ def err(x):
     return dif.max().item() / ref.abs().max().item(), (torch.linalg.norm(x - ref) / torch.linalg.norm(ref)).item()
 
 print("f32 path", err(f32))
-for pgu, pdn, lay in [(3, 2, "umma128u"), (3, 3, "umma128u"), (2, 2, "umma128u"), (2, 2, "umma128"), (3, 2, "umma128")]:
+for pgu, pdn, lay in [(3, 2, "umma128u"), (3, 3, "umma128u"), (2, 2, "umma128u")]:
     layer.prepare_tc(pgu, pdn, layout=lay)
     out = layer(v, path="tc").clone()
     print(f"tc planes gate/up={pgu} down={pdn} {lay}", err(out))

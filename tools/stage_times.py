@@ -26,7 +26,7 @@ def route():
 def experts():
     _lib.check(L.cq_moe_experts(ctypes.byref(dsc), tr["codes_perm"].data_ptr(), tr["scales_perm"].data_ptr(), tr["offsets"].data_ptr(), n * k, fexp.data_ptr(), buf.data_ptr(), buf.numel(), _lib.stream()))
 def combine():
-    _lib.check(L.cq_moe_combine(tr["selected"].data_ptr(), tr["weights"].data_ptr(), tr["inv"].data_ptr(), tr["fout"].data_ptr(), n, k, d, None, out.data_ptr(), _lib.stream()))
+    _lib.check(L.cq_moe_combine(tr["selected"].data_ptr(), tr["weights"].data_ptr(), tr["inv"].data_ptr(), tr["fout"].data_ptr(), n, k, d, None, 0, out.data_ptr(), _lib.stream()))
 def full():
     layer(v, out=out)
 
