@@ -51,7 +51,7 @@ def _lib():
             fn = getattr(lib, name)
             fn.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, vp, ci]
             fn.restype = ci
-        lib.cqo_matmul_f32.argtypes = [vp, vp, vp, i64, i64, i64]
+        lib.cqo_matmul_f32.argtypes = [vp, vp, vp, i64, i64, i64, ci]
         lib.cqo_quantize_f32.argtypes = [vp, i64, i64, vp, vp]
         _LIB = lib
     return _LIB
@@ -78,11 +78,12 @@ def c_lut_gemm(codes, scales, ids_packed, centroids, g, threads=None, table=True
     return out
 
 
-def c_matmul(a, b):
+def c_matmul(a, b, threads=None):
     a = np.ascontiguousarray(a, np.float32)
     b = np.ascontiguousarray(b, np.float32)
     out = np.empty((a.shape[0], b.shape[1]), np.float32)
-    _lib().cqo_matmul_f32(_p(a), _p(b), _p(out), a.shape[0], a.shape[1], b.shape[1])
+    _lib().cqo_matmul_f32(_p(a), _p(b), _p(out), a.shape[0], a.shape[1], b.shape[1],
+                          int(threads or os.cpu_count() or 1))
     return out
 
 

@@ -105,16 +105,47 @@ int cqo_reference_gemm_f32(const int8_t *codes, const float *scales, const uint8
     return run_gemm(codes, scales, ids, cent, n, d_in, d_out, g, out, threads, 0);
 }
 
-void cqo_matmul_f32(const float *a, const float *b, float *out, int64_t m, int64_t k, int64_t n) {
-    for (int64_t i = 0; i < m; ++i) {
-        float *o = out + i * n;
-        for (int64_t j = 0; j < n; ++j) o[j] = 0.0f;
-        for (int64_t kk = 0; kk < k; ++kk) {
-            const float aik = a[i * k + kk];
-            const float *brow = b + kk * n;
-            for (int64_t j = 0; j < n; ++j) o[j] = o[j] + aik * brow[j];
+typedef struct {
+    const float *a, *b;
+    float *out;
+    int64_t k, n, row0, row1;
+} mm_job;
+
+static void *mm_worker(void *arg) {
+    mm_job *jb = (mm_job *)arg;
+    for (int64_t i = jb->row0; i < jb->row1; ++i) {
+        float *o = jb->out + i * jb->n;
+        for (int64_t j = 0; j < jb->n; ++j) o[j] = 0.0f;
+        for (int64_t kk = 0; kk < jb->k; ++kk) {
+            const float aik = jb->a[i * jb->k + kk];
+            const float *brow = jb->b + kk * jb->n;
+            for (int64_t j = 0; j < jb->n; ++j) o[j] = o[j] + aik * brow[j];
         }
     }
+    return NULL;
+}
+
+/* _core.pyx:27-38: i-k-j, every out[i][j] an ordered chain over k (the j loop
+ * vectorizes across independent outputs; -ffp-contract=off keeps mul and add
+ * separate).  Rows split over `threads` POSIX threads (one writer per row). */
+void cqo_matmul_f32(const float *a, const float *b, float *out, int64_t m, int64_t k, int64_t n, int threads) {
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    if (threads > m) threads = (int)(m > 0 ? m : 1);
+    mm_job jobs[256];
+    pthread_t tids[256];
+    const int64_t per = (m + threads - 1) / threads;
+    int launched = 0;
+    for (int w = 0; w < threads; ++w) {
+        int64_t r0 = w * per, r1 = r0 + per;
+        if (r1 > m) r1 = m;
+        if (r0 >= r1) break;
+        jobs[w] = (mm_job){a, b, out, k, n, r0, r1};
+        if (threads == 1) { mm_worker(&jobs[w]); continue; }
+        pthread_create(&tids[w], NULL, mm_worker, &jobs[w]);
+        ++launched;
+    }
+    for (int w = 0; w < launched; ++w) pthread_join(tids[w], NULL);
 }
 
 /* quant.py:89-100 for float32 rows: scale = snap(max|x| / 7), 1 for a zero

@@ -200,7 +200,7 @@ class MoELayer:
         return d
 
     def workspace(self, n: int, path: str | None = None):
-        key = (n, path or self.path)
+        key = (n, path or self.path, self.exact_rotation)
         if key not in self._ws:
             d = self.desc(path)
             offs = (ctypes.c_int64 * len(_lib.WS_NAMES))()

@@ -16,6 +16,12 @@ reference's own functions on the path:
                the hand-summed token (tests/test_lutgemm.py:112-120) and 8-bit codes.
   routing.npz  linalg.matmul fp32 (linalg.py:66-75) and select_top_k
                (model.py:324-330) incl. exact ties (tests/test_model.py:301-305).
+  acceptance8.npz  the 216 instances of acceptance criterion #8
+               (tests/test_acceptance.py:358-387): the instance parameters and a
+               SHA-256 of the reference's reference_gemm output bytes (and of its
+               codes / scales), so the GPU test can regenerate the inputs with the
+               same numpy draws and check the backend bytewise without shipping
+               the arrays.
   moe_*.npz    the MoE block composed from reference functions:
                quantize_activations -> matmul(router) -> select_top_k ->
                per expert ascending lut_gemm(gate/up) -> silu*up ->
@@ -244,6 +250,46 @@ def make_moe(name, seed, n, d, ff, n_exp, top_k, g):
          codes=qa.codes, scales=qa.scales)
 
 
+def acceptance8_instances():
+    """Yields the exact inputs of tests/test_acceptance.py:358-387 (same rng
+    draws, same order) plus the instance parameters."""
+    from itertools import product
+    combos = [(n, d, g) for n, d in product((1, 7, 64, 256), (16, 64, 256)) for g in sorted({16, 64, d}) if g <= d]
+    instances = 0
+    for seed in range(9):
+        for n_tokens, d_in, g in combos:
+            rng = np.random.default_rng(1_000_003 * seed + 1009 * n_tokens + 13 * d_in + g)
+            d_out = 16 if instances % 2 else 8
+            k = 16 if instances % 3 else 5
+            x = rng.standard_normal((n_tokens, d_in))
+            if instances % 3 == 0:
+                x[: max(1, n_tokens // 4)] = 0.0  # all-zero rows
+            centroids = rng.standard_normal((d_out, d_in // g, k)).astype(np.float32)
+            ids = rng.integers(0, k, (d_out, d_in), dtype=np.uint8)
+            yield (seed, n_tokens, d_in, g, d_out, k), x, centroids, ids
+            instances += 1
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def make_acceptance8():
+    params, out_sha, codes_sha, scales_sha = [], [], [], []
+    for p, x, centroids, ids in acceptance8_instances():
+        seed, n_tokens, d_in, g, d_out, k = p
+        qa = quantize_activations(x, QuantSpec(4))
+        pw = pack_weights(centroids, ids, None if g == d_in else g)
+        want = reference_gemm(qa, pw)
+        assert lut_gemm(qa, pw).tobytes() == want.tobytes()
+        params.append(p)
+        out_sha.append(sha(want))
+        codes_sha.append(sha(qa.codes))
+        scales_sha.append(sha(qa.scales.astype(np.float32)))
+    save("acceptance8.npz", params=np.array(params, np.int64), out_sha=np.array(out_sha),
+         codes_sha=np.array(codes_sha), scales_sha=np.array(scales_sha))
+
+
 def make_rng():
     r = RngState(1234)
     save("rng.npz", normal=r.stream("t", 3).standard_normal(8),
@@ -251,6 +297,10 @@ def make_rng():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["acceptance8"]:  # just the new fixture (the others are byte-stable in git)
+        make_acceptance8()
+        sys.exit(0)
+    make_acceptance8()
     make_rng()
     make_quant()
     make_lutgemm()

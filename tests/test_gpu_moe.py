@@ -339,3 +339,41 @@ def test_tensor_core_rotation_fp32_accuracy(dtype):
     f32(x)
     agree = (f32.trace(n)["selected"] == layer.trace(n)["selected"]).all(dim=1).float().mean().item()
     assert agree >= 0.98, agree
+
+
+@pytest.mark.parametrize("path", ["tc", "f32", "ordered"])
+def test_nonfinite_input_raises_divergence_error(path):
+    """A non-finite layer input sets the sticky device flag (no host sync in the
+    forward); check_finite reads it and raises DivergenceError naming the site,
+    like quant.py:93-94 / model.py:307-309, then clears it."""
+    from paper_2604_10496_b200 import DivergenceError
+    n, d, ff, E, k, g = 20, 256, 256, 4, 2, 128
+    v, w, sites, _ = moe_inputs_device(61, n, d, ff, E, g)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=path)
+    if path == "tc":
+        layer.prepare_tc()
+    layer(v, check_finite=True)  # finite: no error
+    bad = v.clone()
+    bad[3, 7] = float("nan")
+    layer(bad)                    # no sync, no raise
+    with pytest.raises(DivergenceError, match="router/gate/up"):
+        layer.check_finite(n)
+    layer.check_finite(n)         # cleared
+    bad[3, 7] = float("inf")
+    with pytest.raises(DivergenceError):
+        layer(bad, check_finite=True)
+
+
+@pytest.mark.parametrize("path", ["f32", "ordered"])
+def test_nonfinite_hidden_raises_at_down_site(path):
+    """An inf centroid makes a gate output non-finite: the down-input
+    re-quantization flags it (model.py:397-399 site)."""
+    from paper_2604_10496_b200 import DivergenceError
+    n, d, ff, E, k, g = 16, 256, 256, 4, 4, 128
+    v, w, sites, _ = moe_inputs_device(62, n, d, ff, E, g)
+    sites["gate"][1][2, 5, 0, :] = float("inf")  # expert 2, row 5, group 0: every centroid
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=path)
+    with pytest.raises(DivergenceError, match="down input"):
+        layer(v, check_finite=True)
