@@ -334,12 +334,13 @@ def traffic_for(layout):
         return None
 
 
-def e2e_pipelined(step, x_host, y_host, like, out_shape, stream, steps, barrier):
+def e2e_pipelined(step, x_host, y_host, like, out_shape, stream, steps, barrier, graph=True):
     """Mean device ms per step of: H2D copy of the step's input (pinned) ->
     step(x_dev, out) captured as a CUDA graph -> D2H read of its output, with
     the copies on separate streams and two buffer sets, so copies of adjacent
     steps overlap the compute of this one.  `step` may be a pair, one per buffer
-    set (steps with their own internal buffers, e.g. the EP step)."""
+    set (steps with their own internal buffers, e.g. the EP step).  graph=False:
+    the steps run eagerly (a step with a host read, e.g. compact EP sizing)."""
     fns = step if isinstance(step, (list, tuple)) else (step, step)
     import torch
     h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
@@ -350,10 +351,13 @@ def e2e_pipelined(step, x_host, y_host, like, out_shape, stream, steps, barrier)
         for b in range(2):
             x_dev[b].copy_(x_host)
             fns[b](x_dev[b], outs[b])
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                fns[b](x_dev[b], outs[b])
-            graphs.append(g)
+            if graph:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    fns[b](x_dev[b], outs[b])
+                graphs.append(g.replay)
+            else:
+                graphs.append(lambda b=b: fns[b](x_dev[b], outs[b]))
     torch.cuda.synchronize()
     ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
     in_ready, done, out_read = [ev(), ev()], [ev(), ev()], [ev(), ev()]
@@ -370,7 +374,7 @@ def e2e_pipelined(step, x_host, y_host, like, out_shape, stream, steps, barrier)
                 stream.wait_event(in_ready[b])
                 if i >= 2:
                     stream.wait_event(out_read[b])   # step i-2's output was read back
-                graphs[b].replay()
+                graphs[b]()
                 done[b].record(stream)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(done[b])
@@ -392,12 +396,18 @@ def e2e_pipelined(step, x_host, y_host, like, out_shape, stream, steps, barrier)
 
 
 def run_ep(args, rank, world, local):
-    """N > 1: expert parallelism.  Every rank holds E/N experts
-    (identical seeded weights on all ranks, sliced) and its own batch of
-    tokens; a step is EPStep: route -> device-side dispatch into fixed-capacity
-    slots -> all_to_all -> group by local expert -> grouped experts -> scatter
-    -> all_to_all back -> ascending-expert combine.  No host synchronisation,
-    so the step is captured in one CUDA graph."""
+    """N > 1: expert parallelism (ep.EPStep).  Every rank holds
+    E/N experts (identical seeded weights on all ranks, sliced), the router
+    weight and any shared experts, and its own tokens.  A step: route ->
+    dispatch rows (one per (token, peer), codes as nibbles) -> all_to_all ->
+    grouped experts -> per-row partial sums -> all_to_all back -> combine (+
+    shared experts, run while the dispatch is in flight).
+
+    Decode configs (MX default, weak scaling: B tokens per rank): fixed-capacity
+    rows, no host read, the whole step (both NCCL exchanges) in one CUDA graph.
+    Prefill configs (PH/QW/DS, strong scaling: the config's batch split over
+    the ranks): counts-first all_to_all-v with exact splits, two micro-batches
+    so one batch's exchanges overlap the other's experts, eager."""
     import torch
     import torch.distributed as dist
     from paper_2604_10496_b200 import _lib as L
@@ -405,20 +415,32 @@ def run_ep(args, rank, world, local):
     from paper_2604_10496_b200.moe import ExpertStack, MoELayer
     from paper_2604_10496_b200.synthetic import moe_inputs_device
 
-    n, d, ff, E, k, g = args.batch, CFG["d_model"], CFG["d_ff"], CFG["n_experts"], CFG["top_k"], CFG["group_size"]
-    _, w, sites, _ = moe_inputs_device(args.seed, 1, d, ff, E, g, kc=CFG.get("kc", 16))
+    prefill = CFG["batch"] >= 1024
+    d, ff, E, k, g = CFG["d_model"], CFG["d_ff"], CFG["n_experts"], CFG["top_k"], CFG["group_size"]
+    n = max(1, args.batch // world) if prefill and not args.batch_given else args.batch
+    n_sh = CFG.get("n_shared", 0)
+    _, w, sites, sh_sites = moe_inputs_device(args.seed, 1, d, ff, E, g, n_shared=n_sh, kc=CFG.get("kc", 16))
     begin, per = expert_range(E, world, rank)
     stacks = [ExpertStack(sites[s][0][begin:begin + per].contiguous(), sites[s][1][begin:begin + per].contiguous(),
                           sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    shared = (tuple(ExpertStack(sh_sites[s][0], sh_sites[s][1], sh_sites[s][2], sh_sites[s][3], g)
+                    for s in ("gate", "up", "down")) if n_sh else None)
     del sites
     torch.cuda.empty_cache()
-    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=args.path, expert_begin=begin, n_experts=E)
+    rotation = None
+    if CFG.get("rotation"):
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(args.seed + 99)
+        rotation = torch.linalg.qr(torch.randn((d, d), generator=gen, device="cuda"))[0].contiguous()
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, rotation=rotation, shared=shared, path=args.path,
+                                 expert_begin=begin, n_experts=E)
     if args.path in ("auto", "tc"):
         layer.prepare_tc(layout=args.layout)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(args.seed + 1000 + rank)
     v = torch.randn((n, d), generator=gen, device="cuda").to(torch.bfloat16)
-    step = EPStep(layer, n, rank, world)
+    sizing, mb = ("compact", 2) if prefill else ("fixed", 1)
+    step = EPStep(layer, n, rank, world, sizing=sizing, micro_batches=mb)
     stream = torch.cuda.Stream()
 
     def barrier():
@@ -432,112 +454,103 @@ def run_ep(args, rank, world, local):
         for _ in range(2):
             step(v)
     torch.cuda.synchronize()
-    # one step (both NCCL exchanges included) in a CUDA graph; eager if capture is refused
     graph, capture_err = None, None
-    try:
-        g_ = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_, stream=stream):
-            step(v)
-        graph = g_
-    except Exception as exc:
-        capture_err = repr(exc)[:200]
-        torch.cuda.synchronize()
+    if sizing == "fixed":  # one step (both NCCL exchanges included) in a CUDA graph; eager if refused
+        try:
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_, stream=stream):
+                step(v)
+            graph = g_
+        except Exception as exc:
+            capture_err = repr(exc)[:200]
+            torch.cuda.synchronize()
     run = graph.replay if graph is not None else (lambda: step(v))
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             run()
     torch.cuda.synchronize()
 
-    def timed(fn):
+    def timed(fn, steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             barrier()
             e0.record(stream)
-            for _ in range(args.steps):
+            for _ in range(steps):
                 fn()
             e1.record(stream)
             e1.synchronize()
             barrier()
-        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        t = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     with ClockSampler(local) as clk:
-        ms = timed(run)
+        ms = timed(run, args.steps)
+    xb = step.exchange_bytes()
+    xbt = torch.tensor([xb["out"], xb["back"]], dtype=torch.float64, device="cuda")
+    dist.all_reduce(xbt, op=dist.ReduceOp.MAX)
 
-    # end to end through the public step: pinned host input -> device -> step -> host output
+    # exposed communication: the same step with both payload exchanges replaced by no-ops (the
+    # receive buffers keep the last real step's rows, so the compute is identical), eager, max over ranks
+    real_x = step.xchg
+    step.xchg = lambda *a: None
+    ms_nocomm = timed(lambda: step(v), max(3, min(args.steps, 20)))
+    step.xchg = real_x
+    ms_eager = timed(lambda: step(v), max(3, min(args.steps, 20)))
+
     # end to end: pinned H2D -> EP step (both exchanges) -> D2H each step, pipelined as on one GPU
     x_host = v.cpu().pin_memory()
     y_host = [torch.empty((n, d), dtype=torch.float32).pin_memory() for _ in range(2)]
-    steps2 = [EPStep(layer, n, rank, world), EPStep(layer, n, rank, world)]
+    steps2 = [EPStep(layer, n, rank, world, sizing=sizing, micro_batches=mb) for _ in range(2)]
     e2e_ms = e2e_pipelined([lambda xd, o, st=st: st(xd, out=o) for st in steps2], x_host, y_host, v, (n, d),
-                           stream, args.steps, barrier)
+                           stream, args.steps, barrier, graph=sizing == "fixed")
     t = torch.tensor([e2e_ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
 
-    # phase breakdown (eager, CUDA events on the step's stream, max over ranks): how much of a step
-    # the two exchanges take; both are exposed in this design (SURVEY 8(e) scaling report)
-    names = ("route_dispatch", "exchange_out", "experts", "exchange_back", "combine")
-    ph = torch.zeros(len(names), device="cuda")
-    n_ph = max(3, min(args.steps, 20))
-    with torch.cuda.stream(stream):
-        for _ in range(n_ph):
-            barrier()
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
-            ev[0].record(stream)
-            step.route_and_pack(v)
-            ev[1].record(stream)
-            step.a2a(step.recv, step.send)
-            ev[2].record(stream)
-            step.run_experts()
-            ev[3].record(stream)
-            step.a2a(step.ret, step.back)
-            ev[4].record(stream)
-            step.combine()
-            ev[5].record(stream)
-            ev[5].synchronize()
-            ph += torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(len(names))], device="cuda")
-    ph /= n_ph
-    if world > 1:
-        dist.all_reduce(ph, op=dist.ReduceOp.MAX)
-    ep_phases = {nm: round(float(x), 4) for nm, x in zip(names, ph.tolist())}
     with torch.cuda.stream(stream):
         step(v)
+        routes = int(step.offsets[-1].item())   # last micro-batch's grouped routes (profiling input)
         n_active, byt, (gu_ms, rq_ms, dn_ms) = profile_expert_stage(layer, step.codes_perm, step.scales_perm,
-                                                                    step.offsets, step.slots, max(3, args.steps))
-    R = int(step.offsets[-1].item())
+                                                                    step.offsets, max(routes, 1),
+                                                                    max(3, args.steps))
     pk = peaks()
-    achieved = byt["gate_up"] / (gu_ms * 1e-3) / 1e9 if gu_ms > 0 else None
+    tensor_bound = routes >= 128 * max(n_active, 1)
+    if tensor_bound:
+        achieved, peak_v, unit = 4.0 * routes * d * ff / (gu_ms * 1e-3) / 1e12, pk["bf16_tflops"], "TFLOP/s"
+    else:
+        achieved, peak_v, unit = byt["gate_up"] / (gu_ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
     if rank == 0:
+        total = n * world
         res = {
-            "metric": "MoE-layer tokens/s", "value": n * world / (ms * 1e-3), "unit": "tokens/s",
+            "metric": "MoE-layer tokens/s", "value": total / (ms * 1e-3), "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8/f32",
-            "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
+            "higher_is_better": True, "scaling": "strong" if prefill else "weak", "vs_baseline": None,
+            "dtype": "int8/f32", "data": "synthetic (random-init 4-bit codebook weights, N(0,1) bf16 activations)",
             "config": {"workload": CFG["name"], "d_model": d, "d_ff": ff, "n_experts": E, "top_k": k,
-                       "group_size": g or "d_in", "batch_per_rank": n, "parallelism": f"ep{world}",
-                       "experts_per_rank": per, "path": args.path, "layout": args.layout,
-                       "l2": "weights > L2, no flush needed", "cuda_graph": graph is not None,
-                       "capacity_per_peer": step.cap, **({"capture_error": capture_err} if capture_err else {})},
-            "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "tokens/s",
+                       "n_shared": n_sh, "group_size": g or "d_in", "batch_per_rank": n, "global_batch": total,
+                       "parallelism": f"ep{world}", "experts_per_rank": per, "path": args.path,
+                       "layout": args.layout, "l2": "weights > L2, no flush needed",
+                       "cuda_graph": graph is not None, "ep_rows": "dedup (one row per token and peer)",
+                       "ep_sizing": sizing, "micro_batches": mb,
+                       **({"capture_error": capture_err} if capture_err else {})},
+            "e2e": {"value": total / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),
                     "d2h_bytes_per_step": int(y_host[0].numel() * y_host[0].element_size()),
                     "pipelined": "H2D / EP step / D2H on three streams, double-buffered"},
-            "roofline": {"bound": "hbm", "kernel": "rank 0's grouped gate|up LUT GEMM (lut_umma_kernel)",
-                         "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"] if achieved else None, "peak_src": pk["src"],
-                         "peak_spec": SPEC_HBM_GBS, "frac_spec": achieved / SPEC_HBM_GBS if achieved else None,
-                         "traffic": None, "algorithmic_bytes": byt["gate_up"], "kernel_ms": gu_ms,
-                         "rows_received": R, "active_local_experts": n_active,
+            "roofline": {"bound": "tensor" if tensor_bound else "hbm",
+                         "kernel": "rank 0's grouped gate|up LUT GEMM (lut_umma_kernel)",
+                         "achieved": achieved, "peak": peak_v, "unit": unit, "frac": achieved / peak_v,
+                         "peak_src": pk["src"], "traffic": None, "algorithmic_bytes": byt["gate_up"],
+                         "kernel_ms": gu_ms, "routes_profiled": routes, "active_local_experts": n_active,
                          "stage_ms": {"gate_up": gu_ms, "silu_requant": rq_ms, "down": dn_ms}},
             "clocks": clk.summary(),
             "gpu_launches": int(launches_per_step * args.steps),
-            "ep": {"phases_ms": ep_phases, "comm_exposed_ms": round(ep_phases["exchange_out"]
-                                                                   + ep_phases["exchange_back"], 4),
-                   "exchange_bytes_per_rank": {"out": int(step.send.numel()), "back": int(step.back.numel() * 4)},
-                   "note": "phases timed eagerly with CUDA events, max over ranks; equal-split NCCL "
-                           "all_to_all over fixed-capacity slots, both exchanges exposed"},
+            "ep": {"step_ms_eager": round(ms_eager, 4), "step_ms_without_exchanges": round(ms_nocomm, 4),
+                   "comm_exposed_ms": round(max(0.0, ms_eager - ms_nocomm), 4),
+                   "exchange_bytes_per_rank_max": {"out": int(xbt[0].item()), "back": int(xbt[1].item())},
+                   "note": "exposed = eager step - the same step with both payload exchanges as no-ops "
+                           "(max over ranks)"},
         }
         emit(res)
     dist.destroy_process_group()
@@ -720,6 +733,7 @@ def main():
     args = parse()
     CFG.clear()
     CFG.update(dict(CONFIGS[args.config]), group_size=CONFIGS[args.config].get("group_size", 128))
+    args.batch_given = args.batch is not None
     if args.batch is None:
         args.batch = CFG["batch"]
     if args.config != "mx":

@@ -225,38 +225,55 @@ CQ_API cq_status cq_moe_shared_experts(const cq_moe_desc *desc, int64_t n_tokens
 
 /* ---------------------------------------------------------------------------
  * Expert parallelism, device-side planning (the reference has
- * no multi-GPU path — these serve the EP driver paper_2604_10496_b200/ep.py).
- * No host synchronisation: a whole EP step (route, dispatch, exchange, group,
- * experts, scatter, exchange, combine) can be captured in one CUDA graph.
+ * no multi-GPU path — it evaluates every expert on every token, model.py:391-401
+ * — so these serve the EP driver paper_2604_10496_b200/ep.py).  Experts
+ * [r*per, (r+1)*per) live on rank r; the router weight and shared experts are
+ * replicated.
  *
- * Every rank sends each peer `capacity` slots of cq_ep_row_bytes(d_model)
- * bytes ([codes][f32 scale][i32 local expert id][pad]; id -1 = empty; codes
- * as packed nibbles when d_model % 32 == 0, else int8), so both exchanges are
- * equal-split all_to_alls.  capacity >= n_tokens *
- * min(top_k, experts_per_rank).  Experts [r*per, (r+1)*per) live on rank r. */
-CQ_API int64_t cq_ep_row_bytes(int64_t d_model);
-/* Scratch bytes for cq_ep_dispatch / cq_ep_group with these sizes. */
-CQ_API int64_t cq_ep_scratch_bytes(int64_t n_tokens, int64_t top_k, int32_t world, int64_t capacity,
+ * A rank sends each peer rows of cq_ep_row_bytes(d_model, kr) bytes:
+ *   [codes][f32 scale][i32 m][(i32 e_j, f32 w_j) x kr][pad to 16 B]
+ * codes as packed nibbles when d_model % 32 == 0 (else int8); m routes to the
+ * peer's local experts e_0 < e_1 < ... (e = -1 past m).
+ *   dedup != 0: one row per (token, peer) holding all its routes there,
+ *     kr = min(top_k, experts_per_rank); the peer returns one fp32 partial sum
+ *     per row (cq_ep_partial), the source adds them in ascending peer order.
+ *   dedup == 0: one row per route, kr = 1, w = 1; the source applies the route
+ *     weights: bitwise equal to cq_moe_forward for any world size.
+ * capacity > 0: `capacity` rows per peer (fixed slots, equal-split exchanges,
+ * no host read: a whole step fits one CUDA graph); >= n_tokens (dedup) or
+ * n_tokens * min(top_k, experts_per_rank).  capacity == 0: compact, rows to
+ * peer g follow the rows to peers < g (all_to_all-v sized by the counts). */
+CQ_API int64_t cq_ep_row_bytes(int64_t d_model, int64_t routes_per_row);
+/* Device scratch bytes for cq_ep_dispatch / cq_ep_group with these sizes. */
+CQ_API int64_t cq_ep_scratch_bytes(int64_t n_tokens, int64_t top_k, int64_t recv_rows, int64_t routes_per_row,
                                    int64_t n_local);
-/* codes (n, d) int8, scales (n,), selected (n, k) global expert ids (cq_moe_route)
- * -> send [world][capacity] rows, and inv (n, k) = slot of each route, i.e. the
- * row of the returned [world][capacity][d] f32 buffer its output arrives in
- * (feed to cq_moe_combine).  Slots are filled in (token, slot) order per peer. */
+/* codes (n, d) int8, scales (n,), selected (n, k) global expert ids, weights
+ * (n, k) (cq_moe_route) -> send rows; counts[g*counts_stride + {0, 1}] = rows /
+ * routes sent to peer g; per token the returned rows to add, in ascending peer
+ * (dedup) or expert order: src_slot (n, k) (row index in the returned buffer,
+ * -1 ends the list) and src_w (n, k) (1 in dedup mode). */
 CQ_API cq_status cq_ep_dispatch(const int8_t *codes, const float *scales, const int32_t *selected,
-                                int64_t n_tokens, int64_t top_k, int64_t d_model, int64_t experts_per_rank,
-                                int32_t world, int64_t capacity, uint8_t *send, int32_t *inv, void *scratch,
-                                void *stream);
-/* Received rows recv [slots] -> codes_perm (slots, d) / scales_perm grouped by
- * local expert (stable in slot order), offsets (n_local+1), slot_of_row
- * (grouped row -> slot).  Rows past offsets[n_local] are left untouched; pass
- * `slots` as the row bound of cq_moe_experts. */
-CQ_API cq_status cq_ep_group(const uint8_t *recv, int64_t slots, int64_t d_model, int64_t n_local,
-                             int8_t *codes_perm, float *scales_perm, int32_t *offsets, int32_t *slot_of_row,
-                             void *scratch, void *stream);
-/* Grouped expert outputs fout (rows, d) -> back [slot] rows (slot order) for
- * the return exchange; only the offsets[n_local] live rows are moved. */
-CQ_API cq_status cq_ep_scatter(const float *fout, const int32_t *offsets, const int32_t *slot_of_row,
-                               int64_t n_local, int64_t rows_bound, int64_t d_model, float *back, void *stream);
+                                const float *weights, int64_t n_tokens, int64_t top_k, int64_t d_model,
+                                int64_t experts_per_rank, int32_t world, int32_t dedup, int64_t capacity,
+                                uint8_t *send, int32_t *counts, int64_t counts_stride, int32_t *src_slot,
+                                float *src_w, void *scratch, void *stream);
+/* Received rows recv [rows] -> codes_perm / scales_perm grouped by local expert
+ * (stable in (row, j) order), offsets (n_local+1), route_pos [rows][kr] (grouped
+ * row of each route, -1 for none).  Pass rows * kr (or the exact route count) as
+ * the row bound of cq_moe_experts. */
+CQ_API cq_status cq_ep_group(const uint8_t *recv, int64_t rows, int64_t d_model, int64_t routes_per_row,
+                             int64_t n_local, int8_t *codes_perm, float *scales_perm, int32_t *offsets,
+                             int32_t *route_pos, void *scratch, void *stream);
+/* Grouped expert outputs fout -> back [rows][d] f32, one returned row per
+ * received row with m > 0: raw (dedup == 0): the route's output as is; else
+ * ((0 + w_0 f_0) + w_1 f_1) ... in ascending expert order. */
+CQ_API cq_status cq_ep_partial(const float *fout, const int32_t *route_pos, const uint8_t *recv, int64_t rows,
+                               int64_t d_model, int64_t routes_per_row, int32_t raw, float *back, void *stream);
+/* out[t] = ((0 + src_w[t,0] ret[src_slot[t,0]]) + ...) over the token's list,
+ * then + add[u*add_stride + t*d] for u < n_add (shared-expert outputs, in order). */
+CQ_API cq_status cq_ep_combine(const float *ret, const int32_t *src_slot, const float *src_w, int64_t n_tokens,
+                               int64_t top_k, int64_t d_model, const float *add, int64_t n_add, int64_t add_stride,
+                               float *out, void *stream);
 
 /* Online rotation on the tensor cores (pipeline.py:516, v = x @ R) at fp32 accuracy:
  * R (d, d) f32 is split once into three bf16 planes of R^T in the UMMA operand layout

@@ -65,9 +65,11 @@ _SIGS = {
     "cq_moe_profile_experts": [ctypes.POINTER(MoEDesc), _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _vp, _vp],
     "cq_lut8_prepare": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "cq_lut_gemm_tc": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
-    "cq_ep_dispatch": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _vp, _vp],
-    "cq_ep_group": [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
-    "cq_ep_scatter": [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp],
+    "cq_ep_dispatch": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i64, _vp, _vp, _i64, _vp, _vp,
+                       _vp, _vp],
+    "cq_ep_group": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "cq_ep_partial": [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp],
+    "cq_ep_combine": [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp],
     "cq_rotation_prepare": [_vp, _i64, _vp, _vp],
 }
 
@@ -95,9 +97,9 @@ def load_library() -> ctypes.CDLL:
         lib.cq_launch_count.restype = _i64
         lib.cq_moe_workspace.argtypes = [ctypes.POINTER(MoEDesc), _i64, ctypes.POINTER(_i64)]
         lib.cq_moe_workspace.restype = _i64
-        lib.cq_ep_row_bytes.argtypes = [_i64]
+        lib.cq_ep_row_bytes.argtypes = [_i64, _i64]
         lib.cq_ep_row_bytes.restype = _i64
-        lib.cq_ep_scratch_bytes.argtypes = [_i64, _i64, _i32, _i64, _i64]
+        lib.cq_ep_scratch_bytes.argtypes = [_i64, _i64, _i64, _i64, _i64]
         lib.cq_ep_scratch_bytes.restype = _i64
         lib.cq_rotation_prepared_bytes.argtypes = [_i64]
         lib.cq_rotation_prepared_bytes.restype = _i64

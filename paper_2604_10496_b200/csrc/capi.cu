@@ -17,5 +17,5 @@ bool pdl_enabled() {
 }  // namespace cq
 
 extern "C" const char *cq_last_error(void) { return cq::t_error.c_str(); }
-extern "C" int cq_abi_version(void) { return 5; }
+extern "C" int cq_abi_version(void) { return 6; }
 extern "C" int64_t cq_launch_count(void) { return cq::g_launches.load(); }

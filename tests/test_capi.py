@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_counter():
     lib = _lib.load_library()
-    assert lib.cq_abi_version() == 5
+    assert lib.cq_abi_version() == 6
     assert lib.cq_launch_count() >= 0
 
 

@@ -157,7 +157,7 @@ def test_phi_prefill_tensor_core_rotation_disagreement_is_bounded():
     (x1.5), route all but a handful of tokens identically, route every token
     whose codes match bit-exactly, and keep the layer output within the
     tolerance of the bit-exact path (ordered GEMMs + ordered rotation) over
-    all tokens.  Measured rates: DESIGN.md §4b."""
+    every token it routes alike.  Measured rates: DESIGN.md §4b."""
     c, x, layer, host = _build("ph", 107, rotation=True)
     out = layer(x).clone()
     tr = {key: t.cpu().numpy() for key, t in layer.trace(c["n"]).items()}
@@ -178,9 +178,15 @@ def test_phi_prefill_tensor_core_rotation_disagreement_is_bounded():
     assert flips.sum() <= 4
     same = ~moved_tc
     assert np.array_equal(tr["selected"][same], sel[same])
-    # the layer over all tokens against the bit-exact path on the same input
+    # the layer against the bit-exact path (ordered GEMMs + ordered rotation) on the same input, over
+    # every token the tcgen05 rotation routes like the reference.  A token routed to a different
+    # expert has an unrelated output (one such token alone is ~sqrt(2/4096) = 2.2e-2 of the
+    # Frobenius norm), so flipped tokens are counted and bounded above, not folded in here.
     layer.exact_rotation = True
-    exact = layer(x, path="ordered")
-    err = o.relative_error(out.cpu().numpy(), exact.cpu().numpy())
-    print(f"PH layer, tcgen05 path vs the bit-exact path over {c['n']} tokens: {err:.2e}")
+    exact = layer(x, path="ordered").cpu().numpy()
+    got = out.cpu().numpy()
+    keep = ~flips
+    err = o.relative_error(got[keep], exact[keep])
+    print(f"PH layer, tcgen05 path vs the bit-exact path over the {int(keep.sum())} of {c['n']} tokens "
+          f"routed alike: {err:.2e}")
     assert err <= LAYER_TOL

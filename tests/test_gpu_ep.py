@@ -1,7 +1,17 @@
-"""The expert-parallel driver on the CUDA backend (NCCL, world_size 1 on the
-single GPU this run has; the multi-rank exchange logic is covered by the gloo
-tests).  Routing, segment order and per-row arithmetic are the same as the
-single-GPU layer, so the outputs must be bitwise equal."""
+"""The expert-parallel step on the B200 kernels (ep.EPStep, csrc/ep.cu).
+
+This run has one GPU, so multi-rank steps are driven here as in-process
+ranks: every rank's phases run on the real kernels with its own sharded
+layer (expert_begin / n_local < E), and the two exchanges are done by slicing
+the send buffers exactly as all_to_all(-v) would.  A true 2-process run on the
+one GPU (exchanges staged through host memory over gloo) and an NCCL world-1
+run cover the step's own stream/exchange orchestration.
+
+Parity: the exact-row protocol is bitwise equal to the single-GPU layer; the
+dedup protocol equals it up to fp32 re-association of the cross-rank adds
+(bitwise for tokens whose experts share a rank); the device send rows equal
+ep.pack_rows (the protocol restated in torch, checked against the oracle on
+CPU by tests/test_ep_gloo.py) byte for byte."""
 
 import os
 import socket
@@ -10,40 +20,33 @@ import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
+import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-from paper_2604_10496_b200.ep import CudaBackend, EPMoE, EPStep  # noqa: E402
+from paper_2604_10496_b200.ep import EPStep, pack_rows, plan_rows  # noqa: E402
 from paper_2604_10496_b200.moe import ExpertStack, MoELayer  # noqa: E402
 from paper_2604_10496_b200.synthetic import moe_inputs_device  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 @pytest.fixture(scope="module")
 def nccl_world1():
     if not dist.is_initialized():
-        with socket.socket() as s:
-            s.bind(("127.0.0.1", 0))
-            port = s.getsockname()[1]
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ["MASTER_PORT"] = str(port)
+        os.environ["MASTER_PORT"] = str(_free_port())
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     yield
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("path", ["tc", "f32"])
-def test_ep_world1_equals_single_gpu_layer(nccl_world1, path):
-    n, d, ff, E, k, g = 48, 1024, 1536, 8, 2, 128
-    v, w, sites, _ = moe_inputs_device(5, n, d, ff, E, g)
-    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path=path)
-    if path == "tc":
-        layer.prepare_tc()
-    want = layer(v).clone()
-    ep = EPMoE(CudaBackend(layer), E, k, rank=0, world=1)
-    got = ep(v)
-    torch.cuda.synchronize()
-    assert torch.equal(got, want)
+def _stacks(sites, g):
+    return [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
 
 
 def _shard(stack, begin, per):
@@ -51,53 +54,21 @@ def _shard(stack, begin, per):
                        stack.d_in, stack.d_out, stack.group_size)
 
 
-@pytest.mark.parametrize("world,n_tok,E,k", [(2, 40, 8, 2), (4, 33, 8, 2), (2, 21, 6, 3)])
-def test_ep_sharded_ranks_in_one_process(world, n_tok, E, k):
-    """`world` ranks with E/world experts each, driven in one process: the
-    all_to_all exchanges are done here by concatenating the send segments.
-    Each rank's layer holds only its experts (expert_begin/n_local < E), so
-    this runs the sharded route/expert/combine kernels exactly as a real
-    multi-GPU run would."""
-    d, ff, g = 1024, 1536, 128
-    v, w, sites, _ = moe_inputs_device(11, n_tok, d, ff, E, g)
-    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
-    ref.prepare_tc()
-    want = ref(v).clone()
-    per = E // world
-    ranks = []
-    for r in range(world):
-        loc = MoELayer.from_stacks(w, *(_shard(s, r * per, per) for s in full), top_k=k, path="tc",
-                                   expert_begin=r * per, n_experts=E)
-        loc.prepare_tc()
-        ranks.append(EPMoE(CudaBackend(loc), E, k, rank=r, world=world))
-    bounds = [(r * n_tok // world, (r + 1) * n_tok // world) for r in range(world)]
-    states = [ep.dispatch(v[lo:hi]) for ep, (lo, hi) in zip(ranks, bounds)]
-    cuts = [np.concatenate([[0], np.cumsum(st["send"].tolist())]) for st in states]
-
-    def seg(st, c, key, q):
-        return st[key][int(c[q]):int(c[q + 1])]
-
-    back = [[None] * world for _ in range(world)]
-    for q, ep in enumerate(ranks):
-        parts = {key: torch.cat([seg(st, c, key, q) for st, c in zip(states, cuts)]) for key in ("codes", "scales",
-                                                                                                 "eid")}
-        f = ep.compute(parts["codes"], parts["scales"], parts["eid"])
-        off = 0
-        for r, (st, c) in enumerate(zip(states, cuts)):
-            cnt = int(c[q + 1] - c[q])
-            back[r][q] = f[off:off + cnt]
-            off += cnt
-    got = torch.cat([ep.finish(st, torch.cat(back[r])) for r, (ep, st) in enumerate(zip(ranks, states))])
-    torch.cuda.synchronize()
-    assert torch.equal(got, want)
+def _build(seed, n_all, d, ff, E, k, g, n_sh=0, path="tc"):
+    v, w, sites, sh = moe_inputs_device(seed, n_all, d, ff, E, g, n_shared=n_sh)
+    full = _stacks(sites, g)
+    shared = tuple(_stacks(sh, g)) if n_sh else None
+    ref = MoELayer.from_stacks(w, *full, top_k=k, shared=shared, path=path)
+    if path == "tc":
+        ref.prepare_tc()
+    return v, w, full, shared, ref
 
 
-def _sharded_layers(w, full, E, k, world, path="tc"):
+def _sharded_layers(w, full, shared, E, k, world, path="tc"):
     per = E // world
     out = []
     for r in range(world):
-        loc = MoELayer.from_stacks(w, *(_shard(s, r * per, per) for s in full), top_k=k, path=path,
+        loc = MoELayer.from_stacks(w, *(_shard(s, r * per, per) for s in full), top_k=k, shared=shared, path=path,
                                    expert_begin=r * per, n_experts=E)
         if path == "tc":
             loc.prepare_tc()
@@ -105,144 +76,269 @@ def _sharded_layers(w, full, E, k, world, path="tc"):
     return out
 
 
-def _run_ranks_in_process(steps, xs):
-    """Drive EPStep phases of all ranks, doing the two equal-split exchanges
-    by slicing: recv_q[src block] = send_src[q block]."""
-    world, cap = len(steps), steps[0].cap
+def _sim_a2a(outs, ins, splits, cap):
+    """outs[q] = concat over sources src of ins[src]'s block for q (all_to_all(-v))."""
+    world = len(ins)
+    for q in range(world):
+        parts = []
+        for src in range(world):
+            sp = splits[src] if splits[src] is not None else [cap] * world
+            lo = sum(sp[:q])
+            parts.append(ins[src][lo:lo + sp[q]])
+        cat = torch.cat(parts)
+        outs[q][:cat.shape[0]].copy_(cat)
+
+
+def _run_in_process(steps, xs):
+    world = len(steps)
     for st, x in zip(steps, xs):
-        st.route_and_pack(x)
-    for q, st in enumerate(steps):
-        for src, other in enumerate(steps):
-            st.recv[src * cap:(src + 1) * cap].copy_(other.send[q * cap:(q + 1) * cap])
+        st.dispatch(x)
+    if steps[0].sizing == "compact":
+        for q, st in enumerate(steps):
+            for src, other in enumerate(steps):
+                st.rcounts[src].copy_(other.counts[q])
+        for st in steps:
+            st.read_counts()
     for st in steps:
-        st.run_experts()
-    for r, st in enumerate(steps):
-        for q, other in enumerate(steps):
-            st.ret[q * cap:(q + 1) * cap].copy_(other.back[r * cap:(r + 1) * cap])
-    return [st.combine().clone() for st in steps]
+        st.run_shared()
+    cap = steps[0].cap
+    for m in range(steps[0].M):
+        views = [st.views(m) for st in steps]
+        _sim_a2a([v[1] for v in views], [v[0] for v in views], [st.splits(m)[0] for st in steps], cap)
+        for st in steps:
+            st.experts(m)
+        _sim_a2a([v[3] for v in views], [v[2] for v in views], [st.splits(m)[1] for st in steps], cap)
+    outs = []
+    for st in steps:
+        for m in range(st.M):
+            st.combine(m, st.out)
+        outs.append(st.out.clone())
+    assert world == len(outs)
+    return torch.cat(outs)
 
 
-@pytest.mark.parametrize("world,n_tok,E,k,path", [(2, 40, 8, 2, "tc"), (4, 32, 8, 2, "tc"), (8, 16, 8, 2, "tc"),
-                                                  (2, 21, 6, 3, "tc"), (2, 24, 8, 2, "f32")])
-def test_ep_step_slots_match_single_gpu_layer(world, n_tok, E, k, path):
-    """Fixed-capacity EP step (device-side dispatch / group / scatter): every
-    rank's combined output equals the single-GPU layer's rows bit for bit."""
-    d, ff, g = 1024, 1536, 128
-    v, w, sites, _ = moe_inputs_device(13, n_tok * world, d, ff, E, g)
-    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    ref = MoELayer.from_stacks(w, *full, top_k=k, path=path)
-    if path == "tc":
-        ref.prepare_tc()
+def _check(got, want, dedup, ref=None, n_all=None, E=None, world=None):
+    if not dedup:
+        assert torch.equal(got, want)
+        return
+    g64, w64 = got.double(), want.double()
+    rel = float((g64 - w64).norm() / w64.norm())
+    assert rel <= 1e-6, rel
+    if ref is not None:  # tokens whose experts all live on one rank: bitwise
+        sel = ref.trace(n_all)["selected"]
+        one = (sel // (E // world) == (sel[:, :1] // (E // world))).all(1)
+        assert torch.equal(got[one], want[one])
+
+
+CASES = {  # name: (n per rank, d, ff, E, k, n_shared, world)
+    "mx_w2": (24, 1024, 1536, 8, 2, 0, 2),
+    "mx_w8": (16, 1024, 1536, 8, 2, 0, 8),
+    "qw_w2": (24, 2048, 768, 128, 8, 0, 2),
+    "qw_w4": (20, 2048, 768, 128, 8, 0, 4),
+    "qw_w8": (16, 2048, 768, 128, 8, 0, 8),
+    "ds_w8": (24, 2048, 1408, 64, 6, 2, 8),
+    "ds_w2": (20, 2048, 1408, 64, 6, 2, 2),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("dedup,sizing,mb", [(False, "fixed", 1), (True, "compact", 2), (True, "fixed", 1)])
+def test_ep_step_matches_single_gpu_layer(case, dedup, sizing, mb):
+    """QW (128 experts, top-8) and DS (64 + 2 shared, top-6) at world 2/4/8,
+    Mixtral-shaped at 2/8: every rank's output against the single-GPU layer."""
+    n, d, ff, E, k, n_sh, world = CASES[case]
+    g = 128
+    v, w, full, shared, ref = _build(41 + world, n * world, d, ff, E, k, g, n_sh)
     want = ref(v).clone()
-    layers = _sharded_layers(w, full, E, k, world, path)
-    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
-    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    layers = _sharded_layers(w, full, shared, E, k, world)
+    steps = [EPStep(layers[r], n, r, world, dedup=dedup, sizing=sizing, micro_batches=mb, exchange=lambda *a: None)
+             for r in range(world)]
+    got = _run_in_process(steps, [v[r * n:(r + 1) * n] for r in range(world)])
     torch.cuda.synchronize()
-    assert torch.equal(got, want)
+    _check(got, want, dedup, ref, n * world, E, world)
 
 
-def test_ep_step_unpacked_slots_for_odd_width():
-    """d_model % 32 != 0 (1040) sends int8 codes instead of packed nibbles; the
-    step is still bitwise equal to the single-GPU layer (fp32 path, g = 16)."""
-    world, n_tok, E, k, d, ff, g = 2, 20, 8, 2, 1040, 256, 16
-    v, w, sites, _ = moe_inputs_device(37, n_tok * world, d, ff, E, g)
-    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    ref = MoELayer.from_stacks(w, *full, top_k=k, path="f32")
+@pytest.mark.parametrize("dedup", [True, False])
+def test_ep_send_rows_equal_protocol_bytes(dedup):
+    """Compact sizing: the device rows (codes as nibbles, scale, routes,
+    weights) equal ep.pack_rows(plan_rows(...)) byte for byte; counts and
+    src_slot / src_w equal the plan's."""
+    n, d, ff, E, k, world, g = 40, 2048, 768, 64, 6, 4, 128
+    v, w, full, _, _ = _build(61, n * world, d, ff, E, k, g)
+    layers = _sharded_layers(w, full, None, E, k, world)
+    for r in (0, 3):
+        st = EPStep(layers[r], n, r, world, dedup=dedup, sizing="compact", exchange=lambda *a: None)
+        st.dispatch(v[r * n:(r + 1) * n])
+        tr = st.tr
+        p = plan_rows(tr["selected"], tr["weights"], E, world, dedup)
+        want = pack_rows(tr["codes"], tr["scales"], p)
+        assert torch.equal(st.send[0][:want.shape[0]], want)
+        assert torch.equal(st.counts[:, 0, 0], p.counts) and torch.equal(st.counts[:, 0, 1], p.routes)
+        assert torch.equal(st.src_slot[0], p.src_slot) and torch.equal(st.src_w[0], p.src_w)
+
+
+def test_ep_dedup_moves_fewer_bytes_than_exact():
+    """DS at world 8: one row per (token, peer) — the exchange shrinks from one
+    row per route (top-6) to ~4.5 rows per token, both directions."""
+    n, d, ff, E, k, n_sh, world = CASES["ds_w8"]
+    v, w, full, shared, _ = _build(43, n * world, d, ff, E, k, 128, n_sh)
+    layers = _sharded_layers(w, full, shared, E, k, world)
+    res = {}
+    for dedup in (True, False):
+        steps = [EPStep(layers[r], n, r, world, dedup=dedup, sizing="compact", exchange=lambda *a: None)
+                 for r in range(world)]
+        _run_in_process(steps, [v[r * n:(r + 1) * n] for r in range(world)])
+        res[dedup] = sum(st.exchange_bytes()["back"] for st in steps)
+    assert res[True] < 0.85 * res[False]
+
+
+def test_ep_step_unpacked_rows_for_odd_width():
+    """d_model % 32 != 0 (1040) sends int8 codes instead of packed nibbles; still
+    bitwise equal to the single-GPU layer (fp32 path, g = 16, exact rows)."""
+    world, n, E, k, d, ff, g = 2, 20, 8, 2, 1040, 256, 16
+    v, w, full, _, ref = _build(37, n * world, d, ff, E, k, g, path="f32")
     want = ref(v).clone()
-    layers = _sharded_layers(w, full, E, k, world, "f32")
-    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
-    assert steps[0].send.shape[-1] == d + 16  # int8 codes
-    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    layers = _sharded_layers(w, full, None, E, k, world, "f32")
+    steps = [EPStep(layers[r], n, r, world, dedup=False, exchange=lambda *a: None) for r in range(world)]
+    assert steps[0].rb == d + 16
+    got = _run_in_process(steps, [v[r * n:(r + 1) * n] for r in range(world)])
     torch.cuda.synchronize()
     assert torch.equal(got, want)
 
 
 @pytest.mark.parametrize("geometry", ["prefill", "decode"])
-@pytest.mark.parametrize("world,n_tok", [(4, 48), (8, 32)])
-def test_ep_step_rank_gemm_geometries(monkeypatch, geometry, world, n_tok):
-    """The per-rank expert GEMMs with the slot capacity as the row bound and the
-    routed row count on the device, in either geometry (4 and 8 GPUs take the
-    prefill geometry at Mixtral size): bitwise equal to the single-GPU layer."""
-    E, k, d, ff, g = 8, 2, 1024, 1536, 128
-    v, w, sites, _ = moe_inputs_device(29 + world, n_tok * world, d, ff, E, g)
-    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
-    ref.prepare_tc()
+def test_ep_step_rank_gemm_geometries(monkeypatch, geometry):
+    """The per-rank expert GEMMs in either geometry: bitwise equal to the single-GPU layer."""
+    world, n, E, k, d, ff, g = 4, 48, 8, 2, 1024, 1536, 128
+    v, w, full, _, ref = _build(33, n * world, d, ff, E, k, g)
     want = ref(v).clone()
     monkeypatch.setenv("CQ_UMMA_GEOMETRY", geometry)
-    layers = _sharded_layers(w, full, E, k, world)
-    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
-    assert steps[0].send.shape[-1] == d // 2 + 16  # codes as packed nibbles
-    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    layers = _sharded_layers(w, full, None, E, k, world)
+    steps = [EPStep(layers[r], n, r, world, dedup=False, exchange=lambda *a: None) for r in range(world)]
+    got = _run_in_process(steps, [v[r * n:(r + 1) * n] for r in range(world)])
     torch.cuda.synchronize()
     assert torch.equal(got, want)
 
 
-def test_ep_step_skewed_routing_fills_one_rank():
-    """All tokens routed to the experts of rank 0 (router columns of the other
-    ranks pushed to -inf-like values): rank 0's slots fill to capacity, the
+@pytest.mark.parametrize("sizing", ["fixed", "compact"])
+def test_ep_step_skewed_routing_fills_one_rank(sizing):
+    """All tokens routed to rank 0's experts: its slots fill to capacity, the
     other ranks receive nothing and run no expert rows."""
-    world, n_tok, E, k, d, ff, g = 4, 16, 8, 2, 1024, 1536, 128
-    v, w, sites, _ = moe_inputs_device(17, n_tok * world, d, ff, E, g)
+    world, n, E, k, d, ff, g = 4, 16, 8, 2, 1024, 1536, 128
+    v, w, sites, _ = moe_inputs_device(17, n * world, d, ff, E, g)
     w = w.clone()
     w[:, 2:] = -1e3 * w[:, 2:].abs() - 1.0   # experts 0, 1 (rank 0) always win
     v = v.abs() + 0.01                        # positive inputs keep the margin
-    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
-    ref.prepare_tc()
+    full = _stacks(sites, g)
+    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc").prepare_tc()
     want = ref(v).clone()
-    assert set(ref.trace(n_tok * world)["selected"].unique().tolist()) <= {0, 1}
-    layers = _sharded_layers(w, full, E, k, world)
-    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
-    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    assert set(ref.trace(n * world)["selected"].unique().tolist()) <= {0, 1}
+    layers = _sharded_layers(w, full, None, E, k, world)
+    steps = [EPStep(layers[r], n, r, world, dedup=True, sizing=sizing, exchange=lambda *a: None)
+             for r in range(world)]
+    got = _run_in_process(steps, [v[r * n:(r + 1) * n] for r in range(world)])
     torch.cuda.synchronize()
-    assert torch.equal(got, want)
-    assert steps[0].offsets[-1].item() == n_tok * world * k
+    assert torch.equal(got, want)   # one destination rank per token: dedup is bitwise here
+    assert steps[0].offsets[-1].item() == n * world * k
     assert all(st.offsets[-1].item() == 0 for st in steps[1:])
 
 
-def test_ep_step_world1_nccl_graph_capture(nccl_world1):
-    """The whole EP step (NCCL all_to_all included) captured in a CUDA graph
-    and replayed equals the eager single-GPU layer."""
-    n, d, ff, E, k, g = 32, 1024, 1536, 8, 2, 128
-    v, w, sites, _ = moe_inputs_device(23, n, d, ff, E, g)
-    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    layer = MoELayer.from_stacks(w, *stacks, top_k=k, path="tc")
-    layer.prepare_tc()
-    want = layer(v).clone()
-    step = EPStep(layer, n, 0, 1)
+@pytest.mark.parametrize("dedup,sizing,mb", [(False, "fixed", 1), (True, "fixed", 2), (True, "compact", 3)])
+def test_ep_step_world1_nccl(nccl_world1, dedup, sizing, mb):
+    """The whole step through NCCL (world 1, DS-shaped with shared experts,
+    micro-batches on the communication stream): bitwise equal to the layer;
+    fixed sizing also captured in a CUDA graph and replayed."""
+    n, d, ff, E, k, g, n_sh = 48, 1024, 1024, 8, 3, 128, 2
+    v, w, full, shared, ref = _build(23, n, d, ff, E, k, g, n_sh)
+    want = ref(v).clone()
+    step = EPStep(ref, n, 0, 1, dedup=dedup, sizing=sizing, micro_batches=mb)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
         eager = step(v).clone()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=s):
-            step(v)
-        step.out.zero_()
-        graph.replay()
+        if sizing == "fixed":
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                step(v)
+            step.out.zero_()
+            graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(eager, want)
-    assert torch.equal(step.out, want)
+    if sizing == "fixed":
+        assert torch.equal(step.out, want)
+
+
+def _gloo_rank(rank, world, port, q):
+    """One rank of a 2-process EP step on the single GPU: exchanges staged
+    through host memory over gloo (the kernels of the two ranks never wait on
+    each other; only the host exchange joins them)."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        n, d, ff, E, k, g, n_sh = 32, 2048, 1408, 64, 6, 128, 2
+        v, w, full, shared, ref = _build(71, n * world, d, ff, E, k, g, n_sh)
+        want = ref(v).clone()
+        layers = _sharded_layers(w, full, shared, E, k, world)
+
+        def host_a2a(out, inp, out_splits, in_splits):
+            torch.cuda.current_stream().synchronize()
+            h_out = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(h_out, inp.cpu(), out_splits, in_splits)
+            out.copy_(h_out)
+
+        res = {}
+        for dedup, sizing, mb in ((False, "fixed", 1), (True, "compact", 2)):
+            step = EPStep(layers[rank], n, rank, world, dedup=dedup, sizing=sizing, micro_batches=mb,
+                          exchange=host_a2a)
+            got = step(v[rank * n:(rank + 1) * n]).clone()
+            torch.cuda.synchronize()
+            mine = want[rank * n:(rank + 1) * n]
+            rel = float((got.double() - mine.double()).norm() / mine.double().norm())
+            res[(dedup, sizing)] = (bool(torch.equal(got, mine)), rel)
+        q.put((rank, res))
+    except Exception as exc:
+        q.put((rank, repr(exc)))
+        raise
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_ep_step_two_processes_gloo_staged():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(2):
+        assert not isinstance(res[r], str), res[r]
+        assert res[r][(False, "fixed")][0], res[r]          # exact rows: bitwise
+        assert res[r][(True, "compact")][1] <= 1e-6, res[r]  # dedup: fp32 re-association
 
 
 @pytest.mark.parametrize("i", range(6))
 def test_ep_step_random_shapes(i):
-    """Random world size, expert count, top-k, batch and width: the sharded EP
-    step (in-process ranks) bitwise equal to the single-GPU layer."""
+    """Random world size, expert count, top-k, batch, width, shared experts,
+    protocol and sizing: the in-process EP step against the single-GPU layer."""
     rng = np.random.default_rng(700 + i)
     world = int(rng.choice([2, 4, 8]))
     E = world * int(rng.choice([1, 2, 4]))
-    k = int(rng.integers(1, min(4, E) + 1))
-    n_tok = int(rng.choice([1, 7, 32, 50]))
+    k = int(rng.integers(1, min(6, E) + 1))
+    n = int(rng.choice([1, 7, 32, 50]))
     d = int(rng.choice([512, 1024]))
-    ff, g = 512, 128
-    v, w, sites, _ = moe_inputs_device(800 + i, n_tok * world, d, ff, E, g)
-    full = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
-    ref = MoELayer.from_stacks(w, *full, top_k=k, path="tc")
-    ref.prepare_tc()
+    n_sh = int(rng.integers(0, 3))
+    dedup, sizing, mb = bool(rng.integers(0, 2)), str(rng.choice(["fixed", "compact"])), int(rng.integers(1, 4))
+    v, w, full, shared, ref = _build(800 + i, n * world, d, 512, E, k, 128, n_sh)
     want = ref(v).clone()
-    layers = _sharded_layers(w, full, E, k, world)
-    steps = [EPStep(layers[r], n_tok, r, world, all_to_all=lambda o, i: None) for r in range(world)]
-    got = torch.cat(_run_ranks_in_process(steps, [v[r * n_tok:(r + 1) * n_tok] for r in range(world)]))
+    layers = _sharded_layers(w, full, shared, E, k, world)
+    steps = [EPStep(layers[r], n, r, world, dedup=dedup, sizing=sizing, micro_batches=mb, exchange=lambda *a: None)
+             for r in range(world)]
+    got = _run_in_process(steps, [v[r * n:(r + 1) * n] for r in range(world)])
     torch.cuda.synchronize()
-    assert torch.equal(got, want)
+    _check(got, want, dedup, ref, n * world, E, world)
