@@ -59,6 +59,9 @@ namespace cq {
 #ifndef LAG_P2
 #define LAG_P2 1
 #endif
+#ifndef UM_KGRP  // k-steps whose lookups all precede their TMEM stores
+#define UM_KGRP 2
+#endif
 #ifndef LAG_P3
 #define LAG_P3 1
 #endif
@@ -136,9 +139,11 @@ struct UmStage {
     // warp issues after chunk c - NA (fires when those MMAs, the last readers
     // of the A stage, complete).  full[] alone still means "data and A stage
     // ready", and the producer is out of the expanders' round trip.
-    static constexpr int LAG = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? UM_LAG : 0;
+    static constexpr int LAG_FIT = ((216 * 1024) / BYTES - NA) / GS * GS;  // most stages the smem holds
+    static constexpr int LAG0 = (LAG_P2 && P == 2) || (LAG_P3 && P == 3) ? UM_LAG : 0;
+    static constexpr int LAG = LAG0 < LAG_FIT ? LAG0 : LAG_FIT;
     static constexpr int NS = NA + LAG;
-    static_assert(NS % GS == 0 && NA % GS == 0 && NS * BYTES <= 200 * 1024, "smem ring");
+    static_assert(NS % GS == 0 && NA % GS == 0 && NS * BYTES <= 216 * 1024, "smem ring");
     static constexpr bool SPLIT_AFREE = UM_SPLIT_AFREE == 1 || (UM_SPLIT_AFREE == 2 && GEO::NT == 128 && P == 3);
 };
 
@@ -156,7 +161,7 @@ struct UmStage {
 // the epilogue.  Integer sums are exact, so the result does not depend on the
 // split.  Every CTA pays the prologue and the pipeline fill once.
 namespace um {
-constexpr int MAX_SEG = 1024;  // segments (experts) per launch, prefix table in smem
+constexpr int MAX_SEG = 512;   // segments (experts) per launch, prefix table in smem
 constexpr int MIN_ITERS = 8;   // fewest chunk iterations per CTA in the tail
 }  // namespace um
 
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
     __shared__ uint32_t tmem_base_sh;
     __shared__ int32_t unit_pre[um::MAX_SEG + 1], seg_off[um::MAX_SEG + 1];
     // per expander warp and column block: 8 token scales, 8 row sums
-    __shared__ __align__(16) uint32_t tok_sh[um::EXP_WARPS][NCB][16];
+    __shared__ __align__(16) uint32_t tok_sh[2][um::EXP_WARPS][NCB][16];  // [unit parity]
     __shared__ int last_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -446,140 +451,45 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
         const int cb = wg * 8;            // epilogue: token columns cb + 32 i .. + 7, i < NCB
-        uint32_t k = 0, nu = 0;
-        int seg = 0;
+        // KG k-steps are looked up before any of their tcgen05.st (a run of independent lookups, then a
+        // burst of stores)
+        constexpr int KG = (KSW % UM_KGRP == 0) ? UM_KGRP : 1;
+        uint32_t k = 0, nu = 0;           // chunks and units this CTA has started
+        int seg = 0, seg_e = 0;           // monotone segment cursors: unit starts / epilogues
         UmSeq q = seq0;
-        int u, c0, c1;
+        // Where a unit's epilogue runs (measured per geometry, tools/gemm_stage.py):
+        //   EPI 2, decode (one column block, TMEM released right after the load): after this warpgroup
+        //     has expanded its first chunk of the next unit (or at once when it has none), so that
+        //     expansion overlaps the MMA drain of the finished unit (MX gate|up 208 -> 203 us);
+        //   EPI 1, prefill with 2 planes: after the next unit's prologue, before its first chunk (the
+        //     next unit's operand prefetch is in flight sooner; QW down 272 -> 255 us);
+        //   EPI 0, prefill with 3 planes: at the end of the unit (deferral measured 7% slower: the next
+        //     unit's MMAs wait longer for TMEM).
+        constexpr int EPI = NCB == 1 ? 2 : (P == 2 ? 1 : 0);
+        bool pending = false;
+        int pu = 0, pc0 = 0, pc1 = 0;
+        float prs = 0.0f;
 #ifdef UM_EXP_TIMING
-        long long t_wait = 0, t_exp = 0, t_st = 0, t_epi = 0, t_afree = 0, t_begin = clock64();
-        long long t_eacc = 0, t_esplit = 0, t_eld = 0, t_est = 0;
+        long long t_wait = 0, t_exp = 0, t_epi = 0, t_begin = clock64();
         int n_ch = 0;
 #endif
-        for (; q.next(W, u, c0, c1); ++nu) {
-            float rscale;
-            {
-                const UmUnit x = um_unit(W, seg_first, u, seg, TPP);
-                rscale = __ldg((x.mat ? rs1 : rs0) + x.tile * 128 + row);
-                // per-token epilogue operands: async copies into this warp's smem slots now, so their
-                // latency hides under the unit's chunks (lanes 0-7 scales, 8-15 row sums)
-#pragma unroll
-                for (int i = 0; i < NCB; ++i)
-                    if (lane < 16 && cb + 32 * i < ((x.ntc + 1) & ~1) * 8) {
-                        const int64_t tok = x.j0 * 8 + cb + 32 * i + (lane & 7);
-                        if (tok >= x.rb && tok < x.re)
-                            cp_async4(&tok_sh[warp][i][lane],
-                                      lane < 8 ? (const void *)(scales + tok) : (const void *)(qsums + tok));
-                    }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-            // stream wg / WPS expands the chunks k = stream (mod GS); this warpgroup does k-steps
-            // ks0 .. ks0 + KSW - 1 of each (see UmStage)
-            for (int c = c0; c < c1; ++c, ++k) {
-                if ((int)(k % GS) != stream) continue;  // warpgroup-uniform
-                const int s = k % NS, sa = k % NA;
-#ifdef UM_EXP_TIMING
-                const long long tw0 = clock64();
-#endif
-                u_bar_wait(full_a + 8 * s, (k / NS) & 1);
-                tc_fence_after();
-#ifdef UM_EXP_TIMING
-                const long long tw1 = clock64();
-                t_wait += tw1 - tw0;
-                ++n_ch;
-#endif
-                const uint8_t *st = smem + (size_t)s * S::BYTES;
-                uint4 L[P];
-                {
-                    const uint4 *lb = reinterpret_cast<const uint4 *>(st + GEO::IDS) + row * P;
-#pragma unroll
-                    for (int p = 0; p < P; ++p) L[p] = lb[p];
-                }
-                const uint32_t abase0 = tmem + lane_addr + a_col0 + (uint32_t)(sa * S::CCOLS);
-#ifdef UM_EXP_NO_EXPAND
-                if (false)
-#endif
-#pragma unroll
-                for (int ks = ks0; ks < ks0 + KSW; ++ks) {
-                    const uint4 w = reinterpret_cast<const uint4 *>(st)[ks * 128 + row];
-                    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-                    uint32_t sel[8], xsel[8];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t xx = wv[q] ^ 0x88888888u;
-                        sel[2 * q] = wv[q];
-                        sel[2 * q + 1] = hi16(wv[q]);
-                        xsel[2 * q] = xx;
-                        xsel[2 * q + 1] = hi16(xx);
-                    }
-                    const uint32_t abase = abase0 + (uint32_t)(ks * S::ACOLS);
-                    if (S::SPLIT_AFREE && ks == ks0) {
-                        // the first k-step expands into registers before the A stage is known free: the
-                        // MMAs of this stage's previous chunk (k - NA) overlap its PRMT work
-                        uint32_t v[P][8];
-#pragma unroll
-                        for (int p = 0; p < P; ++p)
-#pragma unroll
-                            for (int cc = 0; cc < 8; ++cc)
-                                v[p][cc] = NARROW ? u_prmt(L[p].x, L[p].y, sel[cc])
-                                                  : u_merge(u_prmt(L[p].x, L[p].y, sel[cc]),
-                                                            u_prmt(L[p].z, L[p].w, xsel[cc]));
-                        // pin the values: the PRMTs must run before the wait (register-only code may
-                        // otherwise sink past the volatile barrier probe)
-#pragma unroll
-                        for (int p = 0; p < P; ++p)
-#pragma unroll
-                            for (int cc = 0; cc < 8; ++cc) asm volatile("" : "+r"(v[p][cc]));
-#ifdef UM_EXP_TIMING
-                        const long long ta0 = clock64();
-#endif
-                        u_bar_wait(afree_a + 8 * sa, ((k / NA) & 1) ^ 1);  // first use of a stage passes at once
-#ifdef UM_EXP_TIMING
-                        t_afree += clock64() - ta0;
-#endif
-                        tc_fence_after();
-#pragma unroll
-                        for (int p = 0; p < P; ++p) tc_st8(abase + p * 8, v[p]);
-                    } else {
-                        // one 8-column store per plane as soon as it is expanded (keeps the register peak low)
-#pragma unroll
-                        for (int p = 0; p < P; ++p) {
-                            uint32_t v[8];
-#pragma unroll
-                            for (int cc = 0; cc < 8; ++cc)
-                                v[cc] = NARROW ? u_prmt(L[p].x, L[p].y, sel[cc])
-                                               : u_merge(u_prmt(L[p].x, L[p].y, sel[cc]),
-                                                         u_prmt(L[p].z, L[p].w, xsel[cc]));
-                            tc_st8(abase + p * 8, v);
-                        }
-                    }
-                }
-#ifdef UM_EXP_TIMING
-                const long long tx = clock64();
-                t_exp += tx - tw1;
-#endif
-                tc_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) u_bar_arrive(afull_a + 8 * sa);
-#ifdef UM_EXP_TIMING
-                t_st += clock64() - tx;
-#endif
-            }
+        // ---- epilogue of unit pu (the (nu-1)-th).  Warpgroup wg owns token columns cb + 32 i (i < NCB).
+        // newer: the next unit's token operands were prefetched after the pending unit's (one newer
+        // cp.async group, left in flight)
+        auto epilogue = [&](bool newer) {
 #ifdef UM_EXP_TIMING
             const long long te0 = clock64();
 #endif
-            // ---- epilogue of this unit.  Warpgroup wg owns token columns cb + 32 i (i < NCB).
-            u_bar_wait(u_smem(&accfull_bar), nu & 1);
-#ifdef UM_EXP_TIMING
-            t_eacc += clock64() - te0;
-#endif
+            pending = false;
+            const int slot = (nu - 1) & 1;
+            u_bar_wait(u_smem(&accfull_bar), (nu - 1) & 1);
             tc_fence_after();
-            const UmUnit x = um_unit(W, seg_first, u, seg, TPP);  // re-decoded (smem) rather than kept live
+            const UmUnit x = um_unit(W, seg_first, pu, seg_e, TPP);
             const int n = ((x.ntc + 1) & ~1) * 8;
-            const bool split = c0 > 0 || c1 < n_chunks;  // unit shared with neighbouring CTAs (stream-K tail)
+            const bool split = pc0 > 0 || pc1 < n_chunks;  // unit shared with neighbouring CTAs (stream-K tail)
             int bf = 0, bl = 0;
             if (split) {
-                const int64_t ustart = (int64_t)u * n_chunks;
+                const int64_t ustart = (int64_t)pu * n_chunks;
                 bf = W.owner(ustart);
                 bl = W.owner(ustart + n_chunks - 1);
             }
@@ -595,7 +505,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                 for (int b2 = bf; b2 <= bl; ++b2) {
                     if (b2 == cta) continue;
                     const int64_t fu = W.tstart(b2) / n_chunks;
-                    const int32_t *src = part + (size_t)(2 * b2 + (u != fu ? 1 : 0)) * GEO::PART_WORDS;
+                    const int32_t *src = part + (size_t)(2 * b2 + (pu != fu ? 1 : 0)) * GEO::PART_WORDS;
 #pragma unroll
                     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -603,7 +513,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                 }
             };
             auto publish = [&](int cbi, const int32_t (&acc)[P][8]) {
-                int32_t *mine = part + (size_t)(2 * cta + (u != first_tail_unit ? 1 : 0)) * GEO::PART_WORDS;
+                int32_t *mine = part + (size_t)(2 * cta + (pu != first_tail_unit ? 1 : 0)) * GEO::PART_WORDS;
 #pragma unroll
                 for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -620,18 +530,18 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                 asm volatile("bar.sync 1, %0;" ::"r"(um::EXP_WARPS * 32) : "memory");
                 return last_sh != 0;
             };
-            auto store = [&](int i, const int32_t (&acc)[P][8]) {
-                const int cbi = cb + 32 * i;
+            auto store = [&](int ib, const int32_t (&acc)[P][8]) {
+                const int cbi = cb + 32 * ib;
                 float *out = x.mat ? out1 : out0;
                 // the block's 8 token scales and code sums (smem, two vector loads each); entries of
                 // tokens outside [rb, re) are stale and their results are never stored
-                const float4 sa = *reinterpret_cast<const float4 *>(&tok_sh[warp][i][0]);
-                const float4 sb = *reinterpret_cast<const float4 *>(&tok_sh[warp][i][4]);
-                const int4 qa = *reinterpret_cast<const int4 *>(&tok_sh[warp][i][8]);
-                const int4 qb = *reinterpret_cast<const int4 *>(&tok_sh[warp][i][12]);
-                const float tscale[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+                const float4 sa4 = *reinterpret_cast<const float4 *>(&tok_sh[slot][warp][ib][0]);
+                const float4 sb4 = *reinterpret_cast<const float4 *>(&tok_sh[slot][warp][ib][4]);
+                const int4 qa = *reinterpret_cast<const int4 *>(&tok_sh[slot][warp][ib][8]);
+                const int4 qb = *reinterpret_cast<const int4 *>(&tok_sh[slot][warp][ib][12]);
+                const float tscale[8] = {sa4.x, sa4.y, sa4.z, sa4.w, sb4.x, sb4.y, sb4.z, sb4.w};
                 const int32_t tqsum[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-                float v[8];
+                float vv[8];
 #pragma unroll
                 for (int c2 = 0; c2 < 8; ++c2) {  // branch-free, so the 8 conversion chains overlap
                     // exact integer digit sum (|.| < 2^39) in int64, one conversion: the same double
@@ -641,93 +551,67 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                     for (int p = P - 2; p >= 0; --p) s64 = s64 * 128 + (int64_t)acc[p][c2];
                     s64 -= (int64_t)tqsum[c2] << (7 * P - 1);
                     const double sum = (double)s64;
-                    v[c2] = __fmul_rn((float)(sum * (double)rscale), tscale[c2]);
+                    vv[c2] = __fmul_rn((float)(sum * (double)prs), tscale[c2]);
                 }
                 const int64_t tok0 = x.j0 * 8 + cbi;
                 float *o = out + tok0 * d_out + (int64_t)x.rt * 128 + row;
                 if (tok0 >= x.rb && tok0 + 8 <= x.re) {
 #pragma unroll
-                    for (int c2 = 0; c2 < 8; ++c2) o[(int64_t)c2 * d_out] = v[c2];
+                    for (int c2 = 0; c2 < 8; ++c2) o[(int64_t)c2 * d_out] = vv[c2];
                 } else {
 #pragma unroll
                     for (int c2 = 0; c2 < 8; ++c2)
-                        if (tok0 + c2 >= x.rb && tok0 + c2 < x.re) o[(int64_t)c2 * d_out] = v[c2];
+                        if (tok0 + c2 >= x.rb && tok0 + c2 < x.re) o[(int64_t)c2 * d_out] = vv[c2];
                 }
             };
             if constexpr (NCB == 1) {
                 // one block: keep it in registers and release TMEM at once, so the MMAs of the next
                 // unit overlap this epilogue
                 int32_t acc[P][8];
-#ifdef UM_EXP_TIMING
-                const long long f0 = clock64();
-#endif
                 if (cb < n) load_acc(cb, acc);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
-#ifdef UM_EXP_TIMING
-                const long long f1 = clock64();
-                t_eld += f1 - f0;
-#endif
                 bool finish = true;
                 if (split) {
                     if (cb < n) publish(cb, acc);
                     finish = arrive_last();
                     if (finish && cb < n) add_partials(cb, acc);
                 }
-                asm volatile("cp.async.wait_all;" ::: "memory");
+                if (newer)
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else
+                    asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
-#ifdef UM_EXP_TIMING
-                const long long f2 = clock64();
-                t_esplit += f2 - f1;
-#endif
                 if (finish && cb < n) store(0, acc);
-#ifdef UM_EXP_TIMING
-                t_est += clock64() - f2;
-#endif
             } else {
                 // several blocks: read TMEM block by block, release it after the last
-#ifdef UM_EXP_TIMING
-                const long long e0 = clock64();
-#endif
                 bool finish = true;
                 if (split) {
 #pragma unroll 1
-                    for (int i = 0; i < NCB; ++i) {
-                        if (cb + 32 * i >= n) break;
+                    for (int ib = 0; ib < NCB; ++ib) {
+                        if (cb + 32 * ib >= n) break;
                         int32_t acc[P][8];
-                        load_acc(cb + 32 * i, acc);
-                        publish(cb + 32 * i, acc);
+                        load_acc(cb + 32 * ib, acc);
+                        publish(cb + 32 * ib, acc);
                     }
                     finish = arrive_last();
                 }
-                asm volatile("cp.async.wait_all;" ::: "memory");
+                if (newer)
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else
+                    asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
-#ifdef UM_EXP_TIMING
-                const long long e1 = clock64();
-                t_esplit += e1 - e0;
-                long long tl = 0;
-#endif
                 if (finish) {
 #pragma unroll 1
-                    for (int i = 0; i < NCB; ++i) {
-                        if (cb + 32 * i >= n) break;
+                    for (int ib = 0; ib < NCB; ++ib) {
+                        if (cb + 32 * ib >= n) break;
                         int32_t acc[P][8];
-#ifdef UM_EXP_TIMING
-                        const long long l0 = clock64();
-#endif
-                        load_acc(cb + 32 * i, acc);
-#ifdef UM_EXP_TIMING
-                        tl += clock64() - l0;
-#endif
-                        if (split) add_partials(cb + 32 * i, acc);
-                        store(i, acc);
+                        load_acc(cb + 32 * ib, acc);
+                        if (split) add_partials(cb + 32 * ib, acc);
+                        store(ib, acc);
                     }
                 }
-#ifdef UM_EXP_TIMING
-                t_eld += tl;
-                t_est += clock64() - e1 - tl;
-#endif
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
@@ -735,13 +619,130 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
 #ifdef UM_EXP_TIMING
             t_epi += clock64() - te0;
 #endif
+        };
+        for (;;) {
+            int u = 0, c0 = 0, c1 = 0;
+            const bool has = q.next(W, u, c0, c1);
+            float rscale = 0.0f;
+            int first = 0, n_own = 0;
+            if (has) {
+                const UmUnit x = um_unit(W, seg_first, u, seg, TPP);
+                rscale = __ldg((x.mat ? rs1 : rs0) + x.tile * 128 + row);
+                // per-token epilogue operands: async copies into this warp's smem slots now, so their
+                // latency hides under the unit's chunks (lanes 0-7 scales, 8-15 row sums)
+#pragma unroll
+                for (int i = 0; i < NCB; ++i)
+                    if (lane < 16 && cb + 32 * i < ((x.ntc + 1) & ~1) * 8) {
+                        const int64_t tok = x.j0 * 8 + cb + 32 * i + (lane & 7);
+                        if (tok >= x.rb && tok < x.re)
+                            cp_async4(&tok_sh[nu & 1][warp][i][lane],
+                                      lane < 8 ? (const void *)(scales + tok) : (const void *)(qsums + tok));
+                    }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                // this stream's chunks of the unit: those whose CTA-wide index k + (c - c0) = stream (mod GS)
+                first = (stream - (int)(k % GS) + GS) % GS;
+                n_own = c1 - c0 > first ? (c1 - c0 - first + GS - 1) / GS : 0;
+            }
+            for (int i = 0; i <= n_own; ++i) {
+                if constexpr (EPI == 1) {
+                    if (i == 0 && pending) epilogue(has);
+                }
+                if (i < n_own) {
+                    // ---- expand chunk kc (k-steps ks0 .. ks0 + KSW - 1 of it, see UmStage)
+                    const uint32_t kc = k + (uint32_t)(first + i * GS);
+                    const int s = kc % NS, sa = kc % NA;
+#ifdef UM_EXP_TIMING
+                    const long long tw0 = clock64();
+#endif
+                    u_bar_wait(full_a + 8 * s, (kc / NS) & 1);
+                    tc_fence_after();
+#ifdef UM_EXP_TIMING
+                    const long long tw1 = clock64();
+                    t_wait += tw1 - tw0;
+                    ++n_ch;
+#endif
+                    const uint8_t *st = smem + (size_t)s * S::BYTES;
+                    uint4 L[P];
+                    {
+                        const uint4 *lb = reinterpret_cast<const uint4 *>(st + GEO::IDS) + row * P;
+#pragma unroll
+                        for (int p = 0; p < P; ++p) L[p] = lb[p];
+                    }
+                    const uint32_t abase0 = tmem + lane_addr + a_col0 + (uint32_t)(sa * S::CCOLS);
+#ifdef UM_EXP_NO_EXPAND
+                    if (false)
+#endif
+#pragma unroll
+                    for (int kg = 0; kg < KSW; kg += KG) {
+                        uint32_t v[KG][P][8];
+#pragma unroll
+                        for (int h = 0; h < KG; ++h) {
+                            const int ks = ks0 + kg + h;
+                            const uint4 w = reinterpret_cast<const uint4 *>(st)[ks * 128 + row];
+                            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+                            uint32_t sel[8], xsel[8];
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq) {
+                                const uint32_t xx = wv[qq] ^ 0x88888888u;
+                                sel[2 * qq] = wv[qq];
+                                sel[2 * qq + 1] = hi16(wv[qq]);
+                                xsel[2 * qq] = xx;
+                                xsel[2 * qq + 1] = hi16(xx);
+                            }
+#pragma unroll
+                            for (int p = 0; p < P; ++p)
+#pragma unroll
+                                for (int cc = 0; cc < 8; ++cc)
+                                    v[h][p][cc] = NARROW ? u_prmt(L[p].x, L[p].y, sel[cc])
+                                                         : u_merge(u_prmt(L[p].x, L[p].y, sel[cc]),
+                                                                   u_prmt(L[p].z, L[p].w, xsel[cc]));
+                        }
+                        if (S::SPLIT_AFREE && kg == 0) {
+                            // the first k-steps expand into registers before the A stage is known free:
+                            // the MMAs of this stage's previous chunk (kc - NA) overlap their PRMT work.  Pin
+                            // the values: the PRMTs must run before the wait (register-only code may
+                            // otherwise sink past the volatile barrier probe)
+#pragma unroll
+                            for (int h = 0; h < KG; ++h)
+#pragma unroll
+                                for (int p = 0; p < P; ++p)
+#pragma unroll
+                                    for (int cc = 0; cc < 8; ++cc) asm volatile("" : "+r"(v[h][p][cc]));
+                            u_bar_wait(afree_a + 8 * sa, ((kc / NA) & 1) ^ 1);  // first use of a stage passes
+                            tc_fence_after();
+                        }
+#pragma unroll
+                        for (int h = 0; h < KG; ++h)
+#pragma unroll
+                            for (int p = 0; p < P; ++p)
+                                tc_st8(abase0 + (uint32_t)((ks0 + kg + h) * S::ACOLS + p * 8), v[h][p]);
+                    }
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) u_bar_arrive(afull_a + 8 * sa);
+#ifdef UM_EXP_TIMING
+                    t_exp += clock64() - tw1;
+#endif
+                }
+                if constexpr (EPI == 2) {
+                    if (i == 0 && pending) epilogue(has);
+                }
+            }
+            if (!has) break;
+            k += (uint32_t)(c1 - c0);
+            pending = true;
+            pu = u;
+            pc0 = c0;
+            pc1 = c1;
+            prs = rscale;
+            ++nu;
+            if constexpr (EPI == 0) epilogue(false);
         }
 #ifdef UM_EXP_TIMING
         if (blockIdx.x == 0 && lane == 0)
-            printf("warp %2d chunks %d: full-wait %lld expand %lld (of which afree-wait %lld) wait_st %lld epilogue %lld "
-                   "[acc-wait %lld split %lld tmem-ld %lld store %lld] (cycles, total %lld)\n",
-                   warp, n_ch, t_wait, t_exp, t_afree, t_st, t_epi, t_eacc, t_esplit, t_eld, t_est,
-                   clock64() - t_begin);
+            printf("warp %2d chunks %d: full-wait %lld expand %lld epilogue %lld (cycles, total %lld)\n", warp, n_ch,
+                   t_wait, t_exp, t_epi, clock64() - t_begin);
 #endif
     }
     tc_fence_before();
@@ -980,7 +981,7 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         return CQ_ERR_CONFIG;
     }
     if (n_seg > um::MAX_SEG) {
-        set_error("tcgen05 path: at most 1024 segments (experts) per launch");
+        set_error("tcgen05 path: at most 512 segments (experts) per launch");
         return CQ_ERR_UNSUPPORTED;
     }
     // prefill geometry (128-token passes, merged layout only) when segments are long
