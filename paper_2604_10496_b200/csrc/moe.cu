@@ -42,6 +42,10 @@ cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_
 int64_t umma_b_bytes(int64_t rows, int64_t d_in);
 int32_t *umma_row_sums(int8_t *bbuf, int64_t rows, int64_t d_in);
 int64_t rot_tc_act_bytes(int64_t n, int64_t d);
+const float *rot_tc_transposed(const void *prepared, int64_t d);
+cq_status rot_certify(const float *v, const void *x, int dtype, const float *Rt, int64_t n, int64_t d, int8_t *codes,
+                      float *scales, int *nonfinite, float *deq, int32_t *tsum, int32_t *zero, int n_zero,
+                      int *recomputed, cudaStream_t st);
 cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const void *prepared, void *act, float *v,
                        cudaStream_t st);
 
@@ -586,21 +590,25 @@ cq_status shared_experts(const cq_moe_desc *desc, int path, int64_t n, const Ws 
 cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, const Ws &w, cudaStream_t st,
                 bool gather = true, int *deferred = nullptr) {
     const int64_t d = dsc->d_model;
-    const void *qin = x;
-    int qdt = dtype;
-    if (dsc->rotation_tc != nullptr) {  // tensor cores, bf16-split R (rotate_tc.cu)
-        CQ_TRY(rot_tc_apply(x, dtype, n, d, dsc->rotation_tc, w.rot_act, w.rotated, st));
-        qin = w.rotated;
-        qdt = CQ_DTYPE_F32;
-    } else if (dsc->rotation != nullptr) {  // the reference's ordered chain (pipeline.py:516 -> _core.pyx:27-38)
-        CQ_TRY(ordered_matmul(x, dtype, dsc->rotation, n, d, d, w.rotated, st));
-        qin = w.rotated;
-        qdt = CQ_DTYPE_F32;
-    }
     // the dequantized rows (router input) go to the fout buffer, unused until the down GEMM;
     // the quantizer also clears the route counts and the arrival counter (counts[E])
-    CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, w.status, w.fout, st, w.tok_sums, w.counts,
-                       (int)dsc->n_experts + 1));
+    if (dsc->rotation_tc != nullptr) {
+        // tensor cores, bf16-split R (rotate_tc.cu), then the certified quantizer: the codes and scale of
+        // the reference's ordered chain bit for bit (rotq.cu; recomputed elements counted in status[2])
+        CQ_TRY(rot_tc_apply(x, dtype, n, d, dsc->rotation_tc, w.rot_act, w.rotated, st));
+        CQ_TRY(rot_certify(w.rotated, x, dtype, rot_tc_transposed(dsc->rotation_tc, d), n, d, w.codes, w.scales,
+                           w.status, w.fout, w.tok_sums, w.counts, (int)dsc->n_experts + 1, w.status + 2, st));
+    } else {
+        const void *qin = x;
+        int qdt = dtype;
+        if (dsc->rotation != nullptr) {  // the reference's ordered chain (pipeline.py:516 -> _core.pyx:27-38)
+            CQ_TRY(ordered_matmul(x, dtype, dsc->rotation, n, d, d, w.rotated, st));
+            qin = w.rotated;
+            qdt = CQ_DTYPE_F32;
+        }
+        CQ_TRY(quantize_a4(qin, qdt, n, d, w.codes, w.scales, w.status, w.fout, st, w.tok_sums, w.counts,
+                           (int)dsc->n_experts + 1));
+    }
     if (deferred != nullptr) {
         *deferred = 0;
         if (n * dsc->top_k <= RP_MAX_ROUTES && dsc->n_local_experts <= RP_MAX_LOCAL &&

@@ -235,7 +235,13 @@ __global__ void __launch_bounds__(rt::THREADS, 1) rot_gemm_kernel(const uint8_t 
 
 bool rot_tc_ok(int64_t d) { return d % rt::BN == 0 && d % rt::KC == 0; }
 
-int64_t rot_tc_prepared_bytes(int64_t d) { return 3 * d * d * 2; }
+// prepared = [three bf16 planes of R^T in the UMMA layout: 3 d^2 * 2 B][R^T f32: d^2 * 4 B (the certified
+// quantizer's ordered chains, rotq.cu)]
+int64_t rot_tc_prepared_bytes(int64_t d) { return 3 * d * d * 2 + d * d * 4; }
+const float *rot_tc_transposed(const void *prepared, int64_t d) {
+    return reinterpret_cast<const float *>(reinterpret_cast<const uint8_t *>(prepared) + 3 * d * d * 2);
+}
+cq_status transpose_f32(const float *R, int64_t d, float *Rt, cudaStream_t st);
 
 // Activation planes for n tokens (f32 input needs 3, bf16 1; sized for 3).
 int64_t rot_tc_act_bytes(int64_t n, int64_t d) { return 3 * ceil_div(n, rt::BM) * rt::BM * d * 2; }
@@ -247,7 +253,8 @@ cq_status rot_tc_prepare(const float *R, int64_t d, void *out, cudaStream_t st) 
     }
     rot_split_r_kernel<<<(unsigned)std::min<int64_t>(ceil_div(d * d / 8, 256), 148 * 16), 256, 0, st>>>(
         R, d, reinterpret_cast<uint4 *>(out));
-    return check_launch("rotation_prepare");
+    CQ_TRY(check_launch("rotation_prepare"));
+    return transpose_f32(R, d, const_cast<float *>(rot_tc_transposed(out, d)), st);
 }
 
 cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const void *prepared, void *act, float *v,
@@ -261,13 +268,10 @@ cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const voi
     else
         launch_pdl(rot_split_x_kernel<CQ_DTYPE_F32, 3>, blocks, 256, 0, st, x, n, d, tiles, reinterpret_cast<uint4 *>(act));
     CQ_TRY(check_launch("rotation_split_x"));
-    static bool attr = false;
+    // the dynamic-smem opt-in is per device: set it on every launch (cheap next to the kernel)
     const size_t smem = (size_t)rt::STAGES * (rt::A_BYTES + rt::B_BYTES);
-    if (!attr) {
-        cudaFuncSetAttribute(rot_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(rot_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    cudaFuncSetAttribute(rot_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(rot_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const dim3 grid((unsigned)(d / rt::BN), (unsigned)ceil_div(n, rt::BM));
     const uint8_t *a = reinterpret_cast<const uint8_t *>(act), *b = reinterpret_cast<const uint8_t *>(prepared);
     if (dtype == CQ_DTYPE_BF16)
