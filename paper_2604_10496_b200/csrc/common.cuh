@@ -42,6 +42,15 @@ inline cq_status check_launch(const char *what) {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// True the first time a call site asks for the current device (per-device one-time setup such
+// as a kernel's dynamic shared-memory opt-in, which cudaFuncSetAttribute sets per device).
+inline bool first_on_device(std::atomic<uint64_t> &seen) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    return (seen.fetch_or(bit) & bit) == 0;
+}
+
 // ---------------------------------------------------------------------------
 // device helpers
 

@@ -483,15 +483,14 @@ __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *
 template <bool FUSE>
 static void launch_chain(int eg, dim3 grid, size_t smem, cudaStream_t st, const float *xdeq, const float *w,
                          int64_t n, int64_t d, int64_t n_exp, int tt, float *logits, const RouteFuse &f) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};  // devices whose smem opt-in is set
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(router_chain_kernel<8, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)router_chain_smem(8, 4));
         cudaFuncSetAttribute(router_chain_kernel<16, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)router_chain_smem(16, 2));
         cudaFuncSetAttribute(router_chain_kernel<32, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)router_chain_smem(32, 1));
-        attr = true;
     }
     if (eg == 32)
         launch_pdl(router_chain_kernel<32, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
@@ -560,12 +559,11 @@ static cq_status router_tile_launch(const float *xdeq, const float *w, int64_t n
     int rk = (int)std::min<int64_t>(512, (smem_max / 8 - 4 * tt) / (tt + n_exp)) & ~15;
     if (rk < 16) rk = 16;
     const size_t smem = (size_t)8 * ((size_t)tt * (rk + 4) + (size_t)rk * n_exp);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};  // devices whose smem opt-in is set
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(router_tile_kernel<32, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(router_tile_kernel<64, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(router_tile_kernel<128, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
     }
     const dim3 grid((unsigned)ctas);
     if (n_exp == 32)
@@ -604,14 +602,13 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         int rk = (int)std::min<int64_t>(512, ((96 * 1024) / (8 * (tt + n_exp))) & ~15LL);
         if (rk < 16) rk = 16;
         const size_t smem = (size_t)8 * rk * (tt + n_exp);
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<uint64_t> attr{0};  // devices whose smem opt-in is set
+        if (first_on_device(attr)) {
             cudaFuncSetAttribute(router_deq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(router_deq_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(router_deq_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(router_deq_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             cudaFuncSetAttribute(router_deq_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            attr = true;
         }
         const dim3 grid((unsigned)ceil_div(n, tt));
         switch (n_exp) {
