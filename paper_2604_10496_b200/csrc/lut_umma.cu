@@ -91,9 +91,10 @@ struct UmWarps {
 // uses NT 32 / CK 128 (4 A stages of 4 k-steps); prefill NT 128 / CK 64 (the
 // 3 x 128 accumulator columns leave room for 64-column A stages only), which
 // expands each weight chunk once per 128 tokens instead of per 32.
-template <int NT_, int CK_>
+template <int NT_, int CK_, int NACC_ = 1>
 struct UmGeo {
     static constexpr int NT = NT_, CK = CK_;
+    static constexpr int NACC = NACC_;         // accumulator buffers (2: unit u+1's MMAs run during u's epilogue)
     static constexpr int KS = CK / 32;         // MMA k-steps per chunk
     static constexpr int IDS = 128 * CK / 2;   // ids bytes per chunk: 128 rows x CK columns / 2
     static constexpr int BTILE = 8 * CK;       // activation bytes per 8-token tile per chunk
@@ -101,10 +102,16 @@ struct UmGeo {
     static constexpr int PART_WORDS = 3 * NT * 128;  // int32 partial accumulators per slot (P <= 3)
 };
 using UmDecode = UmGeo<32, UM_CK>;
+// prefill passes: 128 tokens, one accumulator (3 x 128 columns).  Measured (tools/gemm_stage.py, PH
+// gate|up): 64-token passes with two accumulators 2228 us, 64 single 1933, 128 single 1187 — the
+// expansion (PRMT, ALU pipe) bounds prefill too, so fewer tokens per expanded chunk loses.
 #ifndef UM_PF_NT
 #define UM_PF_NT 128
 #endif
-using UmPrefill = UmGeo<UM_PF_NT, 64>;
+#ifndef UM_PF_NACC
+#define UM_PF_NACC 1
+#endif
+using UmPrefill = UmGeo<UM_PF_NT, 64, UM_PF_NACC>;
 
 template <int P, class GEO>
 struct UmStage {
@@ -114,7 +121,8 @@ struct UmStage {
     static constexpr int SLICES = P;                             // MMA K-slices per k-step
     static constexpr int ACOLS = SLICES * 8;                     // TMEM columns per k-step
     static constexpr int CCOLS = GEO::KS * ACOLS;                // TMEM columns per A stage (one chunk)
-    static constexpr int ACC = P * GEO::NT;                      // accumulator columns
+    static constexpr int ACC1 = P * GEO::NT;                     // columns of one accumulator buffer
+    static constexpr int ACC = ACC1 * GEO::NACC;                 // accumulator columns
     static constexpr int NCS = (um::TMEM_COLS - ACC) / CCOLS;    // A stages that fit in TMEM
     static_assert(NCS >= 1, "TMEM budget");
     // Chunk c uses smem stage and TMEM A stage c % NS (one ring).  full[s] for
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
     constexpr int TPP = NT / 8;       // token tiles per pass
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS], afull_bar[NA], afree_bar[NA];
-    __shared__ __align__(8) uint64_t accfull_bar, accempty_bar;
+    __shared__ __align__(8) uint64_t accfull_bar[GEO::NACC], accempty_bar[GEO::NACC];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int32_t unit_pre[um::MAX_SEG + 1], seg_off[um::MAX_SEG + 1];
     // per expander warp and column block: 8 token scales, 8 row sums
@@ -316,8 +324,10 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
         }
         // (splitting afull per chunk half, so the MMAs start earlier, measured slower: the extra
         //  tcgen05.wait::st mid-chunk costs more than the overlap gains)
-        u_bar_init(u_smem(&accfull_bar), NMMA);
-        u_bar_init(u_smem(&accempty_bar), um::EXP_WARPS);
+        for (int b = 0; b < GEO::NACC; ++b) {
+            u_bar_init(u_smem(&accfull_bar[b]), NMMA);
+            u_bar_init(u_smem(&accempty_bar[b]), um::EXP_WARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -389,7 +399,9 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
 #ifdef UM_EXP_TIMING
             const long long ma = clock64();
 #endif
-            if (nu > 0) u_bar_wait(u_smem(&accempty_bar), (nu - 1) & 1);
+            // accumulator buffer nu % NACC: free once the epilogue of unit nu - NACC has read it
+            const uint32_t abuf = nu % GEO::NACC, dacc = tm_u + abuf * (uint32_t)S::ACC1;
+            if (nu >= (uint32_t)GEO::NACC) u_bar_wait(u_smem(&accempty_bar[abuf]), ((nu / GEO::NACC) - 1) & 1);
 #ifdef UM_EXP_TIMING
             m_acc += clock64() - ma;
 #endif
@@ -415,12 +427,12 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                     const uint64_t bd = smem_desc(bbase, 128, GEO::BTILE);
                     if constexpr (NMMA > 1) {  // this warp's plane: accumulator columns p * NT, A columns p * 8
                         const uint32_t pl = (uint32_t)(warp - um::MMA_WARP);
-                        tc_mma_plane<GEO::KS>(__shfl_sync(0xffffffffu, tm_u + pl * NT, 0),
+                        tc_mma_plane<GEO::KS>(__shfl_sync(0xffffffffu, dacc + pl * NT, 0),
                                               __shfl_sync(0xffffffffu, abase + pl * 8, 0), (uint32_t)S::ACOLS,
                                               __shfl_sync(0xffffffffu, bd, 0), __shfl_sync(0xffffffffu, idesc, 0),
                                               c == c0u ? 0u : 1u);
                     } else {
-                        tc_mma_chunk<GEO::KS, P>(__shfl_sync(0xffffffffu, tm_u, 0), (uint32_t)NT,
+                        tc_mma_chunk<GEO::KS, P>(__shfl_sync(0xffffffffu, dacc, 0), (uint32_t)NT,
                                                  __shfl_sync(0xffffffffu, abase, 0), __shfl_sync(0xffffffffu, bd, 0),
                                                  __shfl_sync(0xffffffffu, idesc, 0), c == c0u ? 0u : 1u);
                     }
@@ -431,7 +443,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                     tc_commit_elect(afree_a + 8 * sa);  // A stage free for chunk k + NA
                 else if (LAG > 0)
                     tc_commit_elect(full_a + 8 * ((k + NA) % NS));  // A stage free for chunk k + NA
-                if (c == c1u - 1) tc_commit_elect(u_smem(&accfull_bar));
+                if (c == c1u - 1) tc_commit_elect(u_smem(&accfull_bar[abuf]));
 #ifdef UM_EXP_TIMING
                 m_iss += clock64() - mi;
 #endif
@@ -458,14 +470,15 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
         int seg = 0, seg_e = 0;           // monotone segment cursors: unit starts / epilogues
         UmSeq q = seq0;
         // Where a unit's epilogue runs (measured per geometry, tools/gemm_stage.py):
-        //   EPI 2, decode (one column block, TMEM released right after the load): after this warpgroup
+        //   EPI 2, decode (one column block, TMEM released right after the load) and double-buffered
+        //     accumulators (the next unit's MMAs use the other buffer): after this warpgroup
         //     has expanded its first chunk of the next unit (or at once when it has none), so that
         //     expansion overlaps the MMA drain of the finished unit (MX gate|up 208 -> 203 us);
         //   EPI 1, prefill with 2 planes: after the next unit's prologue, before its first chunk (the
         //     next unit's operand prefetch is in flight sooner; QW down 272 -> 255 us);
         //   EPI 0, prefill with 3 planes: at the end of the unit (deferral measured 7% slower: the next
         //     unit's MMAs wait longer for TMEM).
-        constexpr int EPI = NCB == 1 ? 2 : (P == 2 ? 1 : 0);
+        constexpr int EPI = (NCB == 1 || GEO::NACC > 1) ? 2 : (P == 2 ? 1 : 0);
         bool pending = false;
         int pu = 0, pc0 = 0, pc1 = 0;
         float prs = 0.0f;
@@ -482,7 +495,9 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
 #endif
             pending = false;
             const int slot = (nu - 1) & 1;
-            u_bar_wait(u_smem(&accfull_bar), (nu - 1) & 1);
+            const uint32_t pb = (nu - 1) % GEO::NACC;      // the pending unit's accumulator buffer
+            const uint32_t acc_base = tmem + lane_addr + pb * (uint32_t)S::ACC1;
+            u_bar_wait(u_smem(&accfull_bar[pb]), ((nu - 1) / GEO::NACC) & 1);
             tc_fence_after();
             const UmUnit x = um_unit(W, seg_first, pu, seg_e, TPP);
             const int n = ((x.ntc + 1) & ~1) * 8;
@@ -496,7 +511,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
             auto load_acc = [&](int cbi, int32_t (&acc)[P][8]) {
 #pragma unroll
                 for (int p = 0; p < P; ++p)
-                    tc_ld8(tmem + lane_addr + (uint32_t)(p * NT + cbi), reinterpret_cast<uint32_t *>(acc[p]));
+                    tc_ld8(acc_base + (uint32_t)(p * NT + cbi), reinterpret_cast<uint32_t *>(acc[p]));
                 tc_wait_ld();
             };
             // the last CTA of a split unit adds the others' partials (exact int32)
@@ -571,7 +586,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                 if (cb < n) load_acc(cb, acc);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
+                if (lane == 0) u_bar_arrive(u_smem(&accempty_bar[pb]));
                 bool finish = true;
                 if (split) {
                     if (cb < n) publish(cb, acc);
@@ -614,7 +629,7 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) u_bar_arrive(u_smem(&accempty_bar));
+                if (lane == 0) u_bar_arrive(u_smem(&accempty_bar[pb]));
             }
 #ifdef UM_EXP_TIMING
             t_epi += clock64() - te0;

@@ -7,6 +7,10 @@
 // weights (K <= 8 tables), 3 TMEM stores only (no lookups), 5 full with the
 // previous k-step's stored registers kept live until the next k-step's lookups
 // are done (no write-after-read wait on tcgen05.st sources)
+// Caveat (found later): the ids are the same for every chunk except w.x, so the compiler hoists
+// three quarters of the lookups out of the chunk loop; the absolute cycles understate the
+// expansion cost ~4x (the GEMM's own ncu profile, profiles/r02/README.md, is the measurement).
+// The relative effects of store scheduling and unrolling are what this probe showed.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o expand_probe expand_probe.cu
 #include <cstdint>
 #include <cstdio>
