@@ -150,6 +150,10 @@ typedef struct {
    writes only the re-quantized h (codes, scales), and CQ_WS_HIDDEN holds the
    gate output; the f32 and ordered paths always store h. */
 enum { CQ_FLAG_KEEP_HIDDEN = 1 };
+/* CQ_FLAG_SELECT_ONLY: cq_moe_route stops after the top-k (codes, scales, logits,
+   selected, weights, tok_sums): no segment permutation or gathered codes (the
+   expert-parallel driver plans its own rows). */
+enum { CQ_FLAG_SELECT_ONLY = 2 };
 
 enum { CQ_PATH_AUTO = 0, CQ_PATH_F32 = 1, CQ_PATH_TC = 2, CQ_PATH_ORDERED = 3 };
 

@@ -48,6 +48,7 @@ class MoEDesc(ctypes.Structure):
 
 
 FLAG_KEEP_HIDDEN = 1  # CQ_FLAG_KEEP_HIDDEN
+FLAG_SELECT_ONLY = 2  # CQ_FLAG_SELECT_ONLY
 
 
 _SIGS = {

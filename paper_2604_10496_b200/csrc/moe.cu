@@ -625,6 +625,7 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
     CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
     CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, w.counts, dsc->expert_begin,
                 dsc->n_local_experts, st));
+    if (dsc->flags & CQ_FLAG_SELECT_ONLY) return CQ_OK;
     CQ_TRY(permute(w.selected, w.counts, n, dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets,
                    w.perm_token, w.perm_slot, w.inv, st));
     if (!gather) return CQ_OK;
@@ -650,6 +651,10 @@ extern "C" cq_status cq_moe_route(const cq_moe_desc *desc, const void *x, int dt
         return CQ_ERR_SHAPE;
     }
     if (n_tokens == 0) return CQ_OK;
+    if (desc->flags & CQ_FLAG_SELECT_ONLY) {  // the fused decode router + top-k when it applies
+        int fused = 0;
+        return route(desc, x, dtype, n_tokens, carve(workspace, off), as_stream(stream), false, &fused);
+    }
     return route(desc, x, dtype, n_tokens, carve(workspace, off), as_stream(stream));
 }
 

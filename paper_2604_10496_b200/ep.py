@@ -280,6 +280,8 @@ class EPStep:
         self.ws_route, _ = layer.workspace(self.n)
         self.tr = layer.trace(self.n)
         self.desc = layer.desc()
+        self.desc_route = layer.desc()
+        self.desc_route.flags |= _lib.FLAG_SELECT_ONLY  # routing stops at the top-k: rows are planned here
         self.n_shared = layer.shared[0].n if layer.shared is not None else 0
         self.shared_out = (torch.empty((self.n_shared, self.n, self.d), dtype=torch.float32, **z)
                            if self.n_shared else None)
@@ -298,7 +300,7 @@ class EPStep:
         L, tr = _lib.lib(), self.tr
         if x.shape != (self.n, self.d):
             raise ShapeError(f"EPStep is built for ({self.n}, {self.d}) inputs, got {tuple(x.shape)}")
-        _lib.check(L.cq_moe_route(ctypes.byref(self.desc), x.data_ptr(), _lib.dtype_code(x), self.n,
+        _lib.check(L.cq_moe_route(ctypes.byref(self.desc_route), x.data_ptr(), _lib.dtype_code(x), self.n,
                                   self.ws_route.data_ptr(), self.ws_route.numel(), _lib.stream()))
         cap = self.cap if self.sizing == "fixed" else 0
         for m, (lo, hi) in enumerate(self.bounds):
