@@ -500,7 +500,109 @@ static void launch_chain(int eg, dim3 grid, size_t smem, cudaStream_t st, const 
         launch_pdl(router_chain_kernel<8, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
 }
 
-static int chain_mode() {  // CQ_ROUTER_CHAIN: 0 off, 1 chain kernel, 2 chain kernel without the fused tail
+// Decode router, one chain per thread (v2).  A CTA holds tt tokens x EGc experts (thread t:
+// token t / EGc, expert e0 + t % EGc; tt sized so the grid is about one CTA per SM).  W chunks
+// [RV_K][EGc] and x chunks [tt][RV_K] are staged by cp.async through an RV_NR-deep ring (W leaves
+// L2 under the expert weight stream, so chunks come from DRAM: several are kept in flight); every
+// thread then walks its chain through the chunk: per 4 columns one LDS.128 of x (shared by the EGc
+// lanes of a token), 4 LDS.32 of W (consecutive experts, conflict-free), 4 FMUL and the 4 dependent
+// FADDs — the FADD latency is the critical path, and no product buffer is written or synchronised.
+// Summation order and rounding as router_deq_kernel (bit-exact): acc = ((0 + x0 w0) + x1 w1) + ...
+constexpr int RV_K = 256, RV_NR = 3;
+template <int EGc, bool FUSE>
+__global__ void __launch_bounds__(128) router_chain2_kernel(const float *__restrict__ xdeq,
+                                                            const float *__restrict__ w, int64_t n, int64_t d,
+                                                            int64_t n_exp, int tt, float *__restrict__ logits,
+                                                            RouteFuse f) {
+    griddep_wait();
+    constexpr int WP = EGc, XP = RV_K + 4;  // pitches (floats)
+    extern __shared__ __align__(16) float rvs[];
+    const int stage_f = RV_K * WP + tt * XP;  // floats per ring stage: W [RV_K][WP] then x [tt][XP]
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int tl = tid / EGc, el = tid % EGc;
+    const bool chain = tl < tt;
+    const int64_t t0 = blockIdx.x * (int64_t)tt;
+    const int64_t e0 = blockIdx.y * (int64_t)EGc;
+    const int n_chunks = (int)((d + RV_K - 1) / RV_K);
+    auto stage = [&](int i) {
+        if (i < n_chunks) {
+            const int64_t k0 = (int64_t)i * RV_K;
+            const int kn = (int)((d - k0) < RV_K ? (d - k0) : RV_K);
+            float *wb = rvs + (i % RV_NR) * stage_f;
+            for (int x = tid; x < kn * (EGc / 4); x += nthr) {
+                const int r = x / (EGc / 4), q = x - r * (EGc / 4);
+                cp_async16(wb + r * WP + 4 * q, w + (k0 + r) * n_exp + e0 + 4 * q);
+            }
+            float *xb = wb + RV_K * WP;
+            for (int x = tid; x < tt * (kn / 4); x += nthr) {
+                const int t = x / (kn / 4), v = x - t * (kn / 4);
+                const int64_t tg = t0 + t < n ? t0 + t : n - 1;  // rows past n are never stored
+                cp_async16(xb + t * XP + 4 * v, xdeq + tg * d + k0 + 4 * v);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int i = 0; i < RV_NR - 1; ++i) stage(i);
+    float acc = 0.0f;
+    for (int i = 0; i < n_chunks; ++i) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(RV_NR - 2) : "memory");
+        __syncthreads();  // chunk i landed for every thread; chunk i - 1's stage is free
+        stage(i + RV_NR - 1);
+        if (chain) {
+            const int kn = (int)((d - (int64_t)i * RV_K) < RV_K ? (d - (int64_t)i * RV_K) : RV_K);  // % 16 == 0
+            const float *wb = rvs + (i % RV_NR) * stage_f + el;
+            const float4 *xr = reinterpret_cast<const float4 *>(rvs + (i % RV_NR) * stage_f + RV_K * WP + tl * XP);
+#pragma unroll 4
+            for (int j = 0; j < kn / 4; ++j) {
+                const float4 xv = xr[j];
+                const float w0 = wb[(4 * j + 0) * WP], w1 = wb[(4 * j + 1) * WP];
+                const float w2 = wb[(4 * j + 2) * WP], w3 = wb[(4 * j + 3) * WP];
+                acc = __fadd_rn(acc, __fmul_rn(xv.x, w0));
+                acc = __fadd_rn(acc, __fmul_rn(xv.y, w1));
+                acc = __fadd_rn(acc, __fmul_rn(xv.z, w2));
+                acc = __fadd_rn(acc, __fmul_rn(xv.w, w3));
+            }
+        }
+    }
+    if (chain && t0 + tl < n) logits[(t0 + tl) * n_exp + e0 + el] = acc;
+    if constexpr (FUSE) {  // one expert group: the CTA's tokens' top-k from its logits
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        float *lg = rvs;   // [tt][EGc] (the ring is idle now)
+        if (chain) lg[tl * EGc + el] = acc;
+        __syncthreads();
+        const int warp = tid >> 5;
+        for (int t = warp; t < tt; t += nthr / 32)
+            if (t0 + t < n)
+                topk_token(lg + t * EGc, t0 + t, EGc, f.k, tid & 31, f.selected, f.weights, nullptr, 0, 0);
+    }
+}
+
+static size_t router_chain2_smem(int egc, int tt) {
+    return sizeof(float) * (size_t)RV_NR * ((size_t)RV_K * egc + (size_t)tt * (RV_K + 4));
+}
+
+template <bool FUSE>
+static void launch_chain2(int egc, int tt, dim3 grid, cudaStream_t st, const float *xdeq, const float *w, int64_t n,
+                          int64_t d, int64_t n_exp, float *logits, const RouteFuse &f) {
+    static std::atomic<uint64_t> attr{0};  // devices whose smem opt-in is set
+    if (first_on_device(attr)) {
+        cudaFuncSetAttribute(router_chain2_kernel<8, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(router_chain2_kernel<16, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(router_chain2_kernel<32, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    }
+    const size_t smem = router_chain2_smem(egc, tt);
+    const unsigned threads = (unsigned)ceil_div((int64_t)tt * egc, 32) * 32;
+    if (egc == 32)
+        launch_pdl(router_chain2_kernel<32, FUSE>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+    else if (egc == 16)
+        launch_pdl(router_chain2_kernel<16, FUSE>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+    else
+        launch_pdl(router_chain2_kernel<8, FUSE>, grid, threads, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+}
+
+static int chain_mode() {  // CQ_ROUTER_CHAIN: 0 off, 1 chain kernels, 2 without the fused tail, 3 v1 kernel only
     static int mode = -1;
     if (mode < 0) {
         const char *e = getenv("CQ_ROUTER_CHAIN");
@@ -517,6 +619,26 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
                          const RouteFuse *fuse, cudaStream_t st, bool *fused) {
     if (fused) *fused = false;
     if (xdeq == nullptr || d % 16 || n_exp % 8 || chain_mode() == 0) return false;
+    if (chain_mode() != 3 && n_exp % 32 == 0) {
+        // v2 (one chain per thread) for 32-expert groups: four tokens x 32 experts per CTA, every
+        // warp forms its own products (QW decode 64: 37 -> 18 us).  Smaller groups keep v1, whose
+        // producer warps feed one chain warp (v2 measured 2x slower there: one warp issues all).
+        const int egc = 32;
+        const int64_t groups = n_exp / egc;
+        const int tt = 4;
+        const int64_t ctas = ceil_div(n, tt) * groups;
+        if (ctas > 2 * 148 || router_chain2_smem(egc, tt) > 220 * 1024) return false;  // the tiled routers
+        const bool can_fuse = groups == 1 && chain_mode() == 1 && fuse != nullptr;
+        if (fuse != nullptr && !can_fuse) return false;  // the caller runs the separate kernels
+        const dim3 grid((unsigned)ceil_div(n, tt), (unsigned)groups);
+        if (can_fuse) {
+            launch_chain2<true>(egc, tt, grid, st, xdeq, w, n, d, n_exp, logits, *fuse);
+            *fused = true;
+        } else {
+            launch_chain2<false>(egc, tt, grid, st, xdeq, w, n, d, n_exp, logits, RouteFuse{});
+        }
+        return true;
+    }
     const int eg = n_exp % 32 == 0 ? 32 : (n_exp % 16 == 0 ? 16 : 8);
     const int64_t groups = n_exp / eg;
     const int tt = (int)std::min<int64_t>(32 / eg, std::max<int64_t>(1, ceil_div(n * groups, 148)));
