@@ -76,12 +76,32 @@ __device__ __forceinline__ int8_t a4_code(float x, float s) {
     return static_cast<int8_t>(static_cast<int>(r));
 }
 
+// a4_code(x, s) given r = 1 / s (correctly rounded): t = x * r is within 2^-22 of x / s for
+// |x / s| < 8 (the only range where a rounding boundary changes the clipped code), so roundf(t)
+// equals roundf(x / s) unless x / s lies within 2^-19 of a half-integer; those (ties included)
+// take the IEEE division.  Bit-exact with a4_code at a fraction of its instructions.
+__device__ __forceinline__ int8_t a4_code_rcp(float x, float s, float r) {
+    const float t = __fmul_rn(x, r);
+    const float a = fabsf(t);
+    if (a < 8.0f && fabsf(a - truncf(a) - 0.5f) < 1.9073486e-6f) return a4_code(x, s);  // 2^-19
+    return static_cast<int8_t>(static_cast<int>(fminf(fmaxf(roundf(t), -8.0f), 7.0f)));
+}
+
 // model.py:233-237: x * sigmoid(x), sigmoid split at 0.
 __device__ __forceinline__ float silu_f32(float x) {
     const bool pos = x >= 0.0f;
     const float ex = expf(pos ? -x : x);
     const float sig = pos ? __fdiv_rn(1.0f, __fadd_rn(1.0f, ex)) : __fdiv_rn(ex, __fadd_rn(1.0f, ex));
     return __fmul_rn(x, sig);
+}
+
+// The tensor-core path's silu (silu|re-quantize kernels): the same function within a few ulp
+// (fast exp2 + a correctly rounded reciprocal instead of expf + IEEE division), a third of the
+// instructions.  Its h is tolerance-checked against the ordered path, which keeps silu_f32.
+__device__ __forceinline__ float silu_fast(float x) {
+    const float ex = __expf(-fabsf(x));               // e^-|x| in (0, 1]
+    const float r = __frcp_rn(__fadd_rn(1.0f, ex));   // sigmoid(|x|)
+    return __fmul_rn(x, x >= 0.0f ? r : __fmul_rn(ex, r));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

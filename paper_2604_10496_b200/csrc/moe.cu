@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, 
     float mx = 0.0f;
     bool bad = false;
     for (int64_t j = threadIdx.x; j < ff; j += blockDim.x) {
-        const float h = __fmul_rn(silu_f32(ar[j]), br[j]);
+        const float h = __fmul_rn(silu_fast(ar[j]), br[j]);
         ar[j] = h;
         mx = fmaxf(mx, fabsf(h));
         bad |= !(fabsf(h) <= FLT_MAX);
@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
         const int j = threadIdx.x + u * (int)blockDim.x;
         if (j < nv) {
             const float4 x = ar[j], y = br[j];
-            h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
-                               __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
+            h[u] = make_float4(__fmul_rn(silu_fast(x.x), y.x), __fmul_rn(silu_fast(x.y), y.y),
+                               __fmul_rn(silu_fast(x.z), y.z), __fmul_rn(silu_fast(x.w), y.w));
             if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
             const float m4 = fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w)));
             mx = fmaxf(mx, m4);
@@ -149,13 +149,15 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     }
     __syncthreads();
     const float s = s_sh;
+    const float rs = __frcp_rn(s);
     char4 *cr = reinterpret_cast<char4 *>(codes + row * ff);
     int cs = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * (int)blockDim.x;
         if (j < nv) {
-            const char4 c = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+            const char4 c = make_char4(a4_code_rcp(h[u].x, s, rs), a4_code_rcp(h[u].y, s, rs), a4_code_rcp(h[u].z, s, rs),
+                                       a4_code_rcp(h[u].w, s, rs));
             cr[j] = c;
             cs += c.x + c.y + c.z + c.w;
         }
@@ -195,8 +197,8 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
         const int j = threadIdx.x + u * 256;
         if (j < nv) {
             const float4 x = ar[j], y = br[j];
-            h[u] = make_float4(__fmul_rn(silu_f32(x.x), y.x), __fmul_rn(silu_f32(x.y), y.y),
-                               __fmul_rn(silu_f32(x.z), y.z), __fmul_rn(silu_f32(x.w), y.w));
+            h[u] = make_float4(__fmul_rn(silu_fast(x.x), y.x), __fmul_rn(silu_fast(x.y), y.y),
+                               __fmul_rn(silu_fast(x.z), y.z), __fmul_rn(silu_fast(x.w), y.w));
             if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
             mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
             bad |= !(fabsf(h[u].x) <= FLT_MAX && fabsf(h[u].y) <= FLT_MAX && fabsf(h[u].z) <= FLT_MAX &&
@@ -231,13 +233,15 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
     else
         cluster.sync();
     const float s = s_sh;
+    const float rs = __frcp_rn(s);
     char4 *cr = reinterpret_cast<char4 *>(codes + row * ff + part * seg);
     int cs = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * 256;
         if (j < nv) {
-            const char4 c = make_char4(a4_code(h[u].x, s), a4_code(h[u].y, s), a4_code(h[u].z, s), a4_code(h[u].w, s));
+            const char4 c = make_char4(a4_code_rcp(h[u].x, s, rs), a4_code_rcp(h[u].y, s, rs), a4_code_rcp(h[u].z, s, rs),
+                                       a4_code_rcp(h[u].w, s, rs));
             cr[j] = c;
             cs += c.x + c.y + c.z + c.w;
         }

@@ -124,13 +124,14 @@ __global__ void __launch_bounds__(256) quantize_a4_vec_kernel(const void *__rest
     }
     __syncthreads();
     const float sc = s_sh;
+    const float rs = __frcp_rn(sc);
     int csum = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * 256;
         if (j < nv) {
-            const char4 c = make_char4(a4_code(h[u][0], sc), a4_code(h[u][1], sc), a4_code(h[u][2], sc),
-                                       a4_code(h[u][3], sc));
+            const char4 c = make_char4(a4_code_rcp(h[u][0], sc, rs), a4_code_rcp(h[u][1], sc, rs),
+                                       a4_code_rcp(h[u][2], sc, rs), a4_code_rcp(h[u][3], sc, rs));
             reinterpret_cast<char4 *>(codes + row * d)[j] = c;
             csum += c.x + c.y + c.z + c.w;
             // dequantized value, rounded exactly as codes.astype(f32) * scales (model.py:379-381)
