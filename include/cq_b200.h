@@ -154,6 +154,11 @@ enum { CQ_FLAG_KEEP_HIDDEN = 1 };
    selected, weights, tok_sums): no segment permutation or gathered codes (the
    expert-parallel driver plans its own rows). */
 enum { CQ_FLAG_SELECT_ONLY = 2 };
+/* CQ_FLAG_SHARED_MERGED: the tensor-core data of the shared experts (sh_gate/sh_up/sh_down)
+   directly follows the routed experts' in gate/up/down (tc_ids, tc_lut, tc_rowscale), so
+   cq_moe_forward runs them as extra segments of the routed grouped launches (all tokens each,
+   weight 1) instead of separate launches.  Same per-row arithmetic, same results. */
+enum { CQ_FLAG_SHARED_MERGED = 4 };
 
 enum { CQ_PATH_AUTO = 0, CQ_PATH_F32 = 1, CQ_PATH_TC = 2, CQ_PATH_ORDERED = 3 };
 

@@ -49,6 +49,7 @@ class MoEDesc(ctypes.Structure):
 
 FLAG_KEEP_HIDDEN = 1  # CQ_FLAG_KEEP_HIDDEN
 FLAG_SELECT_ONLY = 2  # CQ_FLAG_SELECT_ONLY
+FLAG_SHARED_MERGED = 4  # CQ_FLAG_SHARED_MERGED
 
 
 _SIGS = {

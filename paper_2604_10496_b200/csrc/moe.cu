@@ -394,7 +394,9 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     const int64_t d = dsc->d_model, ff = dsc->d_ff, E = dsc->n_experts, k = dsc->top_k;
     const int64_t R = n * k;
     const int64_t rows_sh = dsc->n_shared > 0 ? n : 0;
-    const int64_t Rh = R > rows_sh ? R : rows_sh;
+    // shared experts as extra segments of the routed launches: rows R + n_shared * n
+    const bool merged = (dsc->flags & CQ_FLAG_SHARED_MERGED) && dsc->n_shared > 0;
+    const int64_t Rh = merged ? R + dsc->n_shared * n : (R > rows_sh ? R : rows_sh);
     int64_t sz[CQ_WS_COUNT_] = {};
     sz[CQ_WS_CODES] = n * d;
     sz[CQ_WS_SCALES] = n * 4;
@@ -402,12 +404,12 @@ int64_t workspace_layout(const cq_moe_desc *dsc, int64_t n, int64_t *off) {
     sz[CQ_WS_SELECTED] = n * k * 4;
     sz[CQ_WS_WEIGHTS] = n * k * 4;
     sz[CQ_WS_COUNTS] = (E + 1) * 4;
-    sz[CQ_WS_OFFSETS] = (E + 2) * 4;
-    sz[CQ_WS_PERM_TOKEN] = R * 4;
+    sz[CQ_WS_OFFSETS] = (E + 2 + (merged ? dsc->n_shared : 0)) * 4;
+    sz[CQ_WS_PERM_TOKEN] = Rh * 4;
     sz[CQ_WS_PERM_SLOT] = R * 4;
     sz[CQ_WS_INV] = R * 4;
     sz[CQ_WS_CODES_PERM] = R * d;
-    sz[CQ_WS_SCALES_PERM] = R * 4;
+    sz[CQ_WS_SCALES_PERM] = Rh * 4;  // the B build writes one scale per expert row
     sz[CQ_WS_HIDDEN] = Rh * ff * 4 * 2;  // h (or gate output a) | up output b
     sz[CQ_WS_HCODES] = Rh * ff;
     sz[CQ_WS_HSCALES] = Rh * 4;
@@ -562,6 +564,19 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
                          down.group_size, fout, st);
     if (ev) cudaEventRecord(ev[3], st);
     return rc;
+}
+
+// Shared experts as segments E .. E + n_shared - 1 of the routed launch (CQ_FLAG_SHARED_MERGED):
+// every token, in order, after the R routed rows: perm[R + s*n + t] = t, offsets[E + 1 + s] =
+// R + (s + 1) * n (offsets[E] = R: every route is local in cq_moe_forward).
+__global__ void shared_segments_kernel(int32_t *perm, int32_t *offsets, int64_t n_exp, int64_t R, int64_t n,
+                                       int64_t n_shared) {
+    griddep_wait();  // PDL: inputs of the previous kernel are visible after this
+    const int64_t total = n_shared * n;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x)
+        perm[R + x] = (int32_t)(x % n);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int64_t sh = 0; sh < n_shared; ++sh) offsets[n_exp + 1 + sh] = (int32_t)(R + (sh + 1) * n);
 }
 
 __global__ void shared_offsets_kernel(int32_t *off, int64_t n_shared, int64_t n) {
@@ -775,11 +790,31 @@ extern "C" cq_status cq_moe_forward(const cq_moe_desc *desc, const void *x, int 
     // tcgen05 layouts: the expert stage's B build gathers the token rows itself (no codes_perm)
     const bool umma = path == CQ_PATH_TC;
     int deferred = 0;
-    CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma, umma ? &deferred : nullptr));
-    // builder-defined shared experts first: they read only the layer-input codes,
-    // and the routed pass after them leaves its own counts / hidden buffers for tracing
-    CQ_TRY(shared_experts(desc, path, n_tokens, w, w.shared, st));
+    const bool want_merged = umma && (desc->flags & CQ_FLAG_SHARED_MERGED) && desc->n_shared > 0;
+    // merged shared segments need the explicit permutation (not the B build's route mode)
+    CQ_TRY(route(desc, x, dtype, n_tokens, w, st, !umma, (umma && !want_merged) ? &deferred : nullptr));
+    const bool merged = want_merged && !deferred;
+    // builder-defined shared experts: extra segments of the routed launches when
+    // merged, else separate launches first (they read only the layer-input codes, and the routed pass
+    // after them leaves its own counts / hidden buffers for tracing)
+    if (!merged) CQ_TRY(shared_experts(desc, path, n_tokens, w, w.shared, st));
     const int64_t R = n_tokens * desc->top_k;
+    if (merged) {
+        const int64_t ns = desc->n_shared, total = ns * n_tokens;
+        launch_pdl(shared_segments_kernel, (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, st,
+                   w.perm_token, w.offsets, desc->n_experts, R, n_tokens, ns);
+        CQ_TRY(check_launch("shared_segments"));
+        UmmaIn in;
+        in.tok_sums = w.tok_sums;
+        in.scales_out = w.scales_perm;
+        in.perm = w.perm_token;
+        CQ_TRY(run_experts(desc, path, desc->gate, desc->up, desc->down, desc->n_experts + ns, 0, w.codes, w.scales,
+                           w.offsets, R + total, w.hidden, w.hcodes, w.hscales, w.fout, w.codes_frag, w.hcodes_frag,
+                           w.status + 1, st, nullptr, in));
+        // out = ((routed + sh_0) + sh_1) ..., the shared outputs are fout rows R + s * n + t
+        return combine_n(w.selected, w.weights, w.inv, w.fout, n_tokens, desc->top_k, desc->d_model,
+                         w.fout + R * desc->d_model, (int)ns, out, stream);
+    }
     if (umma) {
         UmmaIn in;
         in.tok_sums = w.tok_sums;

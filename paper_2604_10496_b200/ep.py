@@ -286,7 +286,9 @@ class EPStep:
         self.shared_out = (torch.empty((self.n_shared, self.n, self.d), dtype=torch.float32, **z)
                            if self.n_shared else None)
         offs = (ctypes.c_int64 * len(_lib.WS_NAMES))()   # expert-stage scratch, separate from routing's
-        size = L.cq_moe_workspace(ctypes.byref(self.desc), -(-routes_max // self.k), offs)
+        self.desc_exp = layer.desc()  # expert stage over received rows: shared experts run separately
+        self.desc_exp.flags &= ~_lib.FLAG_SHARED_MERGED
+        size = L.cq_moe_workspace(ctypes.byref(self.desc_exp), -(-routes_max // self.k), offs)
         self.ws_exp = torch.empty(max(size, 256), dtype=torch.uint8, **z)
         self.xchg = exchange or (lambda o, i, os_, is_: _exchange(o, i, os_, is_, group))
         self.comm = torch.cuda.Stream()
@@ -346,7 +348,7 @@ class EPStep:
                                  self.scales_perm.data_ptr(), self.offsets.data_ptr(), self.route_pos.data_ptr(),
                                  self.scratch.data_ptr(), _lib.stream()))
         if routes:
-            _lib.check(L.cq_moe_experts(ctypes.byref(self.desc), self.codes_perm.data_ptr(),
+            _lib.check(L.cq_moe_experts(ctypes.byref(self.desc_exp), self.codes_perm.data_ptr(),
                                         self.scales_perm.data_ptr(), self.offsets.data_ptr(), routes,
                                         self.fout.data_ptr(), self.ws_exp.data_ptr(), self.ws_exp.numel(),
                                         _lib.stream()))

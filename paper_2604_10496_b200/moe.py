@@ -19,6 +19,7 @@ segments; shared experts added with weight 1 after the routed sum.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -66,23 +67,26 @@ class ExpertStack:
     def n(self) -> int:
         return self.ids.shape[0]
 
-    def prepare_tc(self, planes: int, layout: str = "umma128u") -> None:
-        if self.tc is None or (self.tc["planes"], self.tc["layout"]) != (planes, layout):
+    def prepare_tc(self, planes: int, layout: str = "umma128u", out=None) -> None:
+        """out: (ids, lut, rowscale) destination views (a merged routed + shared buffer)."""
+        if out is not None or self.tc is None or (self.tc["planes"], self.tc["layout"]) != (planes, layout):
             rows = self.n * self.d_out
             self.tc = prepare_tc_site(self.ids.view(rows, -1), self.centroids.view(rows, -1, 16),
-                                      rows, self.d_in, self.group_size, planes, layout)
+                                      rows, self.d_in, self.group_size, planes, layout, out=out)
 
-    def site(self) -> _lib.ExpertSite:
+    def site(self, tc: dict | None = None) -> _lib.ExpertSite:
+        """tc: tensor-core data to describe instead of self.tc (a layer's merged copy)."""
         s = _lib.ExpertSite()
         s.ids = self.ids.data_ptr()
         s.centroids = self.centroids.data_ptr()
         s.group_size = self.group_size
-        if self.tc is not None:
-            s.tc_ids = self.tc["ids"].data_ptr()
-            s.tc_lut = self.tc["lut"].data_ptr()
-            s.tc_rowscale = self.tc["rowscale"].data_ptr()
-            s.tc_planes = self.tc["planes"]
-            s.tc_layout = _lib.TC_LAYOUTS[self.tc["kernel_layout"]]
+        tc = tc if tc is not None else self.tc
+        if tc is not None:
+            s.tc_ids = tc["ids"].data_ptr()
+            s.tc_lut = tc["lut"].data_ptr()
+            s.tc_rowscale = tc["rowscale"].data_ptr()
+            s.tc_planes = tc["planes"]
+            s.tc_layout = _lib.TC_LAYOUTS[tc["kernel_layout"]]
         return s
 
 
@@ -156,6 +160,7 @@ class MoELayer:
         self.exact_rotation = False
         self._ws = {}
         self._rot_tc = None  # R as three bf16 planes for the tensor-core rotation (prepare_tc)
+        self._sh_tc = None  # this layer's tensor-core copy of the shared experts (merged with the routed)
 
     # ------------------------------------------------------------------
     def tc_shapes_ok(self) -> bool:
@@ -168,11 +173,32 @@ class MoELayer:
         """tcgen05 layouts (unsigned base-128 digit planes): 3 planes where the
         output is re-quantized (gate, up), 2 for down."""
         sites = [(self.gate, planes_gate_up), (self.up, planes_gate_up), (self.down, planes_down)]
-        if self.shared is not None:
-            sites += [(self.shared[0], planes_gate_up), (self.shared[1], planes_gate_up),
-                      (self.shared[2], planes_down)]
-        for s, p in sites:
-            s.prepare_tc(p, layout)
+        if self._can_merge_shared():
+            # routed and shared experts of a site in one buffer (shared after the routed ones), so the
+            # forward runs the shared experts as extra segments of the routed grouped launches
+            # routed and shared experts of a site in one buffer (shared after the routed ones), so the
+            # forward runs the shared experts as extra segments of the routed grouped launches.  The
+            # shared stacks may be shared by several layers (EP shards): their copy is this layer's
+            # (self._sh_tc), never written into the stack
+            self._sh_tc = []
+            for (r, p), sh in zip(sites, self.shared):
+                rows_r, rows_s = r.n * r.d_out, sh.n * sh.d_out
+                ids = torch.empty((rows_r + rows_s, r.d_in // 2), dtype=torch.uint8, device="cuda")
+                lut = torch.empty((rows_r + rows_s, r.d_in // r.group_size, p, 16), dtype=torch.int8, device="cuda")
+                rs = torch.empty((rows_r + rows_s,), dtype=torch.float32, device="cuda")
+                r.prepare_tc(p, layout, out=(ids[:rows_r], lut[:rows_r], rs[:rows_r]))
+                tail = prepare_tc_site(sh.ids.view(rows_s, -1), sh.centroids.view(rows_s, -1, 16), rows_s, sh.d_in,
+                                       sh.group_size, p, layout, out=(ids[rows_r:], lut[rows_r:], rs[rows_r:]))
+                if r.tc["kernel_layout"] != tail["kernel_layout"]:  # one launch, one lookup kernel
+                    r.tc["kernel_layout"] = tail["kernel_layout"] = layout
+                self._sh_tc.append(tail)
+        else:
+            self._sh_tc = None
+            if self.shared is not None:
+                sites += [(self.shared[0], planes_gate_up), (self.shared[1], planes_gate_up),
+                          (self.shared[2], planes_down)]
+            for s, p in sites:
+                s.prepare_tc(p, layout)
         if self.rotation is not None and self.d_model % 256 == 0 and self._rot_tc is None:
             lib = _lib.lib()
             buf = torch.empty(lib.cq_rotation_prepared_bytes(self.d_model), dtype=torch.uint8, device="cuda")
@@ -181,6 +207,30 @@ class MoELayer:
             self._rot_tc = buf
             self._ws = {}
         return self
+
+    def _can_merge_shared(self) -> bool:
+        if self.shared is None:
+            return False
+        return all((sh.d_in, sh.d_out, sh.group_size) == (r.d_in, r.d_out, r.group_size)
+                   for r, sh in zip((self.gate, self.up, self.down), self.shared))
+
+    def shared_merged(self) -> bool:
+        """The shared experts' tensor-core data directly follows the routed experts' in every site
+        (prepare_tc of this layer), so cq_moe_forward may run them as extra segments."""
+        if not self._can_merge_shared():
+            return False
+        if self._sh_tc is None:
+            return False
+        for r, tail in zip((self.gate, self.up, self.down), self._sh_tc):
+            if r.tc is None:
+                return False
+            for key in ("ids", "lut", "rowscale"):
+                a, b = r.tc[key], tail[key]
+                if a.data_ptr() + a.numel() * a.element_size() != b.data_ptr():
+                    return False
+            if r.tc["kernel_layout"] != tail["kernel_layout"] or r.tc["planes"] != tail["planes"]:
+                return False
+        return True
 
     def desc(self, path: str | None = None) -> _lib.MoEDesc:
         d = _lib.MoEDesc()
@@ -191,18 +241,23 @@ class MoELayer:
         d.gate, d.up, d.down = self.gate.site(), self.up.site(), self.down.site()
         if self.shared is not None:
             d.n_shared = self.shared[0].n
-            d.sh_gate, d.sh_up, d.sh_down = (s.site() for s in self.shared)
+            sh_tc = self._sh_tc or (None, None, None)
+            d.sh_gate, d.sh_up, d.sh_down = (s.site(t) for s, t in zip(self.shared, sh_tc))
         d.path = _PATHS[path or self.path]
         d.flags = _lib.FLAG_KEEP_HIDDEN if self.keep_hidden else 0
+        # CQ_SHARED_MERGE=0: separate shared-expert launches (A/B measurement)
+        if ((path or self.path) in ("tc", "auto") and os.environ.get("CQ_SHARED_MERGE", "1") != "0"
+                and self.shared_merged()):
+            d.flags |= _lib.FLAG_SHARED_MERGED
         # the tensor-core rotation goes with the tensor-core path; f32 / ordered keep the fp32 rotation
         if self._rot_tc is not None and (path or self.path) in ("tc", "auto") and not self.exact_rotation:
             d.rotation_tc = self._rot_tc.data_ptr()
         return d
 
     def workspace(self, n: int, path: str | None = None):
-        key = (n, path or self.path, self.exact_rotation)
+        d = self.desc(path)
+        key = (n, path or self.path, self.exact_rotation, d.flags)  # the layout follows the flags
         if key not in self._ws:
-            d = self.desc(path)
             offs = (ctypes.c_int64 * len(_lib.WS_NAMES))()
             size = _lib.load_library().cq_moe_workspace(ctypes.byref(d), n, offs)
             buf = torch.empty(max(size, 256), dtype=torch.uint8, device="cuda")

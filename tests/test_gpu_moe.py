@@ -18,6 +18,7 @@ from paper_2604_10496_b200 import MoELayer  # noqa: E402
 from paper_2604_10496_b200.synthetic import (input_digest, moe_inputs_device,  # noqa: E402
                                              moe_inputs_host, to_device_experts)
 from paper_2604_10496_b200.moe import ExpertStack  # noqa: E402
+from paper_2604_10496_b200 import _lib  # noqa: E402
 
 LAYER_TOL = 1e-2
 
@@ -289,6 +290,23 @@ def test_many_expert_layers_tc_vs_oracle(cfg):
                                  shared=_host_experts(sh, n_sh, g) if n_sh else ())
     assert o.relative_error(ordered, want) <= 1e-6
     assert o.relative_error(out, want) <= LAYER_TOL
+
+
+@pytest.mark.parametrize("n", [1, 80, 300])
+def test_shared_experts_merged_segments(n, monkeypatch):
+    """DS-shaped layer: the shared experts as extra segments of the routed launches
+    (CQ_FLAG_SHARED_MERGED) give the same bits as their separate launches."""
+    d, ff, E, k, n_sh, g = 2048, 1408, 64, 6, 2, 128
+    v, w, sites, sh = moe_inputs_device(41, n, d, ff, E, g, n_shared=n_sh)
+    stacks = [ExpertStack(sites[s][0], sites[s][1], sites[s][2], sites[s][3], g) for s in ("gate", "up", "down")]
+    shared = tuple(ExpertStack(sh[s][0], sh[s][1], sh[s][2], sh[s][3], g) for s in ("gate", "up", "down"))
+    layer = MoELayer.from_stacks(w, *stacks, top_k=k, shared=shared, path="tc").prepare_tc()
+    assert layer.shared_merged() and layer.desc().flags & _lib.FLAG_SHARED_MERGED
+    merged = layer(v).cpu()
+    monkeypatch.setenv("CQ_SHARED_MERGE", "0")
+    assert not layer.desc().flags & _lib.FLAG_SHARED_MERGED
+    separate = layer(v).cpu()
+    assert torch.equal(merged, separate)
 
 
 def test_phi_prefill_rotation_tc_vs_oracle():
