@@ -45,7 +45,7 @@ int64_t rot_tc_act_bytes(int64_t n, int64_t d);
 const float *rot_tc_transposed(const void *prepared, int64_t d);
 cq_status rot_certify(const float *v, const void *x, int dtype, const float *Rt, int64_t n, int64_t d, int8_t *codes,
                       float *scales, int *nonfinite, float *deq, int32_t *tsum, int32_t *zero, int n_zero,
-                      int *recomputed, cudaStream_t st);
+                      int *recomputed, void *scratch, int64_t scratch_bytes, cudaStream_t st);
 cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const void *prepared, void *act, float *v,
                        cudaStream_t st);
 
@@ -616,7 +616,8 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
         // the reference's ordered chain bit for bit (rotq.cu; recomputed elements counted in status[2])
         CQ_TRY(rot_tc_apply(x, dtype, n, d, dsc->rotation_tc, w.rot_act, w.rotated, st));
         CQ_TRY(rot_certify(w.rotated, x, dtype, rot_tc_transposed(dsc->rotation_tc, d), n, d, w.codes, w.scales,
-                           w.status, w.fout, w.tok_sums, w.counts, (int)dsc->n_experts + 1, w.status + 2, st));
+                           w.status, w.fout, w.tok_sums, w.counts, (int)dsc->n_experts + 1, w.status + 2,
+                           w.rot_act, rot_tc_act_bytes(n, d), st));
     } else {
         const void *qin = x;
         int qdt = dtype;
