@@ -24,7 +24,8 @@ cq_status router_fused(const float *, const float *, int64_t, int64_t, int64_t, 
                        cudaStream_t, bool *);
 cq_status topk(const float *, int64_t, int64_t, int64_t, int32_t *, float *, int32_t *, int64_t, int64_t,
                cudaStream_t);
-cq_status permute(const int32_t *, const int32_t *, int64_t, int64_t, int64_t, int64_t, int32_t *,
+bool permute_counts_itself(int64_t n);
+cq_status permute(const int32_t *, int32_t *, int64_t, int64_t, int64_t, int64_t, int32_t *,
                   int32_t *, int32_t *, int32_t *, cudaStream_t);
 cq_status gather_rows(const int8_t *, const float *, const int32_t *, const int32_t *, int64_t, int64_t,
                       int64_t, int8_t *, float *, cudaStream_t);
@@ -643,7 +644,10 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
         }
     }
     CQ_TRY(router_logits(w.codes, w.scales, w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, st));
-    CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, w.counts, dsc->expert_begin,
+    // the permutation counts the routes itself (no atomics in the top-k) unless routing stops at the top-k
+    const bool perm_counts = !(dsc->flags & CQ_FLAG_SELECT_ONLY) && permute_counts_itself(n);
+    CQ_TRY(topk(w.logits, n, dsc->n_experts, dsc->top_k, w.selected, w.weights, perm_counts ? nullptr : w.counts,
+                dsc->expert_begin,
                 dsc->n_local_experts, st));
     if (dsc->flags & CQ_FLAG_SELECT_ONLY) return CQ_OK;
     CQ_TRY(permute(w.selected, w.counts, n, dsc->top_k, dsc->expert_begin, dsc->n_local_experts, w.offsets,

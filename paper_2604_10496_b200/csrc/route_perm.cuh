@@ -41,10 +41,11 @@ __device__ __forceinline__ float np_sum(const float *v, int n) {
 // selected logits and counts the routes of the local expert range.
 // `row`: the token's n_exp logits, global or shared memory; weights and counts
 // are nullable.
+// PER: logits per lane (n_exp <= 32 PER).
+template <int PER = 8>
 __device__ __forceinline__ void topk_token(const float *row, int64_t t, int64_t n_exp, int64_t k, int lane,
                                            int32_t *__restrict__ selected, float *__restrict__ weights,
                                            int32_t *__restrict__ counts, int64_t local_begin, int64_t n_local) {
-    constexpr int PER = 256 / 32;  // <= 256 experts
     float lv[PER];
     uint32_t taken = 0;
 #pragma unroll
@@ -53,8 +54,9 @@ __device__ __forceinline__ void topk_token(const float *row, int64_t t, int64_t 
         lv[i] = e < n_exp ? row[e] : 0.0f;
         if (e >= n_exp) taken |= 1u << i;
     }
-    int sel[MAX_TOPK];
-    float val[MAX_TOPK];
+    // round s's winner is kept by lane s (registers, no local-memory arrays)
+    int my_sel = -1;
+    float my_val = 0.0f;
     for (int s = 0; s < k; ++s) {
         int best = -1;
         float bv = 0.0f;
@@ -73,19 +75,35 @@ __device__ __forceinline__ void topk_token(const float *row, int64_t t, int64_t 
                 bv = ov;
             }
         }
-        sel[s] = best;
-        val[s] = bv;
+        if (lane == s) {
+            my_sel = best;
+            my_val = bv;
+        }
         if ((best & 31) == lane) taken |= 1u << (best >> 5);
     }
-    if (lane != 0) return;
-    const float m = val[0];  // max of the selected logits
-    float ex[MAX_TOPK];
-    for (int s = 0; s < k; ++s) ex[s] = expf(__fsub_rn(val[s], m));
-    const float tot = np_sum(ex, (int)k);
-    for (int s = 0; s < k; ++s) {
-        selected[t * k + s] = sel[s];
-        if (weights != nullptr) weights[t * k + s] = __fdiv_rn(ex[s], tot);
-        const int64_t le = sel[s] - local_begin;
+    // softmax over the selected logits, one lane per route; the sum is np_sum's order exactly
+    const float m = __shfl_sync(0xffffffffu, my_val, 0);  // max of the selected logits
+    const float ex = lane < k ? expf(__fsub_rn(my_val, m)) : 0.0f;
+    float tot;
+    if (k < 8) {
+        tot = 0.0f;  // numpy starts from the first element; 0 + x == x exactly
+        for (int i = 0; i < k; ++i) tot = __fadd_rn(tot, __shfl_sync(0xffffffffu, ex, i));
+    } else {
+        float r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __shfl_sync(0xffffffffu, ex, j);
+        int i = 8;
+        for (; i + 8 <= k; i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], __shfl_sync(0xffffffffu, ex, i + j));
+        tot = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+        for (; i < k; ++i) tot = __fadd_rn(tot, __shfl_sync(0xffffffffu, ex, i));
+    }
+    if (lane < k) {
+        selected[t * k + lane] = my_sel;
+        if (weights != nullptr) weights[t * k + lane] = __fdiv_rn(ex, tot);
+        const int64_t le = my_sel - local_begin;
         if (counts != nullptr && le >= 0 && le < n_local) atomicAdd(counts + le, 1);
     }
 }
