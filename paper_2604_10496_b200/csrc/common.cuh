@@ -98,6 +98,17 @@ __device__ __forceinline__ float silu_f32(float x) {
 // The tensor-core path's silu (silu|re-quantize kernels): the same function within a few ulp
 // (fast exp2 + a correctly rounded reciprocal instead of expf + IEEE division), a third of the
 // instructions.  Its h is tolerance-checked against the ordered path, which keeps silu_f32.
+// Two IEEE-rounded fp32 products in one FMUL2 (sm_100): (a0 * b0, a1 * b1), each rounded like
+// __fmul_rn.  The adds that consume them stay scalar __fadd_rn: ptxas keeps FMUL2 + FADD apart
+// (a packed multiply-add pair would be contracted into FFMA2, one rounding).
+__device__ __forceinline__ void fmul2_rn(float a0, float a1, float b0, float b1, float &c0, float &c1) {
+    uint64_t a, b, c;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(c) : "l"(a), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
+}
+
 __device__ __forceinline__ float silu_fast(float x) {
     const float ex = __expf(-fabsf(x));               // e^-|x| in (0, 1]
     const float r = __frcp_rn(__fadd_rn(1.0f, ex));   // sigmoid(|x|)

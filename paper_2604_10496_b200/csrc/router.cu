@@ -211,10 +211,13 @@ __global__ void __launch_bounds__(256) router_tile_kernel(const float *__restric
                 const float xq[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    acc[i][0] = __fadd_rn(acc[i][0], __fmul_rn(xq[q], wv[q].x));
-                    acc[i][1] = __fadd_rn(acc[i][1], __fmul_rn(xq[q], wv[q].y));
-                    acc[i][2] = __fadd_rn(acc[i][2], __fmul_rn(xq[q], wv[q].z));
-                    acc[i][3] = __fadd_rn(acc[i][3], __fmul_rn(xq[q], wv[q].w));
+                    float p0, p1, p2, p3;  // x broadcast against expert pairs: two FMUL2 per 4 products
+                    fmul2_rn(xq[q], xq[q], wv[q].x, wv[q].y, p0, p1);
+                    fmul2_rn(xq[q], xq[q], wv[q].z, wv[q].w, p2, p3);
+                    acc[i][0] = __fadd_rn(acc[i][0], p0);
+                    acc[i][1] = __fadd_rn(acc[i][1], p1);
+                    acc[i][2] = __fadd_rn(acc[i][2], p2);
+                    acc[i][3] = __fadd_rn(acc[i][3], p3);
                 }
             }
         }
@@ -553,7 +556,12 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
             for (int t = 0; t < tt; ++t) {
                 const float xv = xb[t * KC + j];
 #pragma unroll
-                for (int e = 0; e < EG; ++e) pb[(t * EG + e) * PITCH + j] = __fmul_rn(xv, wr[e]);
+                for (int e = 0; e < EG; e += 2) {
+                    float p0, p1;
+                    fmul2_rn(xv, xv, wr[e], wr[e + 1], p0, p1);
+                    pb[(t * EG + e) * PITCH + j] = p0;
+                    pb[(t * EG + e + 1) * PITCH + j] = p1;
+                }
             }
         }
     };
@@ -698,10 +706,10 @@ __global__ void __launch_bounds__(128) router_chain2_kernel(const float *__restr
                 const float4 xv = xr[j];
                 const float w0 = wb[(4 * j + 0) * WP], w1 = wb[(4 * j + 1) * WP];
                 const float w2 = wb[(4 * j + 2) * WP], w3 = wb[(4 * j + 3) * WP];
-                acc = __fadd_rn(acc, __fmul_rn(xv.x, w0));
-                acc = __fadd_rn(acc, __fmul_rn(xv.y, w1));
-                acc = __fadd_rn(acc, __fmul_rn(xv.z, w2));
-                acc = __fadd_rn(acc, __fmul_rn(xv.w, w3));
+                float p0, p1, p2, p3;
+                fmul2_rn(xv.x, xv.y, w0, w1, p0, p1);
+                fmul2_rn(xv.z, xv.w, w2, w3, p2, p3);
+                acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, p0), p1), p2), p3);
             }
         }
     }
