@@ -195,7 +195,25 @@ struct UmmaIn {
     float *scales_out = nullptr;        // gather / route: scales[perm[r]] lands here; the GEMM reads it
     bool sums_ready = false;            // otherwise: the row sums are already in the B buffer
     RoutePerm route;                    // route mode (implies the gather)
+    bool b_ready = false;               // the B operand (tiles, row sums, zeroed counters) is built already
     bool gathers() const { return perm != nullptr || route.on(); }
+};
+
+// Where a re-quantizer writes its codes directly in the tcgen05 GEMM's B layout
+// ([chunk CK][tile8][kstep][khalf][8 rows][16 B], lut_umma.cu's to_umma_b) and
+// the counters that B build would have zeroed.  dst == nullptr: not used.
+struct UmmaBOut {
+    int8_t *dst = nullptr;
+    int64_t tiles = 0;
+    int ck = 128;
+    int32_t *zero = nullptr;
+    int n_zero = 0;
+    // byte offset of codes (row, col .. col + 3), col % 4 == 0
+    __device__ __forceinline__ int64_t off(int64_t row, int64_t col) const {
+        const int64_t c = col / ck, r = col - c * ck;
+        return ((((c * tiles + (row >> 3)) * (ck >> 5) + (r >> 5)) * 2 + ((r >> 4) & 1)) * 8 + (row & 7)) * 16 +
+               (r & 15);
+    }
 };
 
 // launch_pdl with a thread-block cluster of cluster_x CTAs along x.

@@ -957,7 +957,9 @@ cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, c
     int32_t *sums = reinterpret_cast<int32_t *>(bbuf + umma_sums_off(rows, d_in));
     int32_t *part = reinterpret_cast<int32_t *>(bbuf + umma_part_off(rows, d_in));
     int32_t *cnt = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
-    CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), in, scales, offsets + n_seg, st));
+    if (!in.b_ready)  // else the re-quantizer wrote the tiles, the row sums and zeroed cnt (umma_b_out)
+        CQ_TRY(to_umma_b<GEO::CK>(codes, rows, d_in, tiles, bbuf, sums, cnt, umma_grid(), in, scales, offsets + n_seg,
+                                  st));
     if (in.gathers()) scales = in.scales_out;  // per segment row from here on
 #define CQ_UMMA(P_, N_)                                                                                        \
     launch_umma<P_, GEO, N_>(bbuf, tiles, scales, sums, offsets, n_seg, seg_first, a, out_a, b, out_b, d_in, d_out, \
@@ -972,6 +974,28 @@ cq_status lut_umma_geo(const int8_t *codes, int8_t *bbuf, const float *scales, c
 #undef CQ_UMMA
     set_error("tcgen05 path: planes must be 2 or 3");
     return CQ_ERR_CONFIG;
+}
+
+// The geometry of a grouped launch, as its chunk width: prefill (128-token passes, merged layout
+// only) when segments are long.  CQ_UMMA_GEOMETRY=prefill|decode forces one (tests; prefill needs
+// rows >= 64 for its scratch).
+int umma_geo_ck(int64_t rows, int64_t n_seg, int64_t d_in, int64_t d_out, int mats) {
+    const char *geo = getenv("CQ_UMMA_GEOMETRY");
+    const bool force_pf = geo != nullptr && geo[0] == 'p' && rows >= 64;
+    const bool force_dc = (geo != nullptr && geo[0] == 'd') || getenv("CQ_UMMA_NO_PREFILL") != nullptr;
+    return !force_dc && (force_pf || umma_prefill(rows, n_seg, d_in, d_out, mats)) ? UmPrefill::CK : UmDecode::CK;
+}
+
+// Where a producer of B codes writes them so the grouped launch over (rows, d_in) skips its B
+// build (UmmaIn::b_ready): the tile layout for chunk width ck, and the split-unit counters to zero.
+UmmaBOut umma_b_out(int8_t *bbuf, int64_t rows, int64_t d_in, int ck) {
+    UmmaBOut o;
+    o.dst = bbuf;
+    o.tiles = umma_b_tiles(rows);
+    o.ck = ck;
+    o.zero = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
+    o.n_zero = umma_grid();
+    return o;
 }
 
 // Grouped tcgen05 LUT GEMM over segments.  `bbuf` holds umma_b_bytes(rows,
@@ -999,12 +1023,7 @@ cq_status lut_umma_grouped(const int8_t *codes, int8_t *bbuf, const float *scale
         set_error("tcgen05 path: at most 512 segments (experts) per launch");
         return CQ_ERR_UNSUPPORTED;
     }
-    // prefill geometry (128-token passes, merged layout only) when segments are long
-    // CQ_UMMA_GEOMETRY=prefill|decode forces one (tests; prefill needs rows >= 64 for its scratch)
-    const char *geo = getenv("CQ_UMMA_GEOMETRY");
-    const bool force_pf = geo != nullptr && geo[0] == 'p' && rows >= 64;
-    const bool force_dc = (geo != nullptr && geo[0] == 'd') || getenv("CQ_UMMA_NO_PREFILL") != nullptr;
-    if (!force_dc && (force_pf || umma_prefill(rows, n_seg, d_in, d_out, b ? 2 : 1)))
+    if (umma_geo_ck(rows, n_seg, d_in, d_out, b ? 2 : 1) == UmPrefill::CK)
         return lut_umma_geo<UmPrefill>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b,
                                        d_in, d_out, in, st);
     return lut_umma_geo<UmDecode>(codes, bbuf, scales, offsets, n_seg, seg_first, rows, a, out_a, b, out_b, d_in,

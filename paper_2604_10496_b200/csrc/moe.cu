@@ -42,6 +42,8 @@ cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_
                            cudaStream_t, const UmmaIn &in = UmmaIn{});
 int64_t umma_b_bytes(int64_t rows, int64_t d_in);
 int32_t *umma_row_sums(int8_t *bbuf, int64_t rows, int64_t d_in);
+int umma_geo_ck(int64_t rows, int64_t n_seg, int64_t d_in, int64_t d_out, int mats);
+UmmaBOut umma_b_out(int8_t *bbuf, int64_t rows, int64_t d_in, int ck);
 int64_t rot_tc_act_bytes(int64_t n, int64_t d);
 const float *rot_tc_transposed(const void *prepared, int64_t d);
 cq_status rot_certify(const float *v, const void *x, int dtype, const float *Rt, int64_t n, int64_t d, int8_t *codes,
@@ -109,8 +111,10 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
                                                               float *__restrict__ scales,
                                                               const int32_t *__restrict__ live,
                                                               int32_t *__restrict__ sums, int keep,
-                                                              int *__restrict__ nonfinite) {
+                                                              int *__restrict__ nonfinite, UmmaBOut bo) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
+    if (blockIdx.x == 0 && bo.zero != nullptr)  // the counters the B build would have zeroed
+        for (int i = threadIdx.x; i < bo.n_zero; i += blockDim.x) bo.zero[i] = 0;
     const int64_t row = blockIdx.x;
     if (live != nullptr && row >= *live) return;
     float4 *ar = reinterpret_cast<float4 *>(a + row * ff);
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     __syncthreads();
     const float s = s_sh;
     const float rs = __frcp_rn(s);
-    char4 *cr = reinterpret_cast<char4 *>(codes + row * ff);
+    char4 *cr = codes != nullptr ? reinterpret_cast<char4 *>(codes + row * ff) : nullptr;
     int cs = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
@@ -159,7 +163,8 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
         if (j < nv) {
             const char4 c = make_char4(a4_code_rcp(h[u].x, s, rs), a4_code_rcp(h[u].y, s, rs), a4_code_rcp(h[u].z, s, rs),
                                        a4_code_rcp(h[u].w, s, rs));
-            cr[j] = c;
+            if (cr != nullptr) cr[j] = c;
+            if (bo.dst != nullptr) *reinterpret_cast<char4 *>(bo.dst + bo.off(row, 4 * (int64_t)j)) = c;
             cs += c.x + c.y + c.z + c.w;
         }
     }
@@ -179,9 +184,11 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
                                                              float *__restrict__ scales,
                                                              const int32_t *__restrict__ live,
                                                              int32_t *__restrict__ sums, int keep,
-                                                             int *__restrict__ nonfinite) {
+                                                             int *__restrict__ nonfinite, UmmaBOut bo) {
     namespace cg = cooperative_groups;
     griddep_wait();
+    if (blockIdx.x == 0 && bo.zero != nullptr)  // the counters the B build would have zeroed
+        for (int i = threadIdx.x; i < bo.n_zero; i += blockDim.x) bo.zero[i] = 0;
     const int64_t row = blockIdx.x / CL;
     if (live != nullptr && row >= *live) return;  // uniform over the cluster (one row)
     cg::cluster_group cluster = cg::this_cluster();
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
         cluster.sync();
     const float s = s_sh;
     const float rs = __frcp_rn(s);
-    char4 *cr = reinterpret_cast<char4 *>(codes + row * ff + part * seg);
+    char4 *cr = codes != nullptr ? reinterpret_cast<char4 *>(codes + row * ff + part * seg) : nullptr;
     int cs = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
@@ -243,7 +250,9 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
         if (j < nv) {
             const char4 c = make_char4(a4_code_rcp(h[u].x, s, rs), a4_code_rcp(h[u].y, s, rs), a4_code_rcp(h[u].z, s, rs),
                                        a4_code_rcp(h[u].w, s, rs));
-            cr[j] = c;
+            if (cr != nullptr) cr[j] = c;
+            if (bo.dst != nullptr)
+                *reinterpret_cast<char4 *>(bo.dst + bo.off(row, part * seg + 4 * (int64_t)j)) = c;
             cs += c.x + c.y + c.z + c.w;
         }
     }
@@ -257,17 +266,18 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
 
 template <int CL>
 static bool silu_quant_cluster(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                               const int32_t *live, int32_t *sums, int keep, int *nonfinite, cudaStream_t st) {
+                               const int32_t *live, int32_t *sums, int keep, int *nonfinite, const UmmaBOut &bo,
+                               cudaStream_t st) {
     if (ff % (4 * CL)) return false;
     const int64_t v = ceil_div(ff / CL / 4, 256);
     const dim3 grid((unsigned)(rows * CL));
     switch (v) {
-        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
-        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
+        case 1: launch_pdl_cluster(silu_quant_cl_kernel<1, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo); break;
+        case 2: launch_pdl_cluster(silu_quant_cl_kernel<2, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo); break;
         case 3:
-        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
+        case 4: launch_pdl_cluster(silu_quant_cl_kernel<4, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo); break;
         case 5: case 6: case 7:
-        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
+        case 8: launch_pdl_cluster(silu_quant_cl_kernel<8, CL>, grid, 256, 0, st, CL, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo); break;
         default: return false;
     }
     return true;
@@ -277,13 +287,18 @@ static int vec_threads(int64_t ff, int v) {
     return (int)std::min<int64_t>(512, ceil_div(ceil_div(ff / 4, v), 32) * 32);
 }
 
+// The vector / cluster re-quantizers (which can write the B layout) cover the row.
+static bool silu_b_ok(int64_t ff) { return ff % 4 == 0 && ceil_div(ff / 4, 512) <= 8; }
+
 // `live` (device, nullable): rows at or past *live are skipped (EP slot bounds).
 // sums (nullable): per-row code sums (the merged-layout GEMM's bias term).
 // keep: also store h = silu(a) * b over a (fp32, read only by tracing); else a
 // keeps the gate output and only the codes, scales and sums are written.
 // nonfinite (nullable): set to 1 when some h is inf / NaN (the down site's DivergenceError).
+// bo.dst: the codes go (also) straight into the down GEMM's B layout; codes may then be nullptr.
 cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t *codes, float *scales,
-                     const int32_t *live, cudaStream_t st, int32_t *sums, int keep, int *nonfinite) {
+                     const int32_t *live, cudaStream_t st, int32_t *sums, int keep, int *nonfinite,
+                     const UmmaBOut &bo = UmmaBOut{}) {
     if (rows == 0) return CQ_OK;
     static int cl_env = -1;
     if (cl_env < 0) {
@@ -292,10 +307,10 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
     }
     // about two CTAs per SM over the whole grid; long rows only (a cluster CTA keeps >= 256 float4)
     if (cl_env && ff >= 8192) {
-        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, st)) return check_launch("silu_quant");
-        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, st))
+        if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, bo, st)) return check_launch("silu_quant");
+        if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, bo, st))
             return check_launch("silu_quant");
-        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, st))
+        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, bo, st))
             return check_launch("silu_quant");
     }
     const int64_t v = ceil_div(ff / 4, 512);
@@ -303,14 +318,14 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
         switch (v) {
             case 1: {  // short rows: one float4 per thread, CTA sized to the row
                 const int thr = (int)std::max<int64_t>(64, ceil_div(ff / 4, 32) * 32);
-                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite);
+                launch_pdl(silu_quant_vec_kernel<1>, (unsigned)rows, thr, 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo);
                 break;
             }
             // CTA sized to the row at V float4 per thread (PH ff = 6400: 416 threads instead of 512)
-            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, vec_threads(ff, 2), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
+            case 2: launch_pdl(silu_quant_vec_kernel<2>, (unsigned)rows, vec_threads(ff, 2), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo); break;
             case 3:
-            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, vec_threads(ff, 4), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
-            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, vec_threads(ff, 8), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite); break;
+            case 4: launch_pdl(silu_quant_vec_kernel<4>, (unsigned)rows, vec_threads(ff, 4), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo); break;
+            default: launch_pdl(silu_quant_vec_kernel<8>, (unsigned)rows, vec_threads(ff, 8), 0, st, a, b, ff, codes, scales, live, sums, keep, nonfinite, bo); break;
         }
     } else {
         launch_pdl(silu_quant_kernel, (unsigned)rows, 256, 0, st, a, b, ff, codes, scales, live, sums, nonfinite);
@@ -529,12 +544,20 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
         CQ_TRY(lut_umma_grouped(codes, bbuf_in, scales, offsets, n_seg, seg_first, rows, &gate, hidden, &up, bout, d,
                                 ff, st, in));
         if (ev) cudaEventRecord(ev[1], st);
-        // the re-quantizer writes the down GEMM's row sums straight into its B buffer
+        // the re-quantizer writes the down GEMM's row sums straight into its B buffer, and (vector / cluster
+        // kernels) the codes in its tile layout: the down launch then has no B build.  The row-major codes
+        // only for tracing (CQ_FLAG_KEEP_HIDDEN).
         UmmaIn hin;
         hin.sums_ready = true;
         int32_t *hsums = umma_row_sums(bbuf_h, rows, ff);
         const int keep = (dsc->flags & CQ_FLAG_KEEP_HIDDEN) != 0;
-        CQ_TRY(silu_quant(hidden, bout, rows, ff, hcodes, hscales, offsets + n_seg, st, hsums, keep, nonfinite));
+        UmmaBOut bo;
+        if (silu_b_ok(ff)) {
+            bo = umma_b_out(bbuf_h, rows, ff, umma_geo_ck(rows, n_seg, ff, d, 1));
+            hin.b_ready = true;
+        }
+        CQ_TRY(silu_quant(hidden, bout, rows, ff, (keep || !hin.b_ready) ? hcodes : nullptr, hscales, offsets + n_seg,
+                          st, hsums, keep, nonfinite, bo));
         if (ev) cudaEventRecord(ev[2], st);
         CQ_TRY(lut_umma_grouped(hcodes, bbuf_h, hscales, offsets, n_seg, seg_first, rows, &down, fout, nullptr,
                                 nullptr, ff, d, st, hin));

@@ -321,7 +321,9 @@ class MoELayer:
     def trace(self, n: int, path: str | None = None) -> dict:
         """Views of the workspace buffers of the last forward over n tokens.
         "hidden" is h = silu(a) * b on the tensor-core path only with
-        `keep_hidden` set before that forward (else the gate output)."""
+        `keep_hidden` set before that forward (else the gate output), and
+        "hcodes" (row-major) likewise: without it the re-quantizer writes the
+        codes only into the down GEMM's operand tiles."""
         buf, offs = self.workspace(n, path)
         k, d, ff, E, R = self.top_k, self.d_model, self.d_ff, self.n_experts, n * self.top_k
         spec = {"codes": (torch.int8, (n, d)), "scales": (torch.float32, (n,)),
