@@ -146,9 +146,10 @@ typedef struct {
 } cq_moe_desc;
 
 /* CQ_FLAG_KEEP_HIDDEN: the tensor-core path also stores h = silu(a) * b in
-   CQ_WS_HIDDEN (fp32, for tracing / parity checks).  Without it the expert stage
-   writes only the re-quantized h (codes, scales), and CQ_WS_HIDDEN holds the
-   gate output; the f32 and ordered paths always store h. */
+   CQ_WS_HIDDEN (fp32) and its codes row-major in CQ_WS_HCODES (for tracing / parity
+   checks).  Without it the expert stage writes the re-quantized h only into the down
+   GEMM's operand tiles (CQ_WS_HCODES_FRAG) and CQ_WS_HSCALES, and CQ_WS_HIDDEN holds the
+   gate output; the f32 and ordered paths always store h and its codes. */
 enum { CQ_FLAG_KEEP_HIDDEN = 1 };
 /* CQ_FLAG_SELECT_ONLY: cq_moe_route stops after the top-k (codes, scales, logits,
    selected, weights, tok_sums): no segment permutation or gathered codes (the
