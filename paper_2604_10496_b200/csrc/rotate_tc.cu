@@ -140,11 +140,12 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t *v) {
 template <int NPA>
 __global__ void __launch_bounds__(rt::THREADS, 1) rot_gemm_kernel(const uint8_t *__restrict__ xa, int64_t a_tiles,
                                                                    const uint8_t *__restrict__ rb, int64_t d,
-                                                                   int64_t n, float *__restrict__ v) {
+                                                                   int64_t n, float *__restrict__ v, int npair) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     // (activation plane, R plane) products, largest first: x R0, x R1, x R2 for a bf16 x; for an
-    // fp32 x the six terms of relative size >= 2^-16 (x0R0, x0R1, x1R0, x0R2, x1R1, x2R0)
-    constexpr int NPAIR = NPA == 1 ? 3 : 6;
+    // fp32 x the six terms of relative size >= 2^-16 (x0R0, x0R1, x1R0, x0R2, x1R1, x2R0).
+    // npair: the leading pairs used (a bf16 x with npair = 2: R to 16 significand bits)
+    const int NPAIR = npair;
     constexpr int PA1[3] = {0, 0, 0}, PB1[3] = {0, 1, 2};
     constexpr int PA3[6] = {0, 0, 1, 0, 1, 2}, PB3[6] = {0, 1, 0, 2, 1, 0};
     const int *PA = NPA == 1 ? PA1 : PA3, *PB = NPA == 1 ? PB1 : PB3;
@@ -235,6 +236,20 @@ __global__ void __launch_bounds__(rt::THREADS, 1) rot_gemm_kernel(const uint8_t 
 
 bool rot_tc_ok(int64_t d) { return d % rt::BN == 0 && d % rt::KC == 0; }
 
+// R planes the bf16-activation rotation uses: 2 (R to 16 significand bits, the default) or 3 (R
+// exact; CQ_ROT_PLANES=3).  Against the reference's ordered chain the 2-plane form is the more
+// accurate one: its truncation (2^-17 relative per product) is far below the fp32 rounding of the
+// TMEM accumulation, which it does over 2d instead of 3d products (tools/rot_err.py, PH, 3 seeds:
+// max 2.07e-5 vs 2.55e-5 of the row max; the certified quantizer's band is 1.5e-4).
+static int rot_planes() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CQ_ROT_PLANES");
+        v = (e != nullptr && atoi(e) == 3) ? 3 : 2;
+    }
+    return v;
+}
+
 // prepared = [three bf16 planes of R^T in the UMMA layout: 3 d^2 * 2 B][R^T f32: d^2 * 4 B (the certified
 // quantizer's ordered chains, rotq.cu)]
 int64_t rot_tc_prepared_bytes(int64_t d) { return 3 * d * d * 2 + d * d * 4; }
@@ -275,9 +290,9 @@ cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const voi
     const dim3 grid((unsigned)(d / rt::BN), (unsigned)ceil_div(n, rt::BM));
     const uint8_t *a = reinterpret_cast<const uint8_t *>(act), *b = reinterpret_cast<const uint8_t *>(prepared);
     if (dtype == CQ_DTYPE_BF16)
-        launch_pdl(rot_gemm_kernel<1>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v);
+        launch_pdl(rot_gemm_kernel<1>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v, rot_planes());
     else
-        launch_pdl(rot_gemm_kernel<3>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v);
+        launch_pdl(rot_gemm_kernel<3>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v, 6);
     return check_launch("rotation_gemm");
 }
 
