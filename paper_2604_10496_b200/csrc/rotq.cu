@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) rq_pick_kernel(const float *__r
 #define RC_K_ 32
 #endif
 #ifndef RC_S_
-#define RC_S_ 3
+#define RC_S_ 4
 #endif
 constexpr int RC_K = RC_K_;  // chain steps (columns of x / R^T) per stage
 constexpr int RC_S = RC_S_;  // ring stages
@@ -531,12 +531,26 @@ __global__ void __launch_bounds__(RcCfg<DT>::WPC * 32) rq_chain_kernel(const voi
             const int32_t task = act ? sc.bucket[(int64_t)j * sc.cap + r0 + hl] : 0;
             const int64_t row = task >> 8;
             const uint8_t *xg = reinterpret_cast<const uint8_t *>(x) + row * d * C::XB;
+            // the warp loads its rows' x chunks cooperatively: piece i of this lane is piece q of row r
+            // (XCH consecutive lanes per row), so a copy instruction touches 32 / XCH rows instead of 32
+            // scattered 16-byte pieces (the L1 tag lookups of scattered pieces bound the kernel)
+            const uint8_t *xsrc[XCH];
+            int xdst[XCH];
+            bool xok[XCH];
+#pragma unroll
+            for (int i = 0; i < XCH; ++i) {
+                const int pc = lane + 32 * i, r = pc / XCH, q = pc - r * XCH;
+                const uint64_t rp = __shfl_sync(0xffffffffu, (uint64_t)xg, r);
+                xok[i] = __shfl_sync(0xffffffffu, (int)act, r) != 0;
+                xsrc[i] = reinterpret_cast<const uint8_t *>(rp) + q * 16;
+                xdst[i] = r * C::XLS + q * 16;
+            }
             auto issue = [&](int64_t g) {
                 if (g < nst) {
                     uint8_t *st = ring + (g % RC_S) * C::STAGE;
-                    if (act)
 #pragma unroll
-                        for (int q = 0; q < XCH; ++q) rc_cp16(st + lane * C::XLS + q * 16, xg + g * RC_K * C::XB + q * 16);
+                    for (int i = 0; i < XCH; ++i)
+                        if (xok[i]) rc_cp16(st + xdst[i], xsrc[i] + g * RC_K * C::XB);
                     if (uvalid && hl < RC_K / 4)
                         rc_cp16(st + 32 * C::XLS + half * RC_K * 4 + hl * 16, rg + g * RC_K + hl * 4);
                 }
