@@ -94,6 +94,8 @@ __device__ __forceinline__ int rq_collect(const float4 *v4, int64_t nv, int lane
             if (j < nv)
                 m = (pick(a[r].x) ? 1u : 0u) | (pick(a[r].y) ? 2u : 0u) | (pick(a[r].z) ? 4u : 0u) |
                     (pick(a[r].w) ? 8u : 0u);
+            const unsigned any = __ballot_sync(0xffffffffu, m != 0);
+            if (any == 0) continue;  // the common case: nothing picked in these 128 elements
             const int mine = __popc(m);
             int incl = mine;
 #pragma unroll
@@ -170,49 +172,28 @@ __device__ void rq_finish_fast(const float *__restrict__ v, int64_t row, int64_t
     if (lane == 0) scales[row] = sc;
     int8_t *crow = codes + row * d;
     float4 *drow = deq != nullptr ? reinterpret_cast<float4 *>(deq + row * d) : nullptr;
-    int csum = 0, seen = 0;
-    for (int64_t b0 = 0; b0 < nv; b0 += 32 * RQ_RB) {
-      float4 ab[RQ_RB];  // loads first (RQ_RB in flight), then the warp-synchronous passes
-#pragma unroll
-      for (int r = 0; r < RQ_RB; ++r) {
-          const int64_t jj = b0 + r * 32 + lane;
-          ab[r] = jj < nv ? v4[jj] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      }
-#pragma unroll
-      for (int r = 0; r < RQ_RB; ++r) {
-        const int64_t j = b0 + r * 32 + lane;
-        int8_t c[4] = {0, 0, 0, 0};
-        unsigned m = 0;
-        if (j < nv) {
-            const float4 a = ab[r];
-            const float av[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                m |= rr.picked(av[e]) ? 1u << e : 0u;
-                c[e] = (int8_t)rq_code_t(av[e] * rc);  // settled: equals a4_code(av[e], sc)
-            }
-        }
-        const int mine = __popc(m);
-        int incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        int pos = seen + incl - mine;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (m >> e & 1u) c[e] = a4_code(val[pos++], sc);
-        seen += __shfl_sync(0xffffffffu, incl, 31);
-        if (j < nv) {
-            reinterpret_cast<char4 *>(crow)[j] = make_char4(c[0], c[1], c[2], c[3]);
-            csum += c[0] + c[1] + c[2] + c[3];
-            // dequantized value, rounded exactly as codes.astype(f32) * scales (model.py:379-381)
-            if (drow != nullptr)
-                drow[j] = make_float4(__fmul_rn((float)c[0], sc), __fmul_rn((float)c[1], sc),
-                                      __fmul_rn((float)c[2], sc), __fmul_rn((float)c[3], sc));
-        }
-      }
+    int csum = 0;
+    // 1. every element with the settled formula (no band test, no scan) ...
+#pragma unroll 4
+    for (int64_t j = lane; j < nv; j += 32) {
+        const float4 a = v4[j];
+        const int8_t c0 = (int8_t)rq_code_t(a.x * rc), c1 = (int8_t)rq_code_t(a.y * rc);
+        const int8_t c2 = (int8_t)rq_code_t(a.z * rc), c3 = (int8_t)rq_code_t(a.w * rc);
+        reinterpret_cast<char4 *>(crow)[j] = make_char4(c0, c1, c2, c3);
+        csum += c0 + c1 + c2 + c3;
+        // dequantized value, rounded exactly as codes.astype(f32) * scales (model.py:379-381)
+        if (drow != nullptr)
+            drow[j] = make_float4(__fmul_rn((float)c0, sc), __fmul_rn((float)c1, sc), __fmul_rn((float)c2, sc),
+                                  __fmul_rn((float)c3, sc));
+    }
+    __syncwarp();  // the recomputed elements below overwrite what step 1 wrote for them
+    // 2. ... then the recomputed ones (every picked element) from their exact values
+    for (int i = lane; i < total; i += 32) {
+        const int32_t j = idx[i];
+        const int cw = rq_code_t(v[row * d + j] * rc), c = a4_code(val[i], sc);
+        crow[j] = (int8_t)c;
+        csum += c - cw;
+        if (deq != nullptr) deq[row * d + j] = __fmul_rn((float)c, sc);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
