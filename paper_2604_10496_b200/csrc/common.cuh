@@ -115,6 +115,14 @@ __device__ __forceinline__ float silu_fast(float x) {
     return __fmul_rn(x, x >= 0.0f ? r : __fmul_rn(ex, r));
 }
 
+// max of |x|, |y|, |z|, |w| as bit patterns (non-negative floats order like their bits; inf and
+// NaN come out >= 0x7f800000)
+__device__ __forceinline__ uint32_t abs_bits4(float4 v) {
+    const uint32_t a = __float_as_uint(v.x) & 0x7fffffffu, b = __float_as_uint(v.y) & 0x7fffffffu;
+    const uint32_t c = __float_as_uint(v.z) & 0x7fffffffu, d = __float_as_uint(v.w) & 0x7fffffffu;
+    return max(max(a, b), max(c, d));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -205,14 +213,16 @@ struct UmmaIn {
 struct UmmaBOut {
     int8_t *dst = nullptr;
     int64_t tiles = 0;
-    int ck = 128;
+    int ck = 128, ck_shift = 7;  // ck = 1 << ck_shift
     int32_t *zero = nullptr;
     int n_zero = 0;
-    // byte offset of codes (row, col .. col + 3), col % 4 == 0
+    // byte offset of codes (row, col .. col + 3), col % 4 == 0:
+    //   ((((c * tiles + row / 8) * (ck / 32) + ks) * 2 + khalf) * 8 + row % 8) * 16 + col % 16
+    // with c = col / ck, ks = (col % ck) / 32, khalf = (col % 32) / 16, in shifts
     __device__ __forceinline__ int64_t off(int64_t row, int64_t col) const {
-        const int64_t c = col / ck, r = col - c * ck;
-        return ((((c * tiles + (row >> 3)) * (ck >> 5) + (r >> 5)) * 2 + ((r >> 4) & 1)) * 8 + (row & 7)) * 16 +
-               (r & 15);
+        const uint32_t cc = (uint32_t)col, c = cc >> ck_shift, r = cc & (uint32_t)(ck - 1);
+        const uint32_t low = ((r >> 5) << 8) + ((r & 16u) << 3) + (((uint32_t)row & 7u) << 4) + (r & 15u);
+        return (((int64_t)c * tiles + (row >> 3)) << (ck_shift + 3)) + low;
     }
 };
 

@@ -993,6 +993,7 @@ UmmaBOut umma_b_out(int8_t *bbuf, int64_t rows, int64_t d_in, int ck) {
     o.dst = bbuf;
     o.tiles = umma_b_tiles(rows);
     o.ck = ck;
+    o.ck_shift = __builtin_ctz((unsigned)ck);
     o.zero = reinterpret_cast<int32_t *>(bbuf + umma_cnt_off(rows, d_in));
     o.n_zero = umma_grid();
     return o;

@@ -121,8 +121,7 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
     const float4 *br = reinterpret_cast<const float4 *>(b + row * ff);
     const int nv = (int)(ff >> 2);
     float4 h[V];
-    float mx = 0.0f;
-    bool bad = false;
+    uint32_t mb = 0;  // max |h| as bits: ordered like the floats, and inf / NaN (flagged) above every finite value
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * (int)blockDim.x;
@@ -131,24 +130,20 @@ __global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__
             h[u] = make_float4(__fmul_rn(silu_fast(x.x), y.x), __fmul_rn(silu_fast(x.y), y.y),
                                __fmul_rn(silu_fast(x.z), y.z), __fmul_rn(silu_fast(x.w), y.w));
             if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
-            const float m4 = fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w)));
-            mx = fmaxf(mx, m4);
-            // fmaxf drops NaN: test the four values themselves
-            bad |= !(fabsf(h[u].x) <= FLT_MAX && fabsf(h[u].y) <= FLT_MAX && fabsf(h[u].z) <= FLT_MAX &&
-                     fabsf(h[u].w) <= FLT_MAX);
+            mb = max(mb, abs_bits4(h[u]));
         }
     }
-    if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
-    __shared__ float red[16];
+    if (nonfinite != nullptr && __syncthreads_or(mb >= 0x7f800000u) && threadIdx.x == 0) atomicExch(nonfinite, 1);
+    __shared__ uint32_t red[16];
     __shared__ float s_sh;
-    mx = warp_max(mx);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    mb = __reduce_max_sync(0xffffffffu, mb);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mb;
     __syncthreads();
     if (threadIdx.x < 32) {
-        float m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
-        m = warp_max(m);
+        uint32_t m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+        m = __reduce_max_sync(0xffffffffu, m);
         if (threadIdx.x == 0) {
-            s_sh = a4_scale(m);
+            s_sh = a4_scale(__uint_as_float(m));
             scales[row] = s_sh;
         }
     }
@@ -198,8 +193,7 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
     const float4 *br = reinterpret_cast<const float4 *>(b + row * ff + part * seg);
     const int nv = (int)(seg >> 2);
     float4 h[V];
-    float mx = 0.0f;
-    bool bad = false;
+    uint32_t mb = 0;  // max |h| as bits (see silu_quant_vec_kernel)
 #pragma unroll
     for (int u = 0; u < V; ++u) {
         const int j = threadIdx.x + u * 256;
@@ -208,23 +202,21 @@ __global__ void __launch_bounds__(256) silu_quant_cl_kernel(float *__restrict__ 
             h[u] = make_float4(__fmul_rn(silu_fast(x.x), y.x), __fmul_rn(silu_fast(x.y), y.y),
                                __fmul_rn(silu_fast(x.z), y.z), __fmul_rn(silu_fast(x.w), y.w));
             if (keep) ar[j] = h[u];  // h itself only for tracing (CQ_FLAG_KEEP_HIDDEN)
-            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(h[u].x), fabsf(h[u].y)), fmaxf(fabsf(h[u].z), fabsf(h[u].w))));
-            bad |= !(fabsf(h[u].x) <= FLT_MAX && fabsf(h[u].y) <= FLT_MAX && fabsf(h[u].z) <= FLT_MAX &&
-                     fabsf(h[u].w) <= FLT_MAX);
+            mb = max(mb, abs_bits4(h[u]));
         }
     }
-    if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
-    __shared__ float red[8];
+    if (nonfinite != nullptr && __syncthreads_or(mb >= 0x7f800000u) && threadIdx.x == 0) atomicExch(nonfinite, 1);
+    __shared__ uint32_t red[8];
     __shared__ float part_max, s_sh;
     __shared__ int row_sum;  // rank 0's: the cluster's code sum
     if (part == 0 && threadIdx.x == 0) row_sum = 0;
-    mx = warp_max(mx);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    mb = __reduce_max_sync(0xffffffffu, mb);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mb;
     __syncthreads();
     if (threadIdx.x < 32) {
-        float m = threadIdx.x < 8 ? red[threadIdx.x] : 0.0f;
-        m = warp_max(m);
-        if (threadIdx.x == 0) part_max = m;
+        uint32_t m = threadIdx.x < 8 ? red[threadIdx.x] : 0u;
+        m = __reduce_max_sync(0xffffffffu, m);
+        if (threadIdx.x == 0) part_max = __uint_as_float(m);
     }
     cluster.sync();
     if (threadIdx.x == 0) {
