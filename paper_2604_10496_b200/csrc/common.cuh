@@ -82,9 +82,11 @@ __device__ __forceinline__ int8_t a4_code(float x, float s) {
 // take the IEEE division.  Bit-exact with a4_code at a fraction of its instructions.
 __device__ __forceinline__ int8_t a4_code_rcp(float x, float s, float r) {
     const float t = __fmul_rn(x, r);
-    const float a = fabsf(t);
-    if (a < 8.0f && fabsf(a - truncf(a) - 0.5f) < 1.9073486e-6f) return a4_code(x, s);  // 2^-19
-    return static_cast<int8_t>(static_cast<int>(fminf(fmaxf(roundf(t), -8.0f), 7.0f)));
+    const float n = rintf(t);  // the nearest integer: roundf(t) except at half-integers
+    // within 2^-19 of a half-integer <=> |t - n| > 0.5 - 2^-19 (t - n is exact); there roundf and
+    // rintf may differ and t may differ from x / s: the IEEE division decides
+    if (fabsf(t) < 8.0f && fabsf(t - n) > 0.5f - 0x1p-19f) return a4_code(x, s);
+    return static_cast<int8_t>(min(max(__float2int_rn(n), -8), 7));
 }
 
 // model.py:233-237: x * sigmoid(x), sigmoid split at 0.
@@ -95,9 +97,6 @@ __device__ __forceinline__ float silu_f32(float x) {
     return __fmul_rn(x, sig);
 }
 
-// The tensor-core path's silu (silu|re-quantize kernels): the same function within a few ulp
-// (fast exp2 + a correctly rounded reciprocal instead of expf + IEEE division), a third of the
-// instructions.  Its h is tolerance-checked against the ordered path, which keeps silu_f32.
 // Two IEEE-rounded fp32 products in one FMUL2 (sm_100): (a0 * b0, a1 * b1), each rounded like
 // __fmul_rn.  The adds that consume them stay scalar __fadd_rn: ptxas keeps FMUL2 + FADD apart
 // (a packed multiply-add pair would be contracted into FFMA2, one rounding).
@@ -109,9 +108,14 @@ __device__ __forceinline__ void fmul2_rn(float a0, float a1, float b0, float b1,
     asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
 }
 
+// The tensor-core path's silu (silu|re-quantize kernels): the same function within a few ulp
+// (fast exp2 + the hardware reciprocal of 1 + e^-|x| in [1, 2] instead of expf + IEEE division),
+// a fraction of the instructions.  Its h is tolerance-checked against the ordered path, which keeps
+// silu_f32.
 __device__ __forceinline__ float silu_fast(float x) {
-    const float ex = __expf(-fabsf(x));               // e^-|x| in (0, 1]
-    const float r = __frcp_rn(__fadd_rn(1.0f, ex));   // sigmoid(|x|)
+    const float ex = __expf(-fabsf(x));  // e^-|x| in (0, 1]
+    float r;                             // sigmoid(|x|) = 1 / (1 + e^-|x|)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fadd_rn(1.0f, ex)));
     return __fmul_rn(x, x >= 0.0f ? r : __fmul_rn(ex, r));
 }
 
