@@ -12,6 +12,8 @@
 // columns, 4-deep smem ring of (A 16 KB, B 32 KB) chunks of 64 K-elements fed by
 // bulk copies; warp 0 producer, warp 1 MMA issuer, warps 2-5 epilogue (one TMEM
 // lane quarter each).
+#include <cuda.h>  // CUtensorMap (the encode entry point comes from the runtime: no libcuda link)
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -136,11 +138,14 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t *v) {
         : "memory");
 }
 
-// grid: (d / BN, ceil(n / BM)).  NPA: activation planes (1: bf16 input, 3: f32 input).
-template <int NPA>
+// grid: (d / BN, ceil(n / BM)).  NPA: activation planes (1: bf16 input, 3: f32 input).  XT (bf16
+// input): the A tiles come straight from the row-major x by TMA (xmap: [n][d] bf16, box 64 x 128,
+// SWIZZLE_128B; rows past n read as zeros) instead of from planes re-laid out by rot_split_x.
+template <int NPA, bool XT = false>
 __global__ void __launch_bounds__(rt::THREADS, 1) rot_gemm_kernel(const uint8_t *__restrict__ xa, int64_t a_tiles,
                                                                    const uint8_t *__restrict__ rb, int64_t d,
-                                                                   int64_t n, float *__restrict__ v, int npair) {
+                                                                   int64_t n, float *__restrict__ v, int npair,
+                                                                   const __grid_constant__ CUtensorMap xmap) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     // (activation plane, R plane) products, largest first: x R0, x R1, x R2 for a bf16 x; for an
     // fp32 x the six terms of relative size >= 2^-16 (x0R0, x0R1, x1R0, x0R2, x1R1, x2R0).
@@ -187,7 +192,16 @@ __global__ void __launch_bounds__(rt::THREADS, 1) rot_gemm_kernel(const uint8_t 
             const uint32_t dst = stage0 + s * (rt::A_BYTES + rt::B_BYTES);
             u_bar_expect_elect(bar, rt::A_BYTES + rt::B_BYTES);
             // A: 16 tile8 blocks of the token tile (1 KB each, contiguous); B: 32 of the column tile
-            u_bulk_elect(dst, xa + PA[p] * a_plane + ((int64_t)c * a_tiles + m0 / 8) * 1024, rt::A_BYTES, bar);
+            if constexpr (XT) {
+                asm volatile(
+                    "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                    "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];\n\t}" ::"r"(dst),
+                    "l"(&xmap), "r"(c * rt::KC), "r"((int)m0), "r"(bar)
+                    : "memory");
+            } else {
+                u_bulk_elect(dst, xa + PA[p] * a_plane + ((int64_t)c * a_tiles + m0 / 8) * 1024, rt::A_BYTES, bar);
+            }
             u_bulk_elect(dst + rt::A_BYTES, rb + PB[p] * b_plane + ((int64_t)c * b_tiles + n0 / 8) * 1024, rt::B_BYTES,
                          bar);
         }
@@ -202,8 +216,8 @@ __global__ void __launch_bounds__(rt::THREADS, 1) rot_gemm_kernel(const uint8_t 
             const uint32_t abase = stage0 + s * (rt::A_BYTES + rt::B_BYTES), bbase = abase + rt::A_BYTES;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                tc_mma_bf16_ss(tmem, smem_desc(abase + kk * 256, 128, 1024), smem_desc(bbase + kk * 256, 128, 1024),
-                               idesc, (it > 0 || kk > 0) ? 1u : 0u);
+                tc_mma_bf16_ss(tmem, XT ? smem_desc_sw128(abase + kk * 32) : smem_desc(abase + kk * 256, 128, 1024),
+                               smem_desc(bbase + kk * 256, 128, 1024), idesc, (it > 0 || kk > 0) ? 1u : 0u);
             tc_commit_elect(u_smem(&empty_bar[s]));
         }
         tc_commit_elect(u_smem(&acc_bar));
@@ -272,9 +286,53 @@ cq_status rot_tc_prepare(const float *R, int64_t d, void *out, cudaStream_t st) 
     return transpose_f32(R, d, const_cast<float *>(rot_tc_transposed(out, d)), st);
 }
 
+// x [n][d] bf16 as a TMA tile map (box 64 columns x 128 rows, SWIZZLE_128B: the K-major operand
+// layout with 128-byte rows).  The encoder is the driver's, reached through the runtime.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool x_tmap(CUtensorMap *m, const void *x, int64_t n, int64_t d) {
+    static EncodeTiledFn fn = nullptr;
+    if (fn == nullptr) {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || f == nullptr)
+            return false;
+        fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)rt::KC, (cuuint32_t)rt::BM};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(x), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// CQ_ROT_TMA=0: re-lay out x by rot_split_x instead of loading it by TMA (A/B)
+static bool rot_tma_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CQ_ROT_TMA");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const void *prepared, void *act, float *v,
                        cudaStream_t st) {
     if (n == 0) return CQ_OK;
+    const size_t smem = (size_t)rt::STAGES * (rt::A_BYTES + rt::B_BYTES);
+    const dim3 grid((unsigned)(d / rt::BN), (unsigned)ceil_div(n, rt::BM));
+    CUtensorMap xmap{};
+    if (dtype == CQ_DTYPE_BF16 && rot_tma_enabled() && x_tmap(&xmap, x, n, d)) {
+        cudaFuncSetAttribute(rot_gemm_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        launch_pdl(rot_gemm_kernel<1, true>, grid, rt::THREADS, smem, st, (const uint8_t *)nullptr, (int64_t)0,
+                   reinterpret_cast<const uint8_t *>(prepared), d, n, v, rot_planes(), xmap);
+        return check_launch("rotation_gemm");
+    }
     const int64_t tiles = ceil_div(n, rt::BM) * (rt::BM / 8);
     const int64_t pieces = tiles * 8 * d / 8;
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(pieces, 256), 148 * 16);
@@ -284,15 +342,13 @@ cq_status rot_tc_apply(const void *x, int dtype, int64_t n, int64_t d, const voi
         launch_pdl(rot_split_x_kernel<CQ_DTYPE_F32, 3>, blocks, 256, 0, st, x, n, d, tiles, reinterpret_cast<uint4 *>(act));
     CQ_TRY(check_launch("rotation_split_x"));
     // the dynamic-smem opt-in is per device: set it on every launch (cheap next to the kernel)
-    const size_t smem = (size_t)rt::STAGES * (rt::A_BYTES + rt::B_BYTES);
     cudaFuncSetAttribute(rot_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(rot_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const dim3 grid((unsigned)(d / rt::BN), (unsigned)ceil_div(n, rt::BM));
     const uint8_t *a = reinterpret_cast<const uint8_t *>(act), *b = reinterpret_cast<const uint8_t *>(prepared);
     if (dtype == CQ_DTYPE_BF16)
-        launch_pdl(rot_gemm_kernel<1>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v, rot_planes());
+        launch_pdl(rot_gemm_kernel<1>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v, rot_planes(), xmap);
     else
-        launch_pdl(rot_gemm_kernel<3>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v, 6);
+        launch_pdl(rot_gemm_kernel<3>, grid, rt::THREADS, smem, st, a, tiles, b, d, n, v, 6, xmap);
     return check_launch("rotation_gemm");
 }
 

@@ -281,6 +281,19 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
     return d;                // base offset 0, layout SWIZZLE_NONE
 }
 
+// K-major operand with 128-byte rows in SWIZZLE_128B (8-row atoms of 1 KB, atom-aligned base): the
+// layout a TMA tile load with that swizzle writes.  A k-slice inside the row is addressed by
+// advancing the start address (the swizzle applies to the final address).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;            // LBO: unused for swizzled K-major
+    d |= (uint64_t)(1024 >> 4) << 32;  // SBO: 8-row atoms
+    d |= (uint64_t)1 << 46;            // descriptor version (Blackwell)
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+
 // kind::i8 instruction descriptor: s32 accumulate, A and B signed, both K-major.
 __device__ __forceinline__ uint32_t idesc_i8(int n) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
