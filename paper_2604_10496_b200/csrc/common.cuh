@@ -198,7 +198,9 @@ struct RoutePerm {
 
 // Tensor-core layouts: UMMA128U8 is UMMA128U's data with every id < 8.
 inline bool umma_merged(int64_t layout) { return layout == CQ_TC_UMMA128U || layout == CQ_TC_UMMA128U8; }
-inline int64_t umma_family(int64_t layout) { return layout == CQ_TC_UMMA128U8 ? CQ_TC_UMMA128U : layout; }
+inline int64_t umma_family(int64_t layout) {
+    return layout == CQ_TC_UMMA128U8 ? (int64_t)CQ_TC_UMMA128U : layout;
+}
 
 // Optional inputs of the tcgen05 grouped GEMM's B-operand build (lut_umma.cu).
 struct UmmaIn {

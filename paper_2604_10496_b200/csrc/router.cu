@@ -456,7 +456,7 @@ struct RouteFuse {
 // W / x chunks by cp.async (NR buffers) and write the rounded products
 // fmul(x[t][j], w[j][e]) of the next chunk into the other product buffer.
 // Summation order and rounding are those of router_deq_kernel (bit-exact).
-constexpr int RC_THREADS = 128, RC_K = 256, RC_PITCH = RC_K + 4;
+constexpr int RC_THREADS = 128, RC_K = 256;
 // raw stages: W leaves L2 under the expert weight stream, so chunks come from
 // DRAM; prefetch NR - 1 chunks (~0.55 us of chain each) ahead
 template <int EG>
