@@ -342,23 +342,17 @@ __global__ void combine_kernel(const int32_t *__restrict__ selected, const float
     const int64_t t = blockIdx.x;
     __shared__ int32_t pos_sh[16];
     __shared__ float w_sh[16];
-    if (threadIdx.x == 0) {  // this token's routes in ascending expert order (ids are distinct)
-        int32_t ex[16], pos[16];
-        float w[16];
-        for (int s = 0; s < k; ++s) {
-            ex[s] = __ldg(selected + t * k + s);
-            pos[s] = __ldg(inv + t * k + s);
-            w[s] = __ldg(weights + t * k + s);
-        }
-        for (int a = 1; a < k; ++a)
-            for (int b = a; b > 0 && ex[b - 1] > ex[b]; --b) {
-                int32_t te = ex[b]; ex[b] = ex[b - 1]; ex[b - 1] = te;
-                int32_t tp = pos[b]; pos[b] = pos[b - 1]; pos[b - 1] = tp;
-                float tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
-            }
-        for (int s = 0; s < k; ++s) {
-            pos_sh[s] = pos[s];
-            w_sh[s] = w[s];
+    if (threadIdx.x < 32) {  // this token's routes in ascending expert order (ids are distinct): lane s
+        const int lane = threadIdx.x;  // loads route s and places it at its rank among the k ids
+        const bool on = lane < k;
+        const int32_t ex = on ? __ldg(selected + t * k + lane) : INT32_MAX;
+        const int32_t pos = on ? __ldg(inv + t * k + lane) : 0;
+        const float w = on ? __ldg(weights + t * k + lane) : 0.0f;
+        int rank = 0;
+        for (int s = 0; s < k; ++s) rank += __shfl_sync(0xffffffffu, ex, s) < ex ? 1 : 0;
+        if (on) {
+            pos_sh[rank] = pos;
+            w_sh[rank] = w;
         }
     }
     __syncthreads();
