@@ -51,6 +51,11 @@ CONFIGS = {
                batch=4096, rotation=True),
     "qw": dict(name="qwen3-30b-a3b-moe-layer-prefill", d_model=2048, d_ff=768, n_experts=128, top_k=8, batch=4096),
     "qw64": dict(name="qwen3-30b-a3b-moe-layer-decode", d_model=2048, d_ff=768, n_experts=128, top_k=8, batch=64),
+    # SURVEY 8(d)'s QW sizes for the scaling rows: decode N = 256, strong-scaling prefill N = 8192
+    "qw256": dict(name="qwen3-30b-a3b-moe-layer-decode-256", d_model=2048, d_ff=768, n_experts=128, top_k=8,
+                  batch=256),
+    "qw8k": dict(name="qwen3-30b-a3b-moe-layer-prefill-8192", d_model=2048, d_ff=768, n_experts=128, top_k=8,
+                 batch=8192),
     "ds": dict(name="deepseek-v2-lite-moe-block-prefill", d_model=2048, d_ff=1408, n_experts=64, top_k=6,
                batch=8192, n_shared=2),
 }

@@ -1,7 +1,7 @@
 # All SURVEY §8(d) configurations on one B200, one JSON line each (gpurun_out/bench_all/).
 out=gpurun_out/bench_all
 mkdir -p $out
-for c in mx mx1 mx8 mxe mx3 mx2 c1 qw64 qw ph ds; do
+for c in mx mx1 mx8 mxe mx3 mx2 c1 qw64 qw256 qw qw8k ph ds; do
   timeout 600 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline > $out/$c.json 2> $out/$c.err
 done
 timeout 600 python bench.py > $out/default.json 2> $out/default.err
