@@ -42,7 +42,7 @@ cq_status lut_umma_grouped(const int8_t *, int8_t *, const float *, const int32_
                            cudaStream_t, const UmmaIn &in = UmmaIn{});
 int64_t umma_b_bytes(int64_t rows, int64_t d_in);
 int32_t *umma_row_sums(int8_t *bbuf, int64_t rows, int64_t d_in);
-int umma_geo_ck(int64_t rows, int64_t n_seg, int64_t d_in, int64_t d_out, int mats);
+int umma_geo_ck(int64_t rows, int64_t n_seg, int64_t d_in, int64_t d_out, int mats, int planes);
 UmmaBOut umma_b_out(int8_t *bbuf, int64_t rows, int64_t d_in, int ck);
 int64_t rot_tc_act_bytes(int64_t n, int64_t d);
 const float *rot_tc_transposed(const void *prepared, int64_t d);
@@ -539,7 +539,8 @@ cq_status run_experts(const cq_moe_desc *dsc, int path, const cq_expert_site &ga
         const int keep = (dsc->flags & CQ_FLAG_KEEP_HIDDEN) != 0;
         UmmaBOut bo;
         if (silu_b_ok(ff)) {
-            bo = umma_b_out(bbuf_h, rows, ff, umma_geo_ck(rows, n_seg, ff, d, 1));
+            const int gck = umma_geo_ck(rows, n_seg, ff, d, 1, (int)down.tc_planes);  // < 0: prefill
+            bo = umma_b_out(bbuf_h, rows, ff, gck < 0 ? -gck : gck);
             hin.b_ready = true;
         }
         CQ_TRY(silu_quant(hidden, bout, rows, ff, (keep || !hin.b_ready) ? hcodes : nullptr, hscales, offsets + n_seg,
