@@ -50,6 +50,9 @@ namespace cq {
 #ifndef UM_GS4  // chunk streams when >= 4 A stages fit (measured: 4 beats 2 double-buffered)
 #define UM_GS4 4
 #endif
+#ifndef UM_PF2_GS  // chunk streams of the 2-plane prefill GEMM
+#define UM_PF2_GS 2
+#endif
 #ifndef UM_SPLIT_AFREE  // data (full) and A-stage-free (afree) as separate barriers: 0 never, 1 always,
 #define UM_SPLIT_AFREE 2  // 2: prefill geometry, 3 planes only (decode and the 2-plane down GEMM measured slower)
 #endif
@@ -144,7 +147,11 @@ struct UmStage {
     // chunks (staggered waits, bookkeeping paid per GS k-steps) and each owns
     // NA / GS >= 2 A stages, so it expands chunk c + GS while the MMAs of c run.
     static constexpr int NA0 = NCS < um::STAGES ? NCS : um::STAGES;
-    static constexpr int GS = NA0 >= 4 ? UM_GS4 : (NA0 >= 2 ? 2 : 1);
+    // (the 2-plane prefill GEMM with its four 128-column A stages: 2 streams + 2 stages of data lag
+    //  beat 4 streams without lag: PH down 373 -> 354 us)
+    static constexpr int GS = (GEO::NT == 128 && P == 2 && NA0 >= 4) ? UM_PF2_GS
+                              : NA0 >= 4                             ? UM_GS4
+                              : (NA0 >= 2 ? 2 : 1);
     static_assert(GEO::KS % (um::WG / GS) == 0, "a chunk's k-steps split evenly over a stream's warpgroups");
     static constexpr int NA = (NA0 / GS) * GS;
     // LAG > 0: NS = NA + LAG smem stages, so the producer issues chunk c's
