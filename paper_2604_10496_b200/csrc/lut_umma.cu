@@ -920,16 +920,18 @@ static int64_t umma_prefill_min() {  // CQ_UMMA_PREFILL_MIN overrides (experimen
     static int64_t v = -1;
     if (v < 0) {
         const char *e = getenv("CQ_UMMA_PREFILL_MIN");
-        v = e ? atoll(e) : 96;
+        v = e ? atoll(e) : 32;
     }
     return v;
 }
-// 128-token passes pay when segments are long and the decode geometry would have many
-// chunk iterations per CTA (tools/geometry_sweep.py: one 4096x28672 expert at 128 rows 93 vs
-// 140 us, at 32 rows 62 vs 55 us; a 2048x1536 expert at 96 rows 34 vs 23 us).  `rows` is a
-// bound (expert parallelism passes its slot capacity, ~2x the routed rows), hence 96 per segment.
+// 128-token passes pay once the decode geometry's 32-token passes would repeat the expansion of a
+// segment (measured whole layers, bench.py --batch, this round: at 32 rows per segment prefill wins
+// by 5-12% (MX b=128, QW b=512, PH b=256), at 48-64 by 16-37% (DS b=512, MX b=256, PH b=512, QW
+// b=1024); at 16-24 rows decode wins by 9-26%), and when the decode geometry would have many chunk
+// iterations per CTA (small matrices stay fill-bound on it: a 2048x1536 expert at 96 rows 34 vs
+// 23 us).  `rows` is a bound: expert parallelism passes its slot capacity (~2x the routed rows).
 static bool umma_prefill(int64_t rows, int64_t n_seg, int64_t d_in, int64_t d_out, int mats) {
-    if (rows < umma_prefill_min() * n_seg) return false;
+    if (rows < 64 || rows < umma_prefill_min() * n_seg) return false;  // the prefill scratch needs 64 rows
     const int64_t decode_iters = ceil_div(rows / n_seg, 32) * n_seg * (d_out / 128) * mats * (d_in / 128);
     return decode_iters >= 32LL * umma_grid();
 }
