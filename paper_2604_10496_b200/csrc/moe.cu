@@ -642,7 +642,15 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
     }
     if (deferred != nullptr) {
         *deferred = 0;
-        if (n * dsc->top_k <= RP_MAX_ROUTES && dsc->n_local_experts <= RP_MAX_LOCAL &&
+        // most routes the deferred form takes (CQ_ROUTE_DEFER_MAX overrides): every B-build CTA derives
+        // the permutation itself, which stops paying past a few hundred routes (MX: 128 routes 0.310 vs
+        // 0.311 ms deferred / separate, 256 equal, 512 0.468 vs 0.463, 1024 0.754 vs 0.726)
+        static int64_t defer_max = -1;
+        if (defer_max < 0) {
+            const char *e = getenv("CQ_ROUTE_DEFER_MAX");
+            defer_max = e ? atoll(e) : 256;
+        }
+        if (n * dsc->top_k <= std::min<int64_t>(defer_max, RP_MAX_ROUTES) && dsc->n_local_experts <= RP_MAX_LOCAL &&
             dsc->top_k <= MAX_TOPK && dsc->top_k <= dsc->n_experts) {
             bool fused = false;  // logits + top-k in one launch (one expert group)
             CQ_TRY(router_fused(w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, w.selected, w.weights,
