@@ -302,8 +302,7 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
         if (rows <= 74 && silu_quant_cluster<8>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, bo, st)) return check_launch("silu_quant");
         if (rows > 74 && rows <= 148 && silu_quant_cluster<4>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, bo, st))
             return check_launch("silu_quant");
-        if (rows > 148 && rows <= 296 && silu_quant_cluster<2>(a, b, rows, ff, codes, scales, live, sums, keep, nonfinite, bo, st))
-            return check_launch("silu_quant");
+        // (2-CTA clusters for 149-296 rows measured equal or slower than the CTA-per-row kernel)
     }
     const int64_t v = ceil_div(ff / 4, 512);
     if (ff % 4 == 0 && v <= 8) {
