@@ -184,7 +184,13 @@ struct UmStage {
 // split.  Every CTA pays the prologue and the pipeline fill once.
 namespace um {
 constexpr int MAX_SEG = 512;   // segments (experts) per launch, prefix table in smem
-constexpr int MIN_ITERS = 8;   // fewest chunk iterations per CTA in the tail
+#ifndef UM_MIN_ITERS
+#define UM_MIN_ITERS 8
+#endif
+constexpr int MIN_ITERS = UM_MIN_ITERS;   // fewest chunk iterations per CTA in the tail
+#ifndef UM_TAIL_DIV  // tail ranges >= n_chunks / UM_TAIL_DIV (QW gate|up 465 -> 444 us, DS 987 -> 974 at 2)
+#define UM_TAIL_DIV 2
+#endif
 }  // namespace um
 
 struct UmWork {
@@ -315,7 +321,10 @@ __global__ void __launch_bounds__(UmWarps<P>::THREADS, 1) lut_umma_kernel(
     W.T0 = W.full_rounds * W.G * n_chunks;
     W.T = (W.n_units - W.full_rounds * W.G) * n_chunks;
     {
-        const int64_t gt = W.T / um::MIN_ITERS > 0 ? W.T / um::MIN_ITERS : 1;
+        // tail ranges of at least max(MIN_ITERS, n_chunks / UM_TAIL_DIV) chunks: long units split over
+        // fewer CTAs (fewer partial-sum exchanges)
+        const int64_t mi = n_chunks / UM_TAIL_DIV > um::MIN_ITERS ? n_chunks / UM_TAIL_DIV : um::MIN_ITERS;
+        const int64_t gt = W.T / mi > 0 ? W.T / mi : 1;
         W.Gt = (int)(gt < W.G ? gt : W.G);
     }
     const int cta = blockIdx.x;
