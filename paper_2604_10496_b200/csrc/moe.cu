@@ -304,7 +304,15 @@ cq_status silu_quant(float *a, const float *b, int64_t rows, int64_t ff, int8_t 
             return check_launch("silu_quant");
         // (2-CTA clusters for 149-296 rows measured equal or slower than the CTA-per-row kernel)
     }
-    const int64_t v = ceil_div(ff / 4, 512);
+    // short rows (ff <= 2048) on CTAs of <= 128 threads (several float4 each): more rows in flight per SM
+    // (DS 172 -> 140 us, QW 64 -> 53 us); long rows keep up to 512 (PH at 256: 158 -> 182 us).
+    // CQ_SILU_THREADS overrides the short-row cap (experiments).
+    static int max_thr = -1;
+    if (max_thr < 0) {
+        const char *e = getenv("CQ_SILU_THREADS");
+        max_thr = e ? atoi(e) : 128;
+    }
+    const int64_t v = ceil_div(ff / 4, (ff <= 2048 ? max_thr : 512));
     if (ff % 4 == 0 && v <= 8) {
         switch (v) {
             case 1: {  // short rows: one float4 per thread, CTA sized to the row
