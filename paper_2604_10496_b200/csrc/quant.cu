@@ -73,8 +73,9 @@ __global__ void __launch_bounds__(256) quantize_a4_kernel(const void *__restrict
 // Same quantizer with the row held in registers (d % 4 == 0, d <= 8192): 256
 // threads x V groups of 4 values, loaded once with 16-byte (fp32) / 8-byte
 // (bf16) loads; codes, dequantized values and code sums as before.
-template <int DT, int V>
-__global__ void __launch_bounds__(256) quantize_a4_vec_kernel(const void *__restrict__ x, int64_t d,
+// TH threads per row (256, or 128 for short rows: more rows in flight per SM).
+template <int DT, int V, int TH = 256>
+__global__ void __launch_bounds__(TH) quantize_a4_vec_kernel(const void *__restrict__ x, int64_t d,
                                                               int8_t *__restrict__ codes,
                                                               float *__restrict__ scales,
                                                               int *__restrict__ nonfinite,
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(256) quantize_a4_vec_kernel(const void *__rest
     bool bad = false;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
-        const int j = threadIdx.x + u * 256;
+        const int j = threadIdx.x + u * TH;
         if (j < nv) {
             if (DT == CQ_DTYPE_F32) {
                 const float4 v = __ldg(reinterpret_cast<const float4 *>(x) + row * nv + j);
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(256) quantize_a4_vec_kernel(const void *__rest
     if (nonfinite != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicExch(nonfinite, 1);
     __syncthreads();
     if (threadIdx.x < 32) {
-        float m = threadIdx.x < 8 ? red[threadIdx.x] : 0.0f;
+        float m = threadIdx.x < TH / 32 ? red[threadIdx.x] : 0.0f;
         m = warp_max(m);
         if (threadIdx.x == 0) {
             const float sc = a4_scale(m);
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(256) quantize_a4_vec_kernel(const void *__rest
     int csum = 0;
 #pragma unroll
     for (int u = 0; u < V; ++u) {
-        const int j = threadIdx.x + u * 256;
+        const int j = threadIdx.x + u * TH;
         if (j < nv) {
             const char4 c = make_char4(a4_code_rcp(h[u][0], sc, rs), a4_code_rcp(h[u][1], sc, rs),
                                        a4_code_rcp(h[u][2], sc, rs), a4_code_rcp(h[u][3], sc, rs));
@@ -166,10 +167,14 @@ cq_status quantize_a4(const void *x, int dtype, int64_t n, int64_t d, int8_t *co
                       int *nonfinite_dev, float *deq, cudaStream_t st, int32_t *tsum, int32_t *zero, int n_zero) {
     if (n == 0) return CQ_OK;
     if (d % 4 == 0 && d <= 8 * 1024) {  // row in registers
-        const int64_t v = ceil_div(d / 4, 256);
-#define CQ_QVEC(DT_, V_)                                                                                          \
-    launch_pdl(quantize_a4_vec_kernel<DT_, V_>, (unsigned)n, 256, 0, st, x, d, codes, scales, nonfinite_dev, deq, \
-               tsum, zero, n_zero)
+        // short rows (d <= 2048) on 128-thread CTAs (more rows in flight per SM), else 256
+        const bool small = d <= 2048;
+        const int64_t v = ceil_div(d / 4, small ? 128 : 256);
+#define CQ_QVEC(DT_, V_)                                                                                             \
+    (small ? launch_pdl(quantize_a4_vec_kernel<DT_, V_, 128>, (unsigned)n, 128, 0, st, x, d, codes, scales,           \
+                        nonfinite_dev, deq, tsum, zero, n_zero)                                                       \
+           : launch_pdl(quantize_a4_vec_kernel<DT_, V_, 256>, (unsigned)n, 256, 0, st, x, d, codes, scales,           \
+                        nonfinite_dev, deq, tsum, zero, n_zero))
         if (dtype == CQ_DTYPE_F32) {
             if (v == 1) CQ_QVEC(CQ_DTYPE_F32, 1); else if (v == 2) CQ_QVEC(CQ_DTYPE_F32, 2);
             else if (v <= 4) CQ_QVEC(CQ_DTYPE_F32, 4); else CQ_QVEC(CQ_DTYPE_F32, 8);
