@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) silu_quant_kernel(float *__restrict__ a, 
 // ff <= 8192 V), so a and b are read once with 16-byte loads and h never
 // round-trips through memory before it is quantized.
 template <int V>
-__global__ void __launch_bounds__(512) silu_quant_vec_kernel(float *__restrict__ a, const float *__restrict__ b,
+__global__ void __launch_bounds__(512, V == 4 ? 4 : 1) silu_quant_vec_kernel(float *__restrict__ a, const float *__restrict__ b,
                                                               int64_t ff, int8_t *__restrict__ codes,
                                                               float *__restrict__ scales,
                                                               const int32_t *__restrict__ live,
