@@ -341,10 +341,11 @@ __global__ void silu_mul_kernel(float *__restrict__ a, const float *__restrict__
 
 // out[t, :] = ((0 + w_e1 f_e1) + w_e2 f_e2) + ...  with e ascending (model.py:401),
 // then + add[t, :] (shared experts) when given.  grid (n, column blocks).
-__global__ void combine_kernel(const int32_t *__restrict__ selected, const float *__restrict__ weights,
-                               const int32_t *__restrict__ inv, const float *__restrict__ fout, int64_t k,
-                               int64_t d, const float *__restrict__ add, int n_add, int64_t add_stride,
-                               float *__restrict__ out) {
+// 32 registers (8 CTAs of 256 per SM instead of 6): PH 38.5 -> 33.3 us, DS 101 -> 93.5, QW 53 -> 48.4.
+__global__ void __launch_bounds__(256, 8)
+    combine_kernel(const int32_t *__restrict__ selected, const float *__restrict__ weights,
+                   const int32_t *__restrict__ inv, const float *__restrict__ fout, int64_t k, int64_t d,
+                   const float *__restrict__ add, int n_add, int64_t add_stride, float *__restrict__ out) {
     griddep_wait();  // PDL: inputs of the previous kernel are visible after this
     const int64_t t = blockIdx.x;
     __shared__ int32_t pos_sh[16];
