@@ -22,6 +22,9 @@ cq_status router_logits(const int8_t *, const float *, const float *, const floa
                         float *, cudaStream_t);
 cq_status router_fused(const float *, const float *, int64_t, int64_t, int64_t, float *, int32_t *, float *, int64_t,
                        cudaStream_t, bool *);
+cq_status router_fused_quant(const void *, int, int8_t *, float *, int *, int32_t *, int32_t *, int, float *,
+                             const float *, int64_t, int64_t, int64_t, float *, int32_t *, float *, int64_t,
+                             cudaStream_t, bool *);
 cq_status topk(const float *, int64_t, int64_t, int64_t, int32_t *, float *, int32_t *, int64_t, int64_t,
                cudaStream_t);
 bool permute_counts_itself(int64_t n);
@@ -625,6 +628,19 @@ cq_status shared_experts(const cq_moe_desc *desc, int path, int64_t n, const Ws 
 // stop there and set *deferred = 1: the permutation is the GEMM's B build's
 // (UmmaIn::route); 0 = everything done here.
 
+// Routing deferred to the B build (every B-build CTA derives the permutation itself): up to
+// CQ_ROUTE_DEFER_MAX routes, past which it stops paying (MX: 128 routes 0.310 vs 0.311 ms deferred /
+// separate, 256 equal, 512 0.468 vs 0.463, 1024 0.754 vs 0.726).
+static bool route_deferrable(const cq_moe_desc *dsc, int64_t n) {
+    static int64_t defer_max = -1;
+    if (defer_max < 0) {
+        const char *e = getenv("CQ_ROUTE_DEFER_MAX");
+        defer_max = e ? atoll(e) : 256;
+    }
+    return n * dsc->top_k <= std::min<int64_t>(defer_max, RP_MAX_ROUTES) && dsc->n_local_experts <= RP_MAX_LOCAL &&
+           dsc->top_k <= MAX_TOPK && dsc->top_k <= dsc->n_experts;
+}
+
 cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, const Ws &w, cudaStream_t st,
                 bool gather = true, int *deferred = nullptr) {
     const int64_t d = dsc->d_model;
@@ -640,6 +656,18 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
     } else {
         const void *qin = x;
         int qdt = dtype;
+        if (deferred != nullptr && dsc->rotation == nullptr && route_deferrable(dsc, n)) {
+            // decode: the quantizer runs inside the router launch (router_fused_quant), which saves a
+            // launch and the dequantized rows' round trip through memory
+            bool fused = false;
+            CQ_TRY(router_fused_quant(x, dtype, w.codes, w.scales, w.status, w.tok_sums, w.counts,
+                                      (int)dsc->n_experts + 1, w.fout, dsc->w_router, n, d, dsc->n_experts,
+                                      w.logits, w.selected, w.weights, dsc->top_k, st, &fused));
+            if (fused) {
+                *deferred = 1;
+                return CQ_OK;
+            }
+        }
         if (dsc->rotation != nullptr) {  // the reference's ordered chain (pipeline.py:516 -> _core.pyx:27-38)
             CQ_TRY(ordered_matmul(x, dtype, dsc->rotation, n, d, d, w.rotated, st));
             qin = w.rotated;
@@ -650,16 +678,7 @@ cq_status route(const cq_moe_desc *dsc, const void *x, int dtype, int64_t n, con
     }
     if (deferred != nullptr) {
         *deferred = 0;
-        // most routes the deferred form takes (CQ_ROUTE_DEFER_MAX overrides): every B-build CTA derives
-        // the permutation itself, which stops paying past a few hundred routes (MX: 128 routes 0.310 vs
-        // 0.311 ms deferred / separate, 256 equal, 512 0.468 vs 0.463, 1024 0.754 vs 0.726)
-        static int64_t defer_max = -1;
-        if (defer_max < 0) {
-            const char *e = getenv("CQ_ROUTE_DEFER_MAX");
-            defer_max = e ? atoll(e) : 256;
-        }
-        if (n * dsc->top_k <= std::min<int64_t>(defer_max, RP_MAX_ROUTES) && dsc->n_local_experts <= RP_MAX_LOCAL &&
-            dsc->top_k <= MAX_TOPK && dsc->top_k <= dsc->n_experts) {
+        if (route_deferrable(dsc, n)) {
             bool fused = false;  // logits + top-k in one launch (one expert group)
             CQ_TRY(router_fused(w.fout, dsc->w_router, n, d, dsc->n_experts, w.logits, w.selected, w.weights,
                                 dsc->top_k, st, &fused));

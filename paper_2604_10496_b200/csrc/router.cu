@@ -446,6 +446,16 @@ struct RouteFuse {
     int32_t *selected;
     float *weights;
     int64_t k;
+    // quantizer in the router (qx != nullptr): the CTA quantizes its own tokens first
+    // (quantize_a4_vec_kernel's arithmetic) and keeps the dequantized rows in shared memory
+    const void *qx = nullptr;
+    int qdt = 0;
+    int8_t *codes = nullptr;
+    float *scales = nullptr;
+    int *nonfinite = nullptr;
+    int32_t *tsum = nullptr;
+    int32_t *zero = nullptr;
+    int n_zero = 0;
 };
 
 // Decode batches: each chain (token, expert) is d dependent fp32 adds, and with
@@ -502,7 +512,74 @@ __device__ __forceinline__ float chain_add(float acc, const float4 *__restrict__
 // FUSE (one expert group, n_exp == EG): the CTA also selects its tokens'
 // top-k from the logits in shared memory (topk_kernel without its launch; the
 // permutation is derived by the consumer, route_perm.cuh).
-template <int EG, bool FUSE>
+// The CTA's tt token rows quantized as quantize_a4_vec_kernel does them (same max, scale, codes,
+// sums and code * scale products, bit for bit), the dequantized rows left in xs [tt][d].
+__device__ void rc_quantize(const RouteFuse &f, int64_t t0, int tt, int64_t n, int64_t d, float *xs) {
+    __shared__ float red_f[RC_THREADS / 32];
+    __shared__ int red_i[RC_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool pub = blockIdx.y == 0;  // expert groups > 0 recompute the same rows
+    const int nv = (int)(d >> 2);
+    if (pub && blockIdx.x == 0)
+        for (int i = tid; i < f.n_zero; i += RC_THREADS) f.zero[i] = 0;
+    for (int tl = 0; tl < tt; ++tl) {
+        const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // rows past n are never stored
+        float4 *xr = reinterpret_cast<float4 *>(xs + (size_t)tl * d);
+        float mx = 0.0f;
+        bool bad = false;
+        for (int j = tid; j < nv; j += RC_THREADS) {  // (8 loads batched per thread: spills, slower)
+            float h[4];
+            if (f.qdt == CQ_DTYPE_F32) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(f.qx) + tg * nv + j);
+                h[0] = v.x, h[1] = v.y, h[2] = v.z, h[3] = v.w;
+            } else {
+                const uint2 v = __ldg(reinterpret_cast<const uint2 *>(f.qx) + tg * nv + j);
+                h[0] = __uint_as_float(v.x << 16), h[1] = __uint_as_float(v.x & 0xFFFF0000u);
+                h[2] = __uint_as_float(v.y << 16), h[3] = __uint_as_float(v.y & 0xFFFF0000u);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bad |= !isfinite(h[q]);
+                mx = fmaxf(mx, fabsf(h[q]));
+            }
+            xr[j] = make_float4(h[0], h[1], h[2], h[3]);
+        }
+        mx = warp_max(mx);
+        if (lane == 0) red_f[warp] = mx;
+        if (__syncthreads_or(bad) && tid == 0 && pub && f.nonfinite != nullptr) atomicExch(f.nonfinite, 1);
+        float m = red_f[0];
+#pragma unroll
+        for (int w = 1; w < RC_THREADS / 32; ++w) m = fmaxf(m, red_f[w]);
+        const float sc = a4_scale(m);
+        const float rs = __frcp_rn(sc);
+        int csum = 0;
+        const bool live = pub && t0 + tl < n;
+        for (int j = tid; j < nv; j += RC_THREADS) {
+            const float4 h = xr[j];
+            const char4 c = make_char4(a4_code_rcp(h.x, sc, rs), a4_code_rcp(h.y, sc, rs), a4_code_rcp(h.z, sc, rs),
+                                       a4_code_rcp(h.w, sc, rs));
+            if (live) reinterpret_cast<char4 *>(f.codes + tg * d)[j] = c;
+            csum += c.x + c.y + c.z + c.w;
+            xr[j] = make_float4(__fmul_rn((float)c.x, sc), __fmul_rn((float)c.y, sc), __fmul_rn((float)c.z, sc),
+                                __fmul_rn((float)c.w, sc));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+        if (lane == 0) red_i[warp] = csum;
+        __syncthreads();
+        if (tid == 0 && live) {
+            int t = 0;
+            for (int w = 0; w < RC_THREADS / 32; ++w) t += red_i[w];
+            if (f.tsum != nullptr) f.tsum[tg] = t;
+            f.scales[tg] = sc;
+        }
+        __syncthreads();  // red_f / red_i are reused by the next row
+    }
+}
+
+// QIN (with FUSE): the quantizer runs in the router launch (rc_quantize); x comes from shared
+// memory instead of the xdeq ring, and `xdeq` is unused.
+template <int EG, bool FUSE, bool QIN = false>
 __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *__restrict__ xdeq,
                                                                   const float *__restrict__ w, int64_t n,
                                                                   int64_t d, int64_t n_exp, int tt,
@@ -514,7 +591,7 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
     constexpr int NR = RcStages<EG>::NR;
     constexpr int KC = RcStages<EG>::K, PITCH = RcStages<EG>::PITCH;
     float *wraw = pbuf + 2 * nc * PITCH;      // [NR][KC][EG]
-    float *xraw = wraw + NR * KC * EG;         // [NR][tt][KC]
+    float *xraw = wraw + NR * KC * EG;         // [NR][tt][KC]; QIN: [tt][d]
     const int tid = threadIdx.x;
     const int64_t t0 = blockIdx.x * (int64_t)tt;
     const int e0 = blockIdx.y * EG;
@@ -530,7 +607,7 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
                 cp_async16(wb + r * EG + 4 * q, w + (k0 + r) * n_exp + e0 + 4 * q);
             }
             float *xb = xraw + (i % NR) * tt * KC;
-            const int rowv = kn / 4;
+            const int rowv = QIN ? 0 : kn / 4;
             for (int x = ptid; x < tt * rowv; x += RC_THREADS - 32) {
                 const int tl = x / rowv, v = x - tl * rowv;
                 const int64_t tg = t0 + tl < n ? t0 + tl : n - 1;  // rows past n are never stored
@@ -544,7 +621,8 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
         const int64_t k0 = (int64_t)i * KC;
         const int kn = (int)((d - k0) < KC ? (d - k0) : KC);
         const float *wb = wraw + (i % NR) * KC * EG;
-        const float *xb = xraw + (i % NR) * tt * KC;
+        const float *xb = QIN ? xraw + k0 : xraw + (i % NR) * tt * KC;
+        const int64_t xs = QIN ? d : KC;  // x row pitch
         float *pb = pbuf + (i & 1) * nc * PITCH;
         for (int j = ptid; j < kn; j += RC_THREADS - 32) {
             float wr[EG];
@@ -554,7 +632,7 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
                 wr[4 * q] = v.x, wr[4 * q + 1] = v.y, wr[4 * q + 2] = v.z, wr[4 * q + 3] = v.w;
             }
             for (int t = 0; t < tt; ++t) {
-                const float xv = xb[t * KC + j];
+                const float xv = xb[t * xs + j];
 #pragma unroll
                 for (int e = 0; e < EG; e += 2) {
                     float p0, p1;
@@ -568,6 +646,9 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
     if (tid >= 32) {
 #pragma unroll
         for (int i = 0; i < NR - 1; ++i) stage(i);
+    }
+    if constexpr (QIN) rc_quantize(f, t0, tt, n, d, xraw);  // the W chunks land meanwhile
+    if (tid >= 32) {
         asm volatile("cp.async.wait_group %0;" ::"n"(NR - 2) : "memory");
         produce(0);
     }
@@ -602,11 +683,13 @@ __global__ void __launch_bounds__(RC_THREADS) router_chain_kernel(const float *_
     }
 }
 
-static size_t router_chain_smem(int eg, int tt) {
+static size_t router_chain_smem(int eg, int tt, int64_t qin_d = 0) {
     const size_t nr = eg >= 32 ? RcStages<32>::NR : RcStages<8>::NR;
     const size_t kc = eg >= 32 ? RcStages<32>::K : RcStages<8>::K;
-    return sizeof(float) * ((size_t)2 * tt * eg * (kc + 4) + nr * kc * eg + nr * tt * kc);
+    const size_t xf = qin_d > 0 ? (size_t)tt * qin_d : nr * tt * kc;  // QIN: the whole dequantized rows
+    return sizeof(float) * ((size_t)2 * tt * eg * (kc + 4) + nr * kc * eg + xf);
 }
+constexpr size_t RC_QIN_SMEM_MAX = 200 * 1024;
 
 // rows_out[r, :] = rows_in[perm_token[r], :], r < offsets[n_local]; also scales.
 __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *__restrict__ sscale,
@@ -628,24 +711,27 @@ __global__ void gather_rows_kernel(const int8_t *__restrict__ src, const float *
     }
 }
 
-template <bool FUSE>
+template <bool FUSE, bool QIN = false>
 static void launch_chain(int eg, dim3 grid, size_t smem, cudaStream_t st, const float *xdeq, const float *w,
                          int64_t n, int64_t d, int64_t n_exp, int tt, float *logits, const RouteFuse &f) {
     static std::atomic<uint64_t> attr{0};  // devices whose smem opt-in is set
     if (first_on_device(attr)) {
-        cudaFuncSetAttribute(router_chain_kernel<8, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)router_chain_smem(8, 4));
-        cudaFuncSetAttribute(router_chain_kernel<16, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)router_chain_smem(16, 2));
-        cudaFuncSetAttribute(router_chain_kernel<32, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)router_chain_smem(32, 1));
+        cudaFuncSetAttribute(router_chain_kernel<8, FUSE, QIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             QIN ? (int)RC_QIN_SMEM_MAX : (int)router_chain_smem(8, 4));
+        cudaFuncSetAttribute(router_chain_kernel<16, FUSE, QIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             QIN ? (int)RC_QIN_SMEM_MAX : (int)router_chain_smem(16, 2));
+        cudaFuncSetAttribute(router_chain_kernel<32, FUSE, QIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             QIN ? (int)RC_QIN_SMEM_MAX : (int)router_chain_smem(32, 1));
     }
     if (eg == 32)
-        launch_pdl(router_chain_kernel<32, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+        launch_pdl(router_chain_kernel<32, FUSE, QIN>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits,
+                   f);
     else if (eg == 16)
-        launch_pdl(router_chain_kernel<16, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+        launch_pdl(router_chain_kernel<16, FUSE, QIN>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits,
+                   f);
     else
-        launch_pdl(router_chain_kernel<8, FUSE>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits, f);
+        launch_pdl(router_chain_kernel<8, FUSE, QIN>, grid, RC_THREADS, smem, st, xdeq, w, n, d, n_exp, tt, logits,
+                   f);
 }
 
 // Decode router, one chain per thread (v2).  A CTA holds tt tokens x EGc experts (thread t:
@@ -768,6 +854,7 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
     if (fused) *fused = false;
     if (xdeq == nullptr || d % 16 || n_exp % 8 || chain_mode() == 0) return false;
     if (chain_mode() != 3 && n_exp % 32 == 0) {
+        if (fuse != nullptr && fuse->qx != nullptr) return false;  // no quantizer in the v2 form
         // v2 (one chain per thread) for 32-expert groups: four tokens x 32 experts per CTA, every
         // warp forms its own products (QW decode 64: 37 -> 18 us).  Smaller groups keep v1, whose
         // producer warps feed one chain warp (v2 measured 2x slower there: one warp issues all).
@@ -791,14 +878,19 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
     const int64_t groups = n_exp / eg;
     const int tt = (int)std::min<int64_t>(32 / eg, std::max<int64_t>(1, ceil_div(n * groups, 148)));
     const int64_t ctas = ceil_div(n, tt) * groups;
-    const size_t smem = router_chain_smem(eg, tt);
+    const bool qin = fuse != nullptr && fuse->qx != nullptr;
+    const size_t smem = router_chain_smem(eg, tt, qin ? d : 0);
+    if (qin && (groups != 1 || chain_mode() != 1 || d % 4 || smem > RC_QIN_SMEM_MAX)) return false;
     const int64_t per_sm = std::max<int64_t>(1, (int64_t)(227 * 1024) / (int64_t)(smem + 1024));
     if (ctas > per_sm * 148) return false;
     const bool can_fuse = groups == 1 && chain_mode() == 1 && fuse != nullptr;
     if (fuse != nullptr && !can_fuse) return false;  // the caller runs the separate kernels
     const dim3 grid((unsigned)ceil_div(n, tt), (unsigned)groups);
     if (can_fuse) {
-        launch_chain<true>(eg, grid, smem, st, xdeq, w, n, d, n_exp, tt, logits, *fuse);
+        if (qin)
+            launch_chain<true, true>(eg, grid, smem, st, xdeq, w, n, d, n_exp, tt, logits, *fuse);
+        else
+            launch_chain<true>(eg, grid, smem, st, xdeq, w, n, d, n_exp, tt, logits, *fuse);
         *fused = true;
     } else {
         launch_chain<false>(eg, grid, smem, st, xdeq, w, n, d, n_exp, tt, logits, RouteFuse{});
@@ -815,6 +907,21 @@ cq_status router_fused(const float *xdeq, const float *w, int64_t n, int64_t d, 
     RouteFuse f{selected, weights, k};
     if (!router_chain(xdeq, w, n, d, n_exp, logits, &f, st, fused)) return CQ_OK;
     return check_launch("router_fused");
+}
+
+// Quantizer + router logits + top-k in one launch where router_chain can fuse them (*fused:
+// codes, scales, code sums and the cleared counters written as quantize_a4 writes them); otherwise
+// nothing is launched.  xdeq: scratch the caller owns (unused by the fused kernel).
+cq_status router_fused_quant(const void *x, int dtype, int8_t *codes, float *scales, int *nonfinite, int32_t *tsum,
+                             int32_t *zero, int n_zero, float *xdeq, const float *w, int64_t n, int64_t d,
+                             int64_t n_exp, float *logits, int32_t *selected, float *weights, int64_t k,
+                             cudaStream_t st, bool *fused) {
+    *fused = false;
+    if (n * n_exp == 0 || k < 1 || k > MAX_TOPK || k > n_exp) return CQ_OK;
+    if (dtype != CQ_DTYPE_F32 && dtype != CQ_DTYPE_BF16) return CQ_OK;
+    RouteFuse f{selected, weights, k, x, dtype, codes, scales, nonfinite, tsum, zero, n_zero};
+    if (!router_chain(xdeq, w, n, d, n_exp, logits, &f, st, fused)) return CQ_OK;
+    return check_launch("router_fused_quant");
 }
 
 // Token tile: TI x tq tokens, tq groups per expert quad chosen so the grid is about one CTA per SM.
