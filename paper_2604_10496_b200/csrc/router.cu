@@ -5,6 +5,8 @@
 // (k ascending, no FMA) on the exact fake-quant input codes*scale
 // (quant.py:8-13); top-k ids, their order, counts, offsets and the permutation
 // are therefore bit-exact.  Route weights use CUDA expf (ulp-bounded vs numpy).
+#include <type_traits>
+
 #include "common.cuh"
 #include "route_perm.cuh"
 
@@ -748,13 +750,52 @@ static void launch_chain(int eg, dim3 grid, size_t smem, cudaStream_t st, const 
 // lanes of a token), 4 LDS.32 of W (consecutive experts, conflict-free), 4 FMUL and the 4 dependent
 // FADDs — the FADD latency is the critical path, and no product buffer is written or synchronised.
 // Summation order and rounding as router_deq_kernel (bit-exact): acc = ((0 + x0 w0) + x1 w1) + ...
-constexpr int RV_K = 256, RV_NR = 3;
+constexpr int RV_K = 256;
+#ifndef RV_NR16
+#define RV_NR16 4
+#endif
+// ring depth: 3 stages of 36 KB for 32-expert CTAs, RV_NR16 of 25 KB for 16 (two CTAs per SM either way)
+__host__ __device__ constexpr int rv_nr(int egc) { return egc >= 32 ? 3 : RV_NR16; }
+// acc + x[0] w[0] + x[1] w[1] + ... over kn columns (kn % 4 == 0; KN > 0 fixes it at compile time):
+// w column j at wb[j * WP], x as float4s.
+template <int WP, int KN>
+__device__ __forceinline__ float chain2_steps(float acc, const float *__restrict__ wb, const float4 *__restrict__ xr,
+                                              int kn) {
+    // 16 columns per step, pipelined in two stages: a step's 16 products are formed while the previous
+    // step's 16 adds run, from operands loaded before them, so neither the shared-memory latency nor the
+    // multiply sits on the add chain (loads and products right before their adds: ~8-13 cycles per
+    // column against the adds' 4.2)
+    if (KN > 0) kn = KN;
+    float p[16];
+    auto products = [&](int j) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float4 xv = xr[(j >> 2) + u];
+            fmul2_rn(xv.x, xv.y, wb[(j + 4 * u) * WP], wb[(j + 4 * u + 1) * WP], p[4 * u], p[4 * u + 1]);
+            fmul2_rn(xv.z, xv.w, wb[(j + 4 * u + 2) * WP], wb[(j + 4 * u + 3) * WP], p[4 * u + 2], p[4 * u + 3]);
+        }
+    };
+    products(0);
+#pragma unroll 4
+    for (int j = 16; j < kn; j += 16) {
+        float q[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) q[c] = p[c];
+        products(j);  // independent of the adds below: issued alongside them
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc = __fadd_rn(acc, q[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc = __fadd_rn(acc, p[c]);
+    return acc;
+}
 template <int EGc, bool FUSE>
 __global__ void __launch_bounds__(128) router_chain2_kernel(const float *__restrict__ xdeq,
                                                             const float *__restrict__ w, int64_t n, int64_t d,
                                                             int64_t n_exp, int tt, float *__restrict__ logits,
                                                             RouteFuse f) {
     griddep_wait();
+    constexpr int RVN = rv_nr(EGc);
     constexpr int WP = EGc, XP = RV_K + 4;  // pitches (floats)
     extern __shared__ __align__(16) float rvs[];
     const int stage_f = RV_K * WP + tt * XP;  // floats per ring stage: W [RV_K][WP] then x [tt][XP]
@@ -764,11 +805,47 @@ __global__ void __launch_bounds__(128) router_chain2_kernel(const float *__restr
     const int64_t t0 = blockIdx.x * (int64_t)tt;
     const int64_t e0 = blockIdx.y * (int64_t)EGc;
     const int n_chunks = (int)((d + RV_K - 1) / RV_K);
+    // full chunks with 64 or 128 threads: each thread's copies at fixed row / quad offsets from
+    // pointers set up once (the generic loop's 64-bit address arithmetic per 16-byte copy was the
+    // kernel's hottest code: ~20 instructions per copy)
+    constexpr int QW = EGc / 4;
+    const float *wsrc = w + (int64_t)(tid / QW) * n_exp + e0 + 4 * (tid % QW);
+    const int xv = tid & 63, xt = tid >> 6;
+    auto stage_full = [&](int i, auto nth_c) {
+        constexpr int NTH = decltype(nth_c)::value, WRP = NTH / QW, WPASS = RV_K / WRP;
+        const int64_t k0 = (int64_t)i * RV_K;
+        float *wb = rvs + (i % RVN) * stage_f + (tid / QW) * WP + 4 * (tid % QW);
+        const float *ws = wsrc + k0 * n_exp;
+#pragma unroll
+        for (int m = 0; m < WPASS; ++m) cp_async16(wb + m * WRP * WP, ws + (int64_t)m * WRP * n_exp);
+        float *xb = rvs + (i % RVN) * stage_f + RV_K * WP;
+        for (int t = xt; t < tt; t += NTH / 64) {  // a token's 64 float4s per 64 threads
+            const int64_t tg = t0 + t < n ? t0 + t : n - 1;  // rows past n are never stored
+            cp_async16(xb + t * XP + 4 * xv, xdeq + tg * d + k0 + 4 * xv);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     auto stage = [&](int i) {
+#ifdef RV_NO_STAGE  // bounding experiment: chains over whatever the ring holds
+        if (i >= RVN - 1) {
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            return;
+        }
+#endif
+        if (i < n_chunks && (int64_t)(i + 1) * RV_K <= d) {
+            if (nthr == 128) {
+                stage_full(i, std::integral_constant<int, 128>{});
+                return;
+            }
+            if (nthr == 64) {
+                stage_full(i, std::integral_constant<int, 64>{});
+                return;
+            }
+        }
         if (i < n_chunks) {
             const int64_t k0 = (int64_t)i * RV_K;
             const int kn = (int)((d - k0) < RV_K ? (d - k0) : RV_K);
-            float *wb = rvs + (i % RV_NR) * stage_f;
+            float *wb = rvs + (i % RVN) * stage_f;
             for (int x = tid; x < kn * (EGc / 4); x += nthr) {
                 const int r = x / (EGc / 4), q = x - r * (EGc / 4);
                 cp_async16(wb + r * WP + 4 * q, w + (k0 + r) * n_exp + e0 + 4 * q);
@@ -783,26 +860,23 @@ __global__ void __launch_bounds__(128) router_chain2_kernel(const float *__restr
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll
-    for (int i = 0; i < RV_NR - 1; ++i) stage(i);
+    for (int i = 0; i < RVN - 1; ++i) stage(i);
     float acc = 0.0f;
     for (int i = 0; i < n_chunks; ++i) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(RV_NR - 2) : "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(RVN - 2) : "memory");
         __syncthreads();  // chunk i landed for every thread; chunk i - 1's stage is free
-        stage(i + RV_NR - 1);
+        stage(i + RVN - 1);
         if (chain) {
             const int kn = (int)((d - (int64_t)i * RV_K) < RV_K ? (d - (int64_t)i * RV_K) : RV_K);  // % 16 == 0
-            const float *wb = rvs + (i % RV_NR) * stage_f + el;
-            const float4 *xr = reinterpret_cast<const float4 *>(rvs + (i % RV_NR) * stage_f + RV_K * WP + tl * XP);
-#pragma unroll 4
-            for (int j = 0; j < kn / 4; ++j) {
-                const float4 xv = xr[j];
-                const float w0 = wb[(4 * j + 0) * WP], w1 = wb[(4 * j + 1) * WP];
-                const float w2 = wb[(4 * j + 2) * WP], w3 = wb[(4 * j + 3) * WP];
-                float p0, p1, p2, p3;
-                fmul2_rn(xv.x, xv.y, w0, w1, p0, p1);
-                fmul2_rn(xv.z, xv.w, w2, w3, p2, p3);
-                acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, p0), p1), p2), p3);
-            }
+            const float *wb = rvs + (i % RVN) * stage_f + el;
+            const float4 *xr = reinterpret_cast<const float4 *>(rvs + (i % RVN) * stage_f + RV_K * WP + tl * XP);
+            // full chunks with a compile-time trip count: the loads take immediate offsets (a runtime
+            // count cost ~7 instructions per column in address arithmetic and loop control, which one
+            // warp per SMSP issues at ~2.5 cycles each: 17 cycles per column against the 4.2 of the adds)
+            if (kn == RV_K)
+                acc = chain2_steps<WP, RV_K>(acc, wb, xr, kn);
+            else
+                acc = chain2_steps<WP, 0>(acc, wb, xr, kn);
         }
     }
     if (chain && t0 + tl < n) logits[(t0 + tl) * n_exp + e0 + el] = acc;
@@ -820,7 +894,7 @@ __global__ void __launch_bounds__(128) router_chain2_kernel(const float *__restr
 }
 
 static size_t router_chain2_smem(int egc, int tt) {
-    return sizeof(float) * (size_t)RV_NR * ((size_t)RV_K * egc + (size_t)tt * (RV_K + 4));
+    return sizeof(float) * (size_t)rv_nr(egc) * ((size_t)RV_K * egc + (size_t)tt * (RV_K + 4));
 }
 
 template <bool FUSE>
@@ -864,9 +938,22 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
         // v2 (one chain per thread) for 32-expert groups: four tokens x 32 experts per CTA, every
         // warp forms its own products (QW decode 64: 37 -> 18 us).  Smaller groups keep v1, whose
         // producer warps feed one chain warp (v2 measured 2x slower there: one warp issues all).
-        const int egc = 32;
+        static int egc_env = -1;  // CQ_ROUTER_EGC: experts per CTA (experiments)
+        if (egc_env < 0) {
+            const char *e = getenv("CQ_ROUTER_EGC");
+            egc_env = e ? atoi(e) : 32;
+        }
+        const int egc = egc_env == 8 || egc_env == 16 ? egc_env : 32;
         const int64_t groups = n_exp / egc;
-        const int tt = 4;
+        // 64-thread CTAs while they fit one per SM: the four warps of a 128-thread CTA need 5 shared-memory
+        // wavefronts per column (W 1 per warp, x 1 per 4 columns), above the 4.2-cycle add chain
+        static int nth_env = -1;  // CQ_ROUTER_NTH: 64 / 128 forces one (experiments)
+        if (nth_env < 0) {
+            const char *e = getenv("CQ_ROUTER_NTH");
+            nth_env = e ? atoi(e) : 0;
+        }
+        const int nth = nth_env == 64 || nth_env == 128 ? nth_env : (ceil_div(n, 64 / egc) * groups <= 148 ? 64 : 128);
+        const int tt = nth / egc;
         const int64_t ctas = ceil_div(n, tt) * groups;
         if (ctas > 2 * 148 || router_chain2_smem(egc, tt) > 220 * 1024) return false;  // the tiled routers
         const bool can_fuse = groups == 1 && chain_mode() == 1 && fuse != nullptr;
