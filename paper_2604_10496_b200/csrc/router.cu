@@ -153,11 +153,14 @@ __global__ void __launch_bounds__(RD_THREADS) router_deq_kernel(const float *__r
 // CTA streams all of w through shared memory, so the host sizes the token tile
 // to one CTA per SM (QW: 124 us with 16-token tiles on 2 CTAs per SM, 115 us
 // with 32 on 128 SMs, 28 on 147 SMs below; profiles/README.md).
-template <int EC, int TI>
+// RK > 0: the chunk width at compile time (rk == RK): full chunks run with immediate load offsets
+// (a runtime width cost ~13M address / loop instructions of 69M at QW, issued by ~2 warps per SMSP).
+template <int EC, int TI, int RK = 0>
 __global__ void __launch_bounds__(256) router_tile_kernel(const float *__restrict__ xdeq,
                                                                  const float *__restrict__ w, int64_t n, int64_t d,
                                                                  int rk, float *__restrict__ logits) {
     griddep_wait();
+    if (RK > 0) rk = RK;
     constexpr int EQ = EC / 4;                 // expert quads
     const int NT = blockDim.x;
     const int TQ = NT / EQ;                    // token groups of TI
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(256) router_tile_kernel(const float *__restric
         const int kn = (int)((d - (int64_t)c * rk) < rk ? (d - (int64_t)c * rk) : rk);  // multiple of 16
         const float *wr = ws + (size_t)b * rk * EC + 4 * eq;
         const float *xr = xs + (size_t)b * TT * xp + (size_t)(TI * tq) * xp;
-        for (int j = 0; j < kn; j += 4) {
+        auto step4 = [&](int j) {
             float4 wv[4], xv[TI];
 #pragma unroll
             for (int q = 0; q < 4; ++q) wv[q] = *reinterpret_cast<const float4 *>(wr + (j + q) * EC);
@@ -222,6 +225,12 @@ __global__ void __launch_bounds__(256) router_tile_kernel(const float *__restric
                     acc[i][3] = __fadd_rn(acc[i][3], p3);
                 }
             }
+        };
+        if (RK > 0 && kn == RK) {
+#pragma unroll 8
+            for (int j = 0; j < RK; j += 4) step4(j);
+        } else {
+            for (int j = 0; j < kn; j += 4) step4(j);
         }
         __syncthreads();  // buffer b is refilled by the next iteration's prefetch
     }
@@ -1028,20 +1037,36 @@ static cq_status router_tile_launch(const float *xdeq, const float *w, int64_t n
     const int smem_max = ctas <= 148 ? 200 * 1024 : 96 * 1024;  // one CTA per SM, else two
     int rk = (int)std::min<int64_t>(512, (smem_max / 8 - 4 * tt) / (tt + n_exp)) & ~15;
     if (rk < 16) rk = 16;
+    constexpr int RKC = 128, RKS = 64;  // the compile-time chunk widths, when they fit
+    const int fixed = rk >= RKC ? RKC : (rk >= RKS ? RKS : 0);
+    if (fixed) rk = fixed;
     const size_t smem = (size_t)8 * ((size_t)tt * (rk + 4) + (size_t)rk * n_exp);
     static std::atomic<uint64_t> attr{0};  // devices whose smem opt-in is set
     if (first_on_device(attr)) {
         cudaFuncSetAttribute(router_tile_kernel<32, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(router_tile_kernel<64, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(router_tile_kernel<128, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<32, TI, RKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<64, TI, RKC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<128, TI, RKC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<32, TI, RKS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<64, TI, RKS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(router_tile_kernel<128, TI, RKS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
     }
     const dim3 grid((unsigned)ctas);
+#define CQ_TILE(EC_)                                                                                        \
+    (fixed == RKC   ? launch_pdl(router_tile_kernel<EC_, TI, RKC>, grid, nt, smem, st, xdeq, w, n, d, rk, logits) \
+     : fixed == RKS ? launch_pdl(router_tile_kernel<EC_, TI, RKS>, grid, nt, smem, st, xdeq, w, n, d, rk, logits) \
+                    : launch_pdl(router_tile_kernel<EC_, TI>, grid, nt, smem, st, xdeq, w, n, d, rk, logits))
     if (n_exp == 32)
-        launch_pdl(router_tile_kernel<32, TI>, grid, nt, smem, st, xdeq, w, n, d, rk, logits);
+        CQ_TILE(32);
     else if (n_exp == 64)
-        launch_pdl(router_tile_kernel<64, TI>, grid, nt, smem, st, xdeq, w, n, d, rk, logits);
+        CQ_TILE(64);
     else
-        launch_pdl(router_tile_kernel<128, TI>, grid, nt, smem, st, xdeq, w, n, d, rk, logits);
+        CQ_TILE(128);
+#undef CQ_TILE
     return check_launch("router_logits");
 }
 
