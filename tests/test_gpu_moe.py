@@ -195,7 +195,8 @@ def test_tc_decode_route_mode(n, E, k):
     (one expert group) or the GEMM's B build takes it from the logits (E > 32,
     n <= 128), and the B build derives the segment permutation in every CTA
     (route_perm.cuh) and publishes it; n = 200 at E = 128 runs the separate
-    kernels.  Routing arrays bit-exact with the
+    kernels.  With one expert group the router launch quantizes too (fp32 and
+    bf16 inputs).  Routing arrays bit-exact with the
     oracle, the layer output within the layer tolerance of the ordered path,
     and identical across two calls."""
     d, ff, g = 256, 256, 128
@@ -220,9 +221,23 @@ def test_tc_decode_route_mode(n, E, k):
     assert np.array_equal(tr["perm_slot"].cpu().numpy()[:R], slot)
     assert np.array_equal(tr["inv"].cpu().numpy(), inv)
     assert np.array_equal(tr["scales_perm"].cpu().numpy()[:R].view(np.int32), scales[tok].view(np.int32))
+    # the layer-input codes, scales and code sums (decode: quantized inside the router launch)
+    assert np.array_equal(tr["codes"].cpu().numpy(), codes)
+    assert np.array_equal(tr["scales"].cpu().numpy().view(np.int32), scales.view(np.int32))
+    assert np.array_equal(tr["tok_sums"].cpu().numpy(), codes.astype(np.int32).sum(axis=1))
     ordered = layer(v, path="ordered")
     assert o.relative_error(out.cpu().numpy(), ordered.cpu().numpy()) <= LAYER_TOL
     assert torch.equal(layer(v), out)
+    # bf16 input: the same quantizer on the bf16 values, bit for bit
+    vb = v.to(torch.bfloat16)
+    layer(vb)
+    trb = layer.trace(n)
+    cb, sb = oracle.c_quantize(vb.float().cpu().numpy())
+    assert np.array_equal(trb["codes"].cpu().numpy(), cb)
+    assert np.array_equal(trb["scales"].cpu().numpy().view(np.int32), sb.view(np.int32))
+    lb = oracle.c_matmul(cb.astype(np.float32) * sb[:, None], w.cpu().numpy())
+    assert np.array_equal(trb["logits"].cpu().numpy().view(np.int32), lb.view(np.int32))
+    assert np.array_equal(trb["selected"].cpu().numpy(), o.select_top_k(lb, k)[0])
 
 
 @pytest.mark.parametrize("g", [0, 128])
