@@ -1093,8 +1093,14 @@ cq_status router_logits(const int8_t *codes, const float *scales, const float *x
         int tt = (int)std::min<int64_t>(RD_THREADS / n_exp, std::max<int64_t>(1, ceil_div(n, 148)));
         if (tt_env > 0 && tt_env * n_exp <= RD_THREADS) tt = tt_env;
         const int threads = (int)ceil_div(tt * n_exp, 32) * 32;
-        // double-buffered x [tt][rk] + W [rk][E] f32 in <= 96 KB; rk a multiple of 16, <= 512
-        int rk = (int)std::min<int64_t>(512, ((96 * 1024) / (8 * (tt + n_exp))) & ~15LL);
+        // double-buffered x [tt][rk] + W [rk][E] f32 in <= 48 KB; rk a multiple of 16, <= 512
+        static int rd_kb = -1;  // CQ_ROUTER_RD_KB: the CTA's shared-memory budget (experiments)
+        if (rd_kb < 0) {
+            const char *e = getenv("CQ_ROUTER_RD_KB");
+            // PH (E = 16): 96 KB 76.8 us (two CTAs per SM, 1.7 waves), 64 78, 48 72.2, 32 75.3
+            rd_kb = e ? atoi(e) : 48;
+        }
+        int rk = (int)std::min<int64_t>(512, (((int64_t)rd_kb * 1024) / (8 * (tt + n_exp))) & ~15LL);
         if (rk < 16) rk = 16;
         const size_t smem = (size_t)8 * rk * (tt + n_exp);
         static std::atomic<uint64_t> attr{0};  // devices whose smem opt-in is set
