@@ -944,15 +944,15 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
     if (xdeq == nullptr || d % 16 || n_exp % 8 || chain_mode() == 0) return false;
     if (chain_mode() != 3 && n_exp % 32 == 0) {
         if (fuse != nullptr && fuse->qx != nullptr) return false;  // no quantizer in the v2 form
-        // v2 (one chain per thread) for 32-expert groups: four tokens x 32 experts per CTA, every
+        // v2 (one chain per thread) when E % 32 == 0 (16 experts per CTA by default), every
         // warp forms its own products (QW decode 64: 37 -> 18 us).  Smaller groups keep v1, whose
         // producer warps feed one chain warp (v2 measured 2x slower there: one warp issues all).
         static int egc_env = -1;  // CQ_ROUTER_EGC: experts per CTA (experiments)
         if (egc_env < 0) {
             const char *e = getenv("CQ_ROUTER_EGC");
-            egc_env = e ? atoi(e) : 32;
+            egc_env = e ? atoi(e) : 16;  // 16 vs 32, same box x 3: QW decode 64 -0.2 us, 256 -0.45 us
         }
-        const int egc = egc_env == 8 || egc_env == 16 ? egc_env : 32;
+        const int egc = egc_env == 8 || egc_env == 32 ? egc_env : 16;
         const int64_t groups = n_exp / egc;
         // 64-thread CTAs while they fit one per SM: the four warps of a 128-thread CTA need 5 shared-memory
         // wavefronts per column (W 1 per warp, x 1 per 4 columns), above the 4.2-cycle add chain
