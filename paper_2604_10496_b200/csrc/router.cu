@@ -952,7 +952,8 @@ static bool router_chain(const float *xdeq, const float *w, int64_t n, int64_t d
             const char *e = getenv("CQ_ROUTER_EGC");
             egc_env = e ? atoi(e) : 16;  // 16 vs 32, same box x 3: QW decode 64 -0.2 us, 256 -0.45 us
         }
-        const int egc = egc_env == 8 || egc_env == 32 ? egc_env : 16;
+        int egc = egc_env == 8 || egc_env == 32 ? egc_env : 16;
+        if (fuse != nullptr && n_exp == 32) egc = 32;  // one group: the launch also does the top-k
         const int64_t groups = n_exp / egc;
         // 64-thread CTAs while they fit one per SM: the four warps of a 128-thread CTA need 5 shared-memory
         // wavefronts per column (W 1 per warp, x 1 per 4 columns), above the 4.2-cycle add chain
